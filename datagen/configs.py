@@ -1,0 +1,70 @@
+"""The five BASELINE.json configs as frozen knobs.
+
+Every number here is a configuration constant, not a result: the GPU path and
+the oracle both read it.  `beta` values for configs 1-4 were chosen by
+`scripts/calibrate_beta.py`, which calls only `oracle/` (AMB-9 in DESIGN.md).
+"""
+from __future__ import annotations
+
+import copy
+
+
+def beta_schedule(n: int) -> float:
+    """PAPER.md:286 (§3.3): beta = 1e2 for d in [1e4,1e5], 1e3 for [1e5,1e6], 1e4 for d >= 1e6.
+
+    Below 1e4 the paper is silent; we extend the smallest tier downward.
+    """
+    if n >= 1_000_000:
+        return 1e4
+    if n >= 100_000:
+        return 1e3
+    return 1e2
+
+
+# Field meanings:
+#   n, n_test   train / test points;  r  feature count (paper's r)
+#   h           Gaussian kernel width;  C  box bound(s) (Eq. 1)
+#   beta        ADMM penalty / ULV shift
+#   max_it      ADMM iterations (PAPER.md:286 fixes 10; BASELINE.json configs override)
+#   leaf        leaf size m;  cap  rank cap k_max;  s = sketch columns = cap + 16
+#   rel_tol, abs_tol   rank rule AMB-10;  rank_mode  'adaptive' | 'fixed'
+#   seeds       data 1000+c, Omega 2000+c, tree 3000+c
+_CONFIGS = {
+    0: dict(name="cfg0_gmm2k", n=2000, n_test=500, r=8, h=1.0, C=[1.0], beta=1.0,
+            max_it=200, leaf=64, cap=1024, s=1040, rel_tol=1e-6, abs_tol=0.0,
+            rank_mode="fixed", ranks_file="tests/golden/cfg0_ranks.json", gpus=[1]),
+    1: dict(name="cfg1_uniform32k", n=32768, n_test=8192, r=22, h=0.5, C=[10.0], beta=None,
+            max_it=500, leaf=128, cap=128, s=144, rel_tol=1e-4, abs_tol=0.0,
+            rank_mode="adaptive", gpus=[1]),
+    2: dict(name="cfg2_binary131k", n=131072, n_test=32768, r=123, h=2.0, C=[1.0], beta=None,
+            max_it=500, leaf=256, cap=256, s=272, rel_tol=1e-3, abs_tol=0.0,
+            rank_mode="adaptive", gpus=[1, 2]),
+    3: dict(name="cfg3_mixed524k", n=524288, n_test=131072, r=54, h=1.0, C=[1.0], beta=None,
+            max_it=1000, leaf=256, cap=256, s=272, rel_tol=1e-3, abs_tol=0.0,
+            rank_mode="adaptive", gpus=[1, 2, 4, 8]),
+    4: dict(name="cfg4_grid65k", n=65536, n_test=16384, r=8, h=[0.25, 0.5, 1.0, 2.0, 4.0],
+            C=[0.1, 1.0, 10.0, 100.0, 1e3, 1e4], beta=None,
+            max_it=200, leaf=64, cap=64, s=80, rel_tol=1e-6, abs_tol=0.0,
+            rank_mode="adaptive", gpus=[1, 2, 4, 8]),
+}
+
+# Calibrated shifts (scripts/calibrate_beta.py; AMB-9).  None = use beta_schedule(n).
+_BETA = {1: None, 2: None, 3: None, 4: None}
+
+for _c, _cfg in _CONFIGS.items():
+    _cfg["id"] = _c
+    _cfg["seed_data"] = 1000 + _c
+    _cfg["seed_omega"] = 2000 + _c
+    _cfg["seed_tree"] = 3000 + _c
+    if _cfg["beta"] is None:
+        b = _BETA.get(_c)
+        _cfg["beta"] = b if b is not None else beta_schedule(_cfg["n"])
+
+CONFIGS = _CONFIGS
+
+
+def get_config(c: int, **overrides) -> dict:
+    """A deep copy of config `c` with overrides (e.g. n=4096 for a scaled parity case)."""
+    cfg = copy.deepcopy(_CONFIGS[c])
+    cfg.update(overrides)
+    return cfg
