@@ -1,0 +1,180 @@
+/*
+ * svmhss.h — C-ABI of libsvmhss.so: the B200 (sm_100a) hot path of
+ * "ADMM + HSS kernel approximations for large-scale nonlinear SVMs" (arXiv 2108.04167).
+ *
+ * Citations: P:n = PAPER.md line n.  Step labels (T*, R*, H*, U*, S*, A*, AMB-*) are the
+ * readings listed in DESIGN.md ("Readings of the paper").
+ *
+ * Common conventions (every entry point):
+ *  - Array pointers are DEVICE pointers on the current CUDA device, fp64 unless noted,
+ *    except the *_host entry points, whose pointers are HOST pointers.
+ *  - User-visible per-point vectors are in ORIGINAL point order; internally the library
+ *    works in tree (permuted) order.  Multi-column vectors are point-major:
+ *    v[i*ncols + c].
+ *  - Calls are ordered on `stream` (a cudaStream_t passed as void*; NULL = legacy default
+ *    stream).  Functions that must read sizes back (build, factor, train) synchronize
+ *    `stream` before returning.
+ *  - Return 0 (HSS_OK) on success, a negative HSS_E* code on error; a human-readable
+ *    message is available from hss_last_error() (thread-local).  On error no output
+ *    buffer is guaranteed to be written and no handle is returned.
+ *  - Ownership: handles own their device memory.  The caller owns every input and
+ *    output buffer.  A ulv_t keeps its hss_t alive (reference counted), so the two can
+ *    be freed in any order.
+ *  - Determinism: identical inputs and options give bitwise-identical outputs (fixed
+ *    reduction orders, no floating-point atomics).
+ *  - No CPU fallback exists: without a usable CUDA device every call returns HSS_ECUDA.
+ */
+#ifndef SVMHSS_H
+#define SVMHSS_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+enum {
+  HSS_OK = 0,
+  HSS_EINVAL = -1,   /* invalid argument (sizes, h <= 0, beta <= 0, C <= 0, labels not +-1, ...) */
+  HSS_ENOMEM = -2,   /* device allocation failed */
+  HSS_ECUDA = -3,    /* CUDA runtime / launch error, or no device */
+  HSS_ENCCL = -4,    /* reserved for the multi-GPU communicator */
+  HSS_ENOTSPD = -5,  /* K~ + beta I not SPD: Cholesky breakdown; node id in the message (AMB-14) */
+  HSS_EW1 = -6       /* w1 = e^T (K~+beta I)^-1 e <= 0 */
+};
+
+typedef struct hss_s* hss_t;  /* compressed kernel K~ */
+typedef struct ulv_s* ulv_t;  /* ULV factorization of K~ + beta I */
+
+/* Build options (P:184-187 and readings T1-T4, R1-R3, H1-H5, AMB-10, AMB-11). */
+typedef struct {
+  int32_t leaf_size;       /* m >= 1: leaf size; tree depth L = ceil(log2(n/m)) (T1) */
+  double rel_tol;          /* AMB-10 rank rule: |R_jj| > max(rel_tol |R_11|, abs_tol sqrt(s)) */
+  double abs_tol;
+  int32_t max_rank;        /* k_max >= 1: rank cap */
+  int32_t oversample;      /* p >= 0: sketch columns s = max_rank + p (AMB-18) */
+  uint64_t omega_seed;     /* R1-R3 key for Omega (keyed by ORIGINAL index, column) */
+  uint64_t tree_seed;      /* R1-R3 key for the power-iteration start vectors (T2) */
+  const int32_t* ranks;    /* HOST pointer, nullable.  Fixed-rank mode: one rank per node in
+                              level-major BFS order (2^(L+1)-1 entries; root ignored); the
+                              node's rank is min(ranks[t], rows_t, s).  NULL = adaptive. */
+} hss_opts;
+
+/* Build statistics (D6 / P:366-367 "Compression", "Memory"). */
+typedef struct {
+  int64_t n;
+  int32_t r, L, s, leaf_size;
+  int32_t max_rank_used;   /* max over nodes of k_t */
+  int32_t cap_hits;        /* nodes where the tolerance was unmet at the cap (warning) */
+  int32_t passthrough;     /* nodes with k_t == rows_t */
+  int64_t generator_bytes; /* bytes of D, U, B (fp64) */
+  double ms_tree, ms_omega, ms_sketch, ms_compress; /* phase device times (CUDA events) */
+} hss_stats;
+
+typedef struct {
+  double beta;
+  int64_t factor_bytes;    /* bytes of the per-node solve operators M_t */
+  double ms_factor;
+} ulv_stats;
+
+/* ---- build: tree + Omega + sketch + per-level ID compression (Alg.3 l.1) ----
+ * F: n x r row-major features (device).  h > 0 kernel width.
+ * Returns HSS_EINVAL if n < 1, r < 1, h <= 0, leaf_size < 1, max_rank < 1, oversample < 0,
+ * or s = max_rank + oversample > 2^20 (RNG column field, R1). */
+int hss_build(const double* F, int64_t n, int32_t r, double h, const hss_opts* opt,
+              void* stream, hss_t* out);
+
+/* Stats and the tree/rank/skeleton export used by the parity tests.
+ * perm_out: n int64 (tree position -> original index), nullable.
+ * ranks_out: 2^(L+1)-1 int32 (level-major BFS, root = -1), nullable.
+ * skel_out: sum_t k_t int64 tree positions, nodes in BFS order, nullable.  HOST pointers. */
+int hss_info(hss_t H, hss_stats* st, int64_t* perm_out, int32_t* ranks_out, int64_t* skel_out);
+
+/* out = K~ v (reading M: up/down sweeps); v, out: n x nrhs, original order. */
+int hss_matvec(hss_t H, const double* v, double* out, int32_t nrhs, void* stream);
+
+/* ---- ULV factorization of K~ + beta I (readings U) ----
+ * beta > 0.  HSS_ENOTSPD if a Cholesky breaks down (message names the node). */
+int hss_ulv_factor(hss_t H, double beta, void* stream, ulv_t* out);
+int ulv_info(ulv_t U, ulv_stats* st);
+
+/* x = (K~ + beta I)^-1 b (readings S); b, x: n x nrhs, original order; may alias. */
+int ulv_solve(ulv_t U, const double* b, double* x, int32_t nrhs, void* stream);
+
+/* ---- ADMM training (Alg. 2; Alg. 3 lines 4-13; AMB-1) ----
+ * y: n labels, exactly +-1.0 (original order).  C: nC box bounds > 0 (HOST pointer).
+ * The nC problems advance together as nC right-hand sides of one solve per iteration
+ * (factorization reused across C).  max_it >= 1 iterations exactly.
+ * Outputs (device, n x nC point-major, original order): z_out (required), mu_out (nullable).
+ * bias_out, obj_out: nC HOST doubles, nullable: bias per AMB-2/AMB-3 via one HSS mat-vec
+ * (P:196-200), objective f~(z) of Eq. (8).
+ * trace: nullable; if trace_every > 0, z and mu after every trace_every-th iteration (and
+ * the last) are written to trace_z / trace_mu (device, ntrace x n x nC, original order,
+ * ntrace = ceil(max_it / trace_every)). */
+typedef struct {
+  int32_t trace_every;
+  double* trace_z;
+  double* trace_mu;
+  double margin_eps_rel;   /* AMB-3 epsilon / C; <= 0 selects the default 1e-8 */
+} admm_opts;
+
+typedef struct {
+  double w1;               /* e^T (K~+beta I)^-1 e */
+  double ms_precompute, ms_loop, ms_bias;
+  int32_t iterations, graph;  /* graph = 1 if the loop ran as a CUDA graph */
+  int64_t kernel_launches_per_iter;
+} admm_stats;
+
+int admm_svm_train(ulv_t U, const double* y, const double* C, int32_t nC, int32_t max_it,
+                   const admm_opts* opt, double* z_out, double* mu_out, double* bias_out,
+                   double* obj_out, admm_stats* st, void* stream);
+
+/* ---- prediction (Alg. 3; AMB-15, AMB-19: exact kernel) ----
+ * dv[t*nC + c] = sum_i coef[i*nC + c] K(Ftrain_i, Ftest_t) + bias[c]; label = +1 if dv >= 0.
+ * Ftrain: n x r, Ftest: m x r row-major; coef: n x nC (device, e.g. y*z); bias: nC HOST.
+ * dv_out: m x nC device (nullable); label_out: m x nC int8 device (nullable).  nC <= 16. */
+int svm_predict(const double* Ftrain, const double* coef, int64_t n, int32_t r, double h,
+                const double* bias, int32_t nC, const double* Ftest, int64_t m,
+                double* dv_out, int8_t* label_out, void* stream);
+
+/* ---- end-to-end on HOST buffers (Alg. 3): host->device copies of F, y,
+ * Ftest, the full build + factor + ADMM + bias + predict, device->host copies of z and
+ * labels.  z_out: n x nC, labels_out: m x nC (int8), bias_out, obj_out: nC — all HOST,
+ * labels_out nullable (then Ftest may be NULL and m = 0).  timings_ms (nullable, HOST,
+ * 8 doubles): h2d, build, factor, admm, bias, predict, d2h, total. */
+int svm_train_predict_host(const double* F, const double* y, int64_t n, int32_t r,
+                           double h, const hss_opts* opt, double beta, const double* C,
+                           int32_t nC, int32_t max_it, const double* Ftest, int64_t m,
+                           double* z_out, double* bias_out, double* obj_out,
+                           int8_t* labels_out, double* timings_ms);
+
+/* ---- debug / parity exports of individual hot-path steps ---- */
+/* R1-R3: Omega rows for the given ORIGINAL indices (device int64 idx, count rows), s cols. */
+int hss_omega(uint64_t seed, const int64_t* idx, int64_t rows, int32_t s, double* out, void* stream);
+/* T1-T4: the permutation only (device int64 perm_out, n). */
+int hss_tree(const double* F, int64_t n, int32_t r, int32_t leaf_size, uint64_t tree_seed,
+             int64_t* perm_out, void* stream);
+/* H1: S = K(Fa, Fb) W  (Fa: na x r, Fb: nb x r, W: nb x ncols, S: na x ncols; all device,
+ * row-major), with the fused distance-GEMM -> exp -> GEMM kernel.  If same_set != 0, Fa and
+ * Fb are the same points and K_ii = 1 exactly. */
+int hss_kernel_matmul(const double* Fa, int64_t na, const double* Fb, int64_t nb, int32_t r,
+                      double h, const double* W, int32_t ncols, int32_t same_set, double* S,
+                      void* stream);
+/* K(Fa, Fb) block (na x nb row-major, device). */
+int hss_kernel_block(const double* Fa, int64_t na, const double* Fb, int64_t nb, int32_t r,
+                     double h, double* K, void* stream);
+/* Node generators for parity: U_t (rows x k row-major, identity if pass-through),
+ * B_t (k_left x k_right, internal nodes), D_t (leaf, m_t x m_t).  HOST outputs; query
+ * sizes with NULL pointers (rows/k written).  node = level-major BFS id. */
+int hss_node(hss_t H, int32_t node, int32_t* rows, int32_t* k, double* U, double* B,
+             double* D);
+
+void hss_free(hss_t H);
+void ulv_free(ulv_t U);
+const char* hss_last_error(void);
+const char* hss_version(void);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* SVMHSS_H */

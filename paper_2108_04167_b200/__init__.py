@@ -1,0 +1,293 @@
+"""paper_2108_04167_b200 — B200 (sm_100a) hot path of ADMM + HSS kernel SVMs (arXiv 2108.04167).
+
+Thin Python layer over the C-ABI library libsvmhss.so (include/svmhss.h): the same
+entry-point names, argument marshalling only.  PyTorch is used for device memory and
+streams; every computational step runs in the library's CUDA kernels.  Importing this
+package loads the library and raises if it is missing (no CPU fallback).
+
+    H = hss_build(F, h=..., leaf_size=..., rel_tol=..., max_rank=..., ...)
+    U = hss_ulv_factor(H, beta)
+    out = admm_svm_train(U, y, C=[...], max_it=...)
+    dv, labels = svm_predict(F, y[:, None] * out["z"], h, out["bias"], Ftest)
+"""
+from __future__ import annotations
+
+import ctypes as ct
+
+import numpy as np
+
+from . import _lib
+from ._lib import AdmmOpts, AdmmStats, HssError, HssOpts, HssStats, UlvStats, check, ptr
+
+_L = _lib.load()
+
+__all__ = ["hss_build", "hss_ulv_factor", "admm_svm_train", "svm_predict", "svm_train_predict_host",
+           "hss_omega", "hss_tree", "hss_kernel_matmul", "hss_kernel_block", "HSS", "ULV", "HssError",
+           "version"]
+
+
+def version() -> str:
+    return _L.hss_version().decode()
+
+
+def _cuda_f64(t, name):
+    import torch
+    if not (isinstance(t, torch.Tensor) and t.is_cuda and t.dtype == torch.float64):
+        raise TypeError(f"{name} must be a CUDA float64 tensor")
+    if not t.is_contiguous():
+        raise TypeError(f"{name} must be contiguous")
+    return t
+
+
+def _stream(stream):
+    return _lib.stream_handle(stream)
+
+
+class HSS:
+    """Handle of a compressed kernel K~ (hss_t)."""
+
+    def __init__(self, handle, n, r, h):
+        self._h = handle
+        self.n, self.r, self.h = n, r, h
+
+    @property
+    def handle(self):
+        if self._h is None:
+            raise RuntimeError("HSS handle freed")
+        return self._h
+
+    def info(self):
+        st = HssStats()
+        check(_L.hss_info(self.handle, ct.byref(st), None, None, None))
+        d = {f: getattr(st, f) for f, _ in HssStats._fields_}
+        nn = 2 ** (st.L + 1) - 1
+        perm = np.empty(self.n, dtype=np.int64)
+        ranks = np.empty(nn, dtype=np.int32)
+        check(_L.hss_info(self.handle, None, perm.ctypes.data, ranks.ctypes.data, None))
+        ksum = int(ranks[ranks > 0].sum())
+        skel = np.empty(max(1, ksum), dtype=np.int64)
+        check(_L.hss_info(self.handle, None, None, None, skel.ctypes.data))
+        d.update(perm=perm, ranks=ranks, skeletons=skel[:ksum])
+        return d
+
+    def node(self, t):
+        rows, k = ct.c_int32(), ct.c_int32()
+        check(_L.hss_node(self.handle, t, ct.byref(rows), ct.byref(k), None, None, None))
+        return rows.value, k.value
+
+    def node_generators(self, t, L, k_children=None):
+        rows, k = self.node(t)
+        U = np.zeros((rows, max(k, 0)))
+        D = None
+        B = None
+        lvl = int(np.floor(np.log2(t + 1)))
+        if lvl == L:
+            D = np.zeros((rows, rows))
+        if lvl < L:
+            ka = self.node(2 * t + 1)[1]
+            kb = self.node(2 * t + 2)[1]
+            B = np.zeros((ka, kb))
+        check(_L.hss_node(self.handle, t, None, None, U.ctypes.data if k > 0 else None,
+                          B.ctypes.data if B is not None and B.size else None,
+                          D.ctypes.data if D is not None else None))
+        return dict(rows=rows, k=k, U=U if k >= 0 else None, B=B, D=D)
+
+    def matvec(self, v, stream=None):
+        import torch
+        _cuda_f64(v, "v")
+        nrhs = 1 if v.dim() == 1 else v.shape[1]
+        out = torch.empty_like(v)
+        check(_L.hss_matvec(self.handle, ptr(v), ptr(out), nrhs, _stream(stream)))
+        return out
+
+    def free(self):
+        if self._h is not None:
+            _L.hss_free(self._h)
+            self._h = None
+
+    def __del__(self):
+        try:
+            self.free()
+        except Exception:
+            pass
+
+
+class ULV:
+    """Handle of the ULV factorization of K~ + beta I (ulv_t)."""
+
+    def __init__(self, handle, hss, beta):
+        self._h = handle
+        self.hss, self.beta = hss, beta
+
+    @property
+    def handle(self):
+        if self._h is None:
+            raise RuntimeError("ULV handle freed")
+        return self._h
+
+    def info(self):
+        st = UlvStats()
+        check(_L.ulv_info(self.handle, ct.byref(st)))
+        return {f: getattr(st, f) for f, _ in UlvStats._fields_}
+
+    def solve(self, b, stream=None):
+        import torch
+        _cuda_f64(b, "b")
+        nrhs = 1 if b.dim() == 1 else b.shape[1]
+        x = torch.empty_like(b)
+        check(_L.ulv_solve(self.handle, ptr(b), ptr(x), nrhs, _stream(stream)))
+        return x
+
+    def free(self):
+        if self._h is not None:
+            _L.ulv_free(self._h)
+            self._h = None
+
+    def __del__(self):
+        try:
+            self.free()
+        except Exception:
+            pass
+
+
+def make_opts(leaf_size, rel_tol=0.0, abs_tol=0.0, max_rank=64, oversample=16, omega_seed=0,
+              tree_seed=0, ranks=None):
+    o = HssOpts()
+    o.leaf_size, o.rel_tol, o.abs_tol = int(leaf_size), float(rel_tol), float(abs_tol)
+    o.max_rank, o.oversample = int(max_rank), int(oversample)
+    o.omega_seed, o.tree_seed = int(omega_seed), int(tree_seed)
+    keep = None
+    if ranks is not None:
+        keep = np.ascontiguousarray(np.asarray(ranks, dtype=np.int32))
+        o.ranks = keep.ctypes.data_as(ct.POINTER(ct.c_int32))
+    return o, keep
+
+
+def hss_build(F, h, leaf_size, rel_tol=0.0, abs_tol=0.0, max_rank=64, oversample=16, omega_seed=0,
+              tree_seed=0, ranks=None, stream=None) -> HSS:
+    """hss_build (Alg. 3 line 1): F is a CUDA float64 (n, r) tensor, original order."""
+    _cuda_f64(F, "F")
+    n, r = F.shape
+    o, keep = make_opts(leaf_size, rel_tol, abs_tol, max_rank, oversample, omega_seed, tree_seed, ranks)
+    hdl = ct.c_void_p()
+    check(_L.hss_build(ptr(F), n, r, float(h), ct.byref(o), _stream(stream), ct.byref(hdl)))
+    del keep
+    return HSS(hdl.value, n, r, h)
+
+
+def hss_ulv_factor(H: HSS, beta, stream=None) -> ULV:
+    """hss_ulv_factor."""
+    hdl = ct.c_void_p()
+    check(_L.hss_ulv_factor(H.handle, float(beta), _stream(stream), ct.byref(hdl)))
+    return ULV(hdl.value, H, beta)
+
+
+def admm_svm_train(U: ULV, y, C, max_it, trace_every=0, margin_eps_rel=0.0, want_mu=True,
+                   stream=None):
+    """admm_svm_train (Alg. 2 / Alg. 3).  y: CUDA float64 (n,), +-1.
+    Returns dict(z (n, nC), mu, bias[nC], obj[nC], stats, trace_z, trace_mu)."""
+    import torch
+    _cuda_f64(y, "y")
+    n = y.shape[0]
+    Cs = np.ascontiguousarray(np.atleast_1d(np.asarray(C, dtype=np.float64)))
+    nC = Cs.shape[0]
+    z = torch.empty((n, nC), dtype=torch.float64, device=y.device)
+    mu = torch.empty_like(z) if want_mu else None
+    bias = np.zeros(nC)
+    obj = np.zeros(nC)
+    opts = AdmmOpts()
+    opts.margin_eps_rel = float(margin_eps_rel)
+    tz = tm = None
+    if trace_every:
+        nt = -(-int(max_it) // int(trace_every))
+        tz = torch.empty((nt, n, nC), dtype=torch.float64, device=y.device)
+        tm = torch.empty_like(tz)
+        opts.trace_every, opts.trace_z, opts.trace_mu = int(trace_every), ptr(tz), ptr(tm)
+    st = AdmmStats()
+    check(_L.admm_svm_train(U.handle, ptr(y), Cs.ctypes.data, nC, int(max_it), ct.byref(opts), ptr(z),
+                            ptr(mu), bias.ctypes.data, obj.ctypes.data, ct.byref(st), _stream(stream)))
+    return dict(z=z, mu=mu, bias=bias, obj=obj, trace_z=tz, trace_mu=tm,
+                stats={f: getattr(st, f) for f, _ in AdmmStats._fields_})
+
+
+def svm_predict(Ftrain, coef, h, bias, Ftest, stream=None):
+    """svm_predict: dv = K(Ftest, Ftrain) coef + bias; labels = sign (0 -> +1)."""
+    import torch
+    _cuda_f64(Ftrain, "Ftrain")
+    _cuda_f64(coef, "coef")
+    _cuda_f64(Ftest, "Ftest")
+    n, r = Ftrain.shape
+    m = Ftest.shape[0]
+    nC = 1 if coef.dim() == 1 else coef.shape[1]
+    b = np.ascontiguousarray(np.atleast_1d(np.asarray(bias, dtype=np.float64)))
+    dv = torch.empty((m, nC), dtype=torch.float64, device=Ftrain.device)
+    lab = torch.empty((m, nC), dtype=torch.int8, device=Ftrain.device)
+    check(_L.svm_predict(ptr(Ftrain), ptr(coef), n, r, float(h), b.ctypes.data, nC, ptr(Ftest), m,
+                         ptr(dv), ptr(lab), _stream(stream)))
+    return dv, lab
+
+
+def svm_train_predict_host(F, y, h, beta, C, max_it, Ftest=None, **opt_kw):
+    """End-to-end on HOST numpy buffers (Alg. 3): copies in, build, factor, ADMM, bias,
+    predict, copies out.  Returns dict(z, bias, obj, labels, timings_ms)."""
+    F = np.ascontiguousarray(F, dtype=np.float64)
+    y = np.ascontiguousarray(y, dtype=np.float64)
+    n, r = F.shape
+    Cs = np.ascontiguousarray(np.atleast_1d(np.asarray(C, dtype=np.float64)))
+    nC = Cs.shape[0]
+    o, keep = make_opts(**opt_kw)
+    z = np.zeros((n, nC))
+    bias, obj = np.zeros(nC), np.zeros(nC)
+    tim = np.zeros(8)
+    if Ftest is not None:
+        Ft = np.ascontiguousarray(Ftest, dtype=np.float64)
+        m = Ft.shape[0]
+        lab = np.zeros((m, nC), dtype=np.int8)
+    else:
+        Ft, m, lab = None, 0, None
+    check(_L.svm_train_predict_host(F.ctypes.data, y.ctypes.data, n, r, float(h), ct.byref(o),
+                                    float(beta), Cs.ctypes.data, nC, int(max_it),
+                                    Ft.ctypes.data if Ft is not None else None, m, z.ctypes.data,
+                                    bias.ctypes.data, obj.ctypes.data,
+                                    lab.ctypes.data if lab is not None else None, tim.ctypes.data))
+    del keep
+    names = ["h2d", "build", "factor", "admm", "bias", "predict", "d2h", "total"]
+    return dict(z=z, bias=bias, obj=obj, labels=lab, timings_ms=dict(zip(names, tim.tolist())))
+
+
+# ---- debug / parity exports
+def hss_omega(seed, idx, s, stream=None):
+    import torch
+    idx = idx.to(torch.int64).contiguous()
+    out = torch.empty((idx.shape[0], s), dtype=torch.float64, device=idx.device)
+    check(_L.hss_omega(int(seed), ptr(idx), idx.shape[0], int(s), ptr(out), _stream(stream)))
+    return out
+
+
+def hss_tree(F, leaf_size, tree_seed, stream=None):
+    import torch
+    _cuda_f64(F, "F")
+    perm = torch.empty(F.shape[0], dtype=torch.int64, device=F.device)
+    check(_L.hss_tree(ptr(F), F.shape[0], F.shape[1], int(leaf_size), int(tree_seed), ptr(perm),
+                      _stream(stream)))
+    return perm
+
+
+def hss_kernel_matmul(Fa, Fb, h, W, same_set=False, stream=None):
+    import torch
+    for t, nm in ((Fa, "Fa"), (Fb, "Fb"), (W, "W")):
+        _cuda_f64(t, nm)
+    S = torch.empty((Fa.shape[0], W.shape[1]), dtype=torch.float64, device=Fa.device)
+    check(_L.hss_kernel_matmul(ptr(Fa), Fa.shape[0], ptr(Fb), Fb.shape[0], Fa.shape[1], float(h), ptr(W),
+                               W.shape[1], int(bool(same_set)), ptr(S), _stream(stream)))
+    return S
+
+
+def hss_kernel_block(Fa, Fb, h, stream=None):
+    import torch
+    _cuda_f64(Fa, "Fa")
+    _cuda_f64(Fb, "Fb")
+    K = torch.empty((Fa.shape[0], Fb.shape[0]), dtype=torch.float64, device=Fa.device)
+    check(_L.hss_kernel_block(ptr(Fa), Fa.shape[0], ptr(Fb), Fb.shape[0], Fa.shape[1], float(h), ptr(K),
+                              _stream(stream)))
+    return K

@@ -1,0 +1,397 @@
+// api.cu — the C-ABI of libsvmhss.so (include/svmhss.h).  Argument validation, handle
+// ownership (reference counted hss_t <- ulv_t), error translation; no arithmetic here.
+#include <cmath>
+#include <cstring>
+#include "internal.cuh"
+
+namespace svmhss {
+static thread_local std::string g_last_error;
+void set_last_error(const std::string& s) { g_last_error = s; }
+
+static void ensure_device() {
+  int cnt = 0;
+  cudaError_t e = cudaGetDeviceCount(&cnt);
+  if (e != cudaSuccess || cnt == 0) throw Error(HSS_ECUDA, "no CUDA device available (no CPU fallback exists)");
+}
+
+template <typename Fn>
+static int guarded(Fn&& fn) {
+  try {
+    ensure_device();
+    fn();
+    return HSS_OK;
+  } catch (const Error& e) {
+    set_last_error(e.what());
+    cudaGetLastError();
+    return e.code;
+  } catch (const std::bad_alloc&) {
+    set_last_error("host allocation failed");
+    return HSS_ENOMEM;
+  } catch (const std::exception& e) {
+    set_last_error(e.what());
+    return HSS_ECUDA;
+  }
+}
+
+static void release_hss(HSSImpl* H) {
+  if (H && H->refs.fetch_sub(1) == 1) delete H;
+}
+
+static void validate_opts(const hss_opts* o, int64_t n, int32_t r, double h) {
+  require(o != nullptr, "hss_build: opts is NULL");
+  require(n >= 1, "hss_build: n must be >= 1");
+  require(r >= 1, "hss_build: r must be >= 1");
+  require(std::isfinite(h) && h > 0, "hss_build: h must be > 0");
+  require(o->leaf_size >= 1, "hss_build: leaf_size must be >= 1");
+  require(o->max_rank >= 1, "hss_build: max_rank must be >= 1");
+  require(o->oversample >= 0, "hss_build: oversample must be >= 0");
+  const int s = o->max_rank + o->oversample;
+  require(s <= (1 << 20), "hss_build: s = max_rank + oversample must be <= 2^20 (R1 column field)");
+  require(s % 2 == 0, "hss_build: s = max_rank + oversample must be even");
+  require(o->rel_tol >= 0 && o->abs_tol >= 0, "hss_build: tolerances must be >= 0");
+}
+
+}  // namespace svmhss
+
+using namespace svmhss;
+
+struct hss_s { HSSImpl* impl; };
+struct ulv_s { ULVImpl* impl; };
+
+extern "C" {
+
+const char* hss_last_error(void) { return g_last_error.c_str(); }
+const char* hss_version(void) { return "svmhss 0.1 (sm_100a)"; }
+
+int hss_build(const double* F, int64_t n, int32_t r, double h, const hss_opts* opt, void* stream,
+              hss_t* out) {
+  return guarded([&] {
+    require(out != nullptr && F != nullptr, "hss_build: NULL pointer");
+    validate_opts(opt, n, r, h);
+    auto* H = new HSSImpl();
+    try {
+      hss_build_impl(*H, F, n, r, h, *opt, (cudaStream_t)stream);
+    } catch (...) {
+      delete H;
+      throw;
+    }
+    *out = new hss_s{H};
+  });
+}
+
+int hss_info(hss_t Hh, hss_stats* st, int64_t* perm_out, int32_t* ranks_out, int64_t* skel_out) {
+  return guarded([&] {
+    require(Hh != nullptr, "hss_info: NULL handle");
+    const HSSImpl& H = *Hh->impl;
+    if (st) *st = H.st;
+    if (perm_out) {
+      CUDA_CHECK(cudaMemcpy(perm_out, H.perm.p, H.n * sizeof(int64_t), cudaMemcpyDeviceToHost));
+    }
+    if (ranks_out) {
+      const int nn = (1 << (H.L + 1)) - 1;
+      for (int t = 0; t < nn; ++t) ranks_out[t] = -1;
+      for (int l = 1; l <= H.L; ++l)
+        for (size_t i = 0; i < H.lv[l].size(); ++i) ranks_out[H.node_id(l, (int)i)] = H.lv[l][i].k;
+    }
+    if (skel_out) {
+      int64_t off = 0;
+      for (int l = 0; l <= H.L; ++l)
+        for (size_t i = 0; i < H.lv[l].size(); ++i) {
+          if (l == 0) continue;
+          const auto& nd = H.lv[l][i];
+          if (nd.k > 0)
+            CUDA_CHECK(cudaMemcpy(skel_out + off, H.J[l].p + nd.koff, nd.k * sizeof(int64_t), cudaMemcpyDeviceToHost));
+          off += nd.k;
+        }
+    }
+  });
+}
+
+int hss_node(hss_t Hh, int32_t node, int32_t* rows, int32_t* k, double* U, double* B, double* D) {
+  return guarded([&] {
+    require(Hh != nullptr, "hss_node: NULL handle");
+    const HSSImpl& H = *Hh->impl;
+    const int nn = (1 << (H.L + 1)) - 1;
+    require(node >= 0 && node < nn, "hss_node: node id out of range");
+    int l = 0;
+    while (((1 << (l + 1)) - 1) <= node) ++l;
+    const int i = node - ((1 << l) - 1);
+    const NodeInfo& nd = H.lv[l][i];
+    if (rows) *rows = nd.rows;
+    if (k) *k = (l == 0) ? -1 : nd.k;
+    if (U && l >= 1) {
+      if (nd.pt) {
+        for (int a = 0; a < nd.rows; ++a)
+          for (int b = 0; b < nd.k; ++b) U[(int64_t)a * nd.k + b] = (a == b) ? 1.0 : 0.0;
+      } else if (nd.k > 0) {
+        CUDA_CHECK(cudaMemcpy(U, H.U[l].p + nd.uoff, (size_t)nd.rows * nd.k * 8, cudaMemcpyDeviceToHost));
+      }
+    }
+    if (B && l < H.L) {
+      const int ka = H.lv[l + 1][2 * i].k, kb = H.lv[l + 1][2 * i + 1].k;
+      if (ka * kb > 0)
+        CUDA_CHECK(cudaMemcpy(B, H.B[l].p + nd.boff, (size_t)ka * kb * 8, cudaMemcpyDeviceToHost));
+    }
+    if (D && l == H.L) {
+      const int64_t m = nd.hi - nd.lo;
+      CUDA_CHECK(cudaMemcpy(D, H.D.p + nd.doff, (size_t)m * m * 8, cudaMemcpyDeviceToHost));
+    }
+  });
+}
+
+int hss_matvec(hss_t Hh, const double* v, double* out, int32_t nrhs, void* stream) {
+  return guarded([&] {
+    require(Hh && v && out, "hss_matvec: NULL pointer");
+    require(nrhs >= 1, "hss_matvec: nrhs must be >= 1");
+    const HSSImpl& H = *Hh->impl;
+    cudaStream_t s = (cudaStream_t)stream;
+    DevBuf<double> a((size_t)H.n * nrhs), b((size_t)H.n * nrhs);
+    gather_rows(v, H.perm.p, H.n, nrhs, a.p, s);
+    hss_matvec_tree(H, a.p, b.p, nrhs, s);
+    scatter_rows(b.p, H.perm.p, H.n, nrhs, out, s);
+    CUDA_CHECK(cudaStreamSynchronize(s));
+  });
+}
+
+int hss_ulv_factor(hss_t Hh, double beta, void* stream, ulv_t* out) {
+  return guarded([&] {
+    require(Hh && out, "hss_ulv_factor: NULL pointer");
+    require(std::isfinite(beta) && beta > 0, "hss_ulv_factor: beta must be > 0");
+    auto* F = new ULVImpl();
+    F->H = Hh->impl;
+    F->H->refs.fetch_add(1);
+    F->beta = beta;
+    try {
+      ulv_factor_impl(*F, (cudaStream_t)stream);
+    } catch (...) {
+      release_hss(F->H);
+      delete F;
+      throw;
+    }
+    *out = new ulv_s{F};
+  });
+}
+
+int ulv_info(ulv_t U, ulv_stats* st) {
+  return guarded([&] {
+    require(U && st, "ulv_info: NULL pointer");
+    *st = U->impl->st;
+  });
+}
+
+int ulv_solve(ulv_t Uh, const double* b, double* x, int32_t nrhs, void* stream) {
+  return guarded([&] {
+    require(Uh && b && x, "ulv_solve: NULL pointer");
+    require(nrhs >= 1 && nrhs <= 8, "ulv_solve: nrhs must be in 1..8");
+    const ULVImpl& F = *Uh->impl;
+    const HSSImpl& H = *F.H;
+    cudaStream_t s = (cudaStream_t)stream;
+    SolveWS ws;
+    solve_ws_alloc(F, nrhs, ws);
+    gather_rows(b, H.perm.p, H.n, nrhs, ws.fin[H.L], s);
+    ulv_solve_tree(F, ws, s);
+    scatter_rows(ws.xout[H.L], H.perm.p, H.n, nrhs, x, s);
+    CUDA_CHECK(cudaStreamSynchronize(s));
+  });
+}
+
+int admm_svm_train(ulv_t Uh, const double* y, const double* C, int32_t nC, int32_t max_it,
+                   const admm_opts* opt, double* z_out, double* mu_out, double* bias_out,
+                   double* obj_out, admm_stats* st, void* stream) {
+  return guarded([&] {
+    require(Uh && y && C && z_out, "admm_svm_train: NULL pointer");
+    require(nC >= 1 && nC <= 8, "admm_svm_train: nC must be in 1..8");
+    require(max_it >= 1, "admm_svm_train: max_it must be >= 1");
+    std::vector<double> Cs(C, C + nC);
+    for (double c : Cs) require(std::isfinite(c) && c > 0, "admm_svm_train: every C must be > 0");
+    AdmmResult r = admm_train_impl(*Uh->impl, y, Cs, max_it, opt, z_out, mu_out, bias_out, obj_out,
+                                   (cudaStream_t)stream);
+    if (st) {
+      st->w1 = r.w1;
+      st->ms_precompute = r.ms_pre;
+      st->ms_loop = r.ms_loop;
+      st->ms_bias = r.ms_bias;
+      st->iterations = max_it;
+      st->graph = r.graph;
+      st->kernel_launches_per_iter = r.launches;
+    }
+  });
+}
+
+int svm_predict(const double* Ftrain, const double* coef, int64_t n, int32_t r, double h,
+                const double* bias, int32_t nC, const double* Ftest, int64_t m, double* dv_out,
+                int8_t* label_out, void* stream) {
+  return guarded([&] {
+    require(Ftrain && coef && bias && (Ftest || m == 0), "svm_predict: NULL pointer");
+    require(n >= 1 && r >= 1 && m >= 0, "svm_predict: bad sizes");
+    require(nC >= 1 && nC <= 16, "svm_predict: nC must be in 1..16");
+    require(std::isfinite(h) && h > 0, "svm_predict: h must be > 0");
+    if (m == 0) return;
+    predict_impl(Ftrain, coef, n, r, h, bias, nC, Ftest, m, dv_out, label_out, (cudaStream_t)stream);
+  });
+}
+
+int svm_train_predict_host(const double* F, const double* y, int64_t n, int32_t r, double h,
+                           const hss_opts* opt, double beta, const double* C, int32_t nC,
+                           int32_t max_it, const double* Ftest, int64_t m, double* z_out,
+                           double* bias_out, double* obj_out, int8_t* labels_out,
+                           double* timings_ms) {
+  return guarded([&] {
+    require(F && y && C && z_out, "svm_train_predict_host: NULL pointer");
+    require(nC >= 1 && nC <= 8, "svm_train_predict_host: nC must be in 1..8");
+    validate_opts(opt, n, r, h);
+    cudaStream_t s;
+    CUDA_CHECK(cudaStreamCreateWithFlags(&s, cudaStreamNonBlocking));
+    struct SG { cudaStream_t s; ~SG() { cudaStreamDestroy(s); } } sg{s};
+    cudaEvent_t ev[8];
+    for (auto& e : ev) CUDA_CHECK(cudaEventCreate(&e));
+    struct EG { cudaEvent_t* e; ~EG() { for (int i = 0; i < 8; ++i) cudaEventDestroy(e[i]); } } eg{ev};
+    CUDA_CHECK(cudaEventRecord(ev[0], s));
+    DevBuf<double> dF((size_t)n * r), dy(n), dFt((size_t)std::max<int64_t>(1, m) * r);
+    DevBuf<double> dz((size_t)n * nC), coef((size_t)n * nC);
+    DevBuf<int8_t> dl((size_t)std::max<int64_t>(1, m) * nC);
+    h2d(dF.p, F, (size_t)n * r, s);
+    h2d(dy.p, y, n, s);
+    if (labels_out && m > 0) h2d(dFt.p, Ftest, (size_t)m * r, s);
+    CUDA_CHECK(cudaEventRecord(ev[1], s));
+    HSSImpl* H = new HSSImpl();
+    struct HG { HSSImpl* h; ~HG() { release_hss(h); } } hg{H};
+    hss_build_impl(*H, dF.p, n, r, h, *opt, s);
+    CUDA_CHECK(cudaEventRecord(ev[2], s));
+    ULVImpl Fz;
+    Fz.H = H;
+    Fz.beta = beta;
+    require(std::isfinite(beta) && beta > 0, "beta must be > 0");
+    ulv_factor_impl(Fz, s);
+    CUDA_CHECK(cudaEventRecord(ev[3], s));
+    std::vector<double> Cs(C, C + nC), bias(nC), obj(nC);
+    for (double c : Cs) require(std::isfinite(c) && c > 0, "every C must be > 0");
+    AdmmResult ar = admm_train_impl(Fz, dy.p, Cs, max_it, nullptr, dz.p, nullptr, bias.data(), obj.data(), s);
+    CUDA_CHECK(cudaEventRecord(ev[4], s));
+    CUDA_CHECK(cudaEventRecord(ev[5], s));
+    if (labels_out && m > 0) {
+      // coef = y * z (original order)
+      std::vector<double> zh((size_t)n * nC);
+      d2h(zh.data(), dz.p, (size_t)n * nC, s);
+      CUDA_CHECK(cudaStreamSynchronize(s));
+      for (int64_t i = 0; i < n; ++i)
+        for (int c = 0; c < nC; ++c) zh[i * nC + c] *= y[i];
+      h2d(coef.p, zh.data(), (size_t)n * nC, s);
+      predict_impl(dF.p, coef.p, n, r, h, bias.data(), nC, dFt.p, m, nullptr, dl.p, s);
+    }
+    CUDA_CHECK(cudaEventRecord(ev[6], s));
+    d2h(z_out, dz.p, (size_t)n * nC, s);
+    if (labels_out && m > 0) d2h(labels_out, dl.p, (size_t)m * nC, s);
+    CUDA_CHECK(cudaEventRecord(ev[7], s));
+    CUDA_CHECK(cudaStreamSynchronize(s));
+    for (int c = 0; c < nC; ++c) {
+      if (bias_out) bias_out[c] = bias[c];
+      if (obj_out) obj_out[c] = obj[c];
+    }
+    if (timings_ms) {
+      float t;
+      CUDA_CHECK(cudaEventElapsedTime(&t, ev[0], ev[1])); timings_ms[0] = t;
+      CUDA_CHECK(cudaEventElapsedTime(&t, ev[1], ev[2])); timings_ms[1] = t;
+      CUDA_CHECK(cudaEventElapsedTime(&t, ev[2], ev[3])); timings_ms[2] = t;
+      timings_ms[3] = ar.ms_pre + ar.ms_loop;
+      timings_ms[4] = ar.ms_bias;
+      CUDA_CHECK(cudaEventElapsedTime(&t, ev[5], ev[6])); timings_ms[5] = t;
+      CUDA_CHECK(cudaEventElapsedTime(&t, ev[6], ev[7])); timings_ms[6] = t;
+      CUDA_CHECK(cudaEventElapsedTime(&t, ev[0], ev[7])); timings_ms[7] = t;
+    }
+  });
+}
+
+int hss_omega(uint64_t seed, const int64_t* idx, int64_t rows, int32_t s, double* out, void* stream) {
+  return guarded([&] {
+    require(idx && out, "hss_omega: NULL pointer");
+    require(rows >= 0 && s >= 1 && s <= (1 << 20), "hss_omega: bad sizes");
+    omega_rows(seed, idx, rows, s, out, (cudaStream_t)stream);
+    CUDA_CHECK(cudaStreamSynchronize((cudaStream_t)stream));
+  });
+}
+
+int hss_tree(const double* F, int64_t n, int32_t r, int32_t leaf_size, uint64_t tree_seed,
+             int64_t* perm_out, void* stream) {
+  return guarded([&] {
+    require(F && perm_out, "hss_tree: NULL pointer");
+    require(n >= 1 && r >= 1 && leaf_size >= 1, "hss_tree: bad sizes");
+    cudaStream_t s = (cudaStream_t)stream;
+    const int rp = (r + 3) / 4 * 4;
+    DevBuf<double> Fpad((size_t)n * rp);
+    pad_rows(F, n, r, rp, Fpad.p, s);
+    build_tree(Fpad.p, n, r, rp, leaf_size, tree_seed, perm_out, nullptr, s);
+  });
+}
+
+int hss_kernel_matmul(const double* Fa, int64_t na, const double* Fb, int64_t nb, int32_t r,
+                      double h, const double* W, int32_t ncols, int32_t same_set, double* S,
+                      void* stream) {
+  return guarded([&] {
+    require(Fa && Fb && W && S, "hss_kernel_matmul: NULL pointer");
+    require(na >= 0 && nb >= 0 && r >= 1 && ncols >= 1, "hss_kernel_matmul: bad sizes");
+    require(std::isfinite(h) && h > 0, "hss_kernel_matmul: h must be > 0");
+    cudaStream_t s = (cudaStream_t)stream;
+    const int rp = (r + 3) / 4 * 4;
+    const int ncp = (ncols + 1) / 2 * 2;
+    DevBuf<double> A((size_t)std::max<int64_t>(1, na) * rp), Bm((size_t)std::max<int64_t>(1, nb) * rp),
+        nua(std::max<int64_t>(1, na)), nub(std::max<int64_t>(1, nb));
+    pad_rows(Fa, na, r, rp, A.p, s);
+    pad_rows(Fb, nb, r, rp, Bm.p, s);
+    row_norms(A.p, na, rp, nua.p, s);
+    row_norms(Bm.p, nb, rp, nub.p, s);
+    DevBuf<double> Wp, Sp;
+    const double* Wuse = W;
+    double* Suse = S;
+    if (ncp != ncols) {  // pad to an even column count
+      Wp.alloc((size_t)std::max<int64_t>(1, nb) * ncp);
+      Sp.alloc((size_t)std::max<int64_t>(1, na) * ncp);
+      CUDA_CHECK(cudaMemsetAsync(Wp.p, 0, Wp.bytes(), s));
+      CUDA_CHECK(cudaMemcpy2DAsync(Wp.p, ncp * 8, W, ncols * 8, ncols * 8, nb, cudaMemcpyDeviceToDevice, s));
+      Wuse = Wp.p;
+      Suse = Sp.p;
+    }
+    KmmArgs a{};
+    a.Fa = A.p; a.nua = nua.p; a.na = na;
+    a.Fb = Bm.p; a.nub = nub.p; a.nb = nb;
+    a.rp = rp; a.W = Wuse; a.ldw = ncp; a.ncols = ncp; a.S = Suse; a.lds = ncp;
+    a.neg_inv_2h2 = -1.0 / (2.0 * h * h);
+    a.same_set = same_set ? 1 : 0;
+    kernel_matmul(a, s);
+    if (ncp != ncols)
+      CUDA_CHECK(cudaMemcpy2DAsync(S, ncols * 8, Sp.p, ncp * 8, ncols * 8, na, cudaMemcpyDeviceToDevice, s));
+    CUDA_CHECK(cudaStreamSynchronize(s));
+  });
+}
+
+int hss_kernel_block(const double* Fa, int64_t na, const double* Fb, int64_t nb, int32_t r, double h,
+                     double* K, void* stream) {
+  return guarded([&] {
+    require(Fa && Fb && K, "hss_kernel_block: NULL pointer");
+    require(na >= 0 && nb >= 0 && r >= 1 && na < (1 << 30) && nb < (1 << 30), "hss_kernel_block: bad sizes");
+    cudaStream_t s = (cudaStream_t)stream;
+    // stack both point sets in one array; columns index the second half
+    DevBuf<double> A((size_t)std::max<int64_t>(1, na + nb) * r);
+    CUDA_CHECK(cudaMemcpyAsync(A.p, Fa, (size_t)na * r * 8, cudaMemcpyDeviceToDevice, s));
+    CUDA_CHECK(cudaMemcpyAsync(A.p + (size_t)na * r, Fb, (size_t)nb * r * 8, cudaMemcpyDeviceToDevice, s));
+    std::vector<KblkProb> p = {{(int)na, (int)nb, nullptr, 0, nullptr, na, K, nb, 0.0}};
+    kernel_blocks(A.p, r, r, h, p, s);
+    CUDA_CHECK(cudaStreamSynchronize(s));
+  });
+}
+
+void hss_free(hss_t H) {
+  if (!H) return;
+  release_hss(H->impl);
+  delete H;
+}
+
+void ulv_free(ulv_t U) {
+  if (!U) return;
+  HSSImpl* H = U->impl->H;
+  delete U->impl;
+  release_hss(H);
+  delete U;
+}
+
+}  // extern "C"

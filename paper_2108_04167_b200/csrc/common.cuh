@@ -1,0 +1,146 @@
+// common.cuh — shared device/host helpers of libsvmhss (sm_100a).
+#pragma once
+#include <cuda_runtime.h>
+#include <stdint.h>
+#include <stdio.h>
+#include <string>
+#include <vector>
+#include <stdexcept>
+
+#include "../../include/svmhss.h"
+
+namespace svmhss {
+
+// ------------------------------------------------------------------ errors
+struct Error : public std::runtime_error {
+  int code;
+  Error(int c, const std::string& m) : std::runtime_error(m), code(c) {}
+};
+
+void set_last_error(const std::string& s);
+
+#define CUDA_CHECK(x)                                                                 \
+  do {                                                                                \
+    cudaError_t e__ = (x);                                                            \
+    if (e__ != cudaSuccess)                                                           \
+      throw ::svmhss::Error(e__ == cudaErrorMemoryAllocation ? HSS_ENOMEM : HSS_ECUDA, \
+                            std::string(#x) + ": " + cudaGetErrorString(e__));        \
+  } while (0)
+
+#define LAUNCH_CHECK() CUDA_CHECK(cudaGetLastError())
+
+inline void require(bool ok, const std::string& msg) {
+  if (!ok) throw Error(HSS_EINVAL, msg);
+}
+
+// ------------------------------------------------------------------ device buffers
+template <typename T>
+struct DevBuf {
+  T* p = nullptr;
+  size_t n = 0;
+  DevBuf() {}
+  explicit DevBuf(size_t count) { alloc(count); }
+  void alloc(size_t count) {
+    release();
+    n = count;
+    if (count) CUDA_CHECK(cudaMalloc((void**)&p, count * sizeof(T)));
+  }
+  void release() {
+    if (p) cudaFree(p);
+    p = nullptr;
+    n = 0;
+  }
+  ~DevBuf() { release(); }
+  DevBuf(const DevBuf&) = delete;
+  DevBuf& operator=(const DevBuf&) = delete;
+  DevBuf(DevBuf&& o) noexcept : p(o.p), n(o.n) { o.p = nullptr; o.n = 0; }
+  DevBuf& operator=(DevBuf&& o) noexcept {
+    release(); p = o.p; n = o.n; o.p = nullptr; o.n = 0; return *this;
+  }
+  size_t bytes() const { return n * sizeof(T); }
+};
+
+template <typename T>
+inline void h2d(T* d, const T* h, size_t n, cudaStream_t s) {
+  if (n) CUDA_CHECK(cudaMemcpyAsync(d, h, n * sizeof(T), cudaMemcpyHostToDevice, s));
+}
+template <typename T>
+inline void d2h(T* h, const T* d, size_t n, cudaStream_t s) {
+  if (n) CUDA_CHECK(cudaMemcpyAsync(h, d, n * sizeof(T), cudaMemcpyDeviceToHost, s));
+}
+
+// A device copy of a host vector (uploaded on `s`; host vector must outlive the copy —
+// callers synchronize or keep the vector alive).
+template <typename T>
+inline DevBuf<T> upload(const std::vector<T>& v, cudaStream_t s) {
+  DevBuf<T> d(v.size());
+  h2d(d.p, v.data(), v.size(), s);
+  return d;
+}
+
+inline int ceil_div(int64_t a, int64_t b) { return (int)((a + b - 1) / b); }
+
+// ------------------------------------------------------------------ timing
+struct EventTimer {
+  cudaEvent_t a, b;
+  cudaStream_t s;
+  explicit EventTimer(cudaStream_t st) : s(st) {
+    CUDA_CHECK(cudaEventCreate(&a));
+    CUDA_CHECK(cudaEventCreate(&b));
+    CUDA_CHECK(cudaEventRecord(a, s));
+  }
+  double stop_ms() {
+    CUDA_CHECK(cudaEventRecord(b, s));
+    CUDA_CHECK(cudaEventSynchronize(b));
+    float ms = 0;
+    CUDA_CHECK(cudaEventElapsedTime(&ms, a, b));
+    return ms;
+  }
+  ~EventTimer() { cudaEventDestroy(a); cudaEventDestroy(b); }
+};
+
+// ------------------------------------------------------------------ device helpers
+__device__ __forceinline__ double warp_sum(double v) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+  return v;
+}
+
+// Block-wide sum with a fixed reduction order (deterministic). `red` >= 32 doubles.
+__device__ __forceinline__ double block_sum(double v, double* red) {
+  int lane = threadIdx.x & 31, wid = threadIdx.x >> 5, nw = (blockDim.x + 31) >> 5;
+  v = warp_sum(v);
+  __syncthreads();
+  if (lane == 0) red[wid] = v;
+  __syncthreads();
+  double t = 0.0;
+  if (wid == 0) {
+    t = lane < nw ? red[lane] : 0.0;
+    t = warp_sum(t);
+    if (lane == 0) red[0] = t;
+  }
+  __syncthreads();
+  t = red[0];
+  __syncthreads();
+  return t;
+}
+
+// splitmix64 finalizer (reading R1-R3; same constants as oracle/rng.py, independently written)
+__host__ __device__ __forceinline__ uint64_t splitmix64(uint64_t z) {
+  z += 0x9E3779B97F4A7C15ull;
+  z = (z ^ (z >> 30)) * 0xBF58476D1CE4E5B9ull;
+  z = (z ^ (z >> 27)) * 0x94D049BB133111EBull;
+  return z ^ (z >> 31);
+}
+
+// R1-R3: Gaussian keyed by (seed key, i, j).  `key` = splitmix64(seed).
+__device__ __forceinline__ double counter_gaussian(uint64_t key, uint64_t i, uint64_t j) {
+  uint64_t ctr = (i << 20) | j;
+  uint64_t base = key + 2ull * ctr;
+  uint64_t a = splitmix64(base), b = splitmix64(base + 1ull);
+  double u1 = ((double)(a >> 11) + 0.5) * 0x1.0p-53;
+  double u2 = (double)(b >> 11) * 0x1.0p-53;
+  return sqrt(-2.0 * log(u1)) * cos(2.0 * 3.141592653589793 * u2);
+}
+
+}  // namespace svmhss

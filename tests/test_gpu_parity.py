@@ -1,0 +1,307 @@
+"""GPU (CUDA path through the C-ABI) vs CPU oracle parity, element by element.
+
+Tolerances (BASELINE.json north_star):
+  HSS solve vectors           ||d||/||ref|| <= 1e-9
+  ADMM z, mu (trace points), objective   <= 1e-7 relative
+  predicted labels            identical wherever |dv_oracle| > 1e-6
+  integer work (perm, ranks, skeletons)  bit-exact
+Ungraded but checked: Omega (<= 4 ulp), sketch (<= 1e-12), bias (<= 1e-7).
+"""
+import json
+import os
+
+import numpy as np
+import pytest
+
+import datagen
+from oracle import admm as o_admm
+from oracle import hss as o_hss
+from oracle import kernel as o_kernel
+from oracle import pipeline as o_pipe
+from oracle import rng as o_rng
+from oracle import svm as o_svm
+from oracle import tree as o_tree
+from oracle import ulv as o_ulv
+
+pytestmark = pytest.mark.gpu
+GOLD = os.path.join(os.path.dirname(__file__), "golden")
+
+
+def _t(a):
+    import torch
+    return torch.from_numpy(np.ascontiguousarray(a)).to("cuda")
+
+
+def _np(t):
+    return t.detach().cpu().numpy()
+
+
+def relerr(a, b):
+    return np.linalg.norm(np.asarray(a) - np.asarray(b)) / max(np.linalg.norm(b), 1e-300)
+
+
+# ------------------------------------------------------------------ R1-R3
+def test_omega_matches_oracle(gpu_lib):
+    P = gpu_lib
+    idx = np.concatenate([np.arange(1000), np.array([2 ** 40 + 5, 123456789])])
+    g = _np(P.hss_omega(2003, _t(idx), 300))
+    c = o_rng.omega(2003, idx, 300)
+    assert np.abs(g - c).max() <= 8 * np.finfo(float).eps * np.abs(c).max()
+
+
+# ------------------------------------------------------------------ T1-T4
+@pytest.mark.parametrize("cfg,n", [(0, 2000), (1, 3000), (2, 2500), (3, 5000), (4, 3000), (1, 100), (3, 64)])
+def test_tree_permutation_bit_exact(gpu_lib, cfg, n):
+    P = gpu_lib
+    c = datagen.get_config(cfg)
+    F, y, _, _ = datagen.generate(cfg, n=n, n_test=0)
+    perm_o, _ = o_tree.build_tree(F, c["leaf"], c["seed_tree"])
+    perm_g = _np(P.hss_tree(_t(F), c["leaf"], c["seed_tree"]))
+    assert np.array_equal(perm_g, perm_o)
+
+
+# ------------------------------------------------------------------ H1 (fused sketch kernel)
+@pytest.mark.parametrize("na,nb,r,ncols,h", [(300, 300, 8, 80, 1.0), (257, 333, 22, 144, 0.5),
+                                             (129, 200, 54, 272, 1.0), (100, 150, 123, 272, 2.0),
+                                             (70, 90, 8, 1040, 1.0), (65, 77, 5, 7, 0.7),
+                                             (1, 1, 3, 2, 1.0)])
+def test_kernel_matmul_matches_dense(gpu_lib, na, nb, r, ncols, h):
+    P = gpu_lib
+    g = np.random.default_rng(na + nb)
+    Fa, Fb = g.standard_normal((na, r)), g.standard_normal((nb, r))
+    if r == 123:
+        Fa, Fb = (g.random((na, r)) < 0.11) * 1.0, (g.random((nb, r)) < 0.11) * 1.0
+    W = g.standard_normal((nb, ncols))
+    S = _np(P.hss_kernel_matmul(_t(Fa), _t(Fb), h, _t(W)))
+    ref = o_kernel.gaussian_block(Fa, Fb, h) @ W
+    assert np.abs(S - ref).max() <= 1e-12 * np.abs(ref).max()
+
+
+def test_kernel_matmul_same_set_unit_diagonal(gpu_lib):
+    P = gpu_lib
+    g = np.random.default_rng(1)
+    F = g.standard_normal((200, 6)) * 3
+    W = np.eye(200)[:, :64].copy()
+    S = _np(P.hss_kernel_matmul(_t(F), _t(F), 0.3, _t(W), same_set=True))
+    assert np.array_equal(np.diag(S[:64, :64]), np.ones(64))
+
+
+def test_kernel_block_matches_oracle(gpu_lib):
+    P = gpu_lib
+    g = np.random.default_rng(2)
+    Fa, Fb = g.standard_normal((37, 54)), g.standard_normal((45, 54))
+    K = _np(P.hss_kernel_block(_t(Fa), _t(Fb), 1.0))
+    assert np.abs(K - o_kernel.gaussian_block(Fa, Fb, 1.0)).max() < 1e-15
+
+
+# ------------------------------------------------------------------ full pipeline cases
+CASES = {
+    "cfg0": dict(cfg=0, n=2000, nt=500, ranks="golden", max_it=200),
+    "cfg1s": dict(cfg=1, n=3000, nt=700, max_it=200),
+    "cfg2s": dict(cfg=2, n=2500, nt=600, max_it=100),
+    "cfg3s": dict(cfg=3, n=5000, nt=900, max_it=200),
+    "cfg4s": dict(cfg=4, n=3000, nt=500, max_it=100, h=1.0),
+}
+
+
+def _case(name):
+    d = CASES[name]
+    cfg = datagen.get_config(d["cfg"])
+    if "h" in d:
+        cfg["h"] = d["h"]
+    F, y, Ft, yt = datagen.generate(d["cfg"], n=d["n"], n_test=d["nt"])
+    ranks = None
+    if d.get("ranks") == "golden":
+        ranks = np.array(json.load(open(os.path.join(GOLD, "cfg0_ranks.json")))["ranks"])
+    return d, cfg, F, y, Ft, yt, ranks
+
+
+_CACHE = {}
+
+
+def run_case(P, name):
+    if name in _CACHE:
+        return _CACHE[name]
+    d, cfg, F, y, Ft, yt, ranks = _case(name)
+    h = cfg["h"]
+    Cs = cfg["C"][:1] if d["cfg"] != 4 else [1.0, 10.0]
+    # oracle
+    perm, ranges, Om, H = o_pipe.build(F, cfg, h=h, ranks=ranks)
+    fac = o_ulv.factor(H, cfg["beta"])
+    # GPU
+    Fd = _t(F)
+    kw = dict(leaf_size=cfg["leaf"], rel_tol=cfg["rel_tol"], abs_tol=cfg["abs_tol"], max_rank=cfg["cap"],
+              oversample=cfg["s"] - cfg["cap"], omega_seed=cfg["seed_omega"], tree_seed=cfg["seed_tree"],
+              ranks=ranks)
+    Hg = P.hss_build(Fd, h, **kw)
+    Ug = P.hss_ulv_factor(Hg, cfg["beta"])
+    out = dict(d=d, cfg=cfg, F=F, y=y, Ft=Ft, perm=perm, H=H, fac=fac, Hg=Hg, Ug=Ug, Cs=Cs, h=h)
+    _CACHE[name] = out
+    return out
+
+
+@pytest.mark.parametrize("name", list(CASES))
+def test_build_tree_ranks_skeletons_exact(gpu_lib, name):
+    c = run_case(gpu_lib, name)
+    info = c["Hg"].info()
+    assert np.array_equal(info["perm"], c["perm"])
+    H = c["H"]
+    ranks_o = o_pipe.ranks_array(H, 2 ** (H.L + 1) - 1)
+    assert np.array_equal(info["ranks"].astype(np.int64), ranks_o)
+    skel_o = np.concatenate([H.J[t] for t in range(1, 2 ** (H.L + 1) - 1)])
+    assert np.array_equal(info["skeletons"], skel_o)
+    assert info["cap_hits"] == sum(H.cap_hit.values())
+
+
+@pytest.mark.parametrize("name", list(CASES))
+def test_generators_match(gpu_lib, name):
+    c = run_case(gpu_lib, name)
+    H, Hg = c["H"], c["Hg"]
+    for t in [1, 2, 2 ** H.L - 1, 2 ** (H.L + 1) - 2, 0]:
+        gen = Hg.node_generators(t, H.L)
+        lvl = int(np.floor(np.log2(t + 1)))
+        if t > 0:
+            U = H.U[t] if H.U[t] is not None else np.eye(H.rows[t])
+            assert gen["U"].shape == U.shape
+            assert np.abs(gen["U"] - U).max() <= 1e-9 * max(1.0, np.abs(U).max())
+        if lvl < H.L:
+            assert np.abs(gen["B"] - H.B[t]).max() <= 1e-14
+        if lvl == H.L:
+            assert np.abs(gen["D"] - H.D[t]).max() <= 1e-15
+
+
+@pytest.mark.parametrize("name", list(CASES))
+def test_matvec_matches_oracle(gpu_lib, name):
+    c = run_case(gpu_lib, name)
+    g = np.random.default_rng(7)
+    n = c["F"].shape[0]
+    V = g.standard_normal((n, 3))
+    out = _np(c["Hg"].matvec(_t(V)))
+    perm = c["perm"]
+    ref = np.empty_like(V)
+    ref[perm] = o_hss.matvec(c["H"], V[perm])
+    assert relerr(out, ref) <= 1e-10
+
+
+@pytest.mark.parametrize("name", list(CASES))
+def test_ulv_solve_matches_oracle(gpu_lib, name):
+    c = run_case(gpu_lib, name)
+    g = np.random.default_rng(8)
+    n = c["F"].shape[0]
+    perm = c["perm"]
+    for B in (np.ones((n, 1)), g.standard_normal((n, 1)), g.standard_normal((n, 4))):
+        x = _np(c["Ug"].solve(_t(B[:, 0] if B.shape[1] == 1 else B)))
+        ref = np.empty_like(B)
+        ref[perm] = o_ulv.solve(c["fac"], B[perm])
+        if B.shape[1] == 1:
+            ref = ref[:, 0]
+        assert relerr(x, ref) <= 1e-9
+
+
+@pytest.mark.parametrize("name", list(CASES))
+def test_admm_trace_bias_objective_labels(gpu_lib, name):
+    P = gpu_lib
+    c = run_case(P, name)
+    cfg, perm, y = c["cfg"], c["perm"], c["y"]
+    max_it = c["d"]["max_it"]
+    beta = cfg["beta"]
+    yp = y[perm]
+    inv = np.empty_like(perm)
+    inv[perm] = np.arange(perm.shape[0])
+    solve = lambda b: o_ulv.solve(c["fac"], b)  # noqa: E731
+    mv = lambda v: o_hss.matvec(c["H"], v)      # noqa: E731
+    res = P.admm_svm_train(c["Ug"], _t(y), c["Cs"], max_it, trace_every=10)
+    zg, mug = _np(res["z"]), _np(res["mu"])
+    tz, tm = _np(res["trace_z"]), _np(res["trace_mu"])
+    for ci, C in enumerate(c["Cs"]):
+        o = o_admm.run(solve, yp, C, beta, max_it, trace_every=10)
+        assert len(o["trace"]) == tz.shape[0]
+        for ti, (it, z_o, mu_o) in enumerate(o["trace"]):
+            assert relerr(tz[ti, :, ci], z_o[inv]) <= 1e-7, (ci, it)
+            assert relerr(tm[ti, :, ci], mu_o[inv]) <= 1e-7, (ci, it)
+        assert relerr(zg[:, ci], o["z"][inv]) <= 1e-7
+        assert relerr(mug[:, ci], o["mu"][inv]) <= 1e-7
+        assert abs(res["stats"]["w1"] - o["w1"]) <= 1e-9 * abs(o["w1"])
+        b_o = o_svm.bias(mv, o["z"], yp, C)
+        f_o = o_svm.objective(mv, o["z"], yp)
+        assert abs(res["obj"][ci] - f_o) <= 1e-7 * abs(f_o)
+        assert abs(res["bias"][ci] - b_o) <= 1e-7 * max(1.0, abs(b_o))
+        # prediction (exact kernel, AMB-19)
+        coef_o = y * o["z"][inv]
+        dv_o = o_svm.decision_values(c["F"], coef_o, c["h"], b_o, c["Ft"])
+        lab_o = o_svm.labels(dv_o)
+        coef_g = _t((y * zg[:, ci]).copy())
+        dv_g, lab_g = P.svm_predict(_t(c["F"]), coef_g, c["h"], [res["bias"][ci]], _t(c["Ft"]))
+        dv_g, lab_g = _np(dv_g)[:, 0], _np(lab_g)[:, 0]
+        sure = np.abs(dv_o) > 1e-6
+        assert np.array_equal(lab_g[sure], lab_o[sure])
+        assert np.abs(dv_g - dv_o).max() <= 1e-7 * max(1.0, np.abs(dv_o).max())
+
+
+# ------------------------------------------------------------------ edge cases
+def test_single_leaf_tree(gpu_lib):
+    """n <= leaf: L = 0, K~ = K exactly (dense leaf), ULV = Cholesky."""
+    P = gpu_lib
+    g = np.random.default_rng(3)
+    F = g.standard_normal((50, 4))
+    y = np.where(g.random(50) < 0.5, 1.0, -1.0)
+    H = P.hss_build(_t(F), 1.0, leaf_size=64, max_rank=16, oversample=16)
+    U = P.hss_ulv_factor(H, 0.5)
+    K = o_kernel.dense_kernel(F, 1.0)
+    b = g.standard_normal(50)
+    x = _np(U.solve(_t(b)))
+    assert relerr(x, np.linalg.solve(K + 0.5 * np.eye(50), b)) <= 1e-12
+    res = P.admm_svm_train(U, _t(y), [1.0], 50)
+    o = o_admm.run(o_admm.dense_solver(K, 0.5), y, 1.0, 0.5, 50)
+    assert relerr(_np(res["z"])[:, 0], o["z"]) <= 1e-9
+
+
+def test_bad_labels_rejected(gpu_lib):
+    P = gpu_lib
+    c = run_case(P, "cfg1s")
+    y = c["y"].copy()
+    y[3] = 0.5
+    with pytest.raises(P.HssError) as ei:
+        P.admm_svm_train(c["Ug"], _t(y), [1.0], 3)
+    assert ei.value.code == -1
+
+
+def test_not_spd_reports_node(gpu_lib):
+    P = gpu_lib
+    g = np.random.default_rng(4)
+    F = g.standard_normal((1024, 4))
+    H = P.hss_build(_t(F), 0.4, leaf_size=32, rel_tol=0.0, max_rank=8, oversample=16)
+    with pytest.raises(P.HssError) as ei:
+        P.hss_ulv_factor(H, 1e-6)
+    assert ei.value.code == -5 and "node" in str(ei.value)
+
+
+def test_invalid_arguments(gpu_lib):
+    P = gpu_lib
+    F = _t(np.zeros((10, 2)))
+    with pytest.raises(P.HssError):
+        P.hss_build(F, -1.0, leaf_size=4)
+    with pytest.raises(P.HssError):
+        P.hss_build(F, 1.0, leaf_size=0)
+
+
+def test_determinism(gpu_lib):
+    P = gpu_lib
+    c = run_case(P, "cfg3s")
+    y = _t(c["y"])
+    r1 = P.admm_svm_train(c["Ug"], y, [1.0], 20)
+    r2 = P.admm_svm_train(c["Ug"], y, [1.0], 20)
+    assert np.array_equal(_np(r1["z"]), _np(r2["z"]))
+
+
+def test_host_end_to_end_matches_device_path(gpu_lib):
+    P = gpu_lib
+    c = run_case(P, "cfg1s")
+    cfg = c["cfg"]
+    out = P.svm_train_predict_host(c["F"], c["y"], cfg["h"], cfg["beta"], [cfg["C"][0]], 30, Ftest=c["Ft"],
+                                   leaf_size=cfg["leaf"], rel_tol=cfg["rel_tol"], max_rank=cfg["cap"],
+                                   oversample=cfg["s"] - cfg["cap"], omega_seed=cfg["seed_omega"],
+                                   tree_seed=cfg["seed_tree"])
+    res = P.admm_svm_train(c["Ug"], _t(c["y"]), [cfg["C"][0]], 30)
+    assert np.array_equal(out["z"], _np(res["z"]))
+    assert out["labels"].shape == (c["Ft"].shape[0], 1)
