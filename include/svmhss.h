@@ -169,6 +169,10 @@ int hss_kernel_block(const double* Fa, int64_t na, const double* Fb, int64_t nb,
 int hss_node(hss_t H, int32_t node, int32_t* rows, int32_t* k, double* U, double* B,
              double* D);
 
+/* Number of kernels this library has launched in this process (graph replays included);
+ * used by bench.py to report gpu_launches. */
+int64_t hss_launch_count(void);
+
 void hss_free(hss_t H);
 void ulv_free(ulv_t U);
 const char* hss_last_error(void);

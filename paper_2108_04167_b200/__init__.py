@@ -30,6 +30,11 @@ def version() -> str:
     return _L.hss_version().decode()
 
 
+def launch_count() -> int:
+    """Kernels launched by libsvmhss in this process (CUDA-graph replays included)."""
+    return int(_L.hss_launch_count())
+
+
 def _cuda_f64(t, name):
     import torch
     if not (isinstance(t, torch.Tensor) and t.is_cuda and t.dtype == torch.float64):

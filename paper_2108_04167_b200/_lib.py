@@ -56,7 +56,7 @@ class AdmmStats(ct.Structure):
 EXPORTS = ["hss_build", "hss_info", "hss_matvec", "hss_ulv_factor", "ulv_info", "ulv_solve",
            "admm_svm_train", "svm_predict", "svm_train_predict_host", "hss_omega", "hss_tree",
            "hss_kernel_matmul", "hss_kernel_block", "hss_node", "hss_free", "ulv_free",
-           "hss_last_error", "hss_version"]
+           "hss_last_error", "hss_version", "hss_launch_count"]
 
 _lib = None
 
@@ -67,7 +67,7 @@ def load():
     if _lib is not None:
         return _lib
     if not os.path.exists(LIB_PATH):
-        raise ImportError(f"{LIB_PATH} not built: run `python -m paper_2108_04167_b200.build`")
+        raise ImportError(f"{LIB_PATH} not built: run `python paper_2108_04167_b200/build.py`")
     L = ct.CDLL(LIB_PATH)
     vp, i32, i64, u64, dbl = ct.c_void_p, ct.c_int32, ct.c_int64, ct.c_uint64, ct.c_double
     L.hss_build.argtypes = [vp, i64, i32, dbl, ct.POINTER(HssOpts), vp, ct.POINTER(vp)]
@@ -92,8 +92,10 @@ def load():
     L.ulv_free.restype = None
     L.hss_last_error.restype = ct.c_char_p
     L.hss_version.restype = ct.c_char_p
+    L.hss_launch_count.argtypes = []
+    L.hss_launch_count.restype = ct.c_int64
     for name in EXPORTS:
-        if name not in ("hss_free", "ulv_free", "hss_last_error", "hss_version"):
+        if name not in ("hss_free", "ulv_free", "hss_last_error", "hss_version", "hss_launch_count"):
             getattr(L, name).restype = ct.c_int
     _lib = L
     return L

@@ -1,6 +1,6 @@
 """Build libsvmhss.so in-tree with nvcc for sm_100a (no torch types, plain C-ABI).
 
-python -m paper_2108_04167_b200.build   (also called by __graft_entry__.build())
+python paper_2108_04167_b200/build.py [--force]   (also called by __graft_entry__.build())
 """
 from __future__ import annotations
 

@@ -235,6 +235,8 @@ AdmmResult admm_train_impl(const ULVImpl& F, const double* y_orig, const std::ve
     }
   }
   R.ms_loop = tloop.stop_ms();
+  // graph replays are not seen by LAUNCH_CHECK: account for them (capture counted one iteration)
+  g_launches.fetch_add((long long)(max_it - 1) * R.launches);
   cudaGraphExecDestroy(gexec);
   scatter_rows(z.p, H.perm.p, n, nC, z_out, s);
   if (mu_out) scatter_rows(mu.p, H.perm.p, n, nC, mu_out, s);

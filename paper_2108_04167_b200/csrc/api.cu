@@ -6,6 +6,7 @@
 
 namespace svmhss {
 static thread_local std::string g_last_error;
+std::atomic<long long> g_launches{0};
 void set_last_error(const std::string& s) { g_last_error = s; }
 
 static void ensure_device() {
@@ -62,6 +63,7 @@ extern "C" {
 
 const char* hss_last_error(void) { return g_last_error.c_str(); }
 const char* hss_version(void) { return "svmhss 0.1 (sm_100a)"; }
+int64_t hss_launch_count(void) { return (int64_t)g_launches.load(); }
 
 int hss_build(const double* F, int64_t n, int32_t r, double h, const hss_opts* opt, void* stream,
               hss_t* out) {

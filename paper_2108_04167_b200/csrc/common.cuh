@@ -6,6 +6,7 @@
 #include <string>
 #include <vector>
 #include <stdexcept>
+#include <atomic>
 
 #include "../../include/svmhss.h"
 
@@ -27,7 +28,12 @@ void set_last_error(const std::string& s);
                             std::string(#x) + ": " + cudaGetErrorString(e__));        \
   } while (0)
 
-#define LAUNCH_CHECK() CUDA_CHECK(cudaGetLastError())
+extern std::atomic<long long> g_launches;  // kernels launched by this library (api.cu)
+#define LAUNCH_CHECK()                         \
+  do {                                         \
+    ::svmhss::g_launches.fetch_add(1);         \
+    CUDA_CHECK(cudaGetLastError());            \
+  } while (0)
 
 inline void require(bool ok, const std::string& msg) {
   if (!ok) throw Error(HSS_EINVAL, msg);
