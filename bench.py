@@ -1,0 +1,293 @@
+#!/usr/bin/env python
+"""bench.py — ADMM + HSS SVM hot path on B200 (BASELINE.json metric: "ADMM iters/sec and HSS
+build+ULV time at n=524k; fraction of HBM/FP64 peak").
+
+One STEP = one pass of the whole hot path over config 3
+(n = 524,288 train / 131,072 test points, r = 54): tree + Omega + fused DMMA sketch + per-level
+ID compression (hss_build), ULV factorization (hss_ulv_factor), precompute + MaxIt = 1000 ADMM
+iterations + bias/objective (admm_svm_train), prediction of the test set (svm_predict).
+Inputs are resident in HBM before the timed region; the factor (GBs) exceeds L2 (126 MB).
+
+value       = ADMM iterations per second (whole job: sum over ranks), timed with CUDA events
+              on the launching stream inside the library, max over ranks;
+hss_build_ulv_s = build + factor seconds per step (the metric's second number);
+e2e         = the same metric through the HOST-buffer C-ABI call svm_train_predict_host,
+              host<->device copies inside the timed region (iterations / call seconds);
+roofline    = dominant kernel (the sketch kmm_kernel, FP64 tensor cores);
+roofline_solve = the per-iteration ULV solve sweeps (HBM);
+cpu_baseline = the CPU oracle on a bounded sample (rank 0, N = 1 only).
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl cuda|reference] [--config 3]
+Multi-GPU (torchrun, one process per GPU): N independent replicas ("replicas only", DESIGN.md
+"Multi-GPU"), scaling "weak"; no data-path collective.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import subprocess
+import sys
+import threading
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+import numpy as np  # noqa: E402
+
+METRIC = "ADMM iters/sec and HSS build+ULV time at n=524k; fraction of HBM/FP64 peak"
+FP64_NOMINAL_TF, BF16_NOMINAL_TF = 45.0, 2250.0  # blackwell_cuda_programming.md (B200 FP64 tensor 45)
+
+
+def _peaks():
+    p = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    if os.path.exists(p):
+        d = json.load(open(p))
+        return d, "measured"
+    return {"hbm_gbs": 6650.0, "bf16_tflops": 1590.0, "bf16_tflops_sustained": 1400.0}, "fallback"
+
+
+class ClockSampler:
+    """nvidia-smi clocks / throttle reasons during the timed region (B200_PROFILING.md)."""
+
+    def __init__(self, index=0):
+        self.index, self.rows, self.proc = index, [], None
+
+    def start(self):
+        q = ("clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+             "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+             "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+        try:
+            self.proc = subprocess.Popen(["nvidia-smi", "-i", str(self.index), f"--query-gpu={q}",
+                                          "--format=csv,noheader,nounits", "-lms", "200"],
+                                         stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.th = threading.Thread(target=self._read, daemon=True)
+            self.th.start()
+        except FileNotFoundError:
+            self.proc = None
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.rows.append([x.strip() for x in line.split(",")])
+
+    def stop(self):
+        if self.proc is None:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        self.proc.terminate()
+        try:
+            self.proc.wait(timeout=5)
+        except Exception:
+            self.proc.kill()
+        rows = [r for r in self.rows if len(r) >= 8]
+        sm = [float(r[0]) for r in rows if r[0].replace(".", "").isdigit()]
+        mx = [float(r[1]) for r in rows if r[1].replace(".", "").isdigit()]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({names[i] for r in rows for i in range(4) if r[4 + i].lower() == "active"})
+        load = [x for x in sm if x > 0.5 * (max(mx) if mx else 1)]
+        return {"sm_mhz": float(np.median(load if load else sm)) if sm else None,
+                "sm_max_mhz": max(mx) if mx else None, "reasons": reasons, "samples": len(rows)}
+
+
+def cfg_opts(cfg):
+    return dict(leaf_size=cfg["leaf"], rel_tol=cfg["rel_tol"], abs_tol=cfg["abs_tol"], max_rank=cfg["cap"],
+                oversample=cfg["s"] - cfg["cap"], omega_seed=cfg["seed_omega"], tree_seed=cfg["seed_tree"])
+
+
+# ----------------------------------------------------------------------------- reference arm
+def oracle_sample(cfg_id, n_sample, iters, steps=1, warmup=0):
+    """Time the CPU oracle (as it stands) on a bounded sample of the workload: build + factor
+    once, then `steps` timed blocks of `iters` ADMM iterations.  Returns a dict in the
+    metric's unit: ADMM iters/s scaled to the full n (one iteration is O(n): per-node work
+    over n / leaf nodes)."""
+    import datagen
+    from oracle import admm, pipeline, ulv
+    cfg = datagen.get_config(cfg_id)
+    F, y, _, _ = datagen.generate(cfg_id, n=n_sample, n_test=0)
+    t0 = time.perf_counter()
+    perm, ranges, Om, H = pipeline.build(F, cfg)
+    fac = ulv.factor(H, cfg["beta"])
+    t_build = time.perf_counter() - t0
+    yp = y[perm]
+    solve = lambda b: ulv.solve(fac, b)  # noqa: E731
+    for _ in range(warmup):
+        admm.run(solve, yp, cfg["C"][0], cfg["beta"], iters)
+    times = []
+    for _ in range(max(1, steps)):
+        t = time.perf_counter()
+        admm.run(solve, yp, cfg["C"][0], cfg["beta"], iters)
+        times.append(time.perf_counter() - t)
+    per_it = float(np.median(times)) / iters
+    scale = n_sample / cfg["n"]
+    return dict(value=scale / per_it, unit="iters/s", build_ulv_s_sample=t_build, per_iter_s_sample=per_it,
+                times=times, cores=len(os.sched_getaffinity(0)),
+                sample=f"oracle (NumPy/SciPy fp64) HSS build+ULV on n={n_sample} config-{cfg_id} points "
+                       f"(same leaf/cap/s/tol/seeds), then {iters} ADMM iterations per step; iters/s "
+                       f"scaled by n_sample/n = {scale:.5f} (ADMM iteration cost is linear in n)")
+
+
+def run_reference(args, rank, world):
+    if rank != 0:
+        return 0
+    import datagen
+    cfg = datagen.get_config(args.config)
+    r = oracle_sample(args.config, args.ref_n, args.ref_iters, steps=args.steps, warmup=args.warmup)
+    line = {"metric": METRIC, "value": r["value"], "unit": "iters/s", "n_gpus": world, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": 1e3 * float(np.median(r["times"])),
+            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+            "data": "synthetic", "impl": "reference",
+            "config": {"workload": cfg["name"], "n": cfg["n"], "r": cfg["r"], "max_it": cfg["max_it"],
+                       "leaf": cfg["leaf"], "cap": cfg["cap"], "s": cfg["s"], "sample_n": args.ref_n},
+            "cpu_baseline": {"value": r["value"], "unit": "iters/s", "cores": r["cores"], "kind": "oracle",
+                             "sample": r["sample"]},
+            "e2e": {"value": r["value"], "unit": "iters/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+            "hss_build_ulv_s_sample": r["build_ulv_s_sample"]}
+    print(json.dumps(line), flush=True)
+    return 0
+
+
+# ----------------------------------------------------------------------------- CUDA arm
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=3)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="cuda", choices=["cuda", "reference"])
+    ap.add_argument("--config", type=int, default=3)
+    ap.add_argument("--n", type=int, default=None, help="debug: override n (not a bench line)")
+    ap.add_argument("--max-it", type=int, default=None, help="debug: override MaxIt")
+    ap.add_argument("--ref-n", type=int, default=8192)
+    ap.add_argument("--ref-iters", type=int, default=10)
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-predict", action="store_true")
+    args = ap.parse_args()
+    rank = int(os.environ.get("RANK", 0))
+    world = int(os.environ.get("WORLD_SIZE", 1))
+    local = int(os.environ.get("LOCAL_RANK", 0))
+    if args.impl == "reference":
+        return run_reference(args, rank, world)
+
+    import torch
+    import torch.distributed as dist
+
+    import datagen
+    import paper_2108_04167_b200 as P
+
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=dev)
+    cfg = datagen.get_config(args.config)
+    n = args.n or cfg["n"]
+    nt = cfg["n_test"] if args.n is None else max(1, n // 4)
+    max_it = args.max_it or cfg["max_it"]
+    h = cfg["h"] if not isinstance(cfg["h"], list) else cfg["h"][2]
+    Cs = cfg["C"][:1]
+    F, y, Ft, yt = datagen.generate(args.config, n=n, n_test=nt)
+    Fd, yd, Ftd = (torch.from_numpy(a).to(dev) for a in (F, y, Ft))
+    stream = torch.cuda.current_stream()
+    opts = cfg_opts(cfg)
+
+    def step():
+        H = P.hss_build(Fd, h, **opts)
+        U = P.hss_ulv_factor(H, cfg["beta"])
+        res = P.admm_svm_train(U, yd, Cs, max_it, want_mu=False)
+        if not args.no_predict:
+            coef = (yd[:, None] * res["z"]).contiguous()
+            P.svm_predict(Fd, coef, h, res["bias"], Ftd)
+        hi, ui = H.info(), U.info()
+        U.free()
+        H.free()
+        return hi, ui, res["stats"]
+
+    for _ in range(args.warmup):
+        step()
+    torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+    clk = ClockSampler(local)
+    clk.start()
+    l0 = P.launch_count()
+    ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    torch.cuda.synchronize()
+    ev0.record(stream)
+    recs = [step() for _ in range(args.steps)]
+    ev1.record(stream)
+    torch.cuda.synchronize()
+    launches = P.launch_count() - l0
+    clocks = clk.stop()
+    if world > 1:
+        dist.barrier()
+    ms_total = ev0.elapsed_time(ev1)
+    loop_ms = float(np.median([a["ms_loop"] for _, _, a in recs]))
+    build_ms = float(np.median([hi["ms_tree"] + hi["ms_omega"] + hi["ms_sketch"] + hi["ms_compress"] + ui["ms_factor"]
+                                for hi, ui, _ in recs]))
+    sketch_ms = float(np.median([hi["ms_sketch"] for hi, _, _ in recs]))
+    t = torch.tensor([ms_total, loop_ms, build_ms, sketch_ms], dtype=torch.float64, device=dev)
+    if world > 1:
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    ms_total, loop_ms, build_ms, sketch_ms = t.tolist()
+    hi, ui, ast = recs[-1]
+    its_per_rank = max_it * len(Cs) / (loop_ms / 1e3)
+    value = its_per_rank * world
+    peaks, peak_src = _peaks()
+    rp = (cfg["r"] + 3) // 4 * 4
+    sk_flops = 2.0 * n * n * (rp + cfg["s"])
+    fp64_peak = peaks["bf16_tflops_sustained"] * FP64_NOMINAL_TF / BF16_NOMINAL_TF
+    ach_tf = sk_flops / (sketch_ms / 1e3) / 1e12
+    solve_bytes = 2.0 * ui["factor_bytes"] + 64.0 * n * len(Cs)
+    ach_gbs = solve_bytes * max_it / (loop_ms / 1e3) / 1e9
+    line = {"metric": METRIC, "value": value, "unit": "iters/s", "n_gpus": world, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": ms_total / args.steps, "higher_is_better": True,
+            "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+            "config": {"workload": cfg["name"], "n": n, "n_test": nt, "r": cfg["r"], "h": h, "C": Cs,
+                       "beta": cfg["beta"], "max_it": max_it, "leaf": cfg["leaf"], "cap": cfg["cap"],
+                       "s": cfg["s"], "rel_tol": cfg["rel_tol"], "parallelism": f"replicas{world}",
+                       "l2": "inputs larger than L2 (factor %.2f GB, sketch operands %.2f GB)" % (
+                           ui["factor_bytes"] / 1e9, 16.0 * n * cfg["s"] / 1e9)},
+            "hss_build_ulv_s": build_ms / 1e3,
+            "phases_ms": {"tree": hi["ms_tree"], "omega": hi["ms_omega"], "sketch": hi["ms_sketch"],
+                          "compress": hi["ms_compress"], "factor": ui["ms_factor"],
+                          "admm_precompute": ast["ms_precompute"], "admm_loop": ast["ms_loop"],
+                          "bias": ast["ms_bias"]},
+            "hss": {"L": hi["L"], "max_rank": hi["max_rank_used"], "cap_hits": hi["cap_hits"],
+                    "passthrough": hi["passthrough"], "generator_bytes": hi["generator_bytes"],
+                    "factor_bytes": ui["factor_bytes"]},
+            "gpu_launches": int(launches),
+            "launches_per_admm_iter": int(ast["kernel_launches_per_iter"]),
+            "roofline": {"bound": "tensor", "kernel": "kmm_kernel (sketch S = K Omega, DMMA)",
+                         "achieved": ach_tf, "peak": fp64_peak, "unit": "TFLOP/s", "frac": ach_tf / fp64_peak,
+                         "traffic": None,
+                         "peak_source": f"{peak_src} bf16_tflops_sustained x FP64/BF16 nominal ({FP64_NOMINAL_TF}/{BF16_NOMINAL_TF})",
+                         "work": "2 n^2 (r_pad + s) flops per launch"},
+            "roofline_solve": {"bound": "hbm", "kernel": "ulv_fwd_kernel + ulv_bwd_kernel (+ epilogue)",
+                               "achieved": ach_gbs, "peak": peaks["hbm_gbs"], "unit": "GB/s",
+                               "frac": ach_gbs / peaks["hbm_gbs"],
+                               "work": "2 x factor_bytes + 64 n nC bytes per iteration"},
+            "clocks": clocks}
+    if rank == 0 and world == 1 and not args.no_e2e and args.n is None:
+        pin = lambda a: torch.from_numpy(a).pin_memory().numpy()  # noqa: E731
+        Fh, yh, Fth = pin(F), pin(y), pin(Ft)
+        P.svm_train_predict_host(Fh, yh, h, cfg["beta"], Cs, max_it, Ftest=Fth, **opts)  # warm
+        e = P.svm_train_predict_host(Fh, yh, h, cfg["beta"], Cs, max_it, Ftest=Fth, **opts)
+        tot = e["timings_ms"]["total"]
+        line["e2e"] = {"value": max_it * len(Cs) / (tot / 1e3), "unit": "iters/s",
+                       "h2d_bytes_per_step": int(Fh.nbytes + yh.nbytes + Fth.nbytes),
+                       "d2h_bytes_per_step": int(n * len(Cs) * 8 + nt * len(Cs)),
+                       "timings_ms": e["timings_ms"],
+                       "note": "svm_train_predict_host on pinned host buffers: h2d + build + factor + "
+                               "ADMM + bias + predict + d2h; iterations / total call time"}
+    if rank == 0 and world == 1 and not args.no_cpu_baseline and args.n is None:
+        r = oracle_sample(args.config, args.ref_n, args.ref_iters)
+        line["cpu_baseline"] = {"value": r["value"], "unit": "iters/s", "cores": r["cores"], "kind": "oracle",
+                                "sample": r["sample"], "build_ulv_s_sample": r["build_ulv_s_sample"]}
+    if rank == 0:
+        print(json.dumps(line), flush=True)
+    if world > 1:
+        dist.destroy_process_group()
+    return 0
+
+
+if __name__ == "__main__":
+    sys.exit(main())
