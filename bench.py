@@ -156,6 +156,7 @@ def main():
     ap.add_argument("--config", type=int, default=3)
     ap.add_argument("--n", type=int, default=None, help="debug: override n (not a bench line)")
     ap.add_argument("--max-it", type=int, default=None, help="debug: override MaxIt")
+    ap.add_argument("--beta", type=float, default=None, help="debug: override beta (not a bench line)")
     ap.add_argument("--ref-n", type=int, default=8192)
     ap.add_argument("--ref-iters", type=int, default=10)
     ap.add_argument("--no-cpu-baseline", action="store_true")
@@ -179,6 +180,8 @@ def main():
     if world > 1:
         dist.init_process_group("nccl", device_id=dev)
     cfg = datagen.get_config(args.config)
+    if args.beta is not None:
+        cfg["beta"] = args.beta
     n = args.n or cfg["n"]
     nt = cfg["n_test"] if args.n is None else max(1, n // 4)
     max_it = args.max_it or cfg["max_it"]

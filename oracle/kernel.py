@@ -28,12 +28,28 @@ def dense_kernel(F: np.ndarray, h: float, cap: int = 32768) -> np.ndarray:
     return gaussian_block(F, F, h)
 
 
-def sketch(Fp: np.ndarray, h: float, Omega_p: np.ndarray, chunk: int = 2048) -> np.ndarray:
-    """H1: S = K_p Omega_p as a dense product, computed in row chunks."""
+def sketch(Fp: np.ndarray, h: float, Omega_p: np.ndarray, chunk: int = 1024,
+           threads: int | None = None) -> np.ndarray:
+    """H1: S = K_p Omega_p as a dense product, computed in row chunks.
+
+    Row chunks are independent and may run on a thread pool (cdist, exp and dgemm release
+    the GIL); the chunk boundaries, hence the result, do not depend on the thread count."""
+    import os
+    from concurrent.futures import ThreadPoolExecutor
     n = Fp.shape[0]
     S = np.empty((n, Omega_p.shape[1]))
-    for lo in range(0, n, chunk):
+
+    def one(lo):
         S[lo:lo + chunk] = gaussian_block(Fp[lo:lo + chunk], Fp, h) @ Omega_p
+
+    los = list(range(0, n, chunk))
+    nt = threads if threads is not None else min(len(os.sched_getaffinity(0)), 16)
+    if nt <= 1 or len(los) <= 1 or n < 8192:
+        for lo in los:
+            one(lo)
+    else:
+        with ThreadPoolExecutor(nt) as ex:
+            list(ex.map(one, los))
     return S
 
 

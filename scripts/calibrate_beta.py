@@ -38,8 +38,10 @@ def main():
     t0 = time.time()
     tm = {}
     perm, ranges, Om, H = pipeline.build(F, cfg, h=h, timings=tm)
+    print("built", tm, flush=True)
     op = LinearOperator((n, n), matvec=lambda v: hss.matvec(H, v), dtype=np.float64)
-    lmin = float(eigsh(op, k=1, which="SA", tol=1e-6, maxiter=20000)[0][0])
+    lmin = float(eigsh(op, k=1, which="SA", tol=1e-4, maxiter=20000)[0][0])
+    print("lambda_min", lmin, "after", time.time() - t0, "s", flush=True)
     sched = datagen.beta_schedule(n)
     beta = sched if lmin >= 0 else max(sched, 10.0 ** math.ceil(math.log10(-4 * lmin)))
     rec = dict(config=a.config, n=n, h=h, lambda_min=lmin, schedule=sched, beta=beta,
