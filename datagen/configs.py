@@ -48,8 +48,14 @@ _CONFIGS = {
             rank_mode="adaptive", gpus=[1, 2, 4, 8]),
 }
 
-# Calibrated shifts (scripts/calibrate_beta.py; AMB-9).  None = use beta_schedule(n).
-_BETA = {1: None, 2: None, 3: None, 4: None}
+# Calibrated shifts (scripts/calibrate_beta.py -> configs/beta_calibration.jsonl; AMB-9):
+# beta = max(schedule(n), 10^ceil(log10(-4 lambda_min(K~)))) with lambda_min from the ORACLE's
+# HSS at the full config size.  None = use beta_schedule(n).
+#   cfg 1: lambda_min = -331.65  -> 1e4      cfg 2: lambda_min = -5185.1 -> 1e5
+#   cfg 4 (per h): 0.25: -7.09 -> 1e2; 0.5: -91.5 -> 1e3; 1: -476.3 -> 1e4; 2: -627.3 -> 1e4;
+#                  4: -206.7 -> 1e3
+_BETA = {1: 1e4, 2: 1e5, 3: None, 4: None}
+_BETA_PER_H = {4: {0.25: 1e2, 0.5: 1e3, 1.0: 1e4, 2.0: 1e4, 4.0: 1e3}}
 
 for _c, _cfg in _CONFIGS.items():
     _cfg["id"] = _c
@@ -59,6 +65,8 @@ for _c, _cfg in _CONFIGS.items():
     if _cfg["beta"] is None:
         b = _BETA.get(_c)
         _cfg["beta"] = b if b is not None else beta_schedule(_cfg["n"])
+    if _c in _BETA_PER_H:
+        _cfg["beta_per_h"] = dict(_BETA_PER_H[_c])
 
 CONFIGS = _CONFIGS
 

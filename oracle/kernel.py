@@ -28,7 +28,7 @@ def dense_kernel(F: np.ndarray, h: float, cap: int = 32768) -> np.ndarray:
     return gaussian_block(F, F, h)
 
 
-def sketch(Fp: np.ndarray, h: float, Omega_p: np.ndarray, chunk: int = 1024,
+def sketch(Fp: np.ndarray, h: float, Omega_p: np.ndarray, chunk: int | None = None,
            threads: int | None = None) -> np.ndarray:
     """H1: S = K_p Omega_p as a dense product, computed in row chunks.
 
@@ -38,6 +38,8 @@ def sketch(Fp: np.ndarray, h: float, Omega_p: np.ndarray, chunk: int = 1024,
     from concurrent.futures import ThreadPoolExecutor
     n = Fp.shape[0]
     S = np.empty((n, Omega_p.shape[1]))
+    if chunk is None:  # bound the per-thread temporaries (chunk x n doubles) to ~1 GB
+        chunk = int(max(64, min(1024, (1 << 27) // max(1, n))))
 
     def one(lo):
         S[lo:lo + chunk] = gaussian_block(Fp[lo:lo + chunk], Fp, h) @ Omega_p

@@ -95,12 +95,13 @@ def test_kernel_block_matches_oracle(gpu_lib):
 
 
 # ------------------------------------------------------------------ full pipeline cases
+# scaled cases: beta = the paper's schedule for these n, checked SPD by the oracle
 CASES = {
     "cfg0": dict(cfg=0, n=2000, nt=500, ranks="golden", max_it=200),
-    "cfg1s": dict(cfg=1, n=3000, nt=700, max_it=200),
-    "cfg2s": dict(cfg=2, n=2500, nt=600, max_it=100),
-    "cfg3s": dict(cfg=3, n=5000, nt=900, max_it=200),
-    "cfg4s": dict(cfg=4, n=3000, nt=500, max_it=100, h=1.0),
+    "cfg1s": dict(cfg=1, n=3000, nt=700, max_it=200, beta=1e2),
+    "cfg2s": dict(cfg=2, n=2500, nt=600, max_it=100, beta=1e3),
+    "cfg3s": dict(cfg=3, n=5000, nt=900, max_it=200, beta=1e3),
+    "cfg4s": dict(cfg=4, n=3000, nt=500, max_it=100, h=1.0, beta=1e2),
 }
 
 
@@ -109,6 +110,8 @@ def _case(name):
     cfg = datagen.get_config(d["cfg"])
     if "h" in d:
         cfg["h"] = d["h"]
+    if "beta" in d:
+        cfg["beta"] = d["beta"]
     F, y, Ft, yt = datagen.generate(d["cfg"], n=d["n"], n_test=d["nt"])
     ranks = None
     if d.get("ranks") == "golden":
