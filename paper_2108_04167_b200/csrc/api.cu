@@ -7,6 +7,18 @@
 namespace svmhss {
 static thread_local std::string g_last_error;
 std::atomic<long long> g_launches{0};
+thread_local cudaStream_t g_alloc_stream = nullptr;
+void init_mem_pool() {
+  static thread_local int done_dev = -1;
+  int dev = 0;
+  if (cudaGetDevice(&dev) != cudaSuccess || dev == done_dev) return;
+  cudaMemPool_t pool;
+  if (cudaDeviceGetDefaultMemPool(&pool, dev) == cudaSuccess) {
+    uint64_t thr = UINT64_MAX;
+    cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &thr);
+  }
+  done_dev = dev;
+}
 void set_last_error(const std::string& s) { g_last_error = s; }
 
 static void ensure_device() {
@@ -68,6 +80,7 @@ int64_t hss_launch_count(void) { return (int64_t)g_launches.load(); }
 int hss_build(const double* F, int64_t n, int32_t r, double h, const hss_opts* opt, void* stream,
               hss_t* out) {
   return guarded([&] {
+    StreamScope ss__((cudaStream_t)stream);
     require(out != nullptr && F != nullptr, "hss_build: NULL pointer");
     validate_opts(opt, n, r, h);
     auto* H = new HSSImpl();
@@ -143,6 +156,7 @@ int hss_node(hss_t Hh, int32_t node, int32_t* rows, int32_t* k, double* U, doubl
 
 int hss_matvec(hss_t Hh, const double* v, double* out, int32_t nrhs, void* stream) {
   return guarded([&] {
+    StreamScope ss__((cudaStream_t)stream);
     require(Hh && v && out, "hss_matvec: NULL pointer");
     require(nrhs >= 1, "hss_matvec: nrhs must be >= 1");
     const HSSImpl& H = *Hh->impl;
@@ -157,6 +171,7 @@ int hss_matvec(hss_t Hh, const double* v, double* out, int32_t nrhs, void* strea
 
 int hss_ulv_factor(hss_t Hh, double beta, void* stream, ulv_t* out) {
   return guarded([&] {
+    StreamScope ss__((cudaStream_t)stream);
     require(Hh && out, "hss_ulv_factor: NULL pointer");
     require(std::isfinite(beta) && beta > 0, "hss_ulv_factor: beta must be > 0");
     auto* F = new ULVImpl();
@@ -183,6 +198,7 @@ int ulv_info(ulv_t U, ulv_stats* st) {
 
 int ulv_solve(ulv_t Uh, const double* b, double* x, int32_t nrhs, void* stream) {
   return guarded([&] {
+    StreamScope ss__((cudaStream_t)stream);
     require(Uh && b && x, "ulv_solve: NULL pointer");
     require(nrhs >= 1 && nrhs <= 8, "ulv_solve: nrhs must be in 1..8");
     const ULVImpl& F = *Uh->impl;
@@ -201,6 +217,7 @@ int admm_svm_train(ulv_t Uh, const double* y, const double* C, int32_t nC, int32
                    const admm_opts* opt, double* z_out, double* mu_out, double* bias_out,
                    double* obj_out, admm_stats* st, void* stream) {
   return guarded([&] {
+    StreamScope ss__((cudaStream_t)stream);
     require(Uh && y && C && z_out, "admm_svm_train: NULL pointer");
     require(nC >= 1 && nC <= 8, "admm_svm_train: nC must be in 1..8");
     require(max_it >= 1, "admm_svm_train: max_it must be >= 1");
@@ -224,6 +241,7 @@ int svm_predict(const double* Ftrain, const double* coef, int64_t n, int32_t r, 
                 const double* bias, int32_t nC, const double* Ftest, int64_t m, double* dv_out,
                 int8_t* label_out, void* stream) {
   return guarded([&] {
+    StreamScope ss__((cudaStream_t)stream);
     require(Ftrain && coef && bias && (Ftest || m == 0), "svm_predict: NULL pointer");
     require(n >= 1 && r >= 1 && m >= 0, "svm_predict: bad sizes");
     require(nC >= 1 && nC <= 16, "svm_predict: nC must be in 1..16");
@@ -244,7 +262,8 @@ int svm_train_predict_host(const double* F, const double* y, int64_t n, int32_t 
     validate_opts(opt, n, r, h);
     cudaStream_t s;
     CUDA_CHECK(cudaStreamCreateWithFlags(&s, cudaStreamNonBlocking));
-    struct SG { cudaStream_t s; ~SG() { cudaStreamDestroy(s); } } sg{s};
+    struct SG { cudaStream_t s; ~SG() { cudaStreamSynchronize(s); cudaStreamDestroy(s); } } sg{s};
+    StreamScope ss__(s);
     cudaEvent_t ev[8];
     for (auto& e : ev) CUDA_CHECK(cudaEventCreate(&e));
     struct EG { cudaEvent_t* e; ~EG() { for (int i = 0; i < 8; ++i) cudaEventDestroy(e[i]); } } eg{ev};
@@ -306,6 +325,7 @@ int svm_train_predict_host(const double* F, const double* y, int64_t n, int32_t 
 
 int hss_omega(uint64_t seed, const int64_t* idx, int64_t rows, int32_t s, double* out, void* stream) {
   return guarded([&] {
+    StreamScope ss__((cudaStream_t)stream);
     require(idx && out, "hss_omega: NULL pointer");
     require(rows >= 0 && s >= 1 && s <= (1 << 20), "hss_omega: bad sizes");
     omega_rows(seed, idx, rows, s, out, (cudaStream_t)stream);
@@ -316,6 +336,7 @@ int hss_omega(uint64_t seed, const int64_t* idx, int64_t rows, int32_t s, double
 int hss_tree(const double* F, int64_t n, int32_t r, int32_t leaf_size, uint64_t tree_seed,
              int64_t* perm_out, void* stream) {
   return guarded([&] {
+    StreamScope ss__((cudaStream_t)stream);
     require(F && perm_out, "hss_tree: NULL pointer");
     require(n >= 1 && r >= 1 && leaf_size >= 1, "hss_tree: bad sizes");
     cudaStream_t s = (cudaStream_t)stream;
@@ -330,6 +351,7 @@ int hss_kernel_matmul(const double* Fa, int64_t na, const double* Fb, int64_t nb
                       double h, const double* W, int32_t ncols, int32_t same_set, double* S,
                       void* stream) {
   return guarded([&] {
+    StreamScope ss__((cudaStream_t)stream);
     require(Fa && Fb && W && S, "hss_kernel_matmul: NULL pointer");
     require(na >= 0 && nb >= 0 && r >= 1 && ncols >= 1, "hss_kernel_matmul: bad sizes");
     require(std::isfinite(h) && h > 0, "hss_kernel_matmul: h must be > 0");
@@ -369,6 +391,7 @@ int hss_kernel_matmul(const double* Fa, int64_t na, const double* Fb, int64_t nb
 int hss_kernel_block(const double* Fa, int64_t na, const double* Fb, int64_t nb, int32_t r, double h,
                      double* K, void* stream) {
   return guarded([&] {
+    StreamScope ss__((cudaStream_t)stream);
     require(Fa && Fb && K, "hss_kernel_block: NULL pointer");
     require(na >= 0 && nb >= 0 && r >= 1 && na < (1 << 30) && nb < (1 << 30), "hss_kernel_block: bad sizes");
     cudaStream_t s = (cudaStream_t)stream;

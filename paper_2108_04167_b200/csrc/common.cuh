@@ -40,28 +40,41 @@ inline void require(bool ok, const std::string& msg) {
 }
 
 // ------------------------------------------------------------------ device buffers
+// Stream-ordered allocations from the device's default memory pool (release threshold set
+// to "never", so steady-state steps do not call the driver allocator and cudaFree never
+// forces a device synchronization).  The allocation stream is the library call's stream.
+extern thread_local cudaStream_t g_alloc_stream;
+void init_mem_pool();
+struct StreamScope {  // sets the allocation stream for the duration of an API call
+  cudaStream_t prev;
+  explicit StreamScope(cudaStream_t s) : prev(g_alloc_stream) { init_mem_pool(); g_alloc_stream = s; }
+  ~StreamScope() { g_alloc_stream = prev; }
+};
+
 template <typename T>
 struct DevBuf {
   T* p = nullptr;
   size_t n = 0;
+  cudaStream_t st = nullptr;
   DevBuf() {}
   explicit DevBuf(size_t count) { alloc(count); }
   void alloc(size_t count) {
     release();
     n = count;
-    if (count) CUDA_CHECK(cudaMalloc((void**)&p, count * sizeof(T)));
+    st = g_alloc_stream;
+    if (count) CUDA_CHECK(cudaMallocAsync((void**)&p, count * sizeof(T), st));
   }
   void release() {
-    if (p) cudaFree(p);
+    if (p) cudaFreeAsync(p, st);
     p = nullptr;
     n = 0;
   }
   ~DevBuf() { release(); }
   DevBuf(const DevBuf&) = delete;
   DevBuf& operator=(const DevBuf&) = delete;
-  DevBuf(DevBuf&& o) noexcept : p(o.p), n(o.n) { o.p = nullptr; o.n = 0; }
+  DevBuf(DevBuf&& o) noexcept : p(o.p), n(o.n), st(o.st) { o.p = nullptr; o.n = 0; }
   DevBuf& operator=(DevBuf&& o) noexcept {
-    release(); p = o.p; n = o.n; o.p = nullptr; o.n = 0; return *this;
+    release(); p = o.p; n = o.n; st = o.st; o.p = nullptr; o.n = 0; return *this;
   }
   size_t bytes() const { return n * sizeof(T); }
 };

@@ -23,56 +23,90 @@ static P* upload_probs(const std::vector<P>& v, cudaStream_t s) {
 static void free_probs(void* d, cudaStream_t s) { CUDA_CHECK(cudaFreeAsync(d, s)); }
 
 // ------------------------------------------------------------------ GEMM
-constexpr int GBM = 64, GBN = 64, GBK = 16;
+// 128 x 64 x 8 tiles, 256 threads, 8 x 4 outputs per thread (DFMA), register-prefetched
+// double-buffered shared-memory tiles; any operand strides (coalesced load mapping chosen
+// per operand from its unit stride).
+constexpr int GBM = 128, GBN = 64, GBK = 8;
 
 __global__ void __launch_bounds__(256) bgemm_kernel(const GemmProb* __restrict__ probs) {
   const GemmProb P = probs[blockIdx.z];
   const int m0 = blockIdx.y * GBM, n0 = blockIdx.x * GBN;
   if (m0 >= P.m || n0 >= P.n) return;
-  __shared__ double As[GBK][GBM + 1];
-  __shared__ double Bs[GBK][GBN + 1];
+  __shared__ __align__(16) double As[2][GBK][GBM];
+  __shared__ __align__(16) double Bs[2][GBK][GBN];
   const int tid = threadIdx.x, tx = tid & 15, ty = tid >> 4;
-  double acc[4][4];
+  const bool a_rm = (P.acs == 1), b_rm = (P.bcs == 1);
+  double acc[8][4];
 #pragma unroll
-  for (int i = 0; i < 4; ++i)
+  for (int i = 0; i < 8; ++i)
 #pragma unroll
     for (int j = 0; j < 4; ++j) acc[i][j] = 0.0;
-  const bool a_rowmajor = (P.acs == 1), b_rowmajor = (P.bcs == 1);
-  for (int k0 = 0; k0 < P.k; k0 += GBK) {
-    for (int e = tid; e < GBM * GBK; e += 256) {
+  double ra[4], rb[2];
+  auto load = [&](int k0) {
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {
+      const int e = tid + 256 * q;
       int i, kk;
-      if (a_rowmajor) { i = e / GBK; kk = e % GBK; } else { kk = e / GBM; i = e % GBM; }
+      if (a_rm) { i = e >> 3; kk = e & 7; } else { i = e & 127; kk = e >> 7; }
       const int gi = m0 + i, gk = k0 + kk;
-      As[kk][i] = (gi < P.m && gk < P.k) ? P.A[(long long)gi * P.ars + (long long)gk * P.acs] : 0.0;
+      ra[q] = (gi < P.m && gk < P.k) ? P.A[(long long)gi * P.ars + (long long)gk * P.acs] : 0.0;
     }
-    for (int e = tid; e < GBN * GBK; e += 256) {
+#pragma unroll
+    for (int q = 0; q < 2; ++q) {
+      const int e = tid + 256 * q;
       int j, kk;
-      if (b_rowmajor) { kk = e / GBN; j = e % GBN; } else { j = e / GBK; kk = e % GBK; }
+      if (b_rm) { kk = e >> 6; j = e & 63; } else { j = e >> 3; kk = e & 7; }
       const int gj = n0 + j, gk = k0 + kk;
-      Bs[kk][j] = (gj < P.n && gk < P.k) ? P.B[(long long)gk * P.brs + (long long)gj * P.bcs] : 0.0;
+      rb[q] = (gj < P.n && gk < P.k) ? P.B[(long long)gk * P.brs + (long long)gj * P.bcs] : 0.0;
     }
-    __syncthreads();
+  };
+  auto store = [&](int buf) {
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {
+      const int e = tid + 256 * q;
+      int i, kk;
+      if (a_rm) { i = e >> 3; kk = e & 7; } else { i = e & 127; kk = e >> 7; }
+      As[buf][kk][i] = ra[q];
+    }
+#pragma unroll
+    for (int q = 0; q < 2; ++q) {
+      const int e = tid + 256 * q;
+      int j, kk;
+      if (b_rm) { kk = e >> 6; j = e & 63; } else { j = e >> 3; kk = e & 7; }
+      Bs[buf][kk][j] = rb[q];
+    }
+  };
+  const int nk = (P.k + GBK - 1) / GBK;
+  load(0);
+  store(0);
+  __syncthreads();
+  for (int t = 0; t < nk; ++t) {
+    const int buf = t & 1;
+    if (t + 1 < nk) load((t + 1) * GBK);
 #pragma unroll
     for (int kk = 0; kk < GBK; ++kk) {
-      double a[4], b[4];
+      const double2* ap = reinterpret_cast<const double2*>(&As[buf][kk][ty * 8]);
+      const double2* bp = reinterpret_cast<const double2*>(&Bs[buf][kk][tx * 4]);
+      double a[8], b[4];
 #pragma unroll
-      for (int i = 0; i < 4; ++i) a[i] = As[kk][ty + 16 * i];
+      for (int q = 0; q < 4; ++q) { const double2 v = ap[q]; a[2 * q] = v.x; a[2 * q + 1] = v.y; }
 #pragma unroll
-      for (int j = 0; j < 4; ++j) b[j] = Bs[kk][tx + 16 * j];
+      for (int q = 0; q < 2; ++q) { const double2 v = bp[q]; b[2 * q] = v.x; b[2 * q + 1] = v.y; }
 #pragma unroll
-      for (int i = 0; i < 4; ++i)
+      for (int i = 0; i < 8; ++i)
 #pragma unroll
         for (int j = 0; j < 4; ++j) acc[i][j] = fma(a[i], b[j], acc[i][j]);
     }
+    if (t + 1 < nk) store(buf ^ 1);
     __syncthreads();
   }
 #pragma unroll
-  for (int i = 0; i < 4; ++i) {
-    const int gi = m0 + ty + 16 * i;
+  for (int i = 0; i < 8; ++i) {
+    const int gi = m0 + ty * 8 + i;
     if (gi >= P.m) continue;
 #pragma unroll
     for (int j = 0; j < 4; ++j) {
-      const int gj = n0 + tx + 16 * j;
+      const int gj = n0 + tx * 4 + j;
       if (gj >= P.n) continue;
       double* c = P.C + (long long)gi * P.crs + (long long)gj * P.ccs;
       const double v = P.alpha * acc[i][j];
@@ -248,39 +282,122 @@ void btrsm(const std::vector<TrsmProb>& probs_in, bool lower, cudaStream_t s) {
 }
 
 // ------------------------------------------------------------------ Householder QR
-__global__ void __launch_bounds__(256) bgeqr2_kernel(const QrProb* __restrict__ probs) {
+// Blocked right-looking Householder QR, one CTA per node.  The (m - p0) x NB panel is
+// factored in shared memory (dlarfg convention, identical reflectors to unblocked dgeqr2
+// up to rounding); the trailing columns are updated with the compact-WY block reflector
+// (W = V^T A, W = T^T W, A -= V W), reading the trailing matrix twice per panel instead of
+// twice per column.  Each thread owns whole columns (coalesced row-major access).
+template <int NB>
+__global__ void __launch_bounds__(256) bgeqrf_kernel(const QrProb* __restrict__ probs) {
   const QrProb P = probs[blockIdx.x];
-  const int m = P.m, n = P.n, tid = threadIdx.x;
-  extern __shared__ double v[];   // m doubles
+  const int m = P.m, n = P.n, tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
+  extern __shared__ double sm[];
+  double* pan = sm;                 // (m) x NB panel, row-major stride NB
+  __shared__ double T[NB][NB + 1];
+  __shared__ double tau_s[NB];
   __shared__ double red[32];
-  __shared__ double s_tau;
 #define QA(i, j) P.A[(long long)(i) * P.rs + (long long)(j) * P.cs]
-  for (int j = 0; j < n; ++j) {
-    double part = 0.0;
-    for (int i = j + 1 + tid; i < m; i += blockDim.x) { const double x = QA(i, j); part = fma(x, x, part); }
-    const double xs = block_sum(part, red);
-    const double alpha = QA(j, j);
-    double tau, scal, beta;
-    if (xs == 0.0) { tau = 0.0; scal = 0.0; beta = alpha; }
-    else {
-      beta = -copysign(sqrt(alpha * alpha + xs), alpha);
-      tau = (beta - alpha) / beta;
-      scal = 1.0 / (alpha - beta);
-    }
-    if (tid == 0) { s_tau = tau; v[j] = 1.0; }
-    for (int i = j + 1 + tid; i < m; i += blockDim.x) {
-      const double x = (tau == 0.0) ? QA(i, j) : QA(i, j) * scal;
-      v[i] = x;
-      QA(i, j) = x;
+  for (int p0 = 0; p0 < n; p0 += NB) {
+    const int pb = min(NB, n - p0), mr = m - p0;
+    for (int e = tid; e < mr * NB; e += 256) {
+      const int i = e / NB, j = e % NB;
+      pan[e] = (j < pb) ? QA(p0 + i, p0 + j) : 0.0;
     }
     __syncthreads();
-    if (tid == 0) { QA(j, j) = beta; P.tau[j] = tau; }
-    if (tau != 0.0) {
-      for (int c = j + 1 + tid; c < n; c += blockDim.x) {
-        double w = 0.0;
-        for (int i = j; i < m; ++i) w = fma(v[i], QA(i, c), w);
-        w *= tau;
-        for (int i = j; i < m; ++i) QA(i, c) = fma(-w, v[i], QA(i, c));
+    // factor the panel in shared memory
+    for (int j = 0; j < pb; ++j) {
+      double part = 0.0;
+      for (int i = j + 1 + tid; i < mr; i += 256) { const double x = pan[i * NB + j]; part = fma(x, x, part); }
+      const double xs = block_sum(part, red);
+      const double alpha = pan[j * NB + j];
+      double tau, scal, beta;
+      if (xs == 0.0) { tau = 0.0; scal = 1.0; beta = alpha; }
+      else {
+        beta = -copysign(sqrt(alpha * alpha + xs), alpha);
+        tau = (beta - alpha) / beta;
+        scal = 1.0 / (alpha - beta);
+      }
+      if (tau != 0.0)
+        for (int i = j + 1 + tid; i < mr; i += 256) pan[i * NB + j] *= scal;
+      __syncthreads();
+      if (tid == 0) { pan[j * NB + j] = beta; tau_s[j] = tau; }
+      // apply H_j to panel columns c > j: warp per column
+      if (tau != 0.0) {
+        for (int c = j + 1 + wid; c < pb; c += 8) {
+          double w = 0.0;
+          for (int i = j + lane; i < mr; i += 32) {
+            const double vi = (i == j) ? 1.0 : pan[i * NB + j];
+            w = fma(vi, pan[i * NB + c], w);
+          }
+          w = warp_sum(w) * tau;
+          for (int i = j + lane; i < mr; i += 32) {
+            const double vi = (i == j) ? 1.0 : pan[i * NB + j];
+            pan[i * NB + c] = fma(-w, vi, pan[i * NB + c]);
+          }
+        }
+      }
+      __syncthreads();
+    }
+    // T (pb x pb upper): T_jj = tau_j, T[0:j, j] = -tau_j T[0:j,0:j] (V[:,0:j]^T v_j)
+    for (int j = 0; j < pb; ++j) {
+      // s_i = V[:, i]^T v_j for i < j  (warp per i)
+      for (int i = wid; i < j; i += 8) {
+        double a = 0.0;
+        for (int r = j + lane; r < mr; r += 32) {
+          const double vi = (r == i) ? 1.0 : (r > i ? pan[r * NB + i] : 0.0);
+          const double vj = (r == j) ? 1.0 : pan[r * NB + j];
+          a = fma(vi, vj, a);
+        }
+        a = warp_sum(a);
+        if (lane == 0) T[i][j] = a;   // temporarily holds s_i
+      }
+      __syncthreads();
+      if (tid < j) {
+        double a = 0.0;
+        for (int q = tid; q < j; ++q) a = fma(T[tid][q], T[q][j], a);
+        red[tid] = a;
+      }
+      __syncthreads();
+      if (tid < j) T[tid][j] = -tau_s[j] * red[tid];
+      if (tid == 0) T[j][j] = tau_s[j];
+      for (int i = j + 1 + tid; i < NB; i += 256) T[i][j] = 0.0;
+      __syncthreads();
+    }
+    // write the panel back (R on/above the diagonal, V below) and tau
+    for (int e = tid; e < mr * pb; e += 256) {
+      const int i = e / pb, j = e % pb;
+      QA(p0 + i, p0 + j) = pan[i * NB + j];
+    }
+    if (tid < pb) P.tau[p0 + tid] = tau_s[tid];
+    // trailing update: A[p0:, c] -= V T^T V^T A[p0:, c]  for c >= p0 + pb
+    for (int c = p0 + pb + tid; c < n; c += 256) {
+      double w[NB];
+#pragma unroll
+      for (int j = 0; j < NB; ++j) w[j] = 0.0;
+      for (int i = 0; i < mr; ++i) {
+        const double a = QA(p0 + i, c);
+#pragma unroll
+        for (int j = 0; j < NB; ++j) {
+          const double v = (i == j) ? 1.0 : ((i > j) ? pan[i * NB + j] : 0.0);
+          w[j] = fma(v, a, w[j]);
+        }
+      }
+      double w2[NB];
+#pragma unroll
+      for (int j = 0; j < NB; ++j) {
+        double a = 0.0;
+#pragma unroll
+        for (int q = 0; q <= j; ++q) a = fma(T[q][j], w[q], a);   // (T^T w)_j
+        w2[j] = a;
+      }
+      for (int i = 0; i < mr; ++i) {
+        double a = QA(p0 + i, c);
+#pragma unroll
+        for (int j = 0; j < NB; ++j) {
+          const double v = (i == j) ? 1.0 : ((i > j) ? pan[i * NB + j] : 0.0);
+          a = fma(-v, w2[j], a);
+        }
+        QA(p0 + i, c) = a;
       }
     }
     __syncthreads();
@@ -293,11 +410,16 @@ void bgeqr2(const std::vector<QrProb>& probs, cudaStream_t s) {
   int maxm = 0;
   for (auto& p : probs) maxm = std::max(maxm, p.m);
   QrProb* d = upload_probs(probs, s);
-  size_t smem = (size_t)std::max(1, maxm) * sizeof(double);
-  if (smem > 48 * 1024)
-    CUDA_CHECK(cudaFuncSetAttribute(bgeqr2_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                    (int)smem));
-  bgeqr2_kernel<<<(unsigned)probs.size(), 256, smem, s>>>(d);
+  auto launch = [&](auto kern, int nb) {
+    size_t smem = (size_t)std::max(1, maxm) * nb * sizeof(double);
+    if (smem > 48 * 1024)
+      CUDA_CHECK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    kern<<<(unsigned)probs.size(), 256, smem, s>>>(d);
+  };
+  if ((size_t)maxm * 16 * 8 <= 200 * 1024) launch(bgeqrf_kernel<16>, 16);
+  else if ((size_t)maxm * 8 * 8 <= 200 * 1024) launch(bgeqrf_kernel<8>, 8);
+  else if ((size_t)maxm * 4 * 8 <= 200 * 1024) launch(bgeqrf_kernel<4>, 4);
+  else throw Error(HSS_EINVAL, "bgeqr2: node too tall for the shared-memory panel");
   LAUNCH_CHECK();
   free_probs(d, s);
 }
