@@ -304,8 +304,8 @@ void predict_impl(const double* Ftrain, const double* coef, int64_t n, int r, do
                   int8_t* lab, cudaStream_t s) {
   const int rp = (r + 3) / 4 * 4;
   const int ld = 16;
-  DevBuf<double> Ftr((size_t)n * rp), Fte((size_t)std::max<int64_t>(1, m) * rp), nutr(n),
-      nute(std::max<int64_t>(1, m)), W((size_t)n * ld), S((size_t)std::max<int64_t>(1, m) * ld), b(nC);
+  DevBuf<double> Ftr((size_t)n * rp), Fte((size_t)std::max<int64_t>(1, m) * rp), nutr(n + kNormPad),
+      nute(std::max<int64_t>(1, m) + kNormPad), W((size_t)n * ld), S((size_t)std::max<int64_t>(1, m) * ld), b(nC);
   pad_rows(Ftrain, n, r, rp, Ftr.p, s);
   pad_rows(Ftest, m, r, rp, Fte.p, s);
   row_norms(Ftr.p, n, rp, nutr.p, s);

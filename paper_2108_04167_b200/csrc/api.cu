@@ -359,7 +359,7 @@ int hss_kernel_matmul(const double* Fa, int64_t na, const double* Fb, int64_t nb
     const int rp = (r + 3) / 4 * 4;
     const int ncp = (ncols + 1) / 2 * 2;
     DevBuf<double> A((size_t)std::max<int64_t>(1, na) * rp), Bm((size_t)std::max<int64_t>(1, nb) * rp),
-        nua(std::max<int64_t>(1, na)), nub(std::max<int64_t>(1, nb));
+        nua(std::max<int64_t>(1, na) + kNormPad), nub(std::max<int64_t>(1, nb) + kNormPad);
     pad_rows(Fa, na, r, rp, A.p, s);
     pad_rows(Fb, nb, r, rp, Bm.p, s);
     row_norms(A.p, na, rp, nua.p, s);

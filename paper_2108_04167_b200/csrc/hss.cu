@@ -84,7 +84,7 @@ void hss_build_impl(HSSImpl& H, const double* F, int64_t n, int r, double h, con
     H.perm.alloc(n);
     H.Fp.alloc((size_t)n * rp);
     build_tree(Fpad.p, n, r, rp, H.m, o.tree_seed, H.perm.p, H.Fp.p, s);
-    H.nu.alloc(n);
+    H.nu.alloc(n + kNormPad);
     row_norms(H.Fp.p, n, rp, H.nu.p, s);
     H.iperm.alloc(n);
     iperm_kernel<<<ceil_div(n, 256), 256, 0, s>>>(H.perm.p, n, H.iperm.p);
@@ -92,6 +92,7 @@ void hss_build_impl(HSSImpl& H, const double* F, int64_t n, int r, double h, con
     std::vector<int> lof(n);
     for (size_t i = 0; i < rg[L].size(); ++i)
       for (int64_t p = rg[L][i].first; p < rg[L][i].second; ++p) lof[p] = (int)i;
+    lof.resize(n + kLeafPad, -3);
     H.leaf_of = upload(lof, s);
     H.st.ms_tree = tm.stop_ms();
   }

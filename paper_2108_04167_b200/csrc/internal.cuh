@@ -17,7 +17,10 @@ struct KmmArgs {
   double neg_inv_2h2;                               // -1 / (2 h^2)
   int same_set;                                     // K_ii = 1 exactly (Fa == Fb)
   const int* leaf_a; const int* leaf_b;             // nullable: zero pairs in the same leaf
+  // NOTE: nub and leaf_b are read by 16-byte bulk copies: allocate them with >= 2 doubles /
+  // 4 ints of padding past the end (kNormPad / kLeafPad).
 };
+constexpr int kNormPad = 2, kLeafPad = 4;
 // S = K(Fa, Fb) W via DMMA distance GEMM -> exp -> DMMA GEMM (H1).
 void kernel_matmul(const KmmArgs& a, cudaStream_t s);
 // Which kernel_matmul configuration serves (rp, ncols); for reporting.

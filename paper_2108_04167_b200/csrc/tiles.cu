@@ -44,166 +44,163 @@ static inline int pad_stride(int x) {  // smallest S >= x with S % 16 == 4
 
 constexpr int KBM = 64;
 
+// --- mbarrier / bulk-copy (TMA) helpers
+__device__ __forceinline__ unsigned smem_u32(const void* p) { return (unsigned)__cvta_generic_to_shared(p); }
+__device__ __forceinline__ void mbar_init(uint64_t* b, unsigned count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;\n" ::"r"(smem_u32(b)), "r"(count));
+}
+__device__ __forceinline__ void mbar_expect_tx(uint64_t* b, unsigned bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;\n" ::"r"(smem_u32(b)), "r"(bytes) : "memory");
+}
+__device__ __forceinline__ void mbar_arrive(uint64_t* b) {
+  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];\n" ::"r"(smem_u32(b)) : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t* b, unsigned parity) {
+  asm volatile(
+      "{\n .reg .pred p;\n WAIT_%=:\n"
+      " mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n"
+      " @!p bra WAIT_%=;\n}\n" ::"r"(smem_u32(b)), "r"(parity) : "memory");
+}
+__device__ __forceinline__ void bulk_g2s(void* dst, const void* src, unsigned bytes, uint64_t* bar) {
+  asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];\n"
+               ::"r"(smem_u32(dst)), "l"(src), "r"(bytes), "r"(smem_u32(bar)) : "memory");
+}
+
+// 16 warps (4 per SM sub-partition, so DMMA latency and the exp dependency chains of one
+// warp hide under the others).  Warp w: m-tile mt = w & 7 (rows mt*8..mt*8+7) and column half
+// hf = w >> 3.  Per j-step of BJ = 32 points:
+//   (1) distance DMMAs for (mt, its 16 of the BJ columns) -> exp/mask -> E tile in smem,
+//       then a 64-thread named barrier with the partner warp of the same m-tile;
+//   (2) sketch DMMAs S_acc(8 rows x 8*NT cols) += E(8 x BJ) W(BJ x 8*NT cols).
+// Operands arrive by TMA bulk copies (cp.async.bulk, one row per copy into padded smem rows)
+// into a 2-stage ring completed on mbarriers; one CTA barrier per step guards buffer reuse.
 template <int BJ, int NT>
-__global__ void __launch_bounds__(256, 1) kmm_kernel(KmmArgs a, int SA) {
-  constexpr int NCH = 16 * NT, SW = NCH + 4, SE = BJ + 4, HALF = NCH / 2;
-  extern __shared__ __align__(16) double smem[];
-  double* Fa_s = smem;
-  double* nua_s = Fa_s + KBM * SA;
-  double* E_s = nua_s + KBM;
-  double* st0 = E_s + KBM * SE;
-  const int stage_d = BJ * SA + BJ + BJ * SW;
-  int* leafb_s = (int*)(st0 + 2 * stage_d);
+__global__ void __launch_bounds__(512, 1) kmm_kernel(KmmArgs a, int SA) {
+  constexpr int NCH = 16 * NT, SW = NCH + 4, SE = BJ + 4, HQ = BJ / 16;  // n-tiles of distance per warp
+  extern __shared__ __align__(128) double smem[];
+  double* Fa_s = smem;                       // 64 x SA
+  double* nua_s = Fa_s + KBM * SA;           // 64
+  double* E_s = nua_s + KBM;                 // 64 x SE
+  double* wbuf = E_s + KBM * SE;             // 2 x BJ x SW
+  double* fbuf = wbuf + 2 * BJ * SW;         // 2 x (BJ x SA + BJ)
+  int* lbuf = (int*)(fbuf + 2 * (BJ * SA + BJ));  // 2 x BJ
+  __shared__ __align__(8) uint64_t full[2];
 
   const int tid = threadIdx.x, lane = tid & 31, w = tid >> 5, g = lane >> 2, t = lane & 3;
+  const int mt = w & 7, hf = w >> 3;
   const int64_t row0 = (int64_t)blockIdx.x * KBM;
   const int col0 = blockIdx.y * NCH;
   const int rp = a.rp;
+  const int ncl = min(NCH, a.ncols - col0);  // valid columns of this chunk (even)
+  const int64_t nsteps = (a.nb + BJ - 1) / BJ;
 
-  // A tile (Fa rows) and norms
-  for (int e = tid; e < KBM * rp; e += 256) {
+  for (int e = tid; e < KBM * rp; e += 512) {
     const int i = e / rp, f = e % rp;
     const int64_t gi = row0 + i;
     Fa_s[i * SA + f] = (gi < a.na) ? a.Fa[gi * rp + f] : 0.0;
   }
-  for (int i = tid; i < KBM; i += 256) {
+  for (int i = tid; i < KBM; i += 512) {
     const int64_t gi = row0 + i;
     nua_s[i] = (gi < a.na) ? a.nua[gi] : 0.0;
   }
-  const int64_t my_row = row0 + w * 8 + g;
-  const int my_leaf = (a.leaf_a && my_row < a.na) ? a.leaf_a[my_row] : -1;
-  int tile_leaf = -2;
-  if (a.leaf_a) {
-    const int64_t last = min(row0 + KBM, a.na) - 1;
-    const int la = a.leaf_a[row0], lb = a.leaf_a[last];
-    tile_leaf = (la == lb) ? la : -2;
+  for (int e = tid; e < 2 * BJ * SW + 2 * (BJ * SA + BJ); e += 512) wbuf[e] = 0.0;
+  for (int e = tid; e < 2 * BJ; e += 512) lbuf[e] = -3;
+  if (tid == 0) {
+    mbar_init(&full[0], 1); mbar_init(&full[1], 1);
+    asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
   }
+  asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");
+  __syncthreads();
 
-  double acc[2][NT][2];
-#pragma unroll
-  for (int mi = 0; mi < 2; ++mi)
-#pragma unroll
-    for (int ni = 0; ni < NT; ++ni) acc[mi][ni][0] = acc[mi][ni][1] = 0.0;
-
-  const int64_t nsteps = (a.nb + BJ - 1) / BJ;
-  auto issue = [&](int64_t js) {
-    double* st = st0 + (js & 1) * stage_d;
-    double* Fb_s = st;
-    double* nub_s = st + BJ * SA;
-    double* W_s = nub_s + BJ;
-    const int64_t j0 = js * BJ;
-    const int cpr = rp / 2;  // 16B chunks per feature row
-    for (int e = tid; e < BJ * cpr; e += 256) {
-      const int jj = e / cpr, c = e % cpr;
-      const int64_t gj = j0 + jj;
-      const bool ok = gj < a.nb;
-      cp_async16(Fb_s + jj * SA + 2 * c, ok ? (const void*)(a.Fb + gj * rp + 2 * c) : (const void*)a.Fb, ok);
+  auto issue = [&](int64_t j) {  // warp 0: one bulk copy per row
+    const int b = (int)(j & 1);
+    double* W_s = wbuf + b * BJ * SW;
+    double* Fb_s = fbuf + b * (BJ * SA + BJ);
+    double* nub_s = Fb_s + BJ * SA;
+    int* lb = lbuf + b * BJ;
+    const int64_t j0 = j * BJ;
+    const int jv = (int)min((int64_t)BJ, a.nb - j0);
+    const unsigned nb8 = (unsigned)(((jv * 8) + 15) & ~15), lb4 = (unsigned)(((jv * 4) + 15) & ~15);
+    if (lane == 0)
+      mbar_expect_tx(&full[b], (unsigned)jv * (rp * 8 + ncl * 8) + nb8 + (a.leaf_b ? lb4 : 0u));
+    __syncwarp();
+    for (int jj = lane; jj < jv; jj += 32) {
+      bulk_g2s(W_s + jj * SW, a.W + (j0 + jj) * a.ldw + col0, ncl * 8, &full[b]);
+      bulk_g2s(Fb_s + jj * SA, a.Fb + (j0 + jj) * rp, rp * 8, &full[b]);
     }
-    for (int e = tid; e < BJ; e += 256) {
-      const int64_t gj = j0 + e;
-      const bool ok = gj < a.nb;
-      cp_async8(nub_s + e, ok ? (const void*)(a.nub + gj) : (const void*)a.nub, ok);
-    }
-    constexpr int cpw = NCH / 2;
-    for (int e = tid; e < BJ * cpw; e += 256) {
-      const int jj = e / cpw, c = e % cpw;
-      const int64_t gj = j0 + jj;
-      const int gc = col0 + 2 * c;
-      const bool ok = gj < a.nb && gc < a.ncols;
-      cp_async16(W_s + jj * SW + 2 * c, ok ? (const void*)(a.W + gj * a.ldw + gc) : (const void*)a.W, ok);
-    }
-    if (a.leaf_b) {
-      int* lb = leafb_s + (js & 1) * BJ;
-      for (int e = tid; e < BJ; e += 256) {
-        const int64_t gj = j0 + e;
-        const bool ok = gj < a.nb;
-        cp_async4(lb + e, ok ? (const void*)(a.leaf_b + gj) : (const void*)a.leaf_b, ok);
-      }
+    if (lane == 0) {
+      bulk_g2s(nub_s, a.nub + j0, nb8, &full[b]);
+      if (a.leaf_b) bulk_g2s(lb, a.leaf_b + j0, lb4, &full[b]);
     }
   };
 
-  issue(0);
-  cp_async_commit();
+  const int64_t my_row = row0 + mt * 8 + g;
+  const bool row_ok = my_row < a.na;
+  const int my_leaf = (a.leaf_a && row_ok) ? a.leaf_a[my_row] : -1;
+  const double nui = nua_s[mt * 8 + g];
+  const double* Fa_w = Fa_s + (mt * 8 + g) * SA + t;
+  const double* E_w = E_s + (mt * 8 + g) * SE + t;
+
+  double acc[NT][2];
+#pragma unroll
+  for (int ni = 0; ni < NT; ++ni) acc[ni][0] = acc[ni][1] = 0.0;
+  if (w == 0) issue(0);
   for (int64_t js = 0; js < nsteps; ++js) {
-    if (js + 1 < nsteps) { issue(js + 1); cp_async_commit(); cp_async_wait<1>(); }
-    else { cp_async_wait<0>(); }
-    __syncthreads();
-    const double* st = st0 + (js & 1) * stage_d;
-    const double* Fb_s = st;
-    double* nub_s = (double*)(st + BJ * SA);
-    const double* W_s = nub_s + BJ;
-    int* lb = leafb_s + (js & 1) * BJ;
+    const int b = (int)(js & 1);
+    mbar_wait(&full[b], (unsigned)((js >> 1) & 1));
+    __syncthreads();  // every warp is past step js-1: the other stage and E_s are free
+    if (w == 0 && js + 1 < nsteps) issue(js + 1);
+    const double* W_s = wbuf + b * BJ * SW;
+    const double* Fb_s = fbuf + b * (BJ * SA + BJ);
+    const double* nub_s = Fb_s + BJ * SA;
+    const int* lb = lbuf + b * BJ;
     const int64_t j0 = js * BJ;
     const int jvalid = (int)min((int64_t)BJ, a.nb - j0);
-    bool skip = false;
-    if (a.leaf_b && tile_leaf >= 0) skip = (lb[0] == tile_leaf && lb[jvalid - 1] == tile_leaf);
-    if (!skip) {
-      // (1) distances for m-tile w, BJ/8 n-tiles
-      double dacc[BJ / 8][2];
+    // (1) distances: rows mt*8.., columns hf*BJ/2 + [0, BJ/2)
+    double dacc[HQ][2];
 #pragma unroll
-      for (int nt = 0; nt < BJ / 8; ++nt) dacc[nt][0] = dacc[nt][1] = 0.0;
-      for (int kk = 0; kk < rp / 4; ++kk) {
-        const double av = Fa_s[(w * 8 + g) * SA + kk * 4 + t];
+    for (int q = 0; q < HQ; ++q) dacc[q][0] = dacc[q][1] = 0.0;
+    const double* Fb_w = Fb_s + (hf * (BJ / 2) + g) * SA + t;
+    for (int kk = 0; kk < rp / 4; ++kk) {
+      const double av = Fa_w[kk * 4];
 #pragma unroll
-        for (int nt = 0; nt < BJ / 8; ++nt) {
-          const double bv = Fb_s[(nt * 8 + g) * SA + kk * 4 + t];
-          dmma884(dacc[nt][0], dacc[nt][1], av, bv);
-        }
-      }
-      // (2) exp + masks -> E
-      const double nui = nua_s[w * 8 + g];
-#pragma unroll
-      for (int nt = 0; nt < BJ / 8; ++nt) {
-        double ev[2];
-#pragma unroll
-        for (int e = 0; e < 2; ++e) {
-          const int jj = nt * 8 + 2 * t + e;
-          const int64_t gj = j0 + jj;
-          double d2 = nui + nub_s[jj] - 2.0 * dacc[nt][e];
-          d2 = fmax(d2, 0.0);
-          double v = exp(d2 * a.neg_inv_2h2);
-          if (a.same_set && gj == my_row) v = 1.0;
-          if (a.leaf_b && lb[jj] == my_leaf) v = 0.0;
-          if (jj >= jvalid || my_row >= a.na) v = 0.0;
-          ev[e] = v;
-        }
-        *reinterpret_cast<double2*>(&E_s[(w * 8 + g) * SE + nt * 8 + 2 * t]) = make_double2(ev[0], ev[1]);
-      }
-      __syncthreads();
-      // (3) S_acc += E W
-      const int wm = w & 3, wn = w >> 2;
-#pragma unroll
-      for (int kk = 0; kk < BJ / 4; ++kk) {
-        const double a0 = E_s[(wm * 16 + g) * SE + kk * 4 + t];
-        const double a1 = E_s[(wm * 16 + 8 + g) * SE + kk * 4 + t];
-        const double* wrow = W_s + (kk * 4 + t) * SW + wn * HALF + g;
-#pragma unroll
-        for (int ni = 0; ni < NT; ++ni) {
-          const double bv = wrow[ni * 8];
-          dmma884(acc[0][ni][0], acc[0][ni][1], a0, bv);
-          dmma884(acc[1][ni][0], acc[1][ni][1], a1, bv);
-        }
-      }
+      for (int q = 0; q < HQ; ++q) dmma884(dacc[q][0], dacc[q][1], av, Fb_w[q * 8 * SA + kk * 4]);
     }
-    __syncthreads();
+#pragma unroll
+    for (int q = 0; q < HQ; ++q) {
+      double ev[2];
+#pragma unroll
+      for (int e = 0; e < 2; ++e) {
+        const int jj = hf * (BJ / 2) + q * 8 + 2 * t + e;
+        double d2 = fmax(nui + nub_s[jj] - 2.0 * dacc[q][e], 0.0);
+        double v = exp(d2 * a.neg_inv_2h2);
+        if (a.same_set && j0 + jj == my_row) v = 1.0;
+        if (a.leaf_b && lb[jj] == my_leaf) v = 0.0;
+        if (jj >= jvalid || !row_ok) v = 0.0;
+        ev[e] = v;
+      }
+      *reinterpret_cast<double2*>(&E_s[(mt * 8 + g) * SE + hf * (BJ / 2) + q * 8 + 2 * t]) =
+          make_double2(ev[0], ev[1]);
+    }
+    asm volatile("bar.sync %0, 64;\n" ::"r"(1 + mt) : "memory");  // partner warps w, w^8
+    // (2) sketch: columns hf*8*NT .. + 8*NT
+    const double* W_w = W_s + t * SW + hf * (8 * NT) + g;
+#pragma unroll
+    for (int kk = 0; kk < BJ / 4; ++kk) {
+      const double av = E_w[kk * 4];
+#pragma unroll
+      for (int ni = 0; ni < NT; ++ni) dmma884(acc[ni][0], acc[ni][1], av, W_w[kk * 4 * SW + ni * 8]);
+    }
   }
   // epilogue
-  const int wm = w & 3, wn = w >> 2;
-#pragma unroll
-  for (int mi = 0; mi < 2; ++mi) {
-    const int64_t gi = row0 + wm * 16 + mi * 8 + g;
-    if (gi >= a.na) continue;
+  if (row_ok) {
 #pragma unroll
     for (int ni = 0; ni < NT; ++ni) {
-      const int gc = col0 + wn * HALF + ni * 8 + 2 * t;
+      const int gc = col0 + hf * (8 * NT) + ni * 8 + 2 * t;
       if (gc < a.ncols) {
-        double* dst = a.S + gi * a.lds + gc;
-        if (gc + 1 < a.ncols) {
-          dst[0] = acc[mi][ni][0];
-          dst[1] = acc[mi][ni][1];
-        } else {
-          dst[0] = acc[mi][ni][0];
-        }
+        double* dst = a.S + my_row * a.lds + gc;
+        dst[0] = acc[ni][0];
+        if (gc + 1 < a.ncols) dst[1] = acc[ni][1];
       }
     }
   }
@@ -211,7 +208,7 @@ __global__ void __launch_bounds__(256, 1) kmm_kernel(KmmArgs a, int SA) {
 
 static size_t kmm_smem(int BJ, int NT, int SA) {
   const int NCH = 16 * NT, SW = NCH + 4, SE = BJ + 4;
-  return 8 * (size_t)(KBM * SA + KBM + KBM * SE + 2 * (BJ * SA + BJ + BJ * SW)) + 2 * BJ * 4;
+  return 8 * (size_t)(KBM * SA + KBM + KBM * SE + 2 * BJ * SW + 2 * (BJ * SA + BJ)) + 2 * BJ * 4;
 }
 
 static int pick_nt(int ncols) {
@@ -229,7 +226,7 @@ static void launch_kmm(const KmmArgs& a, int SA, cudaStream_t s) {
   CUDA_CHECK(cudaFuncSetAttribute(kmm_kernel<BJ, NT>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                   (int)smem));
   dim3 grid((unsigned)((a.na + KBM - 1) / KBM), (unsigned)ceil_div(a.ncols, 16 * NT));
-  kmm_kernel<BJ, NT><<<grid, 256, smem, s>>>(a, SA);
+  kmm_kernel<BJ, NT><<<grid, 512, smem, s>>>(a, SA);
   LAUNCH_CHECK();
 }
 
