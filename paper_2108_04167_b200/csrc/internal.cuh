@@ -106,12 +106,12 @@ struct SolveNode {
 struct SolveWork { int node, chunk; };
 
 struct ULVLevel {
-  int nnodes = 0, maxR = 0, allpt = 1, maxChunkR = 0;
+  int nnodes = 0, maxR = 0, allpt = 1;
   int64_t sumR = 0, sumK = 0, sumY = 0;
-  DevBuf<double> M;
+  DevBuf<double> M, MT;          // per-node solve operators and their transposes
   DevBuf<SolveNode> nodes;
-  DevBuf<SolveWork> fwd_work, bwd_work;
-  int nfwd = 0, nbwd = 0;
+  DevBuf<SolveWork> work;        // (node, chunk of `ch` rows); leaf level: non-pass-through only
+  int nwork = 0, ch = 32;
 };
 
 struct ULVImpl {
@@ -119,10 +119,13 @@ struct ULVImpl {
   HSSImpl* H = nullptr;
   double beta = 0.0;
   std::vector<ULVLevel> lv;   // 0..L (0 = root)
+  DevBuf<int64_t> ptmap;      // tree position -> level L-1 vector index for pass-through leaves
+  int nleafpt = 0;
   ulv_stats st{};
 };
 
 void ulv_factor_impl(ULVImpl& F, cudaStream_t s);
+void btranspose(const std::vector<SqProb>& probs, const double* base, double* out, cudaStream_t s);
 
 // Solve workspace for nrhs right-hand sides (tree order in/out).
 struct SolveWS {

@@ -54,6 +54,37 @@ __global__ void pack_kernel(const double* __restrict__ A, const PackDesc* __rest
   }
 }
 
+// batched square transpose: out[off + j*R + i] = A[off + i*R + j] (same offsets as A)
+__global__ void btranspose_kernel(const SqProb* __restrict__ probs, const double* __restrict__ base,
+                                  double* __restrict__ out) {
+  const SqProb P = probs[blockIdx.z];
+  const int n = P.n;
+  const int64_t off = P.A - base;
+  __shared__ double tile[32][33];
+  const int i0 = blockIdx.y * 32, j0 = blockIdx.x * 32;
+  if (i0 >= n || j0 >= n) return;
+  for (int r = threadIdx.y; r < 32; r += 8) {
+    const int i = i0 + r, j = j0 + threadIdx.x;
+    tile[r][threadIdx.x] = (i < n && j < n) ? P.A[(int64_t)i * n + j] : 0.0;
+  }
+  __syncthreads();
+  for (int r = threadIdx.y; r < 32; r += 8) {
+    const int j = j0 + r, i = i0 + threadIdx.x;
+    if (i < n && j < n) out[off + (int64_t)j * n + i] = tile[threadIdx.x][r];
+  }
+}
+
+void btranspose(const std::vector<SqProb>& probs, const double* base, double* out, cudaStream_t s) {
+  if (probs.empty()) return;
+  int mx = 0;
+  for (auto& p : probs) mx = std::max(mx, p.n);
+  auto d = upload(probs, s);
+  dim3 grid(ceil_div(mx, 32), ceil_div(mx, 32), (unsigned)probs.size());
+  btranspose_kernel<<<grid, dim3(32, 8), 0, s>>>(d.p, base, out);
+  LAUNCH_CHECK();
+  CUDA_CHECK(cudaStreamSynchronize(s));
+}
+
 static void run_pack(const double* A, const std::vector<PackDesc>& pd, double* out, cudaStream_t s) {
   if (pd.empty()) return;
   auto d = upload(pd, s);
@@ -347,21 +378,44 @@ void ulv_factor_impl(ULVImpl& F, cudaStream_t s) {
     dhoffC = koff2;
     CUDA_CHECK(cudaStreamSynchronize(s));
   }
-  // work lists (fwd: 32-row chunks; bwd: 64-column chunks)
+  // transposed copies M^T (backward sweep = row GEMV too) and work lists
   for (int l = 0; l <= L; ++l) {
     auto& F_l = F.lv[l];
     std::vector<SolveNode> sn(F_l.nnodes);
     d2h(sn.data(), F_l.nodes.p, sn.size(), s);
     CUDA_CHECK(cudaStreamSynchronize(s));
-    std::vector<SolveWork> fw, bw;
+    F_l.MT.alloc(std::max<size_t>(1, F_l.M.n));
+    std::vector<SqProb> tp;
+    for (auto& nd : sn)
+      if (!nd.pt) tp.push_back({nd.R, F_l.M.p + nd.moff, nd.R, 1});
+    btranspose(tp, F_l.M.p, F_l.MT.p, s);
+    // rows per CTA: enough CTAs to fill the chip (>= ~8 per SM), at most 32
+    int64_t rows = 0;
+    for (auto& nd : sn) if (!(l == L && nd.pt)) rows += nd.R;
+    int ch = 32;
+    while (ch > 8 && rows / ch < 148 * 8) ch /= 2;
+    F_l.ch = ch;
+    std::vector<SolveWork> wk;
     for (int i = 0; i < F_l.nnodes; ++i) {
-      for (int c = 0; c < ceil_div(sn[i].R, 32); ++c) fw.push_back({i, c});
-      for (int c = 0; c < ceil_div(sn[i].R, 64); ++c) bw.push_back({i, c});
+      if (l == L && sn[i].pt) continue;  // pass-through leaves: handled by leaf_pt_copy
+      for (int c = 0; c < ceil_div(sn[i].R, ch); ++c) wk.push_back({i, c});
     }
-    F_l.fwd_work = upload(fw, s);
-    F_l.bwd_work = upload(bw, s);
-    F_l.nfwd = (int)fw.size();
-    F_l.nbwd = (int)bw.size();
+    F_l.work = upload(wk, s);
+    F_l.nwork = (int)wk.size();
+    CUDA_CHECK(cudaStreamSynchronize(s));
+  }
+  // pass-through leaves: tree position -> index in level L-1's vectors
+  {
+    std::vector<int64_t> pm(H.n, -1);
+    int npt = 0;
+    if (L >= 1)
+      for (auto& nd : H.lv[L])
+        if (nd.pt) {
+          ++npt;
+          for (int64_t p2 = nd.lo; p2 < nd.hi; ++p2) pm[p2] = nd.koff + (p2 - nd.lo);
+        }
+    F.nleafpt = npt;
+    F.ptmap = upload(pm, s);
     CUDA_CHECK(cudaStreamSynchronize(s));
   }
   F.st.beta = beta;
@@ -370,130 +424,84 @@ void ulv_factor_impl(ULVImpl& F, cudaStream_t s) {
 }
 
 // ------------------------------------------------------------------ solve sweeps
+// One row-GEMV kernel serves both sweeps: forward t = M_t b (rows i < k -> parent's up,
+// i >= k -> y_r), backward x = M_t^T [x_s; y_r] read from the stored transpose (rows j ->
+// x).  A CTA handles `ch` consecutive rows of one node (ch chosen per level so small levels
+// still spread over the chip); each warp streams its rows with 4 independent loads per lane
+// in flight and reduces with shuffles (fixed order).
 template <int NR>
-__global__ void __launch_bounds__(256) ulv_fwd_kernel(const SolveNode* __restrict__ nodes,
-                                                      const SolveWork* __restrict__ work,
-                                                      const double* __restrict__ M,
-                                                      const double* __restrict__ fin,
-                                                      double* __restrict__ fout,
-                                                      double* __restrict__ yr) {
+__global__ void __launch_bounds__(256) ulv_gemv_kernel(const SolveNode* __restrict__ nodes,
+                                                       const SolveWork* __restrict__ work, int ch,
+                                                       const double* __restrict__ M, int bwd,
+                                                       const double* __restrict__ in_a,
+                                                       const double* __restrict__ in_b,
+                                                       double* __restrict__ out_a,
+                                                       double* __restrict__ out_b) {
   const SolveWork wk = work[blockIdx.x];
   const SolveNode N = nodes[wk.node];
   const int R = N.R, tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
-  extern __shared__ double bsh[];  // R * NR
-  const double* b = fin + N.roff * NR;
-  const int i0 = wk.chunk * 32;
-  if (N.pt) {
-    for (int e = tid; e < 32 * NR; e += 256) {
-      const int i = i0 + e / NR;
-      if (i < R) fout[(N.koff + i) * NR + e % NR] = b[(int64_t)i0 * NR + e];
-    }
+  extern __shared__ double vsh[];  // R * NR
+  const int i0 = wk.chunk * ch, i1 = min(R, i0 + ch);
+  if (N.pt) {  // identity operator
+    const int64_t src = bwd ? N.koff : N.roff, dst = bwd ? N.roff : N.koff;
+    for (int e = tid; e < (i1 - i0) * NR; e += 256)
+      out_a[(dst + i0) * NR + e] = in_a[(src + i0) * NR + e];
     return;
   }
-  for (int e = tid; e < R * NR; e += 256) bsh[e] = b[e];
+  if (!bwd) {
+    for (int e = tid; e < R * NR; e += 256) vsh[e] = in_a[N.roff * NR + e];
+  } else {
+    const int kn = N.k * NR;
+    for (int e = tid; e < R * NR; e += 256)
+      vsh[e] = (e < kn) ? in_a[N.koff * NR + e] : in_b[(N.yoff - N.k) * NR + e];
+  }
   __syncthreads();
-  const int ib = i0 + wid * 4;
-  double acc[4][NR];
+  for (int i = i0 + wid; i < i1; i += 8) {
+    const double* Mr = M + N.moff + (int64_t)i * R;
+    double acc[NR];
 #pragma unroll
-  for (int q = 0; q < 4; ++q)
-#pragma unroll
-    for (int c = 0; c < NR; ++c) acc[q][c] = 0.0;
-  const double* Mr = M + N.moff + (int64_t)ib * R;
-  const int nq = min(4, R - ib);
-  if (nq == 4) {
-    for (int j = lane; j < R; j += 32) {
-      const double m0 = Mr[j], m1 = Mr[R + j], m2 = Mr[2 * R + j], m3 = Mr[3 * R + j];
+    for (int c = 0; c < NR; ++c) acc[c] = 0.0;
+    int j = lane;
+    for (; j + 96 < R; j += 128) {
+      const double m0 = Mr[j], m1 = Mr[j + 32], m2 = Mr[j + 64], m3 = Mr[j + 96];
 #pragma unroll
       for (int c = 0; c < NR; ++c) {
-        const double bv = bsh[j * NR + c];
-        acc[0][c] = fma(m0, bv, acc[0][c]);
-        acc[1][c] = fma(m1, bv, acc[1][c]);
-        acc[2][c] = fma(m2, bv, acc[2][c]);
-        acc[3][c] = fma(m3, bv, acc[3][c]);
+        acc[c] = fma(m0, vsh[j * NR + c], acc[c]);
+        acc[c] = fma(m1, vsh[(j + 32) * NR + c], acc[c]);
+        acc[c] = fma(m2, vsh[(j + 64) * NR + c], acc[c]);
+        acc[c] = fma(m3, vsh[(j + 96) * NR + c], acc[c]);
       }
     }
-  } else {
-    for (int q = 0; q < nq; ++q)
-      for (int j = lane; j < R; j += 32) {
-        const double m = Mr[(int64_t)q * R + j];
+    for (; j < R; j += 32) {
+      const double m0 = Mr[j];
 #pragma unroll
-        for (int c = 0; c < NR; ++c) acc[q][c] = fma(m, bsh[j * NR + c], acc[q][c]);
-      }
-  }
+      for (int c = 0; c < NR; ++c) acc[c] = fma(m0, vsh[j * NR + c], acc[c]);
+    }
 #pragma unroll
-  for (int q = 0; q < 4; ++q) {
+    for (int c = 0; c < NR; ++c) acc[c] = warp_sum(acc[c]);
+    if (lane < NR) {
+      double v = acc[0];
 #pragma unroll
-    for (int c = 0; c < NR; ++c) acc[q][c] = warp_sum(acc[q][c]);
-    const int i = ib + q;
-    if (lane < NR && q < nq) {
-      double v = acc[q][0];
-#pragma unroll
-      for (int c = 1; c < NR; ++c) if (lane == c) v = acc[q][c];
-      if (i < N.k) fout[(N.koff + i) * NR + lane] = v;
-      else yr[(N.yoff + i - N.k) * NR + lane] = v;
+      for (int c = 1; c < NR; ++c) if (lane == c) v = acc[c];
+      if (bwd) out_a[(N.roff + i) * NR + lane] = v;
+      else if (i < N.k) out_a[(N.koff + i) * NR + lane] = v;
+      else out_b[(N.yoff + i - N.k) * NR + lane] = v;
     }
   }
 }
 
+// pass-through leaves: fwd  fin_{L-1}[map[p]] = fin_L[p];  bwd  xout_L[p] = xout_{L-1}[map[p]]
 template <int NR>
-__global__ void __launch_bounds__(256) ulv_bwd_kernel(const SolveNode* __restrict__ nodes,
-                                                      const SolveWork* __restrict__ work,
-                                                      const double* __restrict__ M,
-                                                      const double* __restrict__ xin,
-                                                      const double* __restrict__ yr,
-                                                      double* __restrict__ xout) {
-  const SolveWork wk = work[blockIdx.x];
-  const SolveNode N = nodes[wk.node];
-  const int R = N.R, tid = threadIdx.x, tx = tid & 63, ty = tid >> 6;
-  extern __shared__ double u[];  // R * NR
-  __shared__ double red[4][64][NR];
-  const int j0 = wk.chunk * 64;
-  if (N.pt) {
-    for (int e = tid; e < 64 * NR; e += 256) {
-      const int j = j0 + e / NR;
-      if (j < R) xout[(N.roff + j) * NR + e % NR] = xin[(N.koff + j0) * NR + e];
-    }
-    return;
-  }
-  for (int e = tid; e < R * NR; e += 256) {
-    const int i = e / NR;
-    u[e] = (i < N.k) ? xin[N.koff * NR + e] : yr[(N.yoff - N.k) * NR + e];
-  }
-  __syncthreads();
-  const int j = j0 + tx;
-  double acc[NR];
-#pragma unroll
-  for (int c = 0; c < NR; ++c) acc[c] = 0.0;
-  if (j < R) {
-    const double* Mc = M + N.moff + j;
-    int i = ty;
-    for (; i + 12 < R; i += 16) {
-      const double m0 = Mc[(int64_t)i * R], m1 = Mc[(int64_t)(i + 4) * R];
-      const double m2 = Mc[(int64_t)(i + 8) * R], m3 = Mc[(int64_t)(i + 12) * R];
-#pragma unroll
-      for (int c = 0; c < NR; ++c) {
-        acc[c] = fma(m0, u[i * NR + c], acc[c]);
-        acc[c] = fma(m1, u[(i + 4) * NR + c], acc[c]);
-        acc[c] = fma(m2, u[(i + 8) * NR + c], acc[c]);
-        acc[c] = fma(m3, u[(i + 12) * NR + c], acc[c]);
-      }
-    }
-    for (; i < R; i += 4) {
-      const double m = Mc[(int64_t)i * R];
-#pragma unroll
-      for (int c = 0; c < NR; ++c) acc[c] = fma(m, u[i * NR + c], acc[c]);
-    }
-  }
-#pragma unroll
-  for (int c = 0; c < NR; ++c) red[ty][tx][c] = acc[c];
-  __syncthreads();
-  if (ty == 0 && j < R) {
-#pragma unroll
-    for (int c = 0; c < NR; ++c) {
-      const double v = ((red[0][tx][c] + red[1][tx][c]) + red[2][tx][c]) + red[3][tx][c];
-      xout[(N.roff + j) * NR + c] = v;
-    }
-  }
+__global__ void leaf_pt_copy_kernel(const int64_t* __restrict__ map, int64_t n, int bwd,
+                                    const double* __restrict__ src, double* __restrict__ dst) {
+  const int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (e >= n * NR) return;
+  const int64_t p = e / NR;
+  const int c = (int)(e % NR);
+  const int64_t q = map[p];
+  if (q < 0) return;
+  if (bwd) dst[p * NR + c] = src[q * NR + c];
+  else dst[q * NR + c] = src[p * NR + c];
 }
 
 void solve_ws_alloc(const ULVImpl& F, int nrhs, SolveWS& ws) {
@@ -519,33 +527,42 @@ void solve_ws_alloc(const ULVImpl& F, int nrhs, SolveWS& ws) {
 template <int NR>
 static void solve_impl(const ULVImpl& F, SolveWS& ws, cudaStream_t s) {
   const int L = F.H->L;
+  const int64_t n = F.H->n;
   for (int l = L; l >= 0; --l) {
     const auto& lv = F.lv[l];
     if (lv.allpt) continue;
+    if (l == L && F.nleafpt > 0) {
+      leaf_pt_copy_kernel<NR><<<ceil_div(n * NR, 256), 256, 0, s>>>(F.ptmap.p, n, 0, ws.fin[L], ws.fin[L - 1]);
+    }
+    if (lv.nwork == 0) continue;
     const size_t sm = (size_t)lv.maxR * NR * sizeof(double);
-    ulv_fwd_kernel<NR><<<lv.nfwd, 256, sm, s>>>(lv.nodes.p, lv.fwd_work.p, lv.M.p, ws.fin[l],
-                                                l > 0 ? ws.fin[l - 1] : nullptr, ws.yr[l]);
+    ulv_gemv_kernel<NR><<<lv.nwork, 256, sm, s>>>(lv.nodes.p, lv.work.p, lv.ch, lv.M.p, 0, ws.fin[l], nullptr,
+                                                  l > 0 ? ws.fin[l - 1] : nullptr, ws.yr[l]);
   }
   for (int l = 0; l <= L; ++l) {
     const auto& lv = F.lv[l];
     if (lv.allpt) continue;
-    const size_t sm = (size_t)lv.maxR * NR * sizeof(double);
-    ulv_bwd_kernel<NR><<<lv.nbwd, 256, sm, s>>>(lv.nodes.p, lv.bwd_work.p, lv.M.p,
-                                                l > 0 ? ws.xout[l - 1] : nullptr, ws.yr[l], ws.xout[l]);
+    if (lv.nwork > 0) {
+      const size_t sm = (size_t)lv.maxR * NR * sizeof(double);
+      ulv_gemv_kernel<NR><<<lv.nwork, 256, sm, s>>>(lv.nodes.p, lv.work.p, lv.ch, lv.MT.p, 1,
+                                                    l > 0 ? ws.xout[l - 1] : nullptr, ws.yr[l], ws.xout[l], nullptr);
+    }
+    if (l == L && F.nleafpt > 0) {
+      leaf_pt_copy_kernel<NR><<<ceil_div(n * NR, 256), 256, 0, s>>>(F.ptmap.p, n, 1, ws.xout[L - 1], ws.xout[L]);
+    }
   }
 }
 
 template <int NR>
 static void set_smem_attrs(size_t sm) {
-  CUDA_CHECK(cudaFuncSetAttribute(ulv_fwd_kernel<NR>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm));
-  CUDA_CHECK(cudaFuncSetAttribute(ulv_bwd_kernel<NR>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm));
+  CUDA_CHECK(cudaFuncSetAttribute(ulv_gemv_kernel<NR>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm));
 }
 
 void ulv_solve_tree(const ULVImpl& F, SolveWS& ws, cudaStream_t s) {
   int maxR = 0;
   for (auto& lv : F.lv) maxR = std::max(maxR, lv.maxR);
   const size_t sm = (size_t)maxR * ws.nrhs * sizeof(double);
-  require(sm + 4 * 64 * ws.nrhs * 8 <= 227 * 1024, "ulv_solve: node too large for the shared-memory vector");
+  require(sm <= 227 * 1024, "ulv_solve: node too large for the shared-memory vector");
   switch (ws.nrhs) {
 #define NRC(k) case k: if (sm > 48 * 1024) set_smem_attrs<k>(sm); solve_impl<k>(F, ws, s); break;
     NRC(1) NRC(2) NRC(3) NRC(4) NRC(5) NRC(6) NRC(7) NRC(8)
@@ -557,7 +574,8 @@ void ulv_solve_tree(const ULVImpl& F, SolveWS& ws, cudaStream_t s) {
 
 int ulv_solve_launches(const ULVImpl& F) {
   int c = 0;
-  for (auto& lv : F.lv) if (!lv.allpt) c += 2;
+  for (auto& lv : F.lv) if (!lv.allpt) c += (lv.nwork > 0) ? 2 : 0;
+  if (F.nleafpt > 0 && !F.lv[F.H->L].allpt) c += 2;
   return c;
 }
 
