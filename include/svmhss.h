@@ -27,6 +27,7 @@
 #ifndef SVMHSS_H
 #define SVMHSS_H
 
+#include <stddef.h>
 #include <stdint.h>
 
 #ifdef __cplusplus
@@ -45,6 +46,34 @@ enum {
 
 typedef struct hss_s* hss_t;  /* compressed kernel K~ */
 typedef struct ulv_s* ulv_t;  /* ULV factorization of K~ + beta I */
+typedef struct hss_comm_s* hss_comm_t;  /* subtree-sharding communicator */
+
+/* ---- multi-GPU subtree sharding ----
+ * With a communicator of P ranks (P a power of two, P <= 2^L), rank g owns node g of tree
+ * level lg = log2(P) — a contiguous range of tree positions — and all of its descendants.
+ * Levels below lg are computed only by their owner; levels above lg redundantly by every
+ * rank.  The only device<->device traffic is one allgather of fixed-size rank slots:
+ * subtree-root skeleton data (build), reduced Schur blocks (factor), and per ADMM iteration
+ * the reduced right-hand side plus the partial w^T q (the paper's method is sequential,
+ * P:351; this partitioning is ours).  Node-level work and every reduction follow the cluster
+ * tree, so results are bitwise identical for every P.  Every rank passes the same full
+ * inputs (F, y: all n points, original order) and receives the same full outputs.
+ *
+ * hss_allgather_fn: host backend callback.  send: `bytes` HOST bytes of this rank; recv:
+ * nranks * bytes HOST bytes, rank-major.  Return 0 on success (non-zero -> HSS_ENCCL).
+ * The host backend synchronizes the stream at every exchange (not graph-capturable); it
+ * lets P ranks run as P processes sharing fewer GPUs (no kernel ever waits on a peer).
+ * The NCCL backend (libnccl.so.2 loaded at run time) exchanges device buffers with
+ * ncclAllGather, stream-ordered and captured in the ADMM iteration's CUDA graph.
+ * Errors: HSS_EINVAL (nranks < 1, rank out of range, NULL fn), HSS_ENCCL (NCCL missing or
+ * failing).  hss_comm_free may be called while handles built with the comm are alive
+ * (they keep it alive). */
+typedef int (*hss_allgather_fn)(void* ctx, const void* send, void* recv, size_t bytes);
+int hss_comm_nccl_id(void* unique_id_out /* 128 HOST bytes, rank 0 then broadcasts */);
+int hss_comm_init_nccl(int32_t nranks, int32_t rank, const void* unique_id, hss_comm_t* out);
+int hss_comm_init_host(int32_t nranks, int32_t rank, hss_allgather_fn fn, void* ctx,
+                       hss_comm_t* out);
+void hss_comm_free(hss_comm_t comm);
 
 /* Build options (P:184-187 and readings T1-T4, R1-R3, H1-H5, AMB-10, AMB-11). */
 typedef struct {
@@ -58,6 +87,8 @@ typedef struct {
   const int32_t* ranks;    /* HOST pointer, nullable.  Fixed-rank mode: one rank per node in
                               level-major BFS order (2^(L+1)-1 entries; root ignored); the
                               node's rank is min(ranks[t], rows_t, s).  NULL = adaptive. */
+  hss_comm_t comm;         /* nullable: single GPU.  Else subtree sharding over comm's ranks;
+                              the factorization and ADMM inherit it from the hss_t. */
 } hss_opts;
 
 /* Build statistics (D6 / P:366-367 "Compression", "Memory"). */
@@ -86,8 +117,11 @@ int hss_build(const double* F, int64_t n, int32_t r, double h, const hss_opts* o
 
 /* Stats and the tree/rank/skeleton export used by the parity tests.
  * perm_out: n int64 (tree position -> original index), nullable.
- * ranks_out: 2^(L+1)-1 int32 (level-major BFS, root = -1), nullable.
- * skel_out: sum_t k_t int64 tree positions, nodes in BFS order, nullable.  HOST pointers. */
+ * ranks_out: 2^(L+1)-1 int32 (level-major BFS, root = -1), nullable.  Sharded: nodes held
+ *   by another rank (below level lg, outside this rank's subtree) are -2.
+ * skel_out: sum_t k_t int64 tree positions, nodes in BFS order, nullable (sharded: only the
+ *   nodes this rank holds contribute).  HOST pointers.
+ * Stats (cap_hits, passthrough, max_rank_used, generator_bytes) are global over all ranks. */
 int hss_info(hss_t H, hss_stats* st, int64_t* perm_out, int32_t* ranks_out, int64_t* skel_out);
 
 /* out = K~ v (reading M: up/down sweeps); v, out: n x nrhs, original order. */

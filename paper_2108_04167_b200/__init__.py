@@ -17,11 +17,11 @@ import ctypes as ct
 import numpy as np
 
 from . import _lib
-from ._lib import AdmmOpts, AdmmStats, HssError, HssOpts, HssStats, UlvStats, check, ptr
+from ._lib import ALLGATHER_FN, AdmmOpts, AdmmStats, HssError, HssOpts, HssStats, UlvStats, check, ptr
 
 _L = _lib.load()
 
-__all__ = ["hss_build", "hss_ulv_factor", "admm_svm_train", "svm_predict", "svm_train_predict_host",
+__all__ = ["Comm", "hss_build", "hss_ulv_factor", "admm_svm_train", "svm_predict", "svm_train_predict_host",
            "hss_omega", "hss_tree", "hss_kernel_matmul", "hss_kernel_block", "HSS", "ULV", "HssError",
            "version"]
 
@@ -33,6 +33,82 @@ def version() -> str:
 def launch_count() -> int:
     """Kernels launched by libsvmhss in this process (CUDA-graph replays included)."""
     return int(_L.hss_launch_count())
+
+
+def _host_allgather(group):
+    """hss_allgather_fn over torch.distributed (any backend that takes CPU tensors, e.g. gloo):
+    argument marshalling only — the bytes are the library's, gathered rank-major."""
+    import torch
+    import torch.distributed as dist
+
+    def cb(ctx, send, recv, nbytes):
+        try:
+            world = dist.get_world_size(group)
+            if nbytes == 0:
+                return 0
+            sv = np.ctypeslib.as_array((ct.c_uint8 * nbytes).from_address(send))
+            rv = np.ctypeslib.as_array((ct.c_uint8 * (nbytes * world)).from_address(recv))
+            st, rt = torch.from_numpy(sv), torch.from_numpy(rv)
+            dist.all_gather(list(rt.chunk(world)), st, group=group)
+            return 0
+        except Exception as e:  # noqa: BLE001 - reported to the library as a failed exchange
+            print(f"[svmhss] host allgather failed: {e!r}")
+            return 1
+
+    return ALLGATHER_FN(cb)
+
+
+class Comm:
+    """Subtree-sharding communicator (hss_comm_t).
+
+    Comm.nccl(): the library's own NCCL communicator (device buffers, graph-capturable); the
+    128-byte unique id is created by rank 0 and broadcast over torch.distributed.
+    Comm.host(): exchanges through a torch.distributed host group (e.g. gloo) — P ranks may then
+    share fewer GPUs (tests)."""
+
+    def __init__(self, handle, rank, world, keep=None):
+        self._h, self.rank, self.world, self._keep = handle, rank, world, keep
+
+    @classmethod
+    def nccl(cls, group=None):
+        import torch
+        import torch.distributed as dist
+        rank, world = dist.get_rank(group), dist.get_world_size(group)
+        uid = np.zeros(128, dtype=np.uint8)
+        if rank == 0:
+            check(_L.hss_comm_nccl_id(uid.ctypes.data))
+        t = torch.from_numpy(uid)
+        if dist.get_backend(group) == "nccl":
+            t = t.cuda()
+        dist.broadcast(t, src=0, group=group)
+        uid = np.ascontiguousarray(t.cpu().numpy())
+        hdl = ct.c_void_p()
+        check(_L.hss_comm_init_nccl(world, rank, uid.ctypes.data, ct.byref(hdl)))
+        return cls(hdl.value, rank, world)
+
+    @classmethod
+    def host(cls, group=None):
+        import torch.distributed as dist
+        rank, world = dist.get_rank(group), dist.get_world_size(group)
+        fn = _host_allgather(group)
+        hdl = ct.c_void_p()
+        check(_L.hss_comm_init_host(world, rank, fn, None, ct.byref(hdl)))
+        return cls(hdl.value, rank, world, keep=fn)
+
+    @property
+    def handle(self):
+        return self._h
+
+    def free(self):
+        if self._h is not None:
+            _L.hss_comm_free(self._h)
+            self._h = None
+
+    def __del__(self):
+        try:
+            self.free()
+        except Exception:
+            pass
 
 
 def _cuda_f64(t, name):
@@ -156,8 +232,9 @@ class ULV:
 
 
 def make_opts(leaf_size, rel_tol=0.0, abs_tol=0.0, max_rank=64, oversample=16, omega_seed=0,
-              tree_seed=0, ranks=None):
+              tree_seed=0, ranks=None, comm=None):
     o = HssOpts()
+    o.comm = comm.handle if comm is not None else None
     o.leaf_size, o.rel_tol, o.abs_tol = int(leaf_size), float(rel_tol), float(abs_tol)
     o.max_rank, o.oversample = int(max_rank), int(oversample)
     o.omega_seed, o.tree_seed = int(omega_seed), int(tree_seed)
@@ -169,15 +246,18 @@ def make_opts(leaf_size, rel_tol=0.0, abs_tol=0.0, max_rank=64, oversample=16, o
 
 
 def hss_build(F, h, leaf_size, rel_tol=0.0, abs_tol=0.0, max_rank=64, oversample=16, omega_seed=0,
-              tree_seed=0, ranks=None, stream=None) -> HSS:
-    """hss_build (Alg. 3 line 1): F is a CUDA float64 (n, r) tensor, original order."""
+              tree_seed=0, ranks=None, comm=None, stream=None) -> HSS:
+    """hss_build (Alg. 3 line 1): F is a CUDA float64 (n, r) tensor, original order
+    (all n points on every rank when `comm` shards the tree)."""
     _cuda_f64(F, "F")
     n, r = F.shape
-    o, keep = make_opts(leaf_size, rel_tol, abs_tol, max_rank, oversample, omega_seed, tree_seed, ranks)
+    o, keep = make_opts(leaf_size, rel_tol, abs_tol, max_rank, oversample, omega_seed, tree_seed, ranks, comm)
     hdl = ct.c_void_p()
     check(_L.hss_build(ptr(F), n, r, float(h), ct.byref(o), _stream(stream), ct.byref(hdl)))
     del keep
-    return HSS(hdl.value, n, r, h)
+    H = HSS(hdl.value, n, r, h)
+    H.comm = comm  # keep the Python object alive with the handle
+    return H
 
 
 def hss_ulv_factor(H: HSS, beta, stream=None) -> ULV:

@@ -27,7 +27,11 @@ class HssError(RuntimeError):
 class HssOpts(ct.Structure):
     _fields_ = [("leaf_size", ct.c_int32), ("rel_tol", ct.c_double), ("abs_tol", ct.c_double),
                 ("max_rank", ct.c_int32), ("oversample", ct.c_int32), ("omega_seed", ct.c_uint64),
-                ("tree_seed", ct.c_uint64), ("ranks", ct.POINTER(ct.c_int32))]
+                ("tree_seed", ct.c_uint64), ("ranks", ct.POINTER(ct.c_int32)), ("comm", ct.c_void_p)]
+
+
+# int (*hss_allgather_fn)(void* ctx, const void* send, void* recv, size_t bytes)
+ALLGATHER_FN = ct.CFUNCTYPE(ct.c_int, ct.c_void_p, ct.c_void_p, ct.c_void_p, ct.c_size_t)
 
 
 class HssStats(ct.Structure):
@@ -56,7 +60,8 @@ class AdmmStats(ct.Structure):
 EXPORTS = ["hss_build", "hss_info", "hss_matvec", "hss_ulv_factor", "ulv_info", "ulv_solve",
            "admm_svm_train", "svm_predict", "svm_train_predict_host", "hss_omega", "hss_tree",
            "hss_kernel_matmul", "hss_kernel_block", "hss_node", "hss_free", "ulv_free",
-           "hss_last_error", "hss_version", "hss_launch_count"]
+           "hss_last_error", "hss_version", "hss_launch_count", "hss_comm_nccl_id",
+           "hss_comm_init_nccl", "hss_comm_init_host", "hss_comm_free"]
 
 _lib = None
 
@@ -92,10 +97,16 @@ def load():
     L.ulv_free.restype = None
     L.hss_last_error.restype = ct.c_char_p
     L.hss_version.restype = ct.c_char_p
+    L.hss_comm_nccl_id.argtypes = [vp]
+    L.hss_comm_init_nccl.argtypes = [i32, i32, vp, ct.POINTER(vp)]
+    L.hss_comm_init_host.argtypes = [i32, i32, ALLGATHER_FN, vp, ct.POINTER(vp)]
+    L.hss_comm_free.argtypes = [vp]
+    L.hss_comm_free.restype = None
     L.hss_launch_count.argtypes = []
     L.hss_launch_count.restype = ct.c_int64
     for name in EXPORTS:
-        if name not in ("hss_free", "ulv_free", "hss_last_error", "hss_version", "hss_launch_count"):
+        if name not in ("hss_free", "ulv_free", "hss_last_error", "hss_version", "hss_launch_count",
+                        "hss_comm_free"):
             getattr(L, name).restype = ct.c_int
     _lib = L
     return L

@@ -14,7 +14,7 @@ HERE = os.path.dirname(os.path.abspath(__file__))
 CSRC = os.path.join(HERE, "csrc")
 BUILD = os.path.join(HERE, "_build")
 LIB = os.path.join(HERE, "libsvmhss.so")
-SOURCES = ["dense.cu", "tiles.cu", "tree.cu", "hss.cu", "ulv.cu", "admm.cu", "api.cu"]
+SOURCES = ["dense.cu", "tiles.cu", "tree.cu", "hss.cu", "ulv.cu", "admm.cu", "comm.cu", "shard.cu", "api.cu"]
 NVCC = shutil.which("nvcc") or "/usr/local/cuda/bin/nvcc"
 FLAGS = ["-gencode", "arch=compute_100a,code=sm_100a", "-lineinfo", "-O3", "-std=c++17",
          "-Xcompiler", "-fPIC", "--expt-relaxed-constexpr", "-Xptxas", "-v"]
@@ -50,7 +50,7 @@ def build(force: bool = False, verbose: bool = False) -> str:
     if verbose:
         print(logs)
     cmd = [NVCC, "-shared", "-gencode", "arch=compute_100a,code=sm_100a", "-o", LIB + ".tmp",
-           *[r[0] for r in res]]
+           *[r[0] for r in res], "-ldl"]
     p = subprocess.run(cmd, capture_output=True, text=True)
     if p.returncode != 0:
         raise RuntimeError(f"link failed:\n{p.stderr}")

@@ -8,64 +8,251 @@
 //     x = y_i v_i - (w^T q / w1) w_i;  z = clip(x - mu/beta, 0, C_c);  mu -= beta (x - z)
 //     q' = 1 + mu + beta z;  next right-hand side y_i q'; per-block partial w^T q'
 //   fixed-order reduction of the partials -> w^T q' for the next iteration.
-#include "internal.cuh"
+#include <cooperative_groups.h>
+#include "solve_dev.cuh"
+
+namespace cg = cooperative_groups;
 
 namespace svmhss {
 
-constexpr int EPI_BLOCKS = 1024;
-
-__global__ void __launch_bounds__(256) admm_epilogue_kernel(
-    int64_t n, int nC, const double* __restrict__ y, const double* __restrict__ w, double w1,
-    double beta, const double* __restrict__ Cv, const double* __restrict__ swq,
-    const double* __restrict__ v, double* __restrict__ z, double* __restrict__ mu,
-    double* __restrict__ bnext, double* __restrict__ part) {
-  __shared__ double red[32];
-  for (int c = 0; c < nC; ++c) {
-    const double coef = swq[c] / w1, C = Cv[c];
-    double pw = 0.0;
-    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
-         i += (int64_t)gridDim.x * blockDim.x) {
-      const int64_t e = i * nC + c;
-      const double yi = y[i], wi = w[i];
-      const double x = yi * v[e] - coef * wi;
-      const double m = mu[e];
-      const double zn = fmin(fmax(x - m / beta, 0.0), C);
-      const double mn = m - beta * (x - zn);
-      z[e] = zn;
-      mu[e] = mn;
-      const double q = 1.0 + mn + beta * zn;
-      bnext[e] = yi * q;
-      pw = fma(wi, q, pw);
+// Per-leaf fixed-order partials -> pairwise up this rank's subtree (see shard.cu).  The last
+// block to finish (device counter, then reset for the next replay) does the tree reduction,
+// so the reduction adds no launch.
+__device__ void last_block_tree_reduce(double* part, int nl, int ncols, double* out, unsigned* counter) {
+  __shared__ bool last;
+  __threadfence();
+  __syncthreads();
+  if (threadIdx.x == 0) last = (atomicAdd(counter, 1u) == gridDim.x - 1);
+  __syncthreads();
+  if (!last) return;
+  __threadfence();
+  for (int st = 1; st < nl; st <<= 1) {
+    for (int e = threadIdx.x; e < (nl / (2 * st)) * ncols; e += blockDim.x) {
+      const int i = (e / ncols) * 2 * st, c = e % ncols;
+      part[(int64_t)i * ncols + c] += part[(int64_t)(i + st) * ncols + c];
     }
-    const double t = block_sum(pw, red);
-    if (threadIdx.x == 0) part[(int64_t)blockIdx.x * nC + c] = t;
+    __syncthreads();
+  }
+  for (int c = threadIdx.x; c < ncols; c += blockDim.x) out[c] = part[c];
+  if (threadIdx.x == 0) *counter = 0u;
+}
+
+// The per-point ADMM update (A2-A3, P:164-166 with AMB-1) for problem c:
+//   x = y v - (w^T q / w1) w;  z = clip(x - mu/beta, 0, C);  mu -= beta (x - z)
+//   q' = 1 + mu + beta z;  next right-hand side y q'.   Returns w_i q'_i.
+// x of pass-through leaves is read straight from level L-1's solution and their next
+// right-hand side written straight into level L-1's input (ptmap), fusing the leaf level of
+// both sweeps into the epilogue.
+struct EpiArgs {
+  const double *y, *w, *Cv, *swq;
+  double w1, beta;
+  const double *xL, *xL1;
+  const int64_t* ptmap;
+  double *z, *mu, *bL, *bL1;
+  int nC;
+};
+__device__ __forceinline__ double epi_point(const EpiArgs& A, int64_t i, int c) {
+  const double coef = A.swq[c] / A.w1, C = A.Cv[c];
+  const int nC = A.nC;
+  const int64_t e = i * nC + c;
+  const int64_t q = A.ptmap ? A.ptmap[i] : -1;
+  const double vi = (q >= 0) ? A.xL1[q * nC + c] : A.xL[e];
+  const double yi = A.y[i], wi = A.w[i];
+  const double x = yi * vi - coef * wi;
+  const double m = A.mu[e];
+  const double zn = fmin(fmax(x - m / A.beta, 0.0), C);
+  const double mn = m - A.beta * (x - zn);
+  A.z[e] = zn;
+  A.mu[e] = mn;
+  const double qn = 1.0 + mn + A.beta * zn;
+  if (q >= 0) A.bL1[q * nC + c] = yi * qn;
+  else A.bL[e] = yi * qn;
+  return wi * qn;
+}
+// A leaf's w^T q' partial is defined chunk-wise (both epilogue kernels below): chunks of 32
+// consecutive points from the leaf's start, each summed by a warp butterfly, then the chunk sums
+// added in order.  One warp updates one chunk and returns its sums (lane c holds problem c).
+__device__ __forceinline__ double epi_chunk(const EpiArgs& A, int64_t p0, int cnt) {
+  const int lane = threadIdx.x & 31;
+  double mine = 0.0;
+  for (int c = 0; c < A.nC; ++c) {
+    const double v = (lane < cnt) ? epi_point(A, p0 + lane, c) : 0.0;
+    const double t = warp_sum(v);
+    if (lane == c) mine = t;
+  }
+  return mine;
+}
+
+// One block per leaf (leaf list, or all of this rank's leaves when `leaves` is NULL).  With
+// `counter`, the last block to finish reduces the leaf partials up the subtree -> out (so the
+// reduction adds no launch).
+__global__ void __launch_bounds__(256) admm_epilogue_kernel(EpiArgs A, const int64_t* __restrict__ leaf_lo,
+                                                            const int* __restrict__ leaves, int nleaf_all,
+                                                            double* __restrict__ part, double* __restrict__ out,
+                                                            unsigned* __restrict__ counter) {
+  extern __shared__ double cs[];  // chunk sums: nch x nC
+  const int leaf = leaves ? leaves[blockIdx.x] : (int)blockIdx.x;
+  const int64_t i0 = leaf_lo[leaf], i1 = leaf_lo[leaf + 1];
+  const int nch = (int)((i1 - i0 + 31) / 32);
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  for (int ch = wid; ch < nch; ch += 8) {
+    const int64_t p0 = i0 + 32LL * ch;
+    const double t = epi_chunk(A, p0, (int)((i1 - p0) < 32 ? (i1 - p0) : 32));
+    if (lane < A.nC) cs[ch * A.nC + lane] = t;
+  }
+  __syncthreads();
+  if (threadIdx.x < A.nC) {
+    double t = 0.0;
+    for (int ch = 0; ch < nch; ++ch) t += cs[ch * A.nC + threadIdx.x];
+    part[(int64_t)leaf * A.nC + threadIdx.x] = t;
+  }
+  if (counter) {
+    __shared__ bool last;
+    __threadfence();
+    __syncthreads();
+    if (threadIdx.x == 0) last = (atomicAdd(counter, 1u) == gridDim.x - 1);
+    __syncthreads();
+    if (!last) return;
+    __threadfence();
+    for (int st = 1; st < nleaf_all; st <<= 1) {
+      for (int e = threadIdx.x; e < (nleaf_all / (2 * st)) * A.nC; e += blockDim.x) {
+        const int i = (e / A.nC) * 2 * st, c = e % A.nC;
+        part[(int64_t)i * A.nC + c] += part[(int64_t)(i + st) * A.nC + c];
+      }
+      __syncthreads();
+    }
+    for (int c = threadIdx.x; c < A.nC; c += blockDim.x) out[c] = part[c];
+    if (threadIdx.x == 0) *counter = 0u;
   }
 }
 
-// out[c] = sum_b part[b*nC + c]   (fixed order)
-__global__ void reduce_partials_kernel(const double* __restrict__ part, int nb, int nC,
-                                       double* __restrict__ out) {
+// ---- fused bottom level: for a node t of level L-1 whose
+// two children are pass-through leaves (its rows ARE points), one 8-CTA cluster does
+//   backward sweep (iteration k):  x = M_t^T [x_s; y_r]          (reads M_t from HBM)
+//   ADMM epilogue on the node's points (iteration k)
+//   forward sweep (iteration k+1): t = M_t b'                     (re-reads M_t, from L2)
+// with cluster barriers in between, so each such M_t crosses HBM once per iteration instead
+// of twice.  bwd_cols / fwd_rows / epi_chunk are the level kernels' own device functions:
+// the results are bitwise identical to the unfused sweep.
+struct FusedNode {
+  int64_t moff, roff, koff, yoff, plo;
+  int R, k, ma, mb, leafa, pad;
+};
+constexpr int kFCL = 8;  // CTAs per cluster (one node); kFCL * kCW >= max fused R
+constexpr int kMaxChunks = (kFCL * kCW + 31) / 32 + 2;
+
+template <int NR>
+__global__ void __launch_bounds__(kBW * 32) admm_bottom_kernel(EpiArgs A, const FusedNode* __restrict__ nodes, int nf,
+                                                               const double* __restrict__ M,
+                                                               const double* __restrict__ xs, double* __restrict__ yr,
+                                                               double* __restrict__ xb, double* __restrict__ fb,
+                                                               double* __restrict__ fup, double* __restrict__ chunkp,
+                                                               double* __restrict__ part) {
+  cg::cluster_group cl = cg::this_cluster();
+  const int c = (int)cl.block_rank();
+  const int ncl = gridDim.x / kFCL;
+  const int tid = threadIdx.x, wid = tid >> 5, lane = tid & 31;
+  extern __shared__ double sm[];
+  const int j0 = c * kCW;
+  // persistent clusters: few enough nodes in flight that a node's M_t (read from HBM in (1))
+  // is still in L2 when (3) re-reads it
+  for (int f = blockIdx.x / kFCL; f < nf; f += ncl) {
+  const FusedNode N = nodes[f];
+  const int R = N.R;
+  // (1) backward sweep: x (this CTA's kCW columns)
+  if (j0 < R) {
+    double* ush = sm;
+    double* red = sm + R * NR;
+    const int kn = N.k * NR;
+    for (int e = tid; e < R * NR; e += kBW * 32) ush[e] = (e < kn) ? xs[N.koff * NR + e] : yr[(N.yoff - N.k) * NR + e];
+    __syncthreads();
+    bwd_cols<NR>(M + N.moff, R, ush, j0, red, xb + N.roff * NR);
+  }
+  cl.sync();
+  // (2) epilogue on the node's points, chunk by chunk (leaf a: ca chunks, then leaf b)
+  const int ca = (N.ma + 31) / 32, cb = (N.mb + 31) / 32;
+  for (int ch = c * kBW + wid; ch < ca + cb; ch += kFCL * kBW) {
+    const bool inb = ch >= ca;
+    const int64_t p0 = N.plo + (inb ? N.ma + 32LL * (ch - ca) : 32LL * ch);
+    const int64_t rem = inb ? (N.ma + N.mb) - (p0 - N.plo) : N.ma - (p0 - N.plo);
+    const int cnt = (int)(rem < 32 ? rem : 32);
+    const double t = epi_chunk(A, p0, cnt);
+    if (lane < A.nC) chunkp[((int64_t)f * kMaxChunks + ch) * A.nC + lane] = t;
+  }
+  cl.sync();
+  // (3) leaf partials (fixed chunk order) and the forward sweep of iteration k+1
+  if (c == 0 && tid < 2 * A.nC) {
+    const int which = tid / A.nC, cc = tid % A.nC;
+    double t = 0.0;
+    const int lo = which ? ca : 0, hi = which ? ca + cb : ca;
+    for (int ch = lo; ch < hi; ++ch) t += chunkp[((int64_t)f * kMaxChunks + ch) * A.nC + cc];
+    part[(int64_t)(N.leafa + which) * A.nC + cc] = t;
+  }
+  if (j0 < R) {
+    double* vsh = sm;
+    for (int e = tid; e < R * NR; e += kBW * 32) vsh[e] = fb[N.roff * NR + e];
+    __syncthreads();
+    fwd_rows<NR>(M + N.moff, R, vsh, j0, min(R, j0 + kCW), wid, kBW, N.k, N.koff, N.yoff, fup, yr);
+  }
+  cl.sync();  // smem reuse and yr of this node: next node only after every CTA is done
+  }
+}
+
+template <int NR>
+static void launch_bottom(const EpiArgs& A, const FusedNode* nodes, int nf, const double* M, const double* xs,
+                          double* yr, double* xb, double* fb, double* fup, double* chunkp, double* part,
+                          cudaStream_t s) {
+  const size_t smem = ((size_t)kFCL * kCW + (size_t)kBW * kCW) * NR * sizeof(double);
+  if (smem > 48 * 1024)
+    CUDA_CHECK(cudaFuncSetAttribute(admm_bottom_kernel<NR>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+  static int ncl_env = -1;
+  if (ncl_env < 0) {
+    const char* e = getenv("SVMHSS_FUSE_CLUSTERS");
+    ncl_env = e ? std::max(1, atoi(e)) : 36;
+  }
+  const int ncl = std::min(nf, ncl_env);
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3((unsigned)(ncl * kFCL));
+  cfg.blockDim = dim3(kBW * 32);
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = s;
+  cudaLaunchAttribute at[1];
+  at[0].id = cudaLaunchAttributeClusterDimension;
+  at[0].val.clusterDim.x = kFCL;
+  at[0].val.clusterDim.y = 1;
+  at[0].val.clusterDim.z = 1;
+  cfg.attrs = at;
+  cfg.numAttrs = 1;
+  CUDA_CHECK(cudaLaunchKernelEx(&cfg, admm_bottom_kernel<NR>, A, nodes, nf, M, xs, yr, xb, fb, fup, chunkp, part));
+}
+
+static void bottom_dispatch(int NR, const EpiArgs& A, const FusedNode* nodes, int nf, const double* M,
+                            const double* xs, double* yr, double* xb, double* fb, double* fup, double* chunkp,
+                            double* part, cudaStream_t s) {
+  switch (NR) {
+#define BC(k) case k: launch_bottom<k>(A, nodes, nf, M, xs, yr, xb, fb, fup, chunkp, part, s); break;
+    BC(1) BC(2) BC(3) BC(4) BC(5) BC(6) BC(7) BC(8)
+#undef BC
+    default: throw Error(HSS_EINVAL, "admm: nC must be 1..8");
+  }
+  LAUNCH_CHECK();
+}
+
+// Per-leaf partials of column sums: out[leaf*ncols + c] = sum_{i in leaf} f(i, c)
+//   mode 0: A[i*ncols + c]   mode 1: A[i*ncols + c] * B[i*ncols + c]
+__global__ void leaf_colsum_kernel(const int64_t* __restrict__ leaf_lo, int ncols, const double* __restrict__ A,
+                                   int mode, const double* __restrict__ B, double* __restrict__ part) {
   __shared__ double red[32];
-  for (int c = 0; c < nC; ++c) {
+  const int64_t i0 = leaf_lo[blockIdx.x], i1 = leaf_lo[blockIdx.x + 1];
+  for (int c = 0; c < ncols; ++c) {
     double a = 0.0;
-    for (int b = threadIdx.x; b < nb; b += blockDim.x) a += part[(int64_t)b * nC + c];
+    for (int64_t i = i0 + threadIdx.x; i < i1; i += blockDim.x) {
+      const double x = A[i * ncols + c];
+      a += (mode == 0) ? x : x * B[i * ncols + c];
+    }
     const double t = block_sum(a, red);
-    if (threadIdx.x == 0) out[c] = t;
+    if (threadIdx.x == 0) part[(int64_t)blockIdx.x * ncols + c] = t;
   }
-}
-
-// per-column fixed-order sums of f(i, c) for a few reductions used by precompute / bias
-__global__ void colsum_kernel(int64_t n, int ncols, const double* __restrict__ A, int mode,
-                              const double* __restrict__ B, double* __restrict__ out) {
-  __shared__ double red[32];
-  const int c = blockIdx.x;
-  double a = 0.0;
-  for (int64_t i = threadIdx.x; i < n; i += blockDim.x) {
-    const double x = A[i * ncols + c];
-    a += (mode == 0) ? x : x * B[i * ncols + c];
-  }
-  const double t = block_sum(a, red);
-  if (threadIdx.x == 0) out[c] = t;
 }
 
 __global__ void label_check_kernel(const double* __restrict__ y, int64_t n, int* bad) {
@@ -78,9 +265,16 @@ __global__ void fill_kernel(double* a, int64_t n, double v) {
   if (i < n) a[i] = v;
 }
 
-__global__ void init_rhs_kernel(const double* __restrict__ y, int64_t n, int nC, double* __restrict__ b) {
+// initial right-hand side y q0 = y (q0 = e), written where the fused leaf I/O expects it
+__global__ void init_rhs_kernel(const double* __restrict__ y, int64_t n, int nC, const int64_t* __restrict__ ptmap,
+                                double* __restrict__ bL, double* __restrict__ bL1) {
   const int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
-  if (e < n * nC) b[e] = y[e / nC];
+  if (e >= n * nC) return;
+  const int64_t i = e / nC;
+  const int c = (int)(e % nC);
+  const int64_t q = ptmap ? ptmap[i] : -1;
+  if (q >= 0) bL1[q * nC + c] = y[i];
+  else bL[e] = y[i];
 }
 
 __global__ void mul_kernel(const double* __restrict__ a, const double* __restrict__ b, int64_t n,
@@ -89,22 +283,23 @@ __global__ void mul_kernel(const double* __restrict__ a, const double* __restric
   if (i < n) out[i] = a[i] * b[i];
 }
 
-// margin-set counts per c: cnt[2c] = #{eps < z < C-eps}, cnt[2c+1] = #{z > eps}
-__global__ void margin_count_kernel(int64_t n, int nC, const double* __restrict__ z,
-                                    const double* __restrict__ Cv, double eps_rel,
-                                    double* __restrict__ cnt) {
+// per-leaf margin-set counts: part[leaf*2nC + 2c] = #{eps < z < C-eps}, [+1] = #{z > eps}
+__global__ void margin_count_kernel(const int64_t* __restrict__ leaf_lo, int nC, const double* __restrict__ z,
+                                    const double* __restrict__ Cv, double eps_rel, double* __restrict__ part) {
   __shared__ double red[32];
-  const int c = blockIdx.x;
-  const double C = Cv[c], eps = eps_rel * C;
-  double a = 0.0, b = 0.0;
-  for (int64_t i = threadIdx.x; i < n; i += blockDim.x) {
-    const double zi = z[i * nC + c];
-    a += (zi > eps && zi < C - eps) ? 1.0 : 0.0;
-    b += (zi > eps) ? 1.0 : 0.0;
+  const int64_t i0 = leaf_lo[blockIdx.x], i1 = leaf_lo[blockIdx.x + 1];
+  for (int c = 0; c < nC; ++c) {
+    const double C = Cv[c], eps = eps_rel * C;
+    double a = 0.0, b = 0.0;
+    for (int64_t i = i0 + threadIdx.x; i < i1; i += blockDim.x) {
+      const double zi = z[i * nC + c];
+      a += (zi > eps && zi < C - eps) ? 1.0 : 0.0;
+      b += (zi > eps) ? 1.0 : 0.0;
+    }
+    const double ta = block_sum(a, red);
+    const double tb = block_sum(b, red);
+    if (threadIdx.x == 0) { part[(int64_t)blockIdx.x * 2 * nC + 2 * c] = ta; part[(int64_t)blockIdx.x * 2 * nC + 2 * c + 1] = tb; }
   }
-  const double ta = block_sum(a, red);
-  const double tb = block_sum(b, red);
-  if (threadIdx.x == 0) { cnt[2 * c] = ta; cnt[2 * c + 1] = tb; }
 }
 
 // V[:, 2c] = indicator of the chosen margin set, V[:, 2c+1] = z_y = y z
@@ -123,95 +318,183 @@ __global__ void bias_rhs_kernel(int64_t n, int nC, const double* __restrict__ z,
   V[i * 2 * nC + 2 * c + 1] = y[i] * zi;
 }
 
-// sums per c: s[4c+0] = sum_M y, s[4c+1] = z_y . (K~ e_M), s[4c+2] = z_y . (K~ z_y), s[4c+3] = sum z
-__global__ void bias_sums_kernel(int64_t n, int nC, const double* __restrict__ V,
+// per-leaf sums: part[leaf*4nC + 4c + 0] = sum_M y, +1 = z_y . (K~ e_M), +2 = z_y . (K~ z_y),
+// +3 = sum z
+__global__ void bias_sums_kernel(const int64_t* __restrict__ leaf_lo, int nC, const double* __restrict__ V,
                                  const double* __restrict__ KV, const double* __restrict__ y,
-                                 const double* __restrict__ z, double* __restrict__ out) {
+                                 const double* __restrict__ z, double* __restrict__ part) {
   __shared__ double red[32];
-  const int c = blockIdx.x;
-  double a = 0, b = 0, d = 0, f = 0;
-  for (int64_t i = threadIdx.x; i < n; i += blockDim.x) {
-    const double ind = V[i * 2 * nC + 2 * c], zy = V[i * 2 * nC + 2 * c + 1];
-    a += ind * y[i];
-    b += zy * KV[i * 2 * nC + 2 * c];
-    d += zy * KV[i * 2 * nC + 2 * c + 1];
-    f += z[i * nC + c];
+  const int64_t i0 = leaf_lo[blockIdx.x], i1 = leaf_lo[blockIdx.x + 1];
+  for (int c = 0; c < nC; ++c) {
+    double a = 0, b = 0, d = 0, f = 0;
+    for (int64_t i = i0 + threadIdx.x; i < i1; i += blockDim.x) {
+      const double ind = V[i * 2 * nC + 2 * c], zy = V[i * 2 * nC + 2 * c + 1];
+      a += ind * y[i];
+      b += zy * KV[i * 2 * nC + 2 * c];
+      d += zy * KV[i * 2 * nC + 2 * c + 1];
+      f += z[i * nC + c];
+    }
+    a = block_sum(a, red); b = block_sum(b, red); d = block_sum(d, red); f = block_sum(f, red);
+    if (threadIdx.x == 0) {
+      double* o = part + (int64_t)blockIdx.x * 4 * nC + 4 * c;
+      o[0] = a; o[1] = b; o[2] = d; o[3] = f;
+    }
   }
-  a = block_sum(a, red); b = block_sum(b, red); d = block_sum(d, red); f = block_sum(f, red);
-  if (threadIdx.x == 0) { out[4 * c] = a; out[4 * c + 1] = b; out[4 * c + 2] = d; out[4 * c + 3] = f; }
 }
 
-// y_orig: device labels (original order).  z_out / mu_out: device, original order, n x nC.
+// y_orig: device labels (original order, all n).  z_out / mu_out: device, original order,
+// n x nC (every rank gets the full vectors).
 AdmmResult admm_train_impl(const ULVImpl& F, const double* y_orig, const std::vector<double>& Cs,
                            int max_it, const admm_opts* opt, double* z_out, double* mu_out,
                            double* bias_out, double* obj_out, cudaStream_t s) {
   const HSSImpl& H = *F.H;
-  const int64_t n = H.n;
-  const int nC = (int)Cs.size();
+  const Shard& sh = H.sh;
+  const int64_t N = H.n, n = H.nloc();
+  const int L = H.L, nC = (int)Cs.size(), nleaf = H.nleaf_loc();
   const double beta = F.beta;
   AdmmResult R{};
   {
     DevBuf<int> bad(1);
     CUDA_CHECK(cudaMemsetAsync(bad.p, 0, sizeof(int), s));
-    label_check_kernel<<<ceil_div(n, 256), 256, 0, s>>>(y_orig, n, bad.p);
+    label_check_kernel<<<ceil_div(N, 256), 256, 0, s>>>(y_orig, N, bad.p);
     LAUNCH_CHECK();
     int hb = 0;
     d2h(&hb, bad.p, 1, s);
     CUDA_CHECK(cudaStreamSynchronize(s));
     require(hb == 0, "admm_svm_train: labels must be exactly +1 or -1");
   }
-  DevBuf<double> y(n), w(n), z((size_t)n * nC), mu((size_t)n * nC), dC(nC), swq(nC);
-  gather_rows(y_orig, H.perm.p, n, 1, y.p, s);
+  DevBuf<double> y(n), w(n), z((size_t)n * nC), mu((size_t)n * nC), dC(nC), swq(nC), subwq(nC);
+  DevBuf<double> part((size_t)std::max(1, nleaf) * std::max(4 * nC, 2));
+  gather_rows(y_orig, H.perm.p + H.lo_g, n, 1, y.p, s);
   h2d(dC.p, Cs.data(), nC, s);
-  // ---- precompute (A0): v = K_b^-1 e; w = Y v; w1 = e^T v
+  // ---- precompute (A0): v = K_b^-1 e; w = Y v; w1 = e^T v (cluster-tree-ordered sums)
   EventTimer tpre(s);
-  double w1 = 0.0;
+  double w1 = 0.0, wte = 0.0;
   {
     SolveWS ws1;
     solve_ws_alloc(F, 1, ws1);
-    fill_kernel<<<ceil_div(n, 256), 256, 0, s>>>(ws1.fin[H.L], n, 1.0);
+    fill_kernel<<<ceil_div(std::max<int64_t>(1, n), 256), 256, 0, s>>>(ws1.fin[L], n, 1.0);
     LAUNCH_CHECK();
     ulv_solve_tree(F, ws1, s);
-    mul_kernel<<<ceil_div(n, 256), 256, 0, s>>>(y.p, ws1.xout[H.L], n, w.p);
+    mul_kernel<<<ceil_div(std::max<int64_t>(1, n), 256), 256, 0, s>>>(y.p, ws1.xout[L], n, w.p);
     LAUNCH_CHECK();
-    DevBuf<double> t(1);
-    colsum_kernel<<<1, 256, 0, s>>>(n, 1, ws1.xout[H.L], 0, nullptr, t.p);
+    leaf_colsum_kernel<<<nleaf, 256, 0, s>>>(H.leaf_lo.p, 1, ws1.xout[L], 0, nullptr, part.p);
     LAUNCH_CHECK();
-    d2h(&w1, t.p, 1, s);
-    CUDA_CHECK(cudaStreamSynchronize(s));
+    tree_reduce_all(H, part.p, 1, &w1, s);
   }
   R.ms_pre = tpre.stop_ms();
   R.w1 = w1;
   if (!(w1 > 0.0)) throw Error(HSS_EW1, "w1 = e^T (K~+beta I)^-1 e = " + std::to_string(w1) + " <= 0");
-  // ---- state
+  // ---- state: x0 = z0 = mu0 = 0 (AMB-6); q0 = e
+  const bool fused = L >= 1 && F.nleafpt > 0;
   SolveWS ws;
+  ws.nextra = nC;
   solve_ws_alloc(F, nC, ws);
-  double* bvec = ws.fin[H.L];
-  const double* xvec = ws.xout[H.L];
+  ws.fused_leaf_io = fused;
+  DevBuf<double> allwq((size_t)sh.P * nC);
+  if (sh.on()) { ws.extra = subwq.p; ws.extra_all = allwq.p; ws.extra_top = swq.p; }
+  double* bL = ws.fin[L];
+  double* bL1 = fused ? ws.fin[L - 1] : nullptr;
+  const double* xL = ws.xout[L];
+  const double* xL1 = fused ? ws.xout[L - 1] : nullptr;
+  const int64_t* ptm = fused ? F.ptmap.p : nullptr;
   CUDA_CHECK(cudaMemsetAsync(z.p, 0, (size_t)n * nC * 8, s));
   CUDA_CHECK(cudaMemsetAsync(mu.p, 0, (size_t)n * nC * 8, s));
-  init_rhs_kernel<<<ceil_div(n * nC, 256), 256, 0, s>>>(y.p, n, nC, bvec);  // q0 = e
+  init_rhs_kernel<<<ceil_div(std::max<int64_t>(1, n * nC), 256), 256, 0, s>>>(y.p, n, nC, ptm, bL, bL1);
   LAUNCH_CHECK();
   {
-    DevBuf<double> t(1);
-    colsum_kernel<<<1, 256, 0, s>>>(n, 1, w.p, 0, nullptr, t.p);  // w^T e
+    // w^T q0 = w^T e: this rank's subtree partial (exchanged in the first iteration) and total
+    DevBuf<double> sub(1);
+    leaf_colsum_kernel<<<nleaf, 256, 0, s>>>(H.leaf_lo.p, 1, w.p, 0, nullptr, part.p);
     LAUNCH_CHECK();
-    for (int c = 0; c < nC; ++c)
-      CUDA_CHECK(cudaMemcpyAsync(swq.p + c, t.p, 8, cudaMemcpyDeviceToDevice, s));
+    tree_reduce_local(H, part.p, 1, sub.p, s);
+    leaf_colsum_kernel<<<nleaf, 256, 0, s>>>(H.leaf_lo.p, 1, w.p, 0, nullptr, part.p);
+    LAUNCH_CHECK();
+    tree_reduce_all(H, part.p, 1, &wte, s);
+    for (int c = 0; c < nC; ++c) {
+      CUDA_CHECK(cudaMemcpyAsync(subwq.p + c, sub.p, 8, cudaMemcpyDeviceToDevice, s));
+      h2d(swq.p + c, &wte, 1, s);
+    }
     CUDA_CHECK(cudaStreamSynchronize(s));
   }
-  const int eb = (int)std::min<int64_t>(EPI_BLOCKS, std::max<int64_t>(1, (n + 255) / 256));
-  DevBuf<double> part((size_t)eb * nC);
+  DevBuf<unsigned> counter(1);
+  CUDA_CHECK(cudaMemsetAsync(counter.p, 0, sizeof(unsigned), s));
+  double* epi_out = sh.on() ? subwq.p : swq.p;
+  EpiArgs EA{y.p, w.p, dC.p, swq.p, w1, beta, xL, xL1, ptm, z.p, mu.p, bL, bL1, nC};
+  int maxleaf = 1;
+  for (int i = sh.first(L); i < sh.last(L); ++i) maxleaf = std::max<int>(maxleaf, (int)(H.lv[L][i].hi - H.lv[L][i].lo));
+  const size_t epi_smem = (size_t)((maxleaf + 31) / 32) * nC * sizeof(double);
+  if (epi_smem > 48 * 1024)
+    CUDA_CHECK(cudaFuncSetAttribute(admm_epilogue_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)epi_smem));
+  // ---- fused bottom level plan: nodes of level b = L-1 (this rank's) whose children are both
+  // pass-through leaves and whose R fits one cluster; the rest ("G" nodes) take the level
+  // kernels restricted to them.  Needs the bottom level below the exchanged level (b >= lg).
+  const int b = L - 1;
+  std::vector<FusedNode> fnodes;
+  std::vector<SolveWork> gwk, gbwk;
+  std::vector<int> gleaves;
+  const char* env = getenv("SVMHSS_FUSE_BOTTOM");
+  const bool want_fuse = !(env && env[0] == '0');
+  if (fused && b >= 1 && b >= sh.lg && want_fuse && !F.lv[b].allpt) {
+    const auto& Fb = F.lv[b];
+    std::vector<SolveNode> sn(Fb.nnodes);
+    d2h(sn.data(), Fb.nodes.p, sn.size(), s);
+    CUDA_CHECK(cudaStreamSynchronize(s));
+    for (int q = 0; q < Fb.nnodes; ++q) {
+      const int t = sh.first(b) + q;
+      const auto &ca = H.lv[L][2 * t], &cb = H.lv[L][2 * t + 1];
+      const bool ok = ca.pt && cb.pt && !sn[q].pt && sn[q].R <= kFCL * kCW;
+      if (ok) {
+        fnodes.push_back({sn[q].moff, sn[q].roff, sn[q].koff, sn[q].yoff, ca.lo - H.lo_g, sn[q].R, sn[q].k,
+                          (int)(ca.hi - ca.lo), (int)(cb.hi - cb.lo), 2 * t - sh.first(L), 0});
+      } else {
+        for (int c = 0; c < ceil_div(sn[q].R, Fb.ch); ++c) gwk.push_back({q, c});
+        for (int c = 0; c < ceil_div(sn[q].R, kCW); ++c) gbwk.push_back({q, c});
+        gleaves.push_back(2 * t - sh.first(L));
+        gleaves.push_back(2 * t + 1 - sh.first(L));
+      }
+    }
+  }
+  const bool bottom = !fnodes.empty();
+  auto dfn = upload(fnodes, s);
+  auto dgwk = upload(gwk, s), dgbwk = upload(gbwk, s);
+  auto dgleaves = upload(gleaves, s);
+  DevBuf<double> chunkp((size_t)std::max<size_t>(1, fnodes.size()) * kMaxChunks * nC);
+  CUDA_CHECK(cudaStreamSynchronize(s));
+  if (bottom) {
+    // prologue: the forward sweep of iteration 1 up to level b (the loop body starts above it)
+    ulv_solve_steps(F, ws, {SolveStep{SolveStep::FWD, L, b, /*no_exchange=*/true}}, s);
+  }
   auto iteration = [&](cudaStream_t st) {
-    ulv_solve_tree(F, ws, st);
-    admm_epilogue_kernel<<<eb, 256, 0, st>>>(n, nC, y.p, w.p, w1, beta, dC.p, swq.p, xvec,
-                                             z.p, mu.p, bvec, part.p);
-    reduce_partials_kernel<<<1, 256, 0, st>>>(part.p, eb, nC, swq.p);
+    if (!bottom) {
+      ulv_solve_tree(F, ws, st);
+      admm_epilogue_kernel<<<nleaf, 256, epi_smem, st>>>(EA, H.leaf_lo.p, nullptr, nleaf, part.p, epi_out, counter.p);
+      LAUNCH_CHECK();
+      return;
+    }
+    std::vector<SolveStep> top;
+    if (sh.on() && sh.lg == b) top.push_back(SolveStep{SolveStep::EXCHANGE});
+    top.push_back(SolveStep{SolveStep::FWD, b - 1, 0});
+    top.push_back(SolveStep{SolveStep::BWD, 0, b - 1});
+    ulv_solve_steps(F, ws, top, st);
+    bottom_dispatch(nC, EA, dfn.p, (int)fnodes.size(), F.lv[b].M.p, ws.xout[b - 1], ws.yr[b], ws.xout[b], ws.fin[b],
+                    ws.fin[b - 1], chunkp.p, part.p, st);
+    if (!gleaves.empty()) {
+      ulv_solve_steps(F, ws, {SolveStep{SolveStep::BWD_LIST, b, 0, false, dgbwk.p, (int)gbwk.size()},
+                              SolveStep{SolveStep::BWD, L, L}}, st);
+      admm_epilogue_kernel<<<(unsigned)gleaves.size(), 256, epi_smem, st>>>(EA, H.leaf_lo.p, dgleaves.p, nleaf,
+                                                                           part.p, nullptr, nullptr);
+      LAUNCH_CHECK();
+      ulv_solve_steps(F, ws, {SolveStep{SolveStep::FWD, L, L, true},
+                              SolveStep{SolveStep::FWD_LIST, b, 0, false, dgwk.p, (int)gwk.size()}}, st);
+    }
+    tree_reduce_local(H, part.p, nC, epi_out, st);
   };
-  R.launches = ulv_solve_launches(F) + 2;
-  // capture one iteration as a CUDA graph
+  // one iteration as a CUDA graph (needs a capturable exchange when sharded)
   cudaGraphExec_t gexec = nullptr;
-  {
+  const bool use_graph = !sh.on() || sh.comm->capturable();
+  const long long g0 = g_launches.load();  // launches are counted per executed iteration below
+  if (use_graph) {
     cudaStream_t cs;
     CUDA_CHECK(cudaStreamCreateWithFlags(&cs, cudaStreamNonBlocking));
     cudaGraph_t graph = nullptr;
@@ -222,34 +505,54 @@ AdmmResult admm_train_impl(const ULVImpl& F, const double* y_orig, const std::ve
     CUDA_CHECK(cudaGraphDestroy(graph));
     CUDA_CHECK(cudaStreamDestroy(cs));
     R.graph = 1;
+    R.launches = g_launches.load() - g0;
+    g_launches.store(g0);
   }
   const int te = (opt && opt->trace_every > 0) ? opt->trace_every : 0;
+  DevBuf<double> full((te && (opt->trace_z || opt->trace_mu)) ? (size_t)N * nC : 0);
   EventTimer tloop(s);
   int tcount = 0;
   for (int it = 1; it <= max_it; ++it) {
-    CUDA_CHECK(cudaGraphLaunch(gexec, s));
+    const long long gi = g_launches.load();
+    if (use_graph) {
+      CUDA_CHECK(cudaGraphLaunch(gexec, s));
+      g_launches.store(gi + R.launches);
+    } else {
+      iteration(s);
+      R.launches = g_launches.load() - gi;
+    }
     if (te && (it % te == 0 || it == max_it)) {
-      if (opt->trace_z) scatter_rows(z.p, H.perm.p, n, nC, opt->trace_z + (int64_t)tcount * n * nC, s);
-      if (opt->trace_mu) scatter_rows(mu.p, H.perm.p, n, nC, opt->trace_mu + (int64_t)tcount * n * nC, s);
+      if (opt->trace_z) {
+        gather_points(H, z.p, nC, full.p, s);
+        scatter_rows(full.p, H.perm.p, N, nC, opt->trace_z + (int64_t)tcount * N * nC, s);
+      }
+      if (opt->trace_mu) {
+        gather_points(H, mu.p, nC, full.p, s);
+        scatter_rows(full.p, H.perm.p, N, nC, opt->trace_mu + (int64_t)tcount * N * nC, s);
+      }
       ++tcount;
     }
   }
   R.ms_loop = tloop.stop_ms();
-  // graph replays are not seen by LAUNCH_CHECK: account for them (capture counted one iteration)
-  g_launches.fetch_add((long long)(max_it - 1) * R.launches);
-  cudaGraphExecDestroy(gexec);
-  scatter_rows(z.p, H.perm.p, n, nC, z_out, s);
-  if (mu_out) scatter_rows(mu.p, H.perm.p, n, nC, mu_out, s);
+  if (gexec) cudaGraphExecDestroy(gexec);
+  {
+    DevBuf<double> zf((size_t)N * nC);
+    gather_points(H, z.p, nC, zf.p, s);
+    scatter_rows(zf.p, H.perm.p, N, nC, z_out, s);
+    if (mu_out) {
+      gather_points(H, mu.p, nC, zf.p, s);
+      scatter_rows(zf.p, H.perm.p, N, nC, mu_out, s);
+    }
+    CUDA_CHECK(cudaStreamSynchronize(s));
+  }
   // ---- bias + objective (one HSS mat-vec with 2 nC columns)
   if (bias_out || obj_out) {
     EventTimer tb(s);
     const double eps_rel = (opt && opt->margin_eps_rel > 0) ? opt->margin_eps_rel : 1e-8;
-    DevBuf<double> cnt(2 * nC);
-    margin_count_kernel<<<nC, 256, 0, s>>>(n, nC, z.p, dC.p, eps_rel, cnt.p);
+    margin_count_kernel<<<nleaf, 256, 0, s>>>(H.leaf_lo.p, nC, z.p, dC.p, eps_rel, part.p);
     LAUNCH_CHECK();
     std::vector<double> hc(2 * nC);
-    d2h(hc.data(), cnt.p, 2 * nC, s);
-    CUDA_CHECK(cudaStreamSynchronize(s));
+    tree_reduce_all(H, part.p, 2 * nC, hc.data(), s);
     std::vector<int> mode(nC);
     std::vector<double> msize(nC);
     for (int c = 0; c < nC; ++c) {
@@ -258,15 +561,15 @@ AdmmResult admm_train_impl(const ULVImpl& F, const double* y_orig, const std::ve
       else { mode[c] = 2; msize[c] = 0; }
     }
     auto dmode = upload(mode, s);
-    DevBuf<double> V((size_t)n * 2 * nC), KV((size_t)n * 2 * nC), sums(4 * nC);
-    bias_rhs_kernel<<<ceil_div(n * nC, 256), 256, 0, s>>>(n, nC, z.p, y.p, dC.p, dmode.p, eps_rel, V.p);
+    DevBuf<double> V((size_t)std::max<int64_t>(1, n) * 2 * nC), KV((size_t)std::max<int64_t>(1, n) * 2 * nC);
+    bias_rhs_kernel<<<ceil_div(std::max<int64_t>(1, n * nC), 256), 256, 0, s>>>(n, nC, z.p, y.p, dC.p, dmode.p,
+                                                                                eps_rel, V.p);
     LAUNCH_CHECK();
     hss_matvec_tree(H, V.p, KV.p, 2 * nC, s);
-    bias_sums_kernel<<<nC, 256, 0, s>>>(n, nC, V.p, KV.p, y.p, z.p, sums.p);
+    bias_sums_kernel<<<nleaf, 256, 0, s>>>(H.leaf_lo.p, nC, V.p, KV.p, y.p, z.p, part.p);
     LAUNCH_CHECK();
     std::vector<double> hs(4 * nC);
-    d2h(hs.data(), sums.p, 4 * nC, s);
-    CUDA_CHECK(cudaStreamSynchronize(s));
+    tree_reduce_all(H, part.p, 4 * nC, hs.data(), s);
     for (int c = 0; c < nC; ++c) {
       if (bias_out) bias_out[c] = (msize[c] > 0) ? (hs[4 * c] - hs[4 * c + 1]) / msize[c] : 0.0;
       if (obj_out) obj_out[c] = 0.5 * hs[4 * c + 2] - hs[4 * c + 3];

@@ -28,9 +28,9 @@ static void ensure_device() {
 }
 
 template <typename Fn>
-static int guarded(Fn&& fn) {
+static int guarded(Fn&& fn, bool need_device = true) {
   try {
-    ensure_device();
+    if (need_device) ensure_device();
     fn();
     return HSS_OK;
   } catch (const Error& e) {
@@ -44,6 +44,13 @@ static int guarded(Fn&& fn) {
     set_last_error(e.what());
     return HSS_ECUDA;
   }
+}
+
+// node (l, i) has its generators on this rank (always true on one GPU)
+static bool held(const HSSImpl& H, int l, int i) {
+  if (l < H.sh.lg) return true;
+  if (H.sh.on() && l == H.sh.lg) return true;  // exchanged: k and skeletons known everywhere
+  return i >= H.sh.first(l) && i < H.sh.last(l);
 }
 
 static void release_hss(HSSImpl* H) {
@@ -70,6 +77,11 @@ using namespace svmhss;
 
 struct hss_s { HSSImpl* impl; };
 struct ulv_s { ULVImpl* impl; };
+struct hss_comm_s { std::shared_ptr<Comm> c; };
+
+static std::shared_ptr<Comm> comm_of(const hss_opts* o) {
+  return (o && o->comm) ? o->comm->c : std::shared_ptr<Comm>();
+}
 
 extern "C" {
 
@@ -85,7 +97,7 @@ int hss_build(const double* F, int64_t n, int32_t r, double h, const hss_opts* o
     validate_opts(opt, n, r, h);
     auto* H = new HSSImpl();
     try {
-      hss_build_impl(*H, F, n, r, h, *opt, (cudaStream_t)stream);
+      hss_build_impl(*H, F, n, r, h, *opt, comm_of(opt), (cudaStream_t)stream);
     } catch (...) {
       delete H;
       throw;
@@ -106,13 +118,14 @@ int hss_info(hss_t Hh, hss_stats* st, int64_t* perm_out, int32_t* ranks_out, int
       const int nn = (1 << (H.L + 1)) - 1;
       for (int t = 0; t < nn; ++t) ranks_out[t] = -1;
       for (int l = 1; l <= H.L; ++l)
-        for (size_t i = 0; i < H.lv[l].size(); ++i) ranks_out[H.node_id(l, (int)i)] = H.lv[l][i].k;
+        for (size_t i = 0; i < H.lv[l].size(); ++i)
+          ranks_out[H.node_id(l, (int)i)] = held(H, l, (int)i) ? H.lv[l][i].k : -2;
     }
     if (skel_out) {
       int64_t off = 0;
-      for (int l = 0; l <= H.L; ++l)
+      for (int l = 1; l <= H.L; ++l)
         for (size_t i = 0; i < H.lv[l].size(); ++i) {
-          if (l == 0) continue;
+          if (!held(H, l, (int)i)) continue;
           const auto& nd = H.lv[l][i];
           if (nd.k > 0)
             CUDA_CHECK(cudaMemcpy(skel_out + off, H.J[l].p + nd.koff, nd.k * sizeof(int64_t), cudaMemcpyDeviceToHost));
@@ -131,6 +144,8 @@ int hss_node(hss_t Hh, int32_t node, int32_t* rows, int32_t* k, double* U, doubl
     int l = 0;
     while (((1 << (l + 1)) - 1) <= node) ++l;
     const int i = node - ((1 << l) - 1);
+    require(held(H, l, i) && (l != H.sh.lg || !H.sh.on() || i == H.sh.g),
+            "hss_node: node is held by another rank");
     const NodeInfo& nd = H.lv[l][i];
     if (rows) *rows = nd.rows;
     if (k) *k = (l == 0) ? -1 : nd.k;
@@ -161,10 +176,13 @@ int hss_matvec(hss_t Hh, const double* v, double* out, int32_t nrhs, void* strea
     require(nrhs >= 1, "hss_matvec: nrhs must be >= 1");
     const HSSImpl& H = *Hh->impl;
     cudaStream_t s = (cudaStream_t)stream;
-    DevBuf<double> a((size_t)H.n * nrhs), b((size_t)H.n * nrhs);
-    gather_rows(v, H.perm.p, H.n, nrhs, a.p, s);
+    const int64_t nl = H.nloc();
+    DevBuf<double> a((size_t)std::max<int64_t>(1, nl) * nrhs), b((size_t)std::max<int64_t>(1, nl) * nrhs),
+        full((size_t)H.n * nrhs);
+    gather_rows(v, H.perm.p + H.lo_g, nl, nrhs, a.p, s);
     hss_matvec_tree(H, a.p, b.p, nrhs, s);
-    scatter_rows(b.p, H.perm.p, H.n, nrhs, out, s);
+    gather_points(H, b.p, nrhs, full.p, s);
+    scatter_rows(full.p, H.perm.p, H.n, nrhs, out, s);
     CUDA_CHECK(cudaStreamSynchronize(s));
   });
 }
@@ -206,9 +224,12 @@ int ulv_solve(ulv_t Uh, const double* b, double* x, int32_t nrhs, void* stream) 
     cudaStream_t s = (cudaStream_t)stream;
     SolveWS ws;
     solve_ws_alloc(F, nrhs, ws);
-    gather_rows(b, H.perm.p, H.n, nrhs, ws.fin[H.L], s);
+    DevBuf<double> full((size_t)H.n * nrhs);
+    gather_rows(b, H.perm.p + H.lo_g, H.nloc(), nrhs, ws.fin[H.L], s);
+    CUDA_CHECK(cudaStreamSynchronize(s));  // b and x may alias
     ulv_solve_tree(F, ws, s);
-    scatter_rows(ws.xout[H.L], H.perm.p, H.n, nrhs, x, s);
+    gather_points(H, ws.xout[H.L], nrhs, full.p, s);
+    scatter_rows(full.p, H.perm.p, H.n, nrhs, x, s);
     CUDA_CHECK(cudaStreamSynchronize(s));
   });
 }
@@ -277,7 +298,7 @@ int svm_train_predict_host(const double* F, const double* y, int64_t n, int32_t 
     CUDA_CHECK(cudaEventRecord(ev[1], s));
     HSSImpl* H = new HSSImpl();
     struct HG { HSSImpl* h; ~HG() { release_hss(h); } } hg{H};
-    hss_build_impl(*H, dF.p, n, r, h, *opt, s);
+    hss_build_impl(*H, dF.p, n, r, h, *opt, comm_of(opt), s);
     CUDA_CHECK(cudaEventRecord(ev[2], s));
     ULVImpl Fz;
     Fz.H = H;
@@ -404,6 +425,31 @@ int hss_kernel_block(const double* Fa, int64_t na, const double* Fb, int64_t nb,
     CUDA_CHECK(cudaStreamSynchronize(s));
   });
 }
+
+int hss_comm_nccl_id(void* unique_id_out) {
+  return guarded([&] {
+    require(unique_id_out != nullptr, "hss_comm_nccl_id: NULL pointer");
+    nccl_unique_id(unique_id_out);
+  });
+}
+
+int hss_comm_init_nccl(int32_t nranks, int32_t rank, const void* unique_id, hss_comm_t* out) {
+  return guarded([&] {
+    require(out && unique_id, "hss_comm_init_nccl: NULL pointer");
+    require(nranks >= 1 && rank >= 0 && rank < nranks, "hss_comm_init_nccl: bad rank / nranks");
+    *out = new hss_comm_s{make_nccl_comm(nranks, rank, unique_id)};
+  });
+}
+
+int hss_comm_init_host(int32_t nranks, int32_t rank, hss_allgather_fn fn, void* ctx, hss_comm_t* out) {
+  return guarded([&] {
+    require(out && fn, "hss_comm_init_host: NULL pointer");
+    require(nranks >= 1 && rank >= 0 && rank < nranks, "hss_comm_init_host: bad rank / nranks");
+    *out = new hss_comm_s{make_host_comm(nranks, rank, fn, ctx)};
+  }, /*need_device=*/false);
+}
+
+void hss_comm_free(hss_comm_t c) { delete c; }
 
 void hss_free(hss_t H) {
   if (!H) return;

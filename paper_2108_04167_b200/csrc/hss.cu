@@ -11,6 +11,7 @@
 // Because children are consecutive in BFS order, the k-packed outputs of level l are exactly
 // the row-packed inputs of level l-1 (rows of a parent = [J_left; J_right]), so no copies
 // are needed to assemble a parent's Y, Omega^ and active rows.
+#include <cstring>
 #include "internal.cuh"
 
 namespace svmhss {
@@ -56,8 +57,20 @@ __global__ void select_kernel(const SelNode* __restrict__ nd, const int* __restr
   }
 }
 
+__global__ void iota_off_kernel64(int64_t* a, int64_t n, int64_t off) {
+  const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (i < n) a[i] = off + i;
+}
+
+// Build-time exchange record of one rank's subtree root (level lg), followed in the slot by
+// J (S int64), Y_sk (S x S) and Omega' (S x S).
+struct RootRec {
+  int64_t k, rows, pt, cap_hit;
+  int64_t sub_cap_hits, sub_pt, sub_maxk, sub_bytes;  // this rank's subtree (levels >= lg)
+};
+
 void hss_build_impl(HSSImpl& H, const double* F, int64_t n, int r, double h, const hss_opts& o,
-                    cudaStream_t s) {
+                    std::shared_ptr<Comm> comm, cudaStream_t s) {
   H.n = n;
   H.r = r;
   H.rp = (r + 3) / 4 * 4;
@@ -66,6 +79,16 @@ void hss_build_impl(HSSImpl& H, const double* F, int64_t n, int r, double h, con
   H.s = o.max_rank + o.oversample;
   H.L = num_levels(n, H.m);
   const int rp = H.rp, S = H.s, L = H.L;
+  // ---- shard plan: rank g owns node g of level lg = log2 P
+  Shard& sh = H.sh;
+  sh.comm = comm;
+  sh.P = comm ? comm->size : 1;
+  sh.g = comm ? comm->rank : 0;
+  sh.lg = 0;
+  while ((1 << sh.lg) < sh.P) ++sh.lg;
+  require((1 << sh.lg) == sh.P, "hss_build: the number of ranks must be a power of two");
+  require(sh.lg <= L, "hss_build: more ranks than leaves (need P <= 2^L, L = ceil(log2(n/leaf_size)))");
+  const int lg = sh.lg;
   std::vector<std::vector<std::pair<int64_t, int64_t>>> rg;
   node_ranges(n, L, rg);
   H.lv.assign(L + 1, {});
@@ -73,10 +96,24 @@ void hss_build_impl(HSSImpl& H, const double* F, int64_t n, int r, double h, con
     H.lv[l].resize(rg[l].size());
     for (size_t i = 0; i < rg[l].size(); ++i) { H.lv[l][i].lo = rg[l][i].first; H.lv[l][i].hi = rg[l][i].second; }
   }
+  H.lo_g = rg[lg][sh.g].first;
+  H.hi_g = rg[lg][sh.g].second;
+  {
+    std::vector<int64_t> lo(sh.P), cnt(sh.P);
+    H.nmax_g = 0;
+    for (int p = 0; p < sh.P; ++p) {
+      lo[p] = rg[lg][p].first;
+      cnt[p] = rg[lg][p].second - rg[lg][p].first;
+      H.nmax_g = std::max(H.nmax_g, cnt[p]);
+    }
+    H.rank_lo = upload(lo, s);
+    H.rank_cnt = upload(cnt, s);
+  }
+  const int64_t nl = H.nloc();
   H.st = hss_stats{};
   H.st.n = n; H.st.r = r; H.st.L = L; H.st.s = S; H.st.leaf_size = H.m;
 
-  // ---- T1-T4: tree
+  // ---- T1-T4: tree (every rank builds the whole tree: deterministic, identical)
   {
     EventTimer tm(s);
     DevBuf<double> Fpad((size_t)n * rp);
@@ -94,21 +131,27 @@ void hss_build_impl(HSSImpl& H, const double* F, int64_t n, int r, double h, con
       for (int64_t p = rg[L][i].first; p < rg[L][i].second; ++p) lof[p] = (int)i;
     lof.resize(n + kLeafPad, -3);
     H.leaf_of = upload(lof, s);
+    // per-leaf local offsets of this rank's leaves (cluster-tree-ordered reductions)
+    std::vector<int64_t> llo;
+    for (int i = sh.first(L); i < sh.last(L); ++i) llo.push_back(rg[L][i].first - H.lo_g);
+    llo.push_back(nl);
+    H.leaf_lo = upload(llo, s);
     H.st.ms_tree = tm.stop_ms();
   }
-  // ---- leaves: D_t = K(I_t, I_t) (H2)
+  // ---- leaves this rank holds: D_t = K(I_t, I_t) (H2)
   {
     auto& lvL = H.lv[L];
     std::vector<KblkProb> kp;
     int64_t off = 0;
-    for (auto& nd : lvL) {
+    for (int i = sh.first(L); i < sh.last(L); ++i) {
+      auto& nd = lvL[i];
       nd.doff = off;
       const int mloc = (int)(nd.hi - nd.lo);
       kp.push_back({mloc, mloc, nullptr, nd.lo, nullptr, nd.lo, nullptr, mloc, 0.0});
       off += (int64_t)mloc * mloc;
     }
     H.D.alloc(off);
-    for (size_t i = 0; i < lvL.size(); ++i) kp[i].out = H.D.p + lvL[i].doff;
+    for (size_t q = 0; q < kp.size(); ++q) kp[q].out = H.D.p + lvL[sh.first(L) + q].doff;
     kernel_blocks(H.Fp.p, rp, r, h, kp, s);
   }
   H.U.clear(); H.J.clear(); H.B.clear();
@@ -119,8 +162,9 @@ void hss_build_impl(HSSImpl& H, const double* F, int64_t n, int r, double h, con
     CUDA_CHECK(cudaStreamSynchronize(s));
     return;
   }
-  // ---- R1-R3: Omega_p, H1: masked sketch (diagonal leaf blocks excluded -> Y_leaf directly)
-  DevBuf<double> Om((size_t)n * S), Y((size_t)n * S);
+  // ---- R1-R3: Omega_p (all n rows: the sketch's right-hand matrix), H1: this rank's rows of
+  // the masked sketch (diagonal leaf blocks excluded -> Y_leaf directly)
+  DevBuf<double> Om((size_t)n * S), Y((size_t)std::max<int64_t>(1, nl) * S);
   {
     EventTimer tm(s);
     omega_rows(o.omega_seed, H.perm.p, n, S, Om.p, s);
@@ -129,28 +173,31 @@ void hss_build_impl(HSSImpl& H, const double* F, int64_t n, int r, double h, con
   {
     EventTimer tm(s);
     KmmArgs a{};
-    a.Fa = H.Fp.p; a.nua = H.nu.p; a.na = n;
+    a.Fa = H.Fp.p + H.lo_g * rp; a.nua = H.nu.p + H.lo_g; a.na = nl;
     a.Fb = H.Fp.p; a.nub = H.nu.p; a.nb = n;
     a.rp = rp; a.W = Om.p; a.ldw = S; a.ncols = S; a.S = Y.p; a.lds = S;
     a.neg_inv_2h2 = -1.0 / (2.0 * h * h);
     a.same_set = 1;
-    a.leaf_a = H.leaf_of.p; a.leaf_b = H.leaf_of.p;
+    a.diag_off = H.lo_g;
+    a.leaf_a = H.leaf_of.p + H.lo_g; a.leaf_b = H.leaf_of.p;
     kernel_matmul(a, s);
     H.st.ms_sketch = tm.stop_ms();
   }
   EventTimer tmc(s);
-  DevBuf<int64_t> act0(n);
-  iota_kernel64<<<ceil_div(n, 256), 256, 0, s>>>(act0.p, n);
+  DevBuf<int64_t> act0(std::max<int64_t>(1, nl));
+  iota_off_kernel64<<<ceil_div(std::max<int64_t>(1, nl), 256), 256, 0, s>>>(act0.p, nl, H.lo_g);
   LAUNCH_CHECK();
   const int64_t* act = act0.p;
-  DevBuf<double> Ycur = std::move(Y), Omcur = std::move(Om);
-  const int nnodes_all = (1 << (L + 1)) - 1;
-  int cap_hits = 0, maxk = 0, npt = 0;
+  DevBuf<double> Ycur = std::move(Y), Omhold;
+  const double* omcur = Om.p + H.lo_g * S;  // Omega^ of the leaves = this rank's Omega rows
+  int cap_hits = 0, maxk = 0, npt = 0;        // levels < lg (replicated) counted once
+  int64_t sub_bytes = (int64_t)H.D.bytes(), top_bytes = 0;
+  int sub_cap = 0, sub_pt = 0, sub_maxk = 0;  // this rank's subtree (levels >= lg)
   for (int l = L; l >= 1; --l) {
     auto& lv = H.lv[l];
-    const int nn = (int)lv.size();
+    const int f = sh.first(l), e = sh.last(l), nn = e - f;
     int64_t sumR = 0;
-    for (int i = 0; i < nn; ++i) {
+    for (int i = f; i < e; ++i) {
       auto& nd = lv[i];
       if (l == L) nd.rows = (int)(nd.hi - nd.lo);
       else nd.rows = H.lv[l + 1][2 * i].k + H.lv[l + 1][2 * i + 1].k;
@@ -159,23 +206,19 @@ void hss_build_impl(HSSImpl& H, const double* F, int64_t n, int r, double h, con
     }
     // ranks: fixed (known) or adaptive (CPQR decides)
     std::vector<int> kfix(nn, -1);
-    if (o.ranks) {
-      for (int i = 0; i < nn; ++i) {
-        const int t = H.node_id(l, i);
-        (void)nnodes_all;
-        kfix[i] = std::max(0, std::min(std::min(o.ranks[t], lv[i].rows), S));
-      }
-    }
-    DevBuf<double> Wk((size_t)sumR * S);
+    if (o.ranks)
+      for (int q = 0; q < nn; ++q)
+        kfix[q] = std::max(0, std::min(std::min(o.ranks[H.node_id(l, f + q)], lv[f + q].rows), S));
+    DevBuf<double> Wk((size_t)std::max<int64_t>(1, sumR) * S);
     CUDA_CHECK(cudaMemcpyAsync(Wk.p, Ycur.p, (size_t)sumR * S * sizeof(double), cudaMemcpyDeviceToDevice, s));
     DevBuf<int> piv(std::max<int64_t>(1, sumR)), kd(nn), ch(nn);
     CUDA_CHECK(cudaMemsetAsync(ch.p, 0, nn * sizeof(int), s));
     std::vector<CpqrProb> cp;
-    for (int i = 0; i < nn; ++i) {
-      auto& nd = lv[i];
-      if (kfix[i] >= 0 && kfix[i] == nd.rows) continue;  // known pass-through
+    for (int q = 0; q < nn; ++q) {
+      auto& nd = lv[f + q];
+      if (kfix[q] >= 0 && kfix[q] == nd.rows) continue;  // known pass-through
       if (nd.rows == 0) continue;
-      cp.push_back({nd.rows, S, Wk.p + nd.roff * S, piv.p + nd.roff, kfix[i], kd.p + i, ch.p + i});
+      cp.push_back({nd.rows, S, Wk.p + nd.roff * S, piv.p + nd.roff, kfix[q], kd.p + q, ch.p + q});
     }
     bcpqr(cp, o.rel_tol, o.abs_tol, o.max_rank, s);
     std::vector<int> kh(nn, 0), chh(nn, 0);
@@ -183,15 +226,19 @@ void hss_build_impl(HSSImpl& H, const double* F, int64_t n, int r, double h, con
     d2h(chh.data(), ch.p, nn, s);
     CUDA_CHECK(cudaStreamSynchronize(s));
     int64_t sumK = 0, sumU = 0;
-    for (int i = 0; i < nn; ++i) {
-      auto& nd = lv[i];
-      if ((kfix[i] >= 0 && kfix[i] == nd.rows) || nd.rows == 0) nd.k = nd.rows;
-      else nd.k = kh[i];
+    for (int q = 0; q < nn; ++q) {
+      auto& nd = lv[f + q];
+      if ((kfix[q] >= 0 && kfix[q] == nd.rows) || nd.rows == 0) nd.k = nd.rows;
+      else nd.k = kh[q];
       nd.pt = (nd.k == nd.rows);
-      nd.cap_hit = chh[i];
-      cap_hits += chh[i];
-      maxk = std::max(maxk, nd.k);
-      npt += nd.pt ? 1 : 0;
+      nd.cap_hit = chh[q];
+      if (l >= lg) {
+        sub_cap += chh[q]; sub_maxk = std::max(sub_maxk, nd.k); sub_pt += nd.pt ? 1 : 0;
+        if (!nd.pt) sub_bytes += 8LL * nd.rows * nd.k;
+      } else {
+        cap_hits += chh[q]; maxk = std::max(maxk, nd.k); npt += nd.pt ? 1 : 0;
+        if (!nd.pt) top_bytes += 8LL * nd.rows * nd.k;
+      }
       nd.koff = sumK;
       sumK += nd.k;
       nd.uoff = sumU;
@@ -199,44 +246,110 @@ void hss_build_impl(HSSImpl& H, const double* F, int64_t n, int r, double h, con
     }
     // T = R11^-1 R12 (upper triangular solve, in place in Wk)
     std::vector<TrsmProb> tp;
-    for (auto& nd : lv)
+    for (int i = f; i < e; ++i) {
+      auto& nd = lv[i];
       if (!nd.pt && nd.k > 0 && nd.rows > nd.k)
         tp.push_back({nd.k, nd.rows - nd.k, Wk.p + nd.roff * S, 1, S, Wk.p + (nd.roff + nd.k) * S, 1, S});
+    }
     btrsm(tp, false, s);
     H.U[l].alloc(std::max<int64_t>(1, sumU));
     H.J[l].alloc(std::max<int64_t>(1, sumK));
     DevBuf<double> Ysk((size_t)std::max<int64_t>(1, sumK) * S), Omp((size_t)std::max<int64_t>(1, sumK) * S);
     std::vector<SelNode> sn(nn);
-    for (int i = 0; i < nn; ++i) sn[i] = {lv[i].roff, lv[i].koff, lv[i].uoff, lv[i].rows, lv[i].k, lv[i].pt ? 1 : 0, 0};
+    for (int q = 0; q < nn; ++q) {
+      auto& nd = lv[f + q];
+      sn[q] = {nd.roff, nd.koff, nd.uoff, nd.rows, nd.k, nd.pt ? 1 : 0, 0};
+    }
     auto dsn = upload(sn, s);
     scatter_u_kernel<<<nn, 256, 0, s>>>(dsn.p, piv.p, Wk.p, S, H.U[l].p);
     LAUNCH_CHECK();
-    select_kernel<<<nn, 256, 0, s>>>(dsn.p, piv.p, act, Ycur.p, Omcur.p, S, H.J[l].p, Ysk.p, Omp.p);
+    select_kernel<<<nn, 256, 0, s>>>(dsn.p, piv.p, act, Ycur.p, omcur, S, H.J[l].p, Ysk.p, Omp.p);
     LAUNCH_CHECK();
     // Omega'_t = U_t^T Omega^_t
     std::vector<GemmProb> gp;
-    for (auto& nd : lv)
+    for (int i = f; i < e; ++i) {
+      auto& nd = lv[i];
       if (!nd.pt && nd.k > 0)
-        gp.push_back({nd.k, S, nd.rows, H.U[l].p + nd.uoff, 1, nd.k, Omcur.p + nd.roff * S, S, 1,
+        gp.push_back({nd.k, S, nd.rows, H.U[l].p + nd.uoff, 1, nd.k, omcur + nd.roff * S, S, 1,
                       Omp.p + nd.koff * S, S, 1, 1.0, 0.0});
+    }
     bgemm(gp, s);
+    if (l == lg && sh.on()) {
+      // ---- exchange the subtree roots: k, J, Y_sk, Omega' of every rank's level-lg node
+      const auto& own = lv[sh.g];
+      const int64_t hdr = (sizeof(RootRec) + 7) / 8, slot = hdr + S + 2LL * S * S;
+      DevBuf<double> send(slot), recv(slot * sh.P);
+      RootRec rec{own.k, own.rows, own.pt ? 1 : 0, own.cap_hit, sub_cap, sub_pt, sub_maxk, sub_bytes};
+      std::vector<double> hh(hdr, 0.0);
+      std::memcpy(hh.data(), &rec, sizeof(rec));
+      h2d(send.p, hh.data(), hdr, s);
+      if (own.k > 0) {
+        CUDA_CHECK(cudaMemcpyAsync(send.p + hdr, H.J[l].p, own.k * 8, cudaMemcpyDeviceToDevice, s));
+        CUDA_CHECK(cudaMemcpyAsync(send.p + hdr + S, Ysk.p, (size_t)own.k * S * 8, cudaMemcpyDeviceToDevice, s));
+        CUDA_CHECK(cudaMemcpyAsync(send.p + hdr + S + (int64_t)S * S, Omp.p, (size_t)own.k * S * 8,
+                                   cudaMemcpyDeviceToDevice, s));
+      }
+      sh.comm->allgather(send.p, recv.p, slot * 8, s);
+      std::vector<double> hr((size_t)sh.P * hdr);
+      for (int p = 0; p < sh.P; ++p) d2h(hr.data() + (size_t)p * hdr, recv.p + p * slot, hdr, s);
+      CUDA_CHECK(cudaStreamSynchronize(s));
+      int64_t gK = 0;
+      std::vector<int64_t> koffs(sh.P), ks(sh.P);
+      sub_cap = sub_pt = sub_maxk = 0;
+      int64_t all_sub_bytes = 0;
+      for (int p = 0; p < sh.P; ++p) {
+        RootRec rp_;
+        std::memcpy(&rp_, hr.data() + (size_t)p * hdr, sizeof(rp_));
+        auto& nd = lv[p];
+        nd.k = (int)rp_.k; nd.rows = (int)rp_.rows; nd.pt = rp_.pt != 0; nd.cap_hit = (int)rp_.cap_hit;
+        nd.koff = gK;
+        koffs[p] = gK; ks[p] = nd.k;
+        gK += nd.k;
+        sub_cap += (int)rp_.sub_cap_hits; sub_pt += (int)rp_.sub_pt;
+        sub_maxk = std::max<int>(sub_maxk, (int)rp_.sub_maxk);
+        all_sub_bytes += rp_.sub_bytes;
+        H.kmax_lg = std::max(H.kmax_lg, nd.k);
+      }
+      sub_bytes = all_sub_bytes;
+      H.lg_koff = upload(koffs, s);
+      H.lg_k = upload(ks, s);
+      DevBuf<int64_t> Jall(std::max<int64_t>(1, gK));
+      DevBuf<double> Yall((size_t)std::max<int64_t>(1, gK) * S), Oall((size_t)std::max<int64_t>(1, gK) * S);
+      for (int p = 0; p < sh.P; ++p) {
+        const int64_t k = ks[p];
+        if (!k) continue;
+        const double* src = recv.p + p * slot;
+        CUDA_CHECK(cudaMemcpyAsync(Jall.p + koffs[p], src + hdr, k * 8, cudaMemcpyDeviceToDevice, s));
+        CUDA_CHECK(cudaMemcpyAsync(Yall.p + koffs[p] * S, src + hdr + S, (size_t)k * S * 8, cudaMemcpyDeviceToDevice, s));
+        CUDA_CHECK(cudaMemcpyAsync(Oall.p + koffs[p] * S, src + hdr + S + (int64_t)S * S, (size_t)k * S * 8,
+                                   cudaMemcpyDeviceToDevice, s));
+      }
+      CUDA_CHECK(cudaStreamSynchronize(s));
+      H.J[l] = std::move(Jall);
+      Ysk = std::move(Yall);
+      Omp = std::move(Oall);
+    }
     // parents at level l-1: B = K(J_a, J_b); sibling update of Y_sk (H4)
     auto& pv = H.lv[l - 1];
+    const int pf = sh.first(l - 1), pe = sh.last(l - 1);
     int64_t sumB = 0;
-    for (size_t p = 0; p < pv.size(); ++p) {
+    for (int p = pf; p < pe; ++p) {
       pv[p].boff = sumB;
-      sumB += (int64_t)lv[2 * p].k * lv[2 * p + 1].k;
+      const int64_t bb = (int64_t)lv[2 * p].k * lv[2 * p + 1].k;
+      sumB += bb;
+      if (l - 1 >= lg) sub_bytes += 8 * bb;
+      else top_bytes += 8 * bb;
     }
     H.B[l - 1].alloc(std::max<int64_t>(1, sumB));
     std::vector<KblkProb> kb;
-    for (size_t p = 0; p < pv.size(); ++p) {
+    for (int p = pf; p < pe; ++p) {
       auto &a = lv[2 * p], &b = lv[2 * p + 1];
       kb.push_back({a.k, b.k, H.J[l].p + a.koff, 0, H.J[l].p + b.koff, 0, H.B[l - 1].p + pv[p].boff, b.k, 0.0});
     }
     kernel_blocks(H.Fp.p, rp, r, h, kb, s);
     if (l - 1 >= 1) {
       std::vector<GemmProb> up;
-      for (size_t p = 0; p < pv.size(); ++p) {
+      for (int p = pf; p < pe; ++p) {
         auto &a = lv[2 * p], &b = lv[2 * p + 1];
         const double* Bp = H.B[l - 1].p + pv[p].boff;
         if (a.k > 0 && b.k > 0) {
@@ -249,27 +362,33 @@ void hss_build_impl(HSSImpl& H, const double* F, int64_t n, int r, double h, con
     CUDA_CHECK(cudaStreamSynchronize(s));  // host-side descriptors / Wk lifetime
     act = H.J[l].p;
     Ycur = std::move(Ysk);
-    Omcur = std::move(Omp);
+    Omhold = std::move(Omp);
+    omcur = Omhold.p;
+    if (l == L) Om.release();
   }
   H.lv[0][0].rows = H.lv[1][0].k + H.lv[1][1].k;
   H.st.ms_compress = tmc.stop_ms();
-  H.st.cap_hits = cap_hits;
-  H.st.max_rank_used = maxk;
-  H.st.passthrough = npt;
-  int64_t gb = (int64_t)H.D.bytes();
-  for (int l = 0; l <= L; ++l) {
-    for (auto& nd : H.lv[l]) if (l >= 1 && !nd.pt) gb += 8LL * nd.rows * nd.k;
-    if (l < L)
-      for (size_t p = 0; p < H.lv[l].size(); ++p)
-        gb += 8LL * H.lv[l + 1][2 * p].k * H.lv[l + 1][2 * p + 1].k;
-  }
-  H.st.generator_bytes = gb;
+  H.st.cap_hits = cap_hits + sub_cap;
+  H.st.max_rank_used = std::max(maxk, sub_maxk);
+  H.st.passthrough = npt + sub_pt;
+  H.st.generator_bytes = sub_bytes + top_bytes;
   CUDA_CHECK(cudaStreamSynchronize(s));
 }
 
 // ------------------------------------------------------------------ mat-vec (M)
+// Sum of k over the nodes of level l this rank holds k-packed vectors for (all P nodes at the
+// exchanged level lg when sharded).
+int64_t level_sumk(const HSSImpl& H, int l) {
+  int f = H.sh.first(l), e = H.sh.last(l);
+  if (H.sh.on() && l == H.sh.lg) { f = 0; e = H.sh.P; }
+  int64_t sk = 0;
+  for (int i = f; i < e; ++i) sk += H.lv[l][i].k;
+  return sk;
+}
+
 void hss_matvec_tree(const HSSImpl& H, const double* V, double* out, int nrhs, cudaStream_t s) {
   const int L = H.L;
+  const Shard& sh = H.sh;
   if (L == 0) {
     const int n = (int)H.n;
     bgemm({{n, nrhs, n, H.D.p, n, 1, V, nrhs, 1, out, nrhs, 1, 1.0, 0.0}}, s);
@@ -277,18 +396,20 @@ void hss_matvec_tree(const HSSImpl& H, const double* V, double* out, int nrhs, c
   }
   std::vector<DevBuf<double>> up(L + 1), dn(L + 1);
   for (int l = 1; l <= L; ++l) {
-    int64_t sk = 0;
-    for (auto& nd : H.lv[l]) sk += nd.k;
+    const int64_t sk = level_sumk(H, l);
     up[l].alloc(std::max<int64_t>(1, sk) * nrhs);
     dn[l].alloc(std::max<int64_t>(1, sk) * nrhs);
   }
+  ExchWS xw;
+  if (sh.on()) exch_ws_alloc(H, nrhs, 0, xw);
   // upward: up_t = U_t^T [V(I_t) | up_children]
   for (int l = L; l >= 1; --l) {
     const double* in = (l == L) ? V : up[l + 1].p;
     std::vector<GemmProb> gp;
     std::vector<CopyProb> cp;
-    for (auto& nd : H.lv[l]) {
-      const int64_t ro = (l == L) ? nd.lo : nd.roff;
+    for (int i = sh.first(l); i < sh.last(l); ++i) {
+      const auto& nd = H.lv[l][i];
+      const int64_t ro = (l == L) ? nd.lo - H.lo_g : nd.roff;
       if (nd.pt) cp.push_back({nd.rows, nrhs, in + ro * nrhs, nrhs, up[l].p + nd.koff * nrhs, nrhs, 0});
       else if (nd.k > 0)
         gp.push_back({nd.k, nrhs, nd.rows, H.U[l].p + nd.uoff, 1, nd.k, in + ro * nrhs, nrhs, 1,
@@ -296,6 +417,7 @@ void hss_matvec_tree(const HSSImpl& H, const double* V, double* out, int nrhs, c
     }
     bcopy(cp, s);
     bgemm(gp, s);
+    if (l == sh.lg && sh.on()) exchange_lg(H, xw, up[l].p, nullptr, nullptr, s);
   }
   // downward: children of t get U_t g_t (split) + sibling couplings B up_sibling
   for (int l = 0; l < L; ++l) {
@@ -303,7 +425,7 @@ void hss_matvec_tree(const HSSImpl& H, const double* V, double* out, int nrhs, c
     auto& cv = H.lv[l + 1];
     std::vector<GemmProb> gp;
     std::vector<CopyProb> cp;
-    for (size_t p = 0; p < pv.size(); ++p) {
+    for (int p = sh.first(l); p < sh.last(l); ++p) {
       auto& nd = pv[p];
       auto &a = cv[2 * p], &b = cv[2 * p + 1];
       double* dst = dn[l + 1].p + a.koff * nrhs;  // a.koff .. b.koff + b.k contiguous
@@ -322,7 +444,7 @@ void hss_matvec_tree(const HSSImpl& H, const double* V, double* out, int nrhs, c
     bcopy(cp, s);
     bgemm(gp, s);
     std::vector<GemmProb> g2;
-    for (size_t p = 0; p < pv.size(); ++p) {
+    for (int p = sh.first(l); p < sh.last(l); ++p) {
       auto &a = cv[2 * p], &b = cv[2 * p + 1];
       const double* Bp = H.B[l].p + pv[p].boff;
       if (a.k > 0 && b.k > 0) {
@@ -337,18 +459,22 @@ void hss_matvec_tree(const HSSImpl& H, const double* V, double* out, int nrhs, c
   // leaves: out = D V + U g
   std::vector<GemmProb> gp;
   std::vector<CopyProb> cp;
-  for (auto& nd : H.lv[L]) {
+  for (int i = sh.first(L); i < sh.last(L); ++i) {
+    const auto& nd = H.lv[L][i];
     const int mloc = (int)(nd.hi - nd.lo);
-    gp.push_back({mloc, nrhs, mloc, H.D.p + nd.doff, mloc, 1, V + nd.lo * nrhs, nrhs, 1,
-                  out + nd.lo * nrhs, nrhs, 1, 1.0, 0.0});
+    const int64_t lo = nd.lo - H.lo_g;
+    gp.push_back({mloc, nrhs, mloc, H.D.p + nd.doff, mloc, 1, V + lo * nrhs, nrhs, 1,
+                  out + lo * nrhs, nrhs, 1, 1.0, 0.0});
   }
   bgemm(gp, s);
   gp.clear();
-  for (auto& nd : H.lv[L]) {
-    if (nd.pt) cp.push_back({nd.rows, nrhs, dn[L].p + nd.koff * nrhs, nrhs, out + nd.lo * nrhs, nrhs, 1});
+  for (int i = sh.first(L); i < sh.last(L); ++i) {
+    const auto& nd = H.lv[L][i];
+    const int64_t lo = nd.lo - H.lo_g;
+    if (nd.pt) cp.push_back({nd.rows, nrhs, dn[L].p + nd.koff * nrhs, nrhs, out + lo * nrhs, nrhs, 1});
     else if (nd.k > 0)
       gp.push_back({nd.rows, nrhs, nd.k, H.U[L].p + nd.uoff, nd.k, 1, dn[L].p + nd.koff * nrhs, nrhs, 1,
-                    out + nd.lo * nrhs, nrhs, 1, 1.0, 1.0});
+                    out + lo * nrhs, nrhs, 1, 1.0, 1.0});
   }
   bcopy(cp, s);
   bgemm(gp, s);

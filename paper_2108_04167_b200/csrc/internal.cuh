@@ -3,6 +3,7 @@
 #include <atomic>
 #include <memory>
 #include "common.cuh"
+#include "comm.cuh"
 #include "dense.cuh"
 
 namespace svmhss {
@@ -15,7 +16,8 @@ struct KmmArgs {
   const double* W; int64_t ldw; int ncols;          // nb x ncols right-hand matrix
   double* S; int64_t lds;                           // na x ncols output
   double neg_inv_2h2;                               // -1 / (2 h^2)
-  int same_set;                                     // K_ii = 1 exactly (Fa == Fb)
+  int same_set;                                     // K_ii = 1 exactly (Fa rows are Fb rows)
+  int64_t diag_off;                                 // same_set: Fa row i is Fb row diag_off + i
   const int* leaf_a; const int* leaf_b;             // nullable: zero pairs in the same leaf
   // NOTE: nub and leaf_b are read by 16-byte bulk copies: allocate them with >= 2 doubles /
   // 4 ints of padding past the end (kNormPad / kLeafPad).
@@ -73,11 +75,32 @@ struct NodeInfo {
   int64_t doff = 0;        // offset (doubles) of D_t (leaves)
 };
 
+// Subtree sharding plan: rank g of P (a power of two) owns node g of level
+// lg = log2 P and its descendants; levels < lg are replicated.  At level l this rank
+// processes BFS indices [first(l), last(l)).  Level-lg nodes of every rank become known
+// after the build's exchange (k, skeletons, k-packed offsets: "global" packing at level lg).
+struct Shard {
+  std::shared_ptr<Comm> comm;
+  int P = 1, g = 0, lg = 0;
+  int first(int l) const { return l < lg ? 0 : (g << (l - lg)); }
+  int last(int l) const { return l < lg ? (1 << l) : ((g + 1) << (l - lg)); }
+  bool on() const { return P > 1; }
+};
+
 struct HSSImpl {
   std::atomic<int> refs{1};
   int64_t n = 0;
   int r = 0, rp = 0, L = 0, s = 0, m = 0;
   double h = 1.0;
+  Shard sh;
+  int64_t lo_g = 0, hi_g = 0;             // this rank's tree positions [lo_g, hi_g)
+  int64_t nmax_g = 0;                     // max over ranks of hi_g - lo_g (exchange slots)
+  int kmax_lg = 0;                        // max over level-lg nodes of k (exchange slots)
+  DevBuf<int64_t> lg_koff, lg_k;          // level-lg nodes: global k-packed offset and k
+  DevBuf<int64_t> rank_lo, rank_cnt;      // per rank: first tree position and count
+  DevBuf<int64_t> leaf_lo;                // this rank's leaves: local first point (+ end)
+  int nleaf_loc() const { return sh.last(L) - sh.first(L); }
+  int64_t nloc() const { return hi_g - lo_g; }
   std::vector<std::vector<NodeInfo>> lv;  // lv[l][i], l = 0..L
   DevBuf<double> Fp, nu;
   DevBuf<int64_t> perm, iperm;
@@ -91,9 +114,39 @@ struct HSSImpl {
 };
 
 void hss_build_impl(HSSImpl& H, const double* F, int64_t n, int r, double h,
-                    const hss_opts& o, cudaStream_t s);
-// K~ V in TREE order, V/out n x nrhs point-major (device).
+                    const hss_opts& o, std::shared_ptr<Comm> comm, cudaStream_t s);
+// K~ V in TREE order on this rank's points: V/out nloc x nrhs point-major (device),
+// rows [lo_g, hi_g) of the tree order.
 void hss_matvec_tree(const HSSImpl& H, const double* V, double* out, int nrhs, cudaStream_t s);
+int64_t level_sumk(const HSSImpl& H, int l);
+
+// ---------------------------------------------------------------- sharded exchanges
+// Workspace of the per-iteration level-lg exchange (allocated once: graph-capturable).
+struct ExchWS {
+  int ncols = 0, nextra = 0;
+  int64_t slot = 0;              // doubles per rank slot: kmax_lg * ncols + nextra
+  DevBuf<double> send, recv;     // slot, P * slot
+};
+void exch_ws_alloc(const HSSImpl& H, int ncols, int nextra, ExchWS& ws);
+// buf: level-lg k-packed vector (global offsets, ncols per row) in which only this rank's
+// node is valid; fills every rank's node.  extra (nextra doubles, nullable) is appended to
+// the slot and gathered to extra_out (P x nextra, rank-major).  No-op when P == 1 except
+// copying extra to extra_out.
+void exchange_lg(const HSSImpl& H, ExchWS& ws, double* buf, const double* extra,
+                 double* extra_out, cudaStream_t s);
+// local point vector (nloc x ncols, tree order) -> full tree-order vector (n x ncols) on
+// every rank.
+void gather_points(const HSSImpl& H, const double* loc, int ncols, double* full, cudaStream_t s);
+
+// Fixed-order reductions that follow the cluster tree (bitwise P-invariant): `part` holds
+// one partial per leaf this rank holds (nleaf_loc x ncols); reduce pairwise up to the
+// subtree root (this rank) and, after an exchange of the P subtree-root values, pairwise over
+// the top levels.  tree_reduce_local writes ncols values to `out`; tree_reduce_top reduces
+// P x ncols rank-major values to ncols.
+void tree_reduce_local(const HSSImpl& H, double* part, int ncols, double* out, cudaStream_t s);
+void tree_reduce_top(int P, const double* in, int ncols, double* out, cudaStream_t s);
+// Host convenience: full reduction of per-leaf partials to ncols host values.
+void tree_reduce_all(const HSSImpl& H, double* part, int ncols, double* host_out, cudaStream_t s);
 
 // ---------------------------------------------------------------- ULV
 struct SolveNode {
@@ -105,13 +158,16 @@ struct SolveNode {
 };
 struct SolveWork { int node, chunk; };
 
+constexpr int kCW = 64;  // backward sweep: columns per CTA
+constexpr int kBW = 8;   // backward sweep: warps per CTA
 struct ULVLevel {
   int nnodes = 0, maxR = 0, allpt = 1;
   int64_t sumR = 0, sumK = 0, sumY = 0;
-  DevBuf<double> M, MT;          // per-node solve operators and their transposes
+  DevBuf<double> M;              // per-node solve operators (row-major R x R)
   DevBuf<SolveNode> nodes;
-  DevBuf<SolveWork> work;        // (node, chunk of `ch` rows); leaf level: non-pass-through only
-  int nwork = 0, ch = 32;
+  DevBuf<SolveWork> work;        // fwd: (node, chunk of `ch` rows); leaf level: non-pass-through only
+  DevBuf<SolveWork> bwork;       // bwd: (node, chunk of kCW columns)
+  int nwork = 0, nbwork = 0, ch = 32;
 };
 
 struct ULVImpl {
@@ -125,19 +181,37 @@ struct ULVImpl {
 };
 
 void ulv_factor_impl(ULVImpl& F, cudaStream_t s);
-void btranspose(const std::vector<SqProb>& probs, const double* base, double* out, cudaStream_t s);
 
-// Solve workspace for nrhs right-hand sides (tree order in/out).
+// Solve workspace for nrhs right-hand sides (tree order in/out, this rank's points).
 struct SolveWS {
   int nrhs = 0;
   std::vector<double*> fin, yr, xout;  // per level (levels that are all pass-through alias)
   std::vector<DevBuf<double>> own;
+  // sharded: the level-lg exchange; `extra` (nextra doubles per rank, set nextra before
+  // solve_ws_alloc) rides along, gathered to extra_all (P x nextra) and, if extra_top is set,
+  // tree-reduced over the ranks into extra_top.
+  ExchWS xw;
+  int nextra = 0;
+  const double* extra = nullptr;
+  double* extra_all = nullptr;
+  double* extra_top = nullptr;
+  // ADMM: the caller reads x of pass-through leaves from xout[L-1] and writes their next
+  // right-hand side into fin[L-1] itself (via ptmap), so the two leaf copies are skipped.
+  bool fused_leaf_io = false;
 };
 void solve_ws_alloc(const ULVImpl& F, int nrhs, SolveWS& ws);
 // x_tree = (K~+beta I)^-1 b_tree.  b is read from ws.fin[L] and x written to ws.xout[L].
 void ulv_solve_tree(const ULVImpl& F, SolveWS& ws, cudaStream_t s);
-// number of kernel launches of ulv_solve_tree
-int ulv_solve_launches(const ULVImpl& F);
+// Pieces of the solve, for iterations that reorder / fuse levels (admm.cu).
+struct SolveStep {
+  enum Kind { FWD, BWD, FWD_LIST, BWD_LIST, EXCHANGE };
+  int kind = FWD, a = 0, b = 0;
+  bool no_exchange = false;
+  const SolveWork* work = nullptr;  // *_LIST: level a, this work list
+  int nwork = 0;
+};
+void ulv_solve_steps(const ULVImpl& F, SolveWS& ws, const std::vector<SolveStep>& steps, cudaStream_t s);
+
 
 // ---------------------------------------------------------------- ADMM / predict (admm.cu)
 struct AdmmResult { double w1; double ms_pre, ms_loop, ms_bias; int graph; int64_t launches; };

@@ -1,0 +1,141 @@
+// solve_dev.cuh — device functions of the ULV solve sweeps shared by the level kernels
+// (ulv.cu) and the fused bottom-level ADMM kernel (admm.cu), so both produce bitwise-identical
+// values.  Forward sweep t = M_t b (rows i < k -> the parent's input "up", rows >= k -> y_r);
+// backward sweep x = M_t^T [x_s; y_r], both streaming the same stored M_t (no transposed copy):
+//  - fwd_rows: one warp per row (two rows in flight), lane-strided partial sums + butterfly;
+//  - bwd_cols: a CTA of kBW warps owns kCW consecutive columns (lane l -> columns j0 + l and
+//    j0 + 32 + l: fully coalesced row segments); warp w accumulates rows w, w + kBW, ... in
+//    order; the kBW warp partials are summed in warp order.
+// The summation order of every output element depends only on the node's shape.
+#pragma once
+#include "internal.cuh"
+
+namespace svmhss {
+
+// one row's lane-partial dot product: lane sums j = lane, lane + 32, ... in order
+template <int NR, int RU>
+__device__ __forceinline__ void row_partials(const double* const (&Mr)[RU], int R, const double* __restrict__ vsh,
+                                             double (&acc)[RU][NR]) {
+  const int lane = threadIdx.x & 31;
+#pragma unroll
+  for (int u = 0; u < RU; ++u)
+#pragma unroll
+    for (int c = 0; c < NR; ++c) acc[u][c] = 0.0;
+  int j = lane;
+  for (; j + 96 < R; j += 128) {
+    double m[RU][4];
+#pragma unroll
+    for (int u = 0; u < RU; ++u)
+#pragma unroll
+      for (int q = 0; q < 4; ++q) m[u][q] = Mr[u][j + 32 * q];
+#pragma unroll
+    for (int u = 0; u < RU; ++u)
+#pragma unroll
+      for (int q = 0; q < 4; ++q)
+#pragma unroll
+        for (int c = 0; c < NR; ++c) acc[u][c] = fma(m[u][q], vsh[(j + 32 * q) * NR + c], acc[u][c]);
+  }
+  for (; j < R; j += 32) {
+#pragma unroll
+    for (int u = 0; u < RU; ++u) {
+      const double m0 = Mr[u][j];
+#pragma unroll
+      for (int c = 0; c < NR; ++c) acc[u][c] = fma(m0, vsh[j * NR + c], acc[u][c]);
+    }
+  }
+}
+
+template <int NR>
+__device__ __forceinline__ void row_store(double (&acc)[NR], int i, int k, int64_t koff, int64_t yoff,
+                                          double* __restrict__ out_up, double* __restrict__ out_yr) {
+  const int lane = threadIdx.x & 31;
+#pragma unroll
+  for (int c = 0; c < NR; ++c) acc[c] = warp_sum(acc[c]);
+  if (lane < NR) {
+    double v = acc[0];
+#pragma unroll
+    for (int c = 1; c < NR; ++c) if (lane == c) v = acc[c];
+    if (i < k) out_up[(koff + i) * NR + lane] = v;
+    else out_yr[(yoff + i - k) * NR + lane] = v;
+  }
+}
+
+// rows i0 + wid, i0 + wid + nw, ... < i1; two rows per warp in flight (8 loads per lane)
+template <int NR>
+__device__ __forceinline__ void fwd_rows(const double* __restrict__ M, int R, const double* __restrict__ vsh,
+                                         int i0, int i1, int wid, int nw, int k, int64_t koff, int64_t yoff,
+                                         double* __restrict__ out_up, double* __restrict__ out_yr) {
+  int i = i0 + wid;
+  for (; i + nw < i1; i += 2 * nw) {
+    const double* Mr[2] = {M + (int64_t)i * R, M + (int64_t)(i + nw) * R};
+    double acc[2][NR];
+    row_partials<NR, 2>(Mr, R, vsh, acc);
+    row_store<NR>(acc[0], i, k, koff, yoff, out_up, out_yr);
+    row_store<NR>(acc[1], i + nw, k, koff, yoff, out_up, out_yr);
+  }
+  if (i < i1) {
+    const double* Mr[1] = {M + (int64_t)i * R};
+    double acc[1][NR];
+    row_partials<NR, 1>(Mr, R, vsh, acc);
+    row_store<NR>(acc[0], i, k, koff, yoff, out_up, out_yr);
+  }
+}
+
+// x[j] for j in [j0, min(R, j0 + kCW)); ush = u (R x NR) in shared memory; red: kBW*kCW*NR
+// doubles of shared scratch.  Must be called by all kBW*32 threads of the CTA.
+template <int NR>
+__device__ __forceinline__ void bwd_cols(const double* __restrict__ M, int R, const double* __restrict__ ush,
+                                         int j0, double* __restrict__ red, double* __restrict__ out) {
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  const int ja = j0 + lane, jb = j0 + 32 + lane;
+  const bool va = ja < R, vb = jb < R;
+  double aa[NR], ab[NR];
+#pragma unroll
+  for (int c = 0; c < NR; ++c) aa[c] = ab[c] = 0.0;
+  int i = wid;
+  for (; i + 7 * kBW < R; i += 8 * kBW) {
+    double ma[8], mb[8];
+#pragma unroll
+    for (int q = 0; q < 8; ++q) {
+      const double* Mr = M + (int64_t)(i + q * kBW) * R;
+      ma[q] = va ? Mr[ja] : 0.0;
+      mb[q] = vb ? Mr[jb] : 0.0;
+    }
+#pragma unroll
+    for (int q = 0; q < 8; ++q)
+#pragma unroll
+      for (int c = 0; c < NR; ++c) {
+        const double u = ush[(i + q * kBW) * NR + c];
+        aa[c] = fma(ma[q], u, aa[c]);
+        ab[c] = fma(mb[q], u, ab[c]);
+      }
+  }
+  for (; i < R; i += kBW) {
+    const double* Mr = M + (int64_t)i * R;
+    const double ma = va ? Mr[ja] : 0.0, mb = vb ? Mr[jb] : 0.0;
+#pragma unroll
+    for (int c = 0; c < NR; ++c) {
+      const double u = ush[i * NR + c];
+      aa[c] = fma(ma, u, aa[c]);
+      ab[c] = fma(mb, u, ab[c]);
+    }
+  }
+#pragma unroll
+  for (int c = 0; c < NR; ++c) {
+    red[(wid * kCW + lane) * NR + c] = aa[c];
+    red[(wid * kCW + 32 + lane) * NR + c] = ab[c];
+  }
+  __syncthreads();
+  for (int e = threadIdx.x; e < kCW * NR; e += kBW * 32) {
+    const int jj = e / NR, c = e % NR;
+    if (j0 + jj < R) {
+      double t = red[jj * NR + c];
+#pragma unroll
+      for (int w = 1; w < kBW; ++w) t += red[(w * kCW + jj) * NR + c];
+      out[(int64_t)(j0 + jj) * NR + c] = t;
+    }
+  }
+  __syncthreads();
+}
+
+}  // namespace svmhss

@@ -44,6 +44,38 @@ static inline int pad_stride(int x) {  // smallest S >= x with S % 16 == 4
 
 constexpr int KBM = 64;
 
+// exp(x) for the Gaussian kernel entries (x = -d2 / (2h^2) <= 0): Cody-Waite reduction
+// x = n ln2 + r, |r| <= ln2/2, Taylor polynomial of degree 13 (truncation < 5e-18), and the
+// scale 2^n applied as two exact power-of-two factors (gradual underflow; 0 below -745).
+// Only DFMA/DADD and integer moves: no libdevice call, few live registers (the sketch kernel's
+// 34 accumulator doubles stay in registers) and no special-case branches.  Accuracy <= 2 ulp
+// against the correctly rounded exp (tests/test_gpu_parity.py pins the sketch at 1e-12).
+__device__ __forceinline__ double exp_kernel(double x) {
+  x = fmax(x, -1100.0);
+  const double kShift = 6755399441055744.0;  // 1.5 * 2^52: t's low word holds round(x log2 e)
+  const double t = fma(x, 1.4426950408889634, kShift);
+  const double n = t - kShift;
+  const int ni = __double2loint(t);
+  double r = fma(n, -6.93147180369123816490e-01, x);
+  r = fma(n, -1.90821492927058770002e-10, r);
+  double p = 1.6059043836821614599e-10;        // 1/13!
+  p = fma(p, r, 2.0876756987868098979e-09);    // 1/12!
+  p = fma(p, r, 2.5052108385441718775e-08);    // 1/11!
+  p = fma(p, r, 2.7557319223985890653e-07);    // 1/10!
+  p = fma(p, r, 2.7557319223985890653e-06);    // 1/9!
+  p = fma(p, r, 2.4801587301587301566e-05);    // 1/8!
+  p = fma(p, r, 1.9841269841269841253e-04);    // 1/7!
+  p = fma(p, r, 1.3888888888888889419e-03);    // 1/6!
+  p = fma(p, r, 8.3333333333333332177e-03);    // 1/5!
+  p = fma(p, r, 4.1666666666666664354e-02);    // 1/4!
+  p = fma(p, r, 1.6666666666666665741e-01);    // 1/3!
+  p = fma(p, r, 0.5);
+  p = fma(p, r, 1.0);
+  p = fma(p, r, 1.0);
+  const int h1 = ni >> 1, h2 = ni - h1;         // 2^n = 2^h1 * 2^h2, each a normal number
+  return (p * __hiloint2double((h1 + 1023) << 20, 0)) * __hiloint2double((h2 + 1023) << 20, 0);
+}
+
 // --- mbarrier / bulk-copy (TMA) helpers
 __device__ __forceinline__ unsigned smem_u32(const void* p) { return (unsigned)__cvta_generic_to_shared(p); }
 __device__ __forceinline__ void mbar_init(uint64_t* b, unsigned count) {
@@ -161,10 +193,27 @@ __global__ void __launch_bounds__(512, 1) kmm_kernel(KmmArgs a, int SA) {
 #pragma unroll
     for (int q = 0; q < HQ; ++q) dacc[q][0] = dacc[q][1] = 0.0;
     const double* Fb_w = Fb_s + (hf * (BJ / 2) + g) * SA + t;
-    for (int kk = 0; kk < rp / 4; ++kk) {
-      const double av = Fa_w[kk * 4];
+    {
+      // two interleaved partial sums per tile: 2*HQ independent DMMA chains of rp/8 steps
+      double dacc2[HQ][2];
 #pragma unroll
-      for (int q = 0; q < HQ; ++q) dmma884(dacc[q][0], dacc[q][1], av, Fb_w[q * 8 * SA + kk * 4]);
+      for (int q = 0; q < HQ; ++q) dacc2[q][0] = dacc2[q][1] = 0.0;
+      int kk = 0;
+      for (; kk + 1 < rp / 4; kk += 2) {
+        const double av0 = Fa_w[kk * 4], av1 = Fa_w[kk * 4 + 4];
+#pragma unroll
+        for (int q = 0; q < HQ; ++q) {
+          dmma884(dacc[q][0], dacc[q][1], av0, Fb_w[q * 8 * SA + kk * 4]);
+          dmma884(dacc2[q][0], dacc2[q][1], av1, Fb_w[q * 8 * SA + kk * 4 + 4]);
+        }
+      }
+      if (kk < rp / 4) {
+        const double av = Fa_w[kk * 4];
+#pragma unroll
+        for (int q = 0; q < HQ; ++q) dmma884(dacc[q][0], dacc[q][1], av, Fb_w[q * 8 * SA + kk * 4]);
+      }
+#pragma unroll
+      for (int q = 0; q < HQ; ++q) { dacc[q][0] += dacc2[q][0]; dacc[q][1] += dacc2[q][1]; }
     }
 #pragma unroll
     for (int q = 0; q < HQ; ++q) {
@@ -173,8 +222,8 @@ __global__ void __launch_bounds__(512, 1) kmm_kernel(KmmArgs a, int SA) {
       for (int e = 0; e < 2; ++e) {
         const int jj = hf * (BJ / 2) + q * 8 + 2 * t + e;
         double d2 = fmax(nui + nub_s[jj] - 2.0 * dacc[q][e], 0.0);
-        double v = exp(d2 * a.neg_inv_2h2);
-        if (a.same_set && j0 + jj == my_row) v = 1.0;
+        double v = exp_kernel(d2 * a.neg_inv_2h2);
+        if (a.same_set && j0 + jj == my_row + a.diag_off) v = 1.0;
         if (a.leaf_b && lb[jj] == my_leaf) v = 0.0;
         if (jj >= jvalid || !row_ok) v = 0.0;
         ev[e] = v;

@@ -13,7 +13,7 @@
 // (rows x rows), so the forward sweep is t = M_t b (up = t[:k], y_r = t[k:]) and the backward
 // sweep is x = M_t^T [x_s; y_r]: one dense GEMV each way, streaming M_t from HBM once per
 // sweep.  Root: M_0 = L^-1 of its Cholesky factor (k = 0).  Pass-through nodes: M = I.
-#include "internal.cuh"
+#include "solve_dev.cuh"
 
 namespace svmhss {
 
@@ -54,37 +54,6 @@ __global__ void pack_kernel(const double* __restrict__ A, const PackDesc* __rest
   }
 }
 
-// batched square transpose: out[off + j*R + i] = A[off + i*R + j] (same offsets as A)
-__global__ void btranspose_kernel(const SqProb* __restrict__ probs, const double* __restrict__ base,
-                                  double* __restrict__ out) {
-  const SqProb P = probs[blockIdx.z];
-  const int n = P.n;
-  const int64_t off = P.A - base;
-  __shared__ double tile[32][33];
-  const int i0 = blockIdx.y * 32, j0 = blockIdx.x * 32;
-  if (i0 >= n || j0 >= n) return;
-  for (int r = threadIdx.y; r < 32; r += 8) {
-    const int i = i0 + r, j = j0 + threadIdx.x;
-    tile[r][threadIdx.x] = (i < n && j < n) ? P.A[(int64_t)i * n + j] : 0.0;
-  }
-  __syncthreads();
-  for (int r = threadIdx.y; r < 32; r += 8) {
-    const int j = j0 + r, i = i0 + threadIdx.x;
-    if (i < n && j < n) out[off + (int64_t)j * n + i] = tile[threadIdx.x][r];
-  }
-}
-
-void btranspose(const std::vector<SqProb>& probs, const double* base, double* out, cudaStream_t s) {
-  if (probs.empty()) return;
-  int mx = 0;
-  for (auto& p : probs) mx = std::max(mx, p.n);
-  auto d = upload(probs, s);
-  dim3 grid(ceil_div(mx, 32), ceil_div(mx, 32), (unsigned)probs.size());
-  btranspose_kernel<<<grid, dim3(32, 8), 0, s>>>(d.p, base, out);
-  LAUNCH_CHECK();
-  CUDA_CHECK(cudaStreamSynchronize(s));
-}
-
 static void run_pack(const double* A, const std::vector<PackDesc>& pd, double* out, cudaStream_t s) {
   if (pd.empty()) return;
   auto d = upload(pd, s);
@@ -112,14 +81,17 @@ void ulv_factor_impl(ULVImpl& F, cudaStream_t s) {
   F.lv.clear();
   F.lv.resize(L + 1);
   EventTimer tm(s);
+  const Shard& sh = H.sh;
   // per-node reduced blocks passed to the parent: Dh (k x k), Rm (k x k)
   DevBuf<double> DhC, RmC;           // child level
-  std::vector<int64_t> dhoffC;       // offsets (doubles), per child node (k*k packing)
+  std::vector<int64_t> dhoffC;       // offsets (doubles) by the child's BFS index (k*k packing)
   int64_t total_bytes = 0;
   for (int l = L; l >= 0; --l) {
     const bool leaf = (l == L);
-    auto& hv = H.lv[l];
-    const int nn = (int)hv.size();
+    const int f0 = sh.first(l);
+    // this rank's nodes of level l, re-based to 0 (hv[i] = H.lv[l][f0 + i])
+    NodeInfo* hv = H.lv[l].data() + f0;
+    const int nn = sh.last(l) - f0;
     std::vector<int> R(nn), K(nn), PT(nn);
     for (int i = 0; i < nn; ++i) {
       R[i] = (l == 0) ? ((L == 0) ? (int)H.n : hv[i].rows) : hv[i].rows;
@@ -140,7 +112,8 @@ void ulv_factor_impl(ULVImpl& F, cudaStream_t s) {
       LAUNCH_CHECK();
       CUDA_CHECK(cudaStreamSynchronize(s));
     } else {
-      auto& cv = H.lv[l + 1];
+      const NodeInfo* cv = H.lv[l + 1].data() + 2 * f0;  // children of hv[i]: cv[2i], cv[2i+1]
+      const int64_t* dho = dhoffC.data() + 2 * f0;
       std::vector<CopyProb> cp;
       std::vector<GemmProb> g1, g2;
       int64_t sumT = 0;
@@ -150,10 +123,10 @@ void ulv_factor_impl(ULVImpl& F, cudaStream_t s) {
       for (int i = 0; i < nn; ++i) {
         const int ka = cv[2 * i].k, kb = cv[2 * i + 1].k, Rn = R[i];
         double* Dc = Dcur.p + coff[i];
-        const double* Dha = DhC.p + dhoffC[2 * i];
-        const double* Dhb = DhC.p + dhoffC[2 * i + 1];
-        const double* Ra = RmC.p + dhoffC[2 * i];
-        const double* Rb = RmC.p + dhoffC[2 * i + 1];
+        const double* Dha = DhC.p + dho[2 * i];
+        const double* Dhb = DhC.p + dho[2 * i + 1];
+        const double* Ra = RmC.p + dho[2 * i];
+        const double* Rb = RmC.p + dho[2 * i + 1];
         const double* Bp = H.B[l].p + hv[i].boff;
         cp.push_back({ka, ka, Dha, ka, Dc, Rn, 0});
         cp.push_back({kb, kb, Dhb, kb, Dc + (int64_t)ka * Rn + ka, Rn, 0});
@@ -207,10 +180,11 @@ void ulv_factor_impl(ULVImpl& F, cudaStream_t s) {
         if (leaf) {
           cp.push_back({R[i], K[i], Ut, K[i], Ucur.p + uoff[i], K[i], 0});
         } else {
-          auto& cv = H.lv[l + 1];
+          const NodeInfo* cv = H.lv[l + 1].data() + 2 * f0;
+          const int64_t* dho = dhoffC.data() + 2 * f0;
           const int ka = cv[2 * i].k, kb = cv[2 * i + 1].k;
-          const double* Ra = RmC.p + dhoffC[2 * i];
-          const double* Rb = RmC.p + dhoffC[2 * i + 1];
+          const double* Ra = RmC.p + dho[2 * i];
+          const double* Rb = RmC.p + dho[2 * i + 1];
           gp.push_back({ka, K[i], ka, Ra, ka, 1, Ut, K[i], 1, Ucur.p + uoff[i], K[i], 1, 1.0, 0.0});
           gp.push_back({kb, K[i], kb, Rb, kb, 1, Ut + (int64_t)ka * K[i], K[i], 1,
                         Ucur.p + uoff[i] + (int64_t)ka * K[i], K[i], 1, 1.0, 0.0});
@@ -231,11 +205,12 @@ void ulv_factor_impl(ULVImpl& F, cudaStream_t s) {
         if (leaf) {
           pd.push_back({0, koff2[i], K[i], K[i], 2, 0});
         } else {
-          auto& cv = H.lv[l + 1];
+          const NodeInfo* cv = H.lv[l + 1].data() + 2 * f0;
+          const int64_t* dho = dhoffC.data() + 2 * f0;
           const int ka = cv[2 * i].k, kb = cv[2 * i + 1].k;
           CUDA_CHECK(cudaMemsetAsync(RmP.p + koff2[i], 0, (size_t)K[i] * K[i] * 8, s));
-          cp.push_back({ka, ka, RmC.p + dhoffC[2 * i], ka, RmP.p + koff2[i], K[i], 0});
-          cp.push_back({kb, kb, RmC.p + dhoffC[2 * i + 1], kb, RmP.p + koff2[i] + (int64_t)ka * K[i] + ka, K[i], 0});
+          cp.push_back({ka, ka, RmC.p + dho[2 * i], ka, RmP.p + koff2[i], K[i], 0});
+          cp.push_back({kb, kb, RmC.p + dho[2 * i + 1], kb, RmP.p + koff2[i] + (int64_t)ka * K[i] + ka, K[i], 0});
         }
       }
       bcopy(cp, s);
@@ -314,8 +289,8 @@ void ulv_factor_impl(ULVImpl& F, cudaStream_t s) {
       // L_r = chol(Dc_rr)   (also nodes with k == 0: whole block)
       std::vector<SqProb> cp2;
       std::vector<int> ids;
-      for (int i : np) { cp2.push_back({R[i] - K[i], Dcur.p + coff[i] + (int64_t)K[i] * R[i] + K[i], R[i], 1}); ids.push_back(H.node_id(l, i)); }
-      for (int i : nz) { cp2.push_back({R[i], Dcur.p + coff[i], R[i], 1}); ids.push_back(H.node_id(l, i)); }
+      for (int i : np) { cp2.push_back({R[i] - K[i], Dcur.p + coff[i] + (int64_t)K[i] * R[i] + K[i], R[i], 1}); ids.push_back(H.node_id(l, f0 + i)); }
+      for (int i : nz) { cp2.push_back({R[i], Dcur.p + coff[i], R[i], 1}); ids.push_back(H.node_id(l, f0 + i)); }
       DevBuf<int> info(std::max<size_t>(1, cp2.size()));
       bpotrf(cp2, info.p, s);
       check_info(info, ids, s);
@@ -361,59 +336,85 @@ void ulv_factor_impl(ULVImpl& F, cudaStream_t s) {
       bgemm(g, s);
       CUDA_CHECK(cudaStreamSynchronize(s));
     }
-    // solve descriptors
+    // solve descriptors (leaf rows: this rank's local point positions)
     std::vector<SolveNode> sn(nn);
-    std::vector<SolveWork> fw, bw;
     int maxR = 0, allpt = 1;
     for (int i = 0; i < nn; ++i) {
-      sn[i] = {R[i], K[i], PT[i], 0, moff[i], leaf ? hv[i].lo : hv[i].roff, hv[i].koff, yoff[i]};
+      sn[i] = {R[i], K[i], PT[i], 0, moff[i], leaf ? hv[i].lo - H.lo_g : hv[i].roff, hv[i].koff, yoff[i]};
       maxR = std::max(maxR, R[i]);
       if (!PT[i]) allpt = 0;
     }
+    if (sh.on() && l == sh.lg) allpt = 0;  // the exchanged level always has its own buffers
     F_l.nodes = upload(sn, s);
-    F_l.sumR = sumRall; F_l.sumK = sumK; F_l.sumY = sumY; F_l.maxR = maxR; F_l.allpt = allpt;
-    // next level inputs
+    F_l.sumR = sumRall; F_l.sumK = level_sumk(H, l); F_l.sumY = sumY; F_l.maxR = maxR; F_l.allpt = allpt;
+    // next level inputs (offsets by BFS index of this level)
+    dhoffC.assign(H.lv[l].size(), -1);
+    for (int i = 0; i < nn; ++i) dhoffC[f0 + i] = koff2[i];
+    if (sh.on() && l == sh.lg) {
+      // exchange the subtree roots' reduced blocks (Dh, Rm: k x k each) -> every rank
+      const int km = H.kmax_lg;
+      const int64_t slot = std::max<int64_t>(1, 2LL * km * km);
+      DevBuf<double> send(slot), recv(slot * sh.P);
+      const int ko = K[0];
+      if (ko > 0) {
+        CUDA_CHECK(cudaMemcpyAsync(send.p, DhP.p, (size_t)ko * ko * 8, cudaMemcpyDeviceToDevice, s));
+        CUDA_CHECK(cudaMemcpyAsync(send.p + (int64_t)km * km, RmP.p, (size_t)ko * ko * 8, cudaMemcpyDeviceToDevice, s));
+      }
+      sh.comm->allgather(send.p, recv.p, slot * 8, s);
+      int64_t tot = 0;
+      for (int p = 0; p < sh.P; ++p) { dhoffC[p] = tot; tot += (int64_t)H.lv[l][p].k * H.lv[l][p].k; }
+      DevBuf<double> Dall(std::max<int64_t>(1, tot)), Rall(std::max<int64_t>(1, tot));
+      for (int p = 0; p < sh.P; ++p) {
+        const int64_t kk = (int64_t)H.lv[l][p].k * H.lv[l][p].k;
+        if (!kk) continue;
+        CUDA_CHECK(cudaMemcpyAsync(Dall.p + dhoffC[p], recv.p + p * slot, kk * 8, cudaMemcpyDeviceToDevice, s));
+        CUDA_CHECK(cudaMemcpyAsync(Rall.p + dhoffC[p], recv.p + p * slot + (int64_t)km * km, kk * 8,
+                                   cudaMemcpyDeviceToDevice, s));
+      }
+      CUDA_CHECK(cudaStreamSynchronize(s));
+      DhP = std::move(Dall);
+      RmP = std::move(Rall);
+    }
     DhC = std::move(DhP);
     RmC = std::move(RmP);
-    dhoffC = koff2;
     CUDA_CHECK(cudaStreamSynchronize(s));
   }
-  // transposed copies M^T (backward sweep = row GEMV too) and work lists
+  // work lists: forward = (node, chunk of `ch` rows), backward = (node, chunk of kCW columns)
   for (int l = 0; l <= L; ++l) {
     auto& F_l = F.lv[l];
     std::vector<SolveNode> sn(F_l.nnodes);
     d2h(sn.data(), F_l.nodes.p, sn.size(), s);
     CUDA_CHECK(cudaStreamSynchronize(s));
-    F_l.MT.alloc(std::max<size_t>(1, F_l.M.n));
-    std::vector<SqProb> tp;
-    for (auto& nd : sn)
-      if (!nd.pt) tp.push_back({nd.R, F_l.M.p + nd.moff, nd.R, 1});
-    btranspose(tp, F_l.M.p, F_l.MT.p, s);
     // rows per CTA: enough CTAs to fill the chip (>= ~8 per SM), at most 32
     int64_t rows = 0;
     for (auto& nd : sn) if (!(l == L && nd.pt)) rows += nd.R;
     int ch = 32;
     while (ch > 8 && rows / ch < 148 * 8) ch /= 2;
     F_l.ch = ch;
-    std::vector<SolveWork> wk;
+    std::vector<SolveWork> wk, bk;
     for (int i = 0; i < F_l.nnodes; ++i) {
       if (l == L && sn[i].pt) continue;  // pass-through leaves: handled by leaf_pt_copy
       for (int c = 0; c < ceil_div(sn[i].R, ch); ++c) wk.push_back({i, c});
+      for (int c = 0; c < ceil_div(sn[i].R, kCW); ++c) bk.push_back({i, c});
     }
     F_l.work = upload(wk, s);
     F_l.nwork = (int)wk.size();
+    F_l.bwork = upload(bk, s);
+    F_l.nbwork = (int)bk.size();
     CUDA_CHECK(cudaStreamSynchronize(s));
   }
-  // pass-through leaves: tree position -> index in level L-1's vectors
+  // pass-through leaves: local point position -> index in level L-1's vectors
   {
-    std::vector<int64_t> pm(H.n, -1);
+    std::vector<int64_t> pm(std::max<int64_t>(1, H.nloc()), -1);
     int npt = 0;
     if (L >= 1)
-      for (auto& nd : H.lv[L])
+      for (int i = sh.first(L); i < sh.last(L); ++i) {
+        const auto& nd = H.lv[L][i];
         if (nd.pt) {
           ++npt;
-          for (int64_t p2 = nd.lo; p2 < nd.hi; ++p2) pm[p2] = nd.koff + (p2 - nd.lo);
+          for (int64_t p2 = nd.lo; p2 < nd.hi; ++p2) pm[p2 - H.lo_g] = nd.koff + (p2 - nd.lo);
         }
+      }
     F.nleafpt = npt;
     F.ptmap = upload(pm, s);
     CUDA_CHECK(cudaStreamSynchronize(s));
@@ -424,70 +425,51 @@ void ulv_factor_impl(ULVImpl& F, cudaStream_t s) {
 }
 
 // ------------------------------------------------------------------ solve sweeps
-// One row-GEMV kernel serves both sweeps: forward t = M_t b (rows i < k -> parent's up,
-// i >= k -> y_r), backward x = M_t^T [x_s; y_r] read from the stored transpose (rows j ->
-// x).  A CTA handles `ch` consecutive rows of one node (ch chosen per level so small levels
-// still spread over the chip); each warp streams its rows with 4 independent loads per lane
-// in flight and reduces with shuffles (fixed order).
+// (device functions fwd_rows / bwd_cols: solve_dev.cuh)
 template <int NR>
-__global__ void __launch_bounds__(256) ulv_gemv_kernel(const SolveNode* __restrict__ nodes,
-                                                       const SolveWork* __restrict__ work, int ch,
-                                                       const double* __restrict__ M, int bwd,
-                                                       const double* __restrict__ in_a,
-                                                       const double* __restrict__ in_b,
-                                                       double* __restrict__ out_a,
-                                                       double* __restrict__ out_b) {
+__global__ void __launch_bounds__(256) ulv_fwd_kernel(const SolveNode* __restrict__ nodes,
+                                                      const SolveWork* __restrict__ work, int ch,
+                                                      const double* __restrict__ M,
+                                                      const double* __restrict__ in,
+                                                      double* __restrict__ out_up,
+                                                      double* __restrict__ out_yr) {
   const SolveWork wk = work[blockIdx.x];
   const SolveNode N = nodes[wk.node];
-  const int R = N.R, tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
+  const int R = N.R, tid = threadIdx.x;
   extern __shared__ double vsh[];  // R * NR
   const int i0 = wk.chunk * ch, i1 = min(R, i0 + ch);
   if (N.pt) {  // identity operator
-    const int64_t src = bwd ? N.koff : N.roff, dst = bwd ? N.roff : N.koff;
-    for (int e = tid; e < (i1 - i0) * NR; e += 256)
-      out_a[(dst + i0) * NR + e] = in_a[(src + i0) * NR + e];
+    for (int e = tid; e < (i1 - i0) * NR; e += 256) out_up[(N.koff + i0) * NR + e] = in[(N.roff + i0) * NR + e];
     return;
   }
-  if (!bwd) {
-    for (int e = tid; e < R * NR; e += 256) vsh[e] = in_a[N.roff * NR + e];
-  } else {
-    const int kn = N.k * NR;
-    for (int e = tid; e < R * NR; e += 256)
-      vsh[e] = (e < kn) ? in_a[N.koff * NR + e] : in_b[(N.yoff - N.k) * NR + e];
-  }
+  for (int e = tid; e < R * NR; e += 256) vsh[e] = in[N.roff * NR + e];
   __syncthreads();
-  for (int i = i0 + wid; i < i1; i += 8) {
-    const double* Mr = M + N.moff + (int64_t)i * R;
-    double acc[NR];
-#pragma unroll
-    for (int c = 0; c < NR; ++c) acc[c] = 0.0;
-    int j = lane;
-    for (; j + 96 < R; j += 128) {
-      const double m0 = Mr[j], m1 = Mr[j + 32], m2 = Mr[j + 64], m3 = Mr[j + 96];
-#pragma unroll
-      for (int c = 0; c < NR; ++c) {
-        acc[c] = fma(m0, vsh[j * NR + c], acc[c]);
-        acc[c] = fma(m1, vsh[(j + 32) * NR + c], acc[c]);
-        acc[c] = fma(m2, vsh[(j + 64) * NR + c], acc[c]);
-        acc[c] = fma(m3, vsh[(j + 96) * NR + c], acc[c]);
-      }
-    }
-    for (; j < R; j += 32) {
-      const double m0 = Mr[j];
-#pragma unroll
-      for (int c = 0; c < NR; ++c) acc[c] = fma(m0, vsh[j * NR + c], acc[c]);
-    }
-#pragma unroll
-    for (int c = 0; c < NR; ++c) acc[c] = warp_sum(acc[c]);
-    if (lane < NR) {
-      double v = acc[0];
-#pragma unroll
-      for (int c = 1; c < NR; ++c) if (lane == c) v = acc[c];
-      if (bwd) out_a[(N.roff + i) * NR + lane] = v;
-      else if (i < N.k) out_a[(N.koff + i) * NR + lane] = v;
-      else out_b[(N.yoff + i - N.k) * NR + lane] = v;
-    }
+  fwd_rows<NR>(M + N.moff, R, vsh, i0, i1, tid >> 5, 8, N.k, N.koff, N.yoff, out_up, out_yr);
+}
+
+template <int NR>
+__global__ void __launch_bounds__(kBW * 32) ulv_bwd_kernel(const SolveNode* __restrict__ nodes,
+                                                           const SolveWork* __restrict__ work,
+                                                           const double* __restrict__ M,
+                                                           const double* __restrict__ in_s,
+                                                           const double* __restrict__ in_r,
+                                                           double* __restrict__ out) {
+  const SolveWork wk = work[blockIdx.x];
+  const SolveNode N = nodes[wk.node];
+  const int R = N.R, tid = threadIdx.x;
+  const int j0 = wk.chunk * kCW;
+  if (N.pt) {  // identity operator
+    const int j1 = min(R, j0 + kCW);
+    for (int e = tid; e < (j1 - j0) * NR; e += kBW * 32) out[(N.roff + j0) * NR + e] = in_s[(N.koff + j0) * NR + e];
+    return;
   }
+  extern __shared__ double sm[];  // u: R * NR, then red: kBW * kCW * NR
+  double* ush = sm;
+  double* red = sm + R * NR;
+  const int kn = N.k * NR;
+  for (int e = tid; e < R * NR; e += kBW * 32) ush[e] = (e < kn) ? in_s[N.koff * NR + e] : in_r[(N.yoff - N.k) * NR + e];
+  __syncthreads();
+  bwd_cols<NR>(M + N.moff, R, ush, j0, red, out + N.roff * NR);
 }
 
 // pass-through leaves: fwd  fin_{L-1}[map[p]] = fin_L[p];  bwd  xout_L[p] = xout_{L-1}[map[p]]
@@ -517,7 +499,8 @@ void solve_ws_alloc(const ULVImpl& F, int nrhs, SolveWS& ws) {
     return ws.own.back().p;
   };
   ws.own.reserve(3 * (L + 1) + 2);
-  ws.fin[L] = mk(H.n);
+  ws.fin[L] = mk(H.nloc());
+  if (H.sh.on()) exch_ws_alloc(H, nrhs, ws.nextra, ws.xw);
   for (int l = L; l >= 1; --l) ws.fin[l - 1] = F.lv[l].allpt ? ws.fin[l] : mk(F.lv[l].sumK);
   for (int l = 0; l <= L; ++l) if (!F.lv[l].allpt) ws.yr[l] = mk(F.lv[l].sumY);
   ws.xout[0] = mk(F.lv[0].sumR);
@@ -525,58 +508,98 @@ void solve_ws_alloc(const ULVImpl& F, int nrhs, SolveWS& ws) {
 }
 
 template <int NR>
-static void solve_impl(const ULVImpl& F, SolveWS& ws, cudaStream_t s) {
-  const int L = F.H->L;
-  const int64_t n = F.H->n;
-  for (int l = L; l >= 0; --l) {
-    const auto& lv = F.lv[l];
-    if (lv.allpt) continue;
-    if (l == L && F.nleafpt > 0) {
-      leaf_pt_copy_kernel<NR><<<ceil_div(n * NR, 256), 256, 0, s>>>(F.ptmap.p, n, 0, ws.fin[L], ws.fin[L - 1]);
-    }
-    if (lv.nwork == 0) continue;
-    const size_t sm = (size_t)lv.maxR * NR * sizeof(double);
-    ulv_gemv_kernel<NR><<<lv.nwork, 256, sm, s>>>(lv.nodes.p, lv.work.p, lv.ch, lv.M.p, 0, ws.fin[l], nullptr,
-                                                  l > 0 ? ws.fin[l - 1] : nullptr, ws.yr[l]);
-  }
-  for (int l = 0; l <= L; ++l) {
-    const auto& lv = F.lv[l];
-    if (lv.allpt) continue;
-    if (lv.nwork > 0) {
-      const size_t sm = (size_t)lv.maxR * NR * sizeof(double);
-      ulv_gemv_kernel<NR><<<lv.nwork, 256, sm, s>>>(lv.nodes.p, lv.work.p, lv.ch, lv.MT.p, 1,
-                                                    l > 0 ? ws.xout[l - 1] : nullptr, ws.yr[l], ws.xout[l], nullptr);
-    }
-    if (l == L && F.nleafpt > 0) {
-      leaf_pt_copy_kernel<NR><<<ceil_div(n * NR, 256), 256, 0, s>>>(F.ptmap.p, n, 1, ws.xout[L - 1], ws.xout[L]);
-    }
+static void fwd_level(const ULVImpl& F, SolveWS& ws, int l, const SolveWork* work, int nwork, cudaStream_t s) {
+  const auto& lv = F.lv[l];
+  if (nwork <= 0) return;
+  const size_t sm = (size_t)lv.maxR * NR * sizeof(double);
+  ulv_fwd_kernel<NR><<<nwork, 256, sm, s>>>(lv.nodes.p, work, lv.ch, lv.M.p, ws.fin[l], l > 0 ? ws.fin[l - 1] : nullptr,
+                                            ws.yr[l]);
+  g_launches.fetch_add(1);
+}
+
+template <int NR>
+static void bwd_level(const ULVImpl& F, SolveWS& ws, int l, const SolveWork* work, int nwork, cudaStream_t s) {
+  const auto& lv = F.lv[l];
+  if (nwork <= 0) return;
+  const size_t sm = ((size_t)lv.maxR + (size_t)kBW * kCW) * NR * sizeof(double);
+  ulv_bwd_kernel<NR><<<nwork, kBW * 32, sm, s>>>(lv.nodes.p, work, lv.M.p, l > 0 ? ws.xout[l - 1] : nullptr, ws.yr[l],
+                                                 ws.xout[l]);
+  g_launches.fetch_add(1);
+}
+
+template <int NR>
+static void exchange_step(const ULVImpl& F, SolveWS& ws, cudaStream_t s) {
+  const HSSImpl& H = *F.H;
+  // subtree roots' reduced right-hand sides (+ the caller's per-rank extra) -> every rank
+  exchange_lg(H, ws.xw, ws.fin[H.sh.lg - 1], ws.extra, ws.extra_all, s);
+  if (ws.extra && ws.extra_top) tree_reduce_top(H.sh.P, ws.extra_all, ws.nextra, ws.extra_top, s);
+}
+
+template <int NR>
+static void run_step(const ULVImpl& F, SolveWS& ws, const SolveStep& st, cudaStream_t s) {
+  const HSSImpl& H = *F.H;
+  const int L = H.L;
+  const int64_t n = H.nloc();
+  switch (st.kind) {
+    case SolveStep::FWD:  // levels a down to b (a >= b); the exchange after level lg unless told not to
+      for (int l = st.a; l >= st.b; --l) {
+        const auto& lv = F.lv[l];
+        if (!lv.allpt) {
+          if (l == L && F.nleafpt > 0 && !ws.fused_leaf_io) {
+            leaf_pt_copy_kernel<NR><<<ceil_div(n * NR, 256), 256, 0, s>>>(F.ptmap.p, n, 0, ws.fin[L], ws.fin[L - 1]);
+            g_launches.fetch_add(1);
+          }
+          fwd_level<NR>(F, ws, l, lv.work.p, lv.nwork, s);
+        }
+        if (H.sh.on() && l == H.sh.lg && !st.no_exchange) exchange_step<NR>(F, ws, s);
+      }
+      break;
+    case SolveStep::BWD:  // levels a up to b (a <= b)
+      for (int l = st.a; l <= st.b; ++l) {
+        const auto& lv = F.lv[l];
+        if (lv.allpt) continue;
+        bwd_level<NR>(F, ws, l, lv.bwork.p, lv.nbwork, s);
+        if (l == L && F.nleafpt > 0 && !ws.fused_leaf_io) {
+          leaf_pt_copy_kernel<NR><<<ceil_div(n * NR, 256), 256, 0, s>>>(F.ptmap.p, n, 1, ws.xout[L - 1], ws.xout[L]);
+          g_launches.fetch_add(1);
+        }
+      }
+      break;
+    case SolveStep::FWD_LIST: fwd_level<NR>(F, ws, st.a, st.work, st.nwork, s); break;
+    case SolveStep::BWD_LIST: bwd_level<NR>(F, ws, st.a, st.work, st.nwork, s); break;
+    case SolveStep::EXCHANGE: if (H.sh.on()) exchange_step<NR>(F, ws, s); break;
   }
 }
 
 template <int NR>
-static void set_smem_attrs(size_t sm) {
-  CUDA_CHECK(cudaFuncSetAttribute(ulv_gemv_kernel<NR>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm));
+static void set_smem_attrs(size_t fwd, size_t bwd) {
+  CUDA_CHECK(cudaFuncSetAttribute(ulv_fwd_kernel<NR>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)fwd));
+  CUDA_CHECK(cudaFuncSetAttribute(ulv_bwd_kernel<NR>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bwd));
 }
 
-void ulv_solve_tree(const ULVImpl& F, SolveWS& ws, cudaStream_t s) {
+void ulv_solve_steps(const ULVImpl& F, SolveWS& ws, const std::vector<SolveStep>& steps, cudaStream_t s) {
   int maxR = 0;
   for (auto& lv : F.lv) maxR = std::max(maxR, lv.maxR);
-  const size_t sm = (size_t)maxR * ws.nrhs * sizeof(double);
-  require(sm <= 227 * 1024, "ulv_solve: node too large for the shared-memory vector");
+  const size_t smf = (size_t)maxR * ws.nrhs * sizeof(double);
+  const size_t smb = ((size_t)maxR + (size_t)kBW * kCW) * ws.nrhs * sizeof(double);
+  require(smb <= 227 * 1024, "ulv_solve: node too large for the shared-memory vector");
   switch (ws.nrhs) {
-#define NRC(k) case k: if (sm > 48 * 1024) set_smem_attrs<k>(sm); solve_impl<k>(F, ws, s); break;
+#define NRC(k)                                            \
+  case k:                                                 \
+    if (smb > 48 * 1024) set_smem_attrs<k>(smf, smb);     \
+    for (const auto& st : steps) run_step<k>(F, ws, st, s); \
+    break;
     NRC(1) NRC(2) NRC(3) NRC(4) NRC(5) NRC(6) NRC(7) NRC(8)
 #undef NRC
     default: throw Error(HSS_EINVAL, "ulv_solve: nrhs must be 1..8");
   }
-  LAUNCH_CHECK();
+  CUDA_CHECK(cudaGetLastError());
 }
 
-int ulv_solve_launches(const ULVImpl& F) {
-  int c = 0;
-  for (auto& lv : F.lv) if (!lv.allpt) c += (lv.nwork > 0) ? 2 : 0;
-  if (F.nleafpt > 0 && !F.lv[F.H->L].allpt) c += 2;
-  return c;
+void ulv_solve_tree(const ULVImpl& F, SolveWS& ws, cudaStream_t s) {
+  const int L = F.H->L;
+  ulv_solve_steps(F, ws, {SolveStep{SolveStep::FWD, L, 0}, SolveStep{SolveStep::BWD, 0, L}}, s);
 }
+
 
 }  // namespace svmhss
