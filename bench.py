@@ -91,6 +91,18 @@ class ClockSampler:
                 "sm_max_mhz": max(mx) if mx else None, "reasons": reasons, "samples": len(rows)}
 
 
+def _traffic(kernel, workload):
+    """dram__bytes_read.sum + dram__bytes_write.sum per launch of `kernel` from the committed ncu
+    capture (profiles/traffic.json), if it was taken on this workload; else None."""
+    p = os.path.join(ROOT, "profiles", "traffic.json")
+    if not os.path.exists(p):
+        return None
+    d = json.load(open(p)).get(kernel)
+    if not d or d.get("workload") != workload:
+        return None
+    return d["dram_bytes_read"] + d["dram_bytes_write"]
+
+
 def measure_dgemm(dev, N=8192, reps=5):
     """cuBLAS fp64 GEMM (torch.matmul) TFLOP/s on this GPU, best of `reps` (the FP64 peak the
     DMMA sketch kernel is compared with; MEASURED_PEAKS.json has no FP64 figure)."""
@@ -343,7 +355,9 @@ def main():
             "launches_per_admm_iter": int(ast["kernel_launches_per_iter"]),
             "roofline": {"bound": "tensor", "kernel": "kmm_kernel (sketch S = K Omega, DMMA)",
                          "achieved": ach_tf, "peak": fp64_peak, "unit": "TFLOP/s", "frac": ach_tf / fp64_peak,
-                         "traffic": None,
+                         "traffic": _traffic("kmm_kernel", cfg["name"]) if args.n is None else None,
+                         "traffic_unit": "bytes per launch (ncu dram__bytes_read.sum + dram__bytes_write.sum, "
+                                         "profiles/traffic.json)",
                          "peak_source": "max(cuBLAS fp64 DGEMM 8192^3 measured in this run = %.2f, %s bf16_tflops_sustained x FP64/BF16 nominal %g/%g = %.2f)" % (
                              dgemm_tf, peak_src, FP64_NOMINAL_TF, BF16_NOMINAL_TF, fp64_derived),
                          "work": "2 n^2 (r_pad + s) flops per launch"},

@@ -160,14 +160,17 @@ struct SolveWork { int node, chunk; };
 
 constexpr int kCW = 64;  // backward sweep: columns per CTA
 constexpr int kBW = 8;   // backward sweep: warps per CTA
+constexpr int kSplitMaxLevel = 5;  // bwd row split for levels l <= 5 (l < L-1): <= 32 nodes
+constexpr int kRB = 64;            // bwd row split: rows per chunk
 struct ULVLevel {
   int nnodes = 0, maxR = 0, allpt = 1;
   int64_t sumR = 0, sumK = 0, sumY = 0;
   DevBuf<double> M;              // per-node solve operators (row-major R x R)
   DevBuf<SolveNode> nodes;
   DevBuf<SolveWork> work;        // fwd: (node, chunk of `ch` rows); leaf level: non-pass-through only
-  DevBuf<SolveWork> bwork;       // bwd: (node, chunk of kCW columns)
+  DevBuf<SolveWork> bwork;       // bwd: (node, chunk of kCW columns [x row chunks if split])
   int nwork = 0, nbwork = 0, ch = 32;
+  int split = 0;                 // bwd rows split into kRB-row chunks (small top levels)
 };
 
 struct ULVImpl {
@@ -186,7 +189,10 @@ void ulv_factor_impl(ULVImpl& F, cudaStream_t s);
 struct SolveWS {
   int nrhs = 0;
   std::vector<double*> fin, yr, xout;  // per level (levels that are all pass-through alias)
+  std::vector<double*> bpart;          // split bwd levels: row-chunk partials
+  std::vector<unsigned*> bcnt;         // split bwd levels: per (node, column chunk) counters
   std::vector<DevBuf<double>> own;
+  std::vector<DevBuf<unsigned>> cnt_own;
   // sharded: the level-lg exchange; `extra` (nextra doubles per rank, set nextra before
   // solve_ws_alloc) rides along, gathered to extra_all (P x nextra) and, if extra_top is set,
   // tree-reduced over the ranks into extra_top.

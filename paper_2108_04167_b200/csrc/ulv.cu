@@ -392,10 +392,12 @@ void ulv_factor_impl(ULVImpl& F, cudaStream_t s) {
     while (ch > 8 && rows / ch < 148 * 8) ch /= 2;
     F_l.ch = ch;
     std::vector<SolveWork> wk, bk;
+    F_l.split = (l <= kSplitMaxLevel && l < L - 1) ? 1 : 0;
     for (int i = 0; i < F_l.nnodes; ++i) {
       if (l == L && sn[i].pt) continue;  // pass-through leaves: handled by leaf_pt_copy
       for (int c = 0; c < ceil_div(sn[i].R, ch); ++c) wk.push_back({i, c});
-      for (int c = 0; c < ceil_div(sn[i].R, kCW); ++c) bk.push_back({i, c});
+      const int nb = ceil_div(sn[i].R, kCW) * (F_l.split ? ceil_div(sn[i].R, kRB) : 1);
+      for (int c = 0; c < nb; ++c) bk.push_back({i, c});
     }
     F_l.work = upload(wk, s);
     F_l.nwork = (int)wk.size();
@@ -472,6 +474,99 @@ __global__ void __launch_bounds__(kBW * 32) ulv_bwd_kernel(const SolveNode* __re
   bwd_cols<NR>(M + N.moff, R, ush, j0, red, out + N.roff * NR);
 }
 
+// Backward sweep of a small level (few nodes: latency-bound): the rows are split too.  Work item
+// = (node, column chunk cc, row chunk rc of kRB rows); each CTA sums its rows (warp w: rows
+// i0 + w, i0 + w + kBW, ... in order; warps in order) into a partial slab, and the last CTA of
+// (node, cc) adds the row-chunk partials in rc order.  Used for levels l <= kSplitMaxLevel
+// (l < L-1), a rule of the global tree, so results stay P-invariant.
+template <int NR>
+__global__ void __launch_bounds__(kBW * 32) ulv_bwd_split_kernel(const SolveNode* __restrict__ nodes,
+                                                                 const SolveWork* __restrict__ work,
+                                                                 const double* __restrict__ M,
+                                                                 const double* __restrict__ in_s,
+                                                                 const double* __restrict__ in_r,
+                                                                 double* __restrict__ out,
+                                                                 double* __restrict__ part,
+                                                                 unsigned* __restrict__ cnt) {
+  const SolveWork wk = work[blockIdx.x];
+  const SolveNode N = nodes[wk.node];
+  const int R = N.R, tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
+  const int nrc = (R + kRB - 1) / kRB, cc = wk.chunk / nrc, rc = wk.chunk % nrc;
+  const int j0 = cc * kCW, i0 = rc * kRB, i1 = min(R, i0 + kRB);
+  if (N.pt) {  // identity operator (row chunk 0 copies)
+    if (rc == 0) {
+      const int j1 = min(R, j0 + kCW);
+      for (int e = tid; e < (j1 - j0) * NR; e += kBW * 32) out[(N.roff + j0) * NR + e] = in_s[(N.koff + j0) * NR + e];
+    }
+    return;
+  }
+  __shared__ double ush[kRB * NR];
+  __shared__ double red[kBW * kCW * NR];
+  for (int e = tid; e < (i1 - i0) * NR; e += kBW * 32) {
+    const int i = i0 + e / NR, c = e % NR;
+    ush[e] = (i < N.k) ? in_s[(N.koff + i) * NR + c] : in_r[(N.yoff + i - N.k) * NR + c];
+  }
+  __syncthreads();
+  const int ja = j0 + lane, jb = j0 + 32 + lane;
+  const bool va = ja < R, vb = jb < R;
+  const double* Mn = M + N.moff;
+  double aa[NR], ab[NR];
+#pragma unroll
+  for (int c = 0; c < NR; ++c) aa[c] = ab[c] = 0.0;
+  {  // this warp's rows i0 + wid + q*kBW (q < kRB/kBW): all loads in flight, then FMAs in row order
+    constexpr int NQ = kRB / kBW;
+    double ma[NQ], mb[NQ];
+#pragma unroll
+    for (int q = 0; q < NQ; ++q) {
+      const int i = i0 + wid + q * kBW;
+      const double* Mr = Mn + (int64_t)i * R;
+      ma[q] = (i < i1 && va) ? Mr[ja] : 0.0;
+      mb[q] = (i < i1 && vb) ? Mr[jb] : 0.0;
+    }
+#pragma unroll
+    for (int q = 0; q < NQ; ++q) {
+      const int i = i0 + wid + q * kBW;
+      if (i < i1) {
+#pragma unroll
+        for (int c = 0; c < NR; ++c) {
+          const double u = ush[(i - i0) * NR + c];
+          aa[c] = fma(ma[q], u, aa[c]);
+          ab[c] = fma(mb[q], u, ab[c]);
+        }
+      }
+    }
+  }
+#pragma unroll
+  for (int c = 0; c < NR; ++c) {
+    red[(wid * kCW + lane) * NR + c] = aa[c];
+    red[(wid * kCW + 32 + lane) * NR + c] = ab[c];
+  }
+  __syncthreads();
+  double* my = part + (int64_t)blockIdx.x * kCW * NR;
+  for (int e = tid; e < kCW * NR; e += kBW * 32) {
+    double t = red[e];
+#pragma unroll
+    for (int w = 1; w < kBW; ++w) t += red[w * kCW * NR + e];
+    my[e] = t;
+  }
+  __shared__ bool last;
+  __threadfence();
+  __syncthreads();
+  const int g = blockIdx.x - rc;  // first work item of (node, cc)
+  if (tid == 0) last = (atomicAdd(&cnt[g], 1u) == (unsigned)(nrc - 1));
+  __syncthreads();
+  if (!last) return;
+  __threadfence();
+  for (int e = tid; e < kCW * NR; e += kBW * 32) {
+    const int jj = e / NR;
+    if (j0 + jj >= R) continue;
+    double t = 0.0;
+    for (int q = 0; q < nrc; ++q) t += part[((int64_t)(g + q) * kCW) * NR + e];
+    out[(N.roff + j0) * NR + e] = t;
+  }
+  if (tid == 0) cnt[g] = 0u;
+}
+
 // pass-through leaves: fwd  fin_{L-1}[map[p]] = fin_L[p];  bwd  xout_L[p] = xout_{L-1}[map[p]]
 template <int NR>
 __global__ void leaf_pt_copy_kernel(const int64_t* __restrict__ map, int64_t n, int bwd,
@@ -498,12 +593,22 @@ void solve_ws_alloc(const ULVImpl& F, int nrhs, SolveWS& ws) {
     ws.own.emplace_back(std::max<int64_t>(1, rows) * nrhs);
     return ws.own.back().p;
   };
-  ws.own.reserve(3 * (L + 1) + 2);
+  ws.own.reserve(4 * (L + 1) + 2);
+  ws.cnt_own.reserve(L + 1);
   ws.fin[L] = mk(H.nloc());
   if (H.sh.on()) exch_ws_alloc(H, nrhs, ws.nextra, ws.xw);
   for (int l = L; l >= 1; --l) ws.fin[l - 1] = F.lv[l].allpt ? ws.fin[l] : mk(F.lv[l].sumK);
   for (int l = 0; l <= L; ++l) if (!F.lv[l].allpt) ws.yr[l] = mk(F.lv[l].sumY);
   ws.xout[0] = mk(F.lv[0].sumR);
+  ws.bpart.assign(L + 1, nullptr);
+  ws.bcnt.assign(L + 1, nullptr);
+  for (int l = 0; l <= L; ++l)
+    if (F.lv[l].split && F.lv[l].nbwork > 0) {
+      ws.bpart[l] = mk((int64_t)F.lv[l].nbwork * kCW);
+      ws.cnt_own.emplace_back(F.lv[l].nbwork);
+      CUDA_CHECK(cudaMemsetAsync(ws.cnt_own.back().p, 0, F.lv[l].nbwork * sizeof(unsigned), g_alloc_stream));
+      ws.bcnt[l] = ws.cnt_own.back().p;
+    }
   for (int l = 1; l <= L; ++l) ws.xout[l] = F.lv[l].allpt ? ws.xout[l - 1] : mk(F.lv[l].sumR);
 }
 
@@ -521,6 +626,12 @@ template <int NR>
 static void bwd_level(const ULVImpl& F, SolveWS& ws, int l, const SolveWork* work, int nwork, cudaStream_t s) {
   const auto& lv = F.lv[l];
   if (nwork <= 0) return;
+  if (lv.split) {
+    ulv_bwd_split_kernel<NR><<<nwork, kBW * 32, 0, s>>>(lv.nodes.p, work, lv.M.p, l > 0 ? ws.xout[l - 1] : nullptr,
+                                                        ws.yr[l], ws.xout[l], ws.bpart[l], ws.bcnt[l]);
+    g_launches.fetch_add(1);
+    return;
+  }
   const size_t sm = ((size_t)lv.maxR + (size_t)kBW * kCW) * NR * sizeof(double);
   ulv_bwd_kernel<NR><<<nwork, kBW * 32, sm, s>>>(lv.nodes.p, work, lv.M.p, l > 0 ? ws.xout[l - 1] : nullptr, ws.yr[l],
                                                  ws.xout[l]);

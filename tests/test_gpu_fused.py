@@ -1,6 +1,6 @@
 """The fused bottom level of the ADMM iteration (one 8-CTA cluster per level-(L-1) node:
 backward sweep -> epilogue -> next forward sweep) must give BITWISE the same iterates as the
-unfused level-by-level sweep (SVMHSS_FUSE_BOTTOM=0): both use the same device functions and
+unfused level-by-level sweep (the default; SVMHSS_FUSE_BOTTOM=1 fuses): both use the same device functions and
 the same chunk-ordered leaf sums.  Also pinned to the oracle (tests/test_gpu_parity.py covers
 the unfused order at the north-star tolerances)."""
 import os
