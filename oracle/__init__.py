@@ -15,4 +15,4 @@ It shares no code with the CUDA path; the only shared module is `datagen`
 Parity status: every function is pinned by `tests/test_oracle_*.py` against
 closed forms, brute force or library routines.
 """
-from . import rng, kernel, tree, hss, ulv, admm, svm, qp  # noqa: F401
+from . import rng, kernel, tree, hss, ann, ulv, admm, svm, qp  # noqa: F401
