@@ -125,9 +125,13 @@ def measure_dgemm(dev, N=8192, reps=5):
     return 2.0 * N ** 3 / best / 1e12
 
 
-def cfg_opts(cfg):
-    return dict(leaf_size=cfg["leaf"], rel_tol=cfg["rel_tol"], abs_tol=cfg["abs_tol"], max_rank=cfg["cap"],
-                oversample=cfg["s"] - cfg["cap"], omega_seed=cfg["seed_omega"], tree_seed=cfg["seed_tree"])
+def cfg_opts(cfg, sampling="sketch"):
+    o = dict(leaf_size=cfg["leaf"], rel_tol=cfg["rel_tol"], abs_tol=cfg["abs_tol"], max_rank=cfg["cap"],
+             oversample=cfg["s"] - cfg["cap"], omega_seed=cfg["seed_omega"], tree_seed=cfg["seed_tree"])
+    if sampling == "ann":
+        o.update(sampling="ann", ann_neighbors=cfg["ann_neighbors"], ann_trees=cfg["ann_trees"],
+                 ann_leaf=cfg["ann_leaf"], ann_seed=cfg["ann_seed"])
+    return o
 
 
 # ----------------------------------------------------------------------------- reference arm
@@ -245,6 +249,9 @@ def main():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-predict", action="store_true")
+    ap.add_argument("--sampling", default="sketch", choices=["sketch", "ann"],
+                    help="compression sampling: the randomized sketch (north star, default) or HSS-ANN "
+                         "column sampling (SURVEY 8(f) N1)")
     args = ap.parse_args()
     rank = int(os.environ.get("RANK", 0))
     world = int(os.environ.get("WORLD_SIZE", 1))
@@ -280,7 +287,7 @@ def main():
     t0, t1 = rank * nt // world, (rank + 1) * nt // world
     Fd, yd, Ftd = (torch.from_numpy(a).to(dev) for a in (F, y, np.ascontiguousarray(Ft[t0:t1])))
     stream = torch.cuda.current_stream()
-    opts = cfg_opts(cfg)
+    opts = cfg_opts(cfg, args.sampling)
     opts["comm"] = comm
 
     def step():
@@ -336,7 +343,8 @@ def main():
     line = {"metric": METRIC, "value": value, "unit": "iters/s", "n_gpus": world, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": ms_total / args.steps, "higher_is_better": True,
             "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-            "config": {"workload": cfg["name"], "n": n, "n_test": nt, "r": cfg["r"], "h": h, "C": Cs,
+            "config": {"workload": cfg["name"] + ("" if args.sampling == "sketch" else "+ann"),
+                       "sampling": args.sampling, "n": n, "n_test": nt, "r": cfg["r"], "h": h, "C": Cs,
                        "beta": cfg["beta"], "max_it": max_it, "leaf": cfg["leaf"], "cap": cfg["cap"],
                        "s": cfg["s"], "rel_tol": cfg["rel_tol"],
                        "parallelism": f"subtree-sharded over {world} (NCCL allgather per phase / iteration)"

@@ -57,11 +57,20 @@ _CONFIGS = {
 _BETA = {1: 1e4, 2: 1e5, 3: None, 4: None}
 _BETA_PER_H = {4: {0.25: 1e2, 0.5: 1e3, 1.0: 1e4, 2.0: 1e4, 4.0: 1e3}}
 
+# HSS-ANN sampling knobs (readings N1-N3): neighbours per point (the paper's
+# Table 4 setting "hss_approximate_neighbors 64"), random-projection trees, their leaf
+# size (<= 256; leaf * r * 8 bytes must fit shared memory, hence 128 for r = 123), seed 4000+c.
+_ANN = dict(ann_neighbors=64, ann_trees=4, ann_leaf=256)
+_ANN_LEAF = {2: 128}
+
 for _c, _cfg in _CONFIGS.items():
     _cfg["id"] = _c
     _cfg["seed_data"] = 1000 + _c
     _cfg["seed_omega"] = 2000 + _c
     _cfg["seed_tree"] = 3000 + _c
+    _cfg.update(_ANN)
+    _cfg["ann_leaf"] = _ANN_LEAF.get(_c, _ANN["ann_leaf"])
+    _cfg["ann_seed"] = 4000 + _c
     if _cfg["beta"] is None:
         b = _BETA.get(_c)
         _cfg["beta"] = b if b is not None else beta_schedule(_cfg["n"])

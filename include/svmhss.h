@@ -89,7 +89,18 @@ typedef struct {
                               node's rank is min(ranks[t], rows_t, s).  NULL = adaptive. */
   hss_comm_t comm;         /* nullable: single GPU.  Else subtree sharding over comm's ranks;
                               the factorization and ADMM inherit it from the hss_t. */
+  /* Column sampling of the compression:
+   *  HSS_SAMPLING_SKETCH (0): randomized sketch S = K Omega of all columns (H1-H5);
+   *  HSS_SAMPLING_ANN (1): HSS-ANN (readings N1-N3): per node, Y = K(A_t, C_t) on
+   *    s sampled columns chosen from the active rows' approximate nearest neighbours
+   *    (ann_trees random-projection trees of leaf size ann_leaf <= 256, ann_neighbors per
+   *    point, ann_trees * ann_neighbors <= 256, ann_leaf * r * 8 <= 227 KB), random-filled
+   *    from ann_seed; omega_seed is unused. */
+  int32_t sampling;
+  int32_t ann_neighbors, ann_trees, ann_leaf;
+  uint64_t ann_seed;
 } hss_opts;
+enum { HSS_SAMPLING_SKETCH = 0, HSS_SAMPLING_ANN = 1 };
 
 /* Build statistics (D6 / P:366-367 "Compression", "Memory"). */
 typedef struct {
@@ -183,6 +194,11 @@ int svm_train_predict_host(const double* F, const double* y, int64_t n, int32_t 
                            int8_t* labels_out, double* timings_ms);
 
 /* ---- debug / parity exports of individual hot-path steps ---- */
+/* N1: the ANN lists of HSS-ANN sampling.  F: n x r row-major (device, ORIGINAL order);
+ * idx_out: n x kappa int64 original indices sorted by (squared distance, index), -1 padded;
+ * d_out: n x kappa squared distances (+inf padded).  Same limits as hss_opts' ann fields. */
+int hss_ann_lists(const double* F, int64_t n, int32_t r, int32_t kappa, int32_t trees, int32_t leaf,
+                  uint64_t seed, int64_t* idx_out, double* d_out, void* stream);
 /* R1-R3: Omega rows for the given ORIGINAL indices (device int64 idx, count rows), s cols. */
 int hss_omega(uint64_t seed, const int64_t* idx, int64_t rows, int32_t s, double* out, void* stream);
 /* T1-T4: the permutation only (device int64 perm_out, n). */

@@ -34,6 +34,25 @@ def build(F, cfg, h=None, ranks=None, S=None, timings=None):
     return perm, ranges, Om, H
 
 
+def build_ann(F, cfg, h=None, ranks=None, timings=None):
+    """Tree + ANN lists + HSS-ANN compression (N1-N3).  Returns (perm, ranges, (idx, d), hss)."""
+    from . import ann as _ann
+    t = time.perf_counter()
+    h = cfg["h"] if h is None else h
+    perm, ranges = _tree.build_tree(F, cfg["leaf"], cfg["seed_tree"])
+    t1 = time.perf_counter()
+    idx, d = _ann.knn(F, cfg["ann_neighbors"], cfg["ann_trees"], cfg["ann_leaf"], cfg["ann_seed"])
+    t2 = time.perf_counter()
+    kw = dict(ranks=ranks) if ranks is not None else dict(
+        rel_tol=cfg["rel_tol"], abs_tol=cfg["abs_tol"], cap=cfg["cap"])
+    H = _ann.compress_ann(F[perm], h, ranges, perm, idx, d, cfg["s"], cfg["ann_seed"], **kw)
+    if timings is not None:
+        timings["tree"] = t1 - t
+        timings["ann"] = t2 - t1
+        timings["compress"] = time.perf_counter() - t2
+    return perm, ranges, (idx, d), H
+
+
 def train(F, y, cfg, *, h=None, C_list=None, ranks=None, max_it=None, trace_every=0,
           Ftest=None, timings=None):
     timings = {} if timings is None else timings

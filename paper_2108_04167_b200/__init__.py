@@ -231,10 +231,16 @@ class ULV:
             pass
 
 
+SAMPLING = {"sketch": 0, "ann": 1}
+
+
 def make_opts(leaf_size, rel_tol=0.0, abs_tol=0.0, max_rank=64, oversample=16, omega_seed=0,
-              tree_seed=0, ranks=None, comm=None):
+              tree_seed=0, ranks=None, comm=None, sampling="sketch", ann_neighbors=64, ann_trees=4,
+              ann_leaf=256, ann_seed=0):
     o = HssOpts()
     o.comm = comm.handle if comm is not None else None
+    o.sampling = SAMPLING[sampling]
+    o.ann_neighbors, o.ann_trees, o.ann_leaf, o.ann_seed = int(ann_neighbors), int(ann_trees), int(ann_leaf), int(ann_seed)
     o.leaf_size, o.rel_tol, o.abs_tol = int(leaf_size), float(rel_tol), float(abs_tol)
     o.max_rank, o.oversample = int(max_rank), int(oversample)
     o.omega_seed, o.tree_seed = int(omega_seed), int(tree_seed)
@@ -246,12 +252,15 @@ def make_opts(leaf_size, rel_tol=0.0, abs_tol=0.0, max_rank=64, oversample=16, o
 
 
 def hss_build(F, h, leaf_size, rel_tol=0.0, abs_tol=0.0, max_rank=64, oversample=16, omega_seed=0,
-              tree_seed=0, ranks=None, comm=None, stream=None) -> HSS:
+              tree_seed=0, ranks=None, comm=None, sampling="sketch", ann_neighbors=64, ann_trees=4,
+              ann_leaf=256, ann_seed=0, stream=None) -> HSS:
     """hss_build (Alg. 3 line 1): F is a CUDA float64 (n, r) tensor, original order
-    (all n points on every rank when `comm` shards the tree)."""
+    (all n points on every rank when `comm` shards the tree).  sampling="ann" selects HSS-ANN
+    column sampling instead of the randomized sketch."""
     _cuda_f64(F, "F")
     n, r = F.shape
-    o, keep = make_opts(leaf_size, rel_tol, abs_tol, max_rank, oversample, omega_seed, tree_seed, ranks, comm)
+    o, keep = make_opts(leaf_size, rel_tol, abs_tol, max_rank, oversample, omega_seed, tree_seed, ranks, comm,
+                        sampling, ann_neighbors, ann_trees, ann_leaf, ann_seed)
     hdl = ct.c_void_p()
     check(_L.hss_build(ptr(F), n, r, float(h), ct.byref(o), _stream(stream), ct.byref(hdl)))
     del keep
@@ -341,6 +350,18 @@ def svm_train_predict_host(F, y, h, beta, C, max_it, Ftest=None, **opt_kw):
 
 
 # ---- debug / parity exports
+def hss_ann_lists(F, kappa, trees, leaf, seed, stream=None):
+    """N1 ANN lists of the rows of F (original order): (idx (n, kappa) int64, d (n, kappa))."""
+    import torch
+    _cuda_f64(F, "F")
+    n, r = F.shape
+    idx = torch.empty((n, kappa), dtype=torch.int64, device=F.device)
+    d = torch.empty((n, kappa), dtype=torch.float64, device=F.device)
+    check(_L.hss_ann_lists(ptr(F), n, r, int(kappa), int(trees), int(leaf), int(seed), ptr(idx), ptr(d),
+                           _stream(stream)))
+    return idx, d
+
+
 def hss_omega(seed, idx, s, stream=None):
     import torch
     idx = idx.to(torch.int64).contiguous()

@@ -27,7 +27,9 @@ class HssError(RuntimeError):
 class HssOpts(ct.Structure):
     _fields_ = [("leaf_size", ct.c_int32), ("rel_tol", ct.c_double), ("abs_tol", ct.c_double),
                 ("max_rank", ct.c_int32), ("oversample", ct.c_int32), ("omega_seed", ct.c_uint64),
-                ("tree_seed", ct.c_uint64), ("ranks", ct.POINTER(ct.c_int32)), ("comm", ct.c_void_p)]
+                ("tree_seed", ct.c_uint64), ("ranks", ct.POINTER(ct.c_int32)), ("comm", ct.c_void_p),
+                ("sampling", ct.c_int32), ("ann_neighbors", ct.c_int32), ("ann_trees", ct.c_int32),
+                ("ann_leaf", ct.c_int32), ("ann_seed", ct.c_uint64)]
 
 
 # int (*hss_allgather_fn)(void* ctx, const void* send, void* recv, size_t bytes)
@@ -61,7 +63,7 @@ EXPORTS = ["hss_build", "hss_info", "hss_matvec", "hss_ulv_factor", "ulv_info", 
            "admm_svm_train", "svm_predict", "svm_train_predict_host", "hss_omega", "hss_tree",
            "hss_kernel_matmul", "hss_kernel_block", "hss_node", "hss_free", "ulv_free",
            "hss_last_error", "hss_version", "hss_launch_count", "hss_comm_nccl_id",
-           "hss_comm_init_nccl", "hss_comm_init_host", "hss_comm_free"]
+           "hss_comm_init_nccl", "hss_comm_init_host", "hss_comm_free", "hss_ann_lists"]
 
 _lib = None
 
@@ -87,6 +89,7 @@ def load():
     L.svm_train_predict_host.argtypes = [vp, vp, i64, i32, dbl, ct.POINTER(HssOpts), dbl, vp, i32,
                                          i32, vp, i64, vp, vp, vp, vp, vp]
     L.hss_omega.argtypes = [u64, vp, i64, i32, vp, vp]
+    L.hss_ann_lists.argtypes = [vp, i64, i32, i32, i32, i32, u64, vp, vp, vp]
     L.hss_tree.argtypes = [vp, i64, i32, i32, u64, vp, vp]
     L.hss_kernel_matmul.argtypes = [vp, i64, vp, i64, i32, dbl, vp, i32, i32, vp, vp]
     L.hss_kernel_block.argtypes = [vp, i64, vp, i64, i32, dbl, vp, vp]

@@ -69,6 +69,14 @@ static void validate_opts(const hss_opts* o, int64_t n, int32_t r, double h) {
   require(s <= (1 << 20), "hss_build: s = max_rank + oversample must be <= 2^20 (R1 column field)");
   require(s % 2 == 0, "hss_build: s = max_rank + oversample must be even");
   require(o->rel_tol >= 0 && o->abs_tol >= 0, "hss_build: tolerances must be >= 0");
+  require(o->sampling == HSS_SAMPLING_SKETCH || o->sampling == HSS_SAMPLING_ANN, "hss_build: unknown sampling");
+  if (o->sampling == HSS_SAMPLING_ANN) {
+    require(o->ann_neighbors >= 1 && o->ann_trees >= 1 && o->ann_leaf >= 2 && o->ann_leaf <= 256,
+            "hss_build: ANN needs ann_neighbors >= 1, ann_trees >= 1, 2 <= ann_leaf <= 256");
+    require((int64_t)o->ann_trees * o->ann_neighbors <= 256, "hss_build: ann_trees * ann_neighbors must be <= 256");
+    require((int64_t)o->ann_leaf * r * 8 <= 227 * 1024, "hss_build: ann_leaf * r too large (lower ann_leaf)");
+    require(s <= 1152, "hss_build: s must be <= 1152");
+  }
 }
 
 }  // namespace svmhss
@@ -341,6 +349,20 @@ int svm_train_predict_host(const double* F, const double* y, int64_t n, int32_t 
       CUDA_CHECK(cudaEventElapsedTime(&t, ev[6], ev[7])); timings_ms[6] = t;
       CUDA_CHECK(cudaEventElapsedTime(&t, ev[0], ev[7])); timings_ms[7] = t;
     }
+  });
+}
+
+int hss_ann_lists(const double* F, int64_t n, int32_t r, int32_t kappa, int32_t trees, int32_t leaf,
+                  uint64_t seed, int64_t* idx_out, double* d_out, void* stream) {
+  return guarded([&] {
+    StreamScope ss__((cudaStream_t)stream);
+    require(F && idx_out && d_out, "hss_ann_lists: NULL pointer");
+    require(n >= 1 && r >= 1, "hss_ann_lists: bad sizes");
+    cudaStream_t s = (cudaStream_t)stream;
+    const int rp = (r + 3) / 4 * 4;
+    DevBuf<double> Fpad((size_t)n * rp);
+    pad_rows(F, n, r, rp, Fpad.p, s);
+    ann_build(Fpad.p, n, r, rp, kappa, trees, leaf, seed, idx_out, d_out, s);
   });
 }
 

@@ -51,8 +51,10 @@ __global__ void select_kernel(const SelNode* __restrict__ nd, const int* __restr
   for (int64_t e = threadIdx.x; e < tot; e += blockDim.x) {
     const int j = (int)(e / s), c = (int)(e % s);
     const int sel = N.pt ? j : piv[N.roff + j];
-    Ysk[(N.koff + j) * s + c] = Y[(N.roff + sel) * s + c];
-    if (N.pt) Omp[(N.koff + j) * s + c] = Om[(N.roff + j) * s + c];
+    if (Y) {
+      Ysk[(N.koff + j) * s + c] = Y[(N.roff + sel) * s + c];
+      if (N.pt) Omp[(N.koff + j) * s + c] = Om[(N.roff + j) * s + c];
+    }
     if (c == 0) J[N.koff + j] = act[N.roff + sel];
   }
 }
@@ -114,9 +116,10 @@ void hss_build_impl(HSSImpl& H, const double* F, int64_t n, int r, double h, con
   H.st.n = n; H.st.r = r; H.st.L = L; H.st.s = S; H.st.leaf_size = H.m;
 
   // ---- T1-T4: tree (every rank builds the whole tree: deterministic, identical)
+  const bool ann = o.sampling == HSS_SAMPLING_ANN;
+  DevBuf<double> Fpad((size_t)n * rp);
   {
     EventTimer tm(s);
-    DevBuf<double> Fpad((size_t)n * rp);
     pad_rows(F, n, r, rp, Fpad.p, s);
     H.perm.alloc(n);
     H.Fp.alloc((size_t)n * rp);
@@ -164,13 +167,26 @@ void hss_build_impl(HSSImpl& H, const double* F, int64_t n, int r, double h, con
   }
   // ---- R1-R3: Omega_p (all n rows: the sketch's right-hand matrix), H1: this rank's rows of
   // the masked sketch (diagonal leaf blocks excluded -> Y_leaf directly)
-  DevBuf<double> Om((size_t)n * S), Y((size_t)std::max<int64_t>(1, nl) * S);
-  {
+  DevBuf<double> Om(ann ? 0 : (size_t)n * S), Y(ann ? 0 : (size_t)std::max<int64_t>(1, nl) * S);
+  // HSS-ANN (N1): neighbour lists of all points, re-indexed by tree position
+  const int kap = ann ? o.ann_neighbors : 0;
+  DevBuf<int64_t> ann_pos(ann ? (size_t)n * kap : 0);
+  DevBuf<double> ann_dp(ann ? (size_t)n * kap : 0);
+  if (ann) {
+    EventTimer tm(s);
+    DevBuf<int64_t> aidx((size_t)n * kap);
+    DevBuf<double> ad((size_t)n * kap);
+    ann_build(Fpad.p, n, r, rp, kap, o.ann_trees, o.ann_leaf, o.ann_seed, aidx.p, ad.p, s);
+    ann_to_tree(H, kap, aidx.p, ad.p, ann_pos.p, ann_dp.p, s);
+    CUDA_CHECK(cudaStreamSynchronize(s));
+    H.st.ms_sketch = tm.stop_ms();
+  } else {
     EventTimer tm(s);
     omega_rows(o.omega_seed, H.perm.p, n, S, Om.p, s);
     H.st.ms_omega = tm.stop_ms();
   }
-  {
+  Fpad.release();
+  if (!ann) {
     EventTimer tm(s);
     KmmArgs a{};
     a.Fa = H.Fp.p + H.lo_g * rp; a.nua = H.nu.p + H.lo_g; a.na = nl;
@@ -189,7 +205,7 @@ void hss_build_impl(HSSImpl& H, const double* F, int64_t n, int r, double h, con
   LAUNCH_CHECK();
   const int64_t* act = act0.p;
   DevBuf<double> Ycur = std::move(Y), Omhold;
-  const double* omcur = Om.p + H.lo_g * S;  // Omega^ of the leaves = this rank's Omega rows
+  const double* omcur = ann ? nullptr : Om.p + H.lo_g * S;  // Omega^ of the leaves = this rank's rows
   int cap_hits = 0, maxk = 0, npt = 0;        // levels < lg (replicated) counted once
   int64_t sub_bytes = (int64_t)H.D.bytes(), top_bytes = 0;
   int sub_cap = 0, sub_pt = 0, sub_maxk = 0;  // this rank's subtree (levels >= lg)
@@ -210,7 +226,13 @@ void hss_build_impl(HSSImpl& H, const double* F, int64_t n, int r, double h, con
       for (int q = 0; q < nn; ++q)
         kfix[q] = std::max(0, std::min(std::min(o.ranks[H.node_id(l, f + q)], lv[f + q].rows), S));
     DevBuf<double> Wk((size_t)std::max<int64_t>(1, sumR) * S);
-    CUDA_CHECK(cudaMemcpyAsync(Wk.p, Ycur.p, (size_t)sumR * S * sizeof(double), cudaMemcpyDeviceToDevice, s));
+    if (ann) {  // N2-N3: Y_t = K(A_t, C_t) on the sampled columns
+      DevBuf<int64_t> Cs((size_t)std::max(1, nn) * S);
+      ann_sample_level(H, l, act, ann_pos.p, ann_dp.p, kap, o.ann_seed, Cs.p, s);
+      ann_y_level(H, l, act, Cs.p, Wk.p, s);
+    } else {
+      CUDA_CHECK(cudaMemcpyAsync(Wk.p, Ycur.p, (size_t)sumR * S * sizeof(double), cudaMemcpyDeviceToDevice, s));
+    }
     DevBuf<int> piv(std::max<int64_t>(1, sumR)), kd(nn), ch(nn);
     CUDA_CHECK(cudaMemsetAsync(ch.p, 0, nn * sizeof(int), s));
     std::vector<CpqrProb> cp;
@@ -254,7 +276,7 @@ void hss_build_impl(HSSImpl& H, const double* F, int64_t n, int r, double h, con
     btrsm(tp, false, s);
     H.U[l].alloc(std::max<int64_t>(1, sumU));
     H.J[l].alloc(std::max<int64_t>(1, sumK));
-    DevBuf<double> Ysk((size_t)std::max<int64_t>(1, sumK) * S), Omp((size_t)std::max<int64_t>(1, sumK) * S);
+    DevBuf<double> Ysk(ann ? 1 : (size_t)std::max<int64_t>(1, sumK) * S), Omp(ann ? 1 : (size_t)std::max<int64_t>(1, sumK) * S);
     std::vector<SelNode> sn(nn);
     for (int q = 0; q < nn; ++q) {
       auto& nd = lv[f + q];
@@ -263,11 +285,11 @@ void hss_build_impl(HSSImpl& H, const double* F, int64_t n, int r, double h, con
     auto dsn = upload(sn, s);
     scatter_u_kernel<<<nn, 256, 0, s>>>(dsn.p, piv.p, Wk.p, S, H.U[l].p);
     LAUNCH_CHECK();
-    select_kernel<<<nn, 256, 0, s>>>(dsn.p, piv.p, act, Ycur.p, omcur, S, H.J[l].p, Ysk.p, Omp.p);
+    select_kernel<<<nn, 256, 0, s>>>(dsn.p, piv.p, act, ann ? nullptr : Ycur.p, omcur, S, H.J[l].p, Ysk.p, Omp.p);
     LAUNCH_CHECK();
     // Omega'_t = U_t^T Omega^_t
     std::vector<GemmProb> gp;
-    for (int i = f; i < e; ++i) {
+    for (int i = f; i < e && !ann; ++i) {
       auto& nd = lv[i];
       if (!nd.pt && nd.k > 0)
         gp.push_back({nd.k, S, nd.rows, H.U[l].p + nd.uoff, 1, nd.k, omcur + nd.roff * S, S, 1,
@@ -283,8 +305,8 @@ void hss_build_impl(HSSImpl& H, const double* F, int64_t n, int r, double h, con
       std::vector<double> hh(hdr, 0.0);
       std::memcpy(hh.data(), &rec, sizeof(rec));
       h2d(send.p, hh.data(), hdr, s);
-      if (own.k > 0) {
-        CUDA_CHECK(cudaMemcpyAsync(send.p + hdr, H.J[l].p, own.k * 8, cudaMemcpyDeviceToDevice, s));
+      if (own.k > 0) CUDA_CHECK(cudaMemcpyAsync(send.p + hdr, H.J[l].p, own.k * 8, cudaMemcpyDeviceToDevice, s));
+      if (own.k > 0 && !ann) {
         CUDA_CHECK(cudaMemcpyAsync(send.p + hdr + S, Ysk.p, (size_t)own.k * S * 8, cudaMemcpyDeviceToDevice, s));
         CUDA_CHECK(cudaMemcpyAsync(send.p + hdr + S + (int64_t)S * S, Omp.p, (size_t)own.k * S * 8,
                                    cudaMemcpyDeviceToDevice, s));
@@ -314,12 +336,13 @@ void hss_build_impl(HSSImpl& H, const double* F, int64_t n, int r, double h, con
       H.lg_koff = upload(koffs, s);
       H.lg_k = upload(ks, s);
       DevBuf<int64_t> Jall(std::max<int64_t>(1, gK));
-      DevBuf<double> Yall((size_t)std::max<int64_t>(1, gK) * S), Oall((size_t)std::max<int64_t>(1, gK) * S);
+      DevBuf<double> Yall(ann ? 1 : (size_t)std::max<int64_t>(1, gK) * S), Oall(ann ? 1 : (size_t)std::max<int64_t>(1, gK) * S);
       for (int p = 0; p < sh.P; ++p) {
         const int64_t k = ks[p];
         if (!k) continue;
         const double* src = recv.p + p * slot;
         CUDA_CHECK(cudaMemcpyAsync(Jall.p + koffs[p], src + hdr, k * 8, cudaMemcpyDeviceToDevice, s));
+        if (ann) continue;
         CUDA_CHECK(cudaMemcpyAsync(Yall.p + koffs[p] * S, src + hdr + S, (size_t)k * S * 8, cudaMemcpyDeviceToDevice, s));
         CUDA_CHECK(cudaMemcpyAsync(Oall.p + koffs[p] * S, src + hdr + S + (int64_t)S * S, (size_t)k * S * 8,
                                    cudaMemcpyDeviceToDevice, s));
@@ -347,7 +370,7 @@ void hss_build_impl(HSSImpl& H, const double* F, int64_t n, int r, double h, con
       kb.push_back({a.k, b.k, H.J[l].p + a.koff, 0, H.J[l].p + b.koff, 0, H.B[l - 1].p + pv[p].boff, b.k, 0.0});
     }
     kernel_blocks(H.Fp.p, rp, r, h, kb, s);
-    if (l - 1 >= 1) {
+    if (l - 1 >= 1 && !ann) {
       std::vector<GemmProb> up;
       for (int p = pf; p < pe; ++p) {
         auto &a = lv[2 * p], &b = lv[2 * p + 1];
@@ -364,7 +387,7 @@ void hss_build_impl(HSSImpl& H, const double* F, int64_t n, int r, double h, con
     Ycur = std::move(Ysk);
     Omhold = std::move(Omp);
     omcur = Omhold.p;
-    if (l == L) Om.release();
+    if (l == L && !ann) Om.release();
   }
   H.lv[0][0].rows = H.lv[1][0].k + H.lv[1][1].k;
   H.st.ms_compress = tmc.stop_ms();

@@ -57,8 +57,10 @@ void bcopy(const std::vector<CopyProb>& probs, cudaStream_t s);
 // ---------------------------------------------------------------- tree (tree.cu)
 // T1-T4 on the GPU. F: n x rp (padded, device). Outputs perm (n int64, device) and the
 // permuted features Fp (n x rp) / norms nu.
+// rp_tree_index >= 0: random-projection tree of HSS-ANN (reading N1; tree_seed = ann seed)
+// instead of the PCA tree.
 void build_tree(const double* Fpad, int64_t n, int r, int rp, int m, uint64_t tree_seed,
-                int64_t* perm, double* Fp_out, cudaStream_t s);
+                int64_t* perm, double* Fp_out, cudaStream_t s, int rp_tree_index = -1);
 int num_levels(int64_t n, int m);
 void node_ranges(int64_t n, int L, std::vector<std::vector<std::pair<int64_t, int64_t>>>& out);
 
@@ -119,6 +121,19 @@ void hss_build_impl(HSSImpl& H, const double* F, int64_t n, int r, double h,
 // rows [lo_g, hi_g) of the tree order.
 void hss_matvec_tree(const HSSImpl& H, const double* V, double* out, int nrhs, cudaStream_t s);
 int64_t level_sumk(const HSSImpl& H, int l);
+
+// ---------------------------------------------------------------- HSS-ANN (ann.cu; N1-N3)
+// ANN lists of all n points (ORIGINAL order in and out): idx n x kappa original indices, d the
+// squared distances; -1 / +inf padding.
+void ann_build(const double* Fpad, int64_t n, int r, int rp, int kappa, int trees, int leaf, uint64_t seed,
+               int64_t* idx_out, double* d_out, cudaStream_t s);
+void ann_to_tree(const HSSImpl& H, int kappa, const int64_t* idx, const double* d, int64_t* pos, double* dp,
+                 cudaStream_t s);
+// sampled columns C (this rank's nodes of level l, nn x s, sorted tree positions, -1 padded)
+void ann_sample_level(const HSSImpl& H, int l, const int64_t* act, const int64_t* ann_pos, const double* ann_d,
+                      int kappa, uint64_t seed, int64_t* C, cudaStream_t s);
+// Y_t = K(A_t, C_t) into the level's row-packed W (rows x s per node)
+void ann_y_level(const HSSImpl& H, int l, const int64_t* act, const int64_t* C, double* W, cudaStream_t s);
 
 // ---------------------------------------------------------------- sharded exchanges
 // Workspace of the per-iteration level-lg exchange (allocated once: graph-capturable).

@@ -158,6 +158,24 @@ __global__ void project_kernel(const double* __restrict__ F, int rp, int r, int6
   pos[i] = (int)i;
 }
 
+// N1: random-projection key p = sum_f s_f F[i, f] (features in order; s_f = +-1 from bit 63 of
+// splitmix64(key_t + 2^20 * node_id + f)); s_f * x is exact, so the sum is the same with or
+// without contraction.
+__global__ void rp_project_kernel(const double* __restrict__ F, int rp, int r, int64_t n,
+                                  const int* __restrict__ node_of, uint64_t key_t, int id0,
+                                  uint64_t* __restrict__ key, int* __restrict__ pos) {
+  const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  const uint64_t base = key_t + (uint64_t)(id0 + node_of[i]) * (1ull << 20);
+  double p = 0.0;
+  for (int f = 0; f < r; ++f) {
+    const double x = F[i * rp + f];
+    p = __dadd_rn(p, (splitmix64(base + (uint64_t)f) >> 63) ? -x : x);
+  }
+  key[i] = order_key(p);
+  pos[i] = (int)i;
+}
+
 __global__ void gather_key_kernel(const uint64_t* __restrict__ key, const int* __restrict__ order,
                                   int64_t n, uint64_t* __restrict__ out) {
   const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
@@ -182,7 +200,7 @@ __global__ void iota64_kernel(int64_t* a, int64_t n) {
 }
 
 void build_tree(const double* Fpad, int64_t n, int r, int rp, int m, uint64_t tree_seed,
-                int64_t* perm, double* Fp_out, cudaStream_t s) {
+                int64_t* perm, double* Fp_out, cudaStream_t s, int rp_tree_index) {
   const int L = num_levels(n, m);
   require(n < ((int64_t)1 << 31), "tree: n must be < 2^31");
   std::vector<std::vector<std::pair<int64_t, int64_t>>> rg;
@@ -218,6 +236,12 @@ void build_tree(const double* Fpad, int64_t n, int r, int rp, int m, uint64_t tr
     auto d_cnt = upload(cnt, s);
     auto d_nof = upload(nof, s);
     auto d_sb = upload(segb, s), d_se = upload(sege, s);
+    if (rp_tree_index >= 0) {  // N1: random-projection tree
+      rp_project_kernel<<<ceil_div(n, 256), 256, 0, s>>>(Fa.p, rp, r, n, d_nof.p,
+                                                         splitmix64(tree_seed + (uint64_t)rp_tree_index),
+                                                         (1 << l) - 1, k1.p, p1.p);
+      LAUNCH_CHECK();
+    } else {
     const int nch = (int)ch.size();
     DevBuf<double> part((size_t)nch * r * r), mean((size_t)nn * r), dir((size_t)nn * r);
     chunk_sum_kernel<<<nch, 128, 0, s>>>(Fa.p, rp, r, d_ch.p, part.p);
@@ -237,6 +261,7 @@ void build_tree(const double* Fpad, int64_t n, int r, int rp, int m, uint64_t tr
     }
     project_kernel<<<ceil_div(n, 256), 256, 0, s>>>(Fa.p, rp, r, n, d_nof.p, mean.p, dir.p, k1.p, p1.p);
     LAUNCH_CHECK();
+    }
     // pass 1: stable sort positions by original index within each node
     size_t tb1 = 0, tb2 = 0;
     CUDA_CHECK(cub::DeviceSegmentedSort::StableSortPairs(nullptr, tb1, ia.p, ik.p, p1.p, p2.p,
