@@ -1,5 +1,6 @@
 // api.cu — the C-ABI of libsvmhss.so (include/svmhss.h).  Argument validation, handle
 // ownership (reference counted hss_t <- ulv_t), error translation; no arithmetic here.
+#include <chrono>
 #include <cmath>
 #include <cstring>
 #include "internal.cuh"
@@ -20,6 +21,35 @@ void init_mem_pool() {
   done_dev = dev;
 }
 void set_last_error(const std::string& s) { g_last_error = s; }
+
+double PhaseTrace::now_ms() {
+  return std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now().time_since_epoch()).count();
+}
+PhaseTrace::PhaseTrace(const char* nm, cudaStream_t st) : s(st), name(nm) {
+  const char* e = getenv("SVMHSS_TRACE");
+  on = e && e[0] == '1';
+  if (on) { t0 = now_ms(); mark("start"); }
+}
+void PhaseTrace::mark(const std::string& tag) {
+  if (!on) return;
+  cudaEvent_t e;
+  cudaEventCreate(&e);
+  cudaEventRecord(e, s);
+  ev.push_back({tag, e});
+  host_ms.push_back(now_ms() - t0);
+}
+PhaseTrace::~PhaseTrace() {
+  if (!on) return;
+  mark("end");
+  cudaEventSynchronize(ev.back().second);
+  fprintf(stderr, "[svmhss trace] %s\n", name.c_str());
+  for (size_t i = 1; i < ev.size(); ++i) {
+    float ms = 0;
+    cudaEventElapsedTime(&ms, ev[i - 1].second, ev[i].second);
+    fprintf(stderr, "  %-28s gpu %9.3f ms   host@ %9.3f ms\n", ev[i].first.c_str(), ms, host_ms[i]);
+  }
+  for (auto& x : ev) cudaEventDestroy(x.second);
+}
 
 static void ensure_device() {
   int cnt = 0;

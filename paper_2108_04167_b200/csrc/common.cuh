@@ -118,6 +118,21 @@ struct EventTimer {
   ~EventTimer() { cudaEventDestroy(a); cudaEventDestroy(b); }
 };
 
+// Optional phase trace (env SVMHSS_TRACE=1): host wall time and stream time between marks,
+// printed to stderr when the tracer goes out of scope.  Off: no events, no cost.
+struct PhaseTrace {
+  bool on = false;
+  cudaStream_t s = nullptr;
+  std::string name;
+  std::vector<std::pair<std::string, cudaEvent_t>> ev;
+  std::vector<double> host_ms;
+  double t0 = 0;
+  static double now_ms();
+  PhaseTrace(const char* nm, cudaStream_t st);
+  void mark(const std::string& tag);
+  ~PhaseTrace();
+};
+
 // ------------------------------------------------------------------ device helpers
 __device__ __forceinline__ double warp_sum(double v) {
 #pragma unroll

@@ -28,7 +28,7 @@ static void free_probs(void* d, cudaStream_t s) { CUDA_CHECK(cudaFreeAsync(d, s)
 // per operand from its unit stride).
 constexpr int GBM = 128, GBN = 64, GBK = 8;
 
-__global__ void __launch_bounds__(256) bgemm_kernel(const GemmProb* __restrict__ probs) {
+__global__ void __launch_bounds__(256, 2) bgemm_kernel(const GemmProb* __restrict__ probs) {
   const GemmProb P = probs[blockIdx.z];
   const int m0 = blockIdx.y * GBM, n0 = blockIdx.x * GBN;
   if (m0 >= P.m || n0 >= P.n) return;
@@ -287,12 +287,20 @@ void btrsm(const std::vector<TrsmProb>& probs_in, bool lower, cudaStream_t s) {
 // up to rounding); the trailing columns are updated with the compact-WY block reflector
 // (W = V^T A, W = T^T W, A -= V W), reading the trailing matrix twice per panel instead of
 // twice per column.  Each thread owns whole columns (coalesced row-major access).
+// shared memory of the QR kernel: panel m x nb, trailing column block m x cb, W and T^T W (nb x cb)
+inline size_t qr_smem(int m, int nb, int cb) {
+  return ((size_t)m * nb + (size_t)m * cb + 2 * (size_t)nb * cb) * 8;
+}
+
 template <int NB>
-__global__ void __launch_bounds__(256) bgeqrf_kernel(const QrProb* __restrict__ probs) {
+__global__ void __launch_bounds__(256) bgeqrf_kernel(const QrProb* __restrict__ probs, int cb) {
   const QrProb P = probs[blockIdx.x];
   const int m = P.m, n = P.n, tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
   extern __shared__ double sm[];
   double* pan = sm;                 // (m) x NB panel, row-major stride NB
+  double* ablk = pan + (size_t)m * NB;   // m x cb (cb: trailing-update column block)
+  double* wsh = ablk + (size_t)m * cb;   // NB x cb
+  double* w2sh = wsh + NB * cb;          // NB x cb
   __shared__ double T[NB][NB + 1];
   __shared__ double tau_s[NB];
   __shared__ double red[32];
@@ -369,36 +377,47 @@ __global__ void __launch_bounds__(256) bgeqrf_kernel(const QrProb* __restrict__ 
       QA(p0 + i, p0 + j) = pan[i * NB + j];
     }
     if (tid < pb) P.tau[p0 + tid] = tau_s[tid];
-    // trailing update: A[p0:, c] -= V T^T V^T A[p0:, c]  for c >= p0 + pb
-    for (int c = p0 + pb + tid; c < n; c += 256) {
-      double w[NB];
-#pragma unroll
-      for (int j = 0; j < NB; ++j) w[j] = 0.0;
-      for (int i = 0; i < mr; ++i) {
-        const double a = QA(p0 + i, c);
-#pragma unroll
-        for (int j = 0; j < NB; ++j) {
-          const double v = (i == j) ? 1.0 : ((i > j) ? pan[i * NB + j] : 0.0);
-          w[j] = fma(v, a, w[j]);
-        }
+    // trailing update: A[p0:, c] -= V T^T V^T A[p0:, c]  for c >= p0 + pb, in blocks of cb
+    // columns staged through shared memory (coalesced global traffic, one read and one write
+    // per panel).  Per column the arithmetic order is the plain one: w_j = sum_i v_ij a_i in
+    // row order, w2 = T^T w, a_i -= sum_j v_ij w2_j in j order.
+    for (int c0 = p0 + pb; c0 < n; c0 += cb) {
+      const int nc = min(cb, n - c0);
+      for (int e = tid; e < mr * nc; e += 256) {
+        const int i = e / nc, c = e % nc;
+        ablk[i * cb + c] = QA(p0 + i, c0 + c);
       }
-      double w2[NB];
-#pragma unroll
-      for (int j = 0; j < NB; ++j) {
+      __syncthreads();
+      for (int e = tid; e < NB * nc; e += 256) {  // W[j][c] = V[:, j]^T a_c
+        const int j = e / nc, c = e % nc;
+        double w = 0.0;
+        if (j < pb) {
+          for (int i = j; i < mr; ++i) {
+            const double v = (i == j) ? 1.0 : pan[i * NB + j];
+            w = fma(v, ablk[i * cb + c], w);
+          }
+        }
+        wsh[j * cb + c] = w;
+      }
+      __syncthreads();
+      for (int e = tid; e < NB * nc; e += 256) {  // W2 = T^T W (column c)
+        const int j = e / nc, c = e % nc;
         double a = 0.0;
-#pragma unroll
-        for (int q = 0; q <= j; ++q) a = fma(T[q][j], w[q], a);   // (T^T w)_j
-        w2[j] = a;
+        for (int q = 0; q <= j; ++q) a = fma(T[q][j], wsh[q * cb + c], a);
+        w2sh[j * cb + c] = a;
       }
-      for (int i = 0; i < mr; ++i) {
-        double a = QA(p0 + i, c);
+      __syncthreads();
+      for (int e = tid; e < mr * nc; e += 256) {  // a -= V W2
+        const int i = e / nc, c = e % nc;
+        double a = ablk[i * cb + c];
 #pragma unroll
         for (int j = 0; j < NB; ++j) {
           const double v = (i == j) ? 1.0 : ((i > j) ? pan[i * NB + j] : 0.0);
-          a = fma(-v, w2[j], a);
+          a = fma(-v, w2sh[j * cb + c], a);
         }
-        QA(p0 + i, c) = a;
+        QA(p0 + i, c0 + c) = a;
       }
+      __syncthreads();
     }
     __syncthreads();
   }
@@ -410,15 +429,20 @@ void bgeqr2(const std::vector<QrProb>& probs, cudaStream_t s) {
   int maxm = 0;
   for (auto& p : probs) maxm = std::max(maxm, p.m);
   QrProb* d = upload_probs(probs, s);
-  auto launch = [&](auto kern, int nb) {
-    size_t smem = (size_t)std::max(1, maxm) * nb * sizeof(double);
+  // panel width NB and trailing column block cb: the largest that fit 200 KB for the tallest problem
+  auto launch = [&](auto kern, int nb) -> bool {
+    int cb = 32;
+    while (cb > 1 && qr_smem(std::max(1, maxm), nb, cb) > 200 * 1024) cb >>= 1;
+    const size_t smem = qr_smem(std::max(1, maxm), nb, cb);
+    if (smem > 200 * 1024) return false;
     if (smem > 48 * 1024)
       CUDA_CHECK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-    kern<<<(unsigned)probs.size(), 256, smem, s>>>(d);
+    kern<<<(unsigned)probs.size(), 256, smem, s>>>(d, cb);
+    return true;
   };
-  if ((size_t)maxm * 16 * 8 <= 200 * 1024) launch(bgeqrf_kernel<16>, 16);
-  else if ((size_t)maxm * 8 * 8 <= 200 * 1024) launch(bgeqrf_kernel<8>, 8);
-  else if ((size_t)maxm * 4 * 8 <= 200 * 1024) launch(bgeqrf_kernel<4>, 4);
+  if (launch(bgeqrf_kernel<16>, 16)) {}
+  else if (launch(bgeqrf_kernel<8>, 8)) {}
+  else if (launch(bgeqrf_kernel<4>, 4)) {}
   else throw Error(HSS_EINVAL, "bgeqr2: node too tall for the shared-memory panel");
   LAUNCH_CHECK();
   free_probs(d, s);

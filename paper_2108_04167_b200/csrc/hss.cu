@@ -209,7 +209,9 @@ void hss_build_impl(HSSImpl& H, const double* F, int64_t n, int r, double h, con
   int cap_hits = 0, maxk = 0, npt = 0;        // levels < lg (replicated) counted once
   int64_t sub_bytes = (int64_t)H.D.bytes(), top_bytes = 0;
   int sub_cap = 0, sub_pt = 0, sub_maxk = 0;  // this rank's subtree (levels >= lg)
+  PhaseTrace ptr_("hss_compress", s);
   for (int l = L; l >= 1; --l) {
+    ptr_.mark("L" + std::to_string(l) + " begin");
     auto& lv = H.lv[l];
     const int f = sh.first(l), e = sh.last(l), nn = e - f;
     int64_t sumR = 0;
@@ -242,7 +244,9 @@ void hss_build_impl(HSSImpl& H, const double* F, int64_t n, int r, double h, con
       if (nd.rows == 0) continue;
       cp.push_back({nd.rows, S, Wk.p + nd.roff * S, piv.p + nd.roff, kfix[q], kd.p + q, ch.p + q});
     }
+    ptr_.mark("  Y ready");
     bcpqr(cp, o.rel_tol, o.abs_tol, o.max_rank, s);
+    ptr_.mark("  cpqr");
     std::vector<int> kh(nn, 0), chh(nn, 0);
     d2h(kh.data(), kd.p, nn, s);
     d2h(chh.data(), ch.p, nn, s);

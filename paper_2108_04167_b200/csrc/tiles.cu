@@ -106,8 +106,15 @@ __device__ __forceinline__ void bulk_g2s(void* dst, const void* src, unsigned by
 //   (2) sketch DMMAs S_acc(8 rows x 8*NT cols) += E(8 x BJ) W(BJ x 8*NT cols).
 // Operands arrive by TMA bulk copies (cp.async.bulk, one row per copy into padded smem rows)
 // into a 2-stage ring completed on mbarriers; one CTA barrier per step guards buffer reuse.
+// Persistent, wave-synchronous schedule: gridDim.x CTAs (one per SM) walk the 64-row tiles
+// tile = blockIdx.x + it * gridDim.x, and a grid barrier after every tile keeps the whole wave
+// on the same j-step of the (tile-independent) operand stream, so each W / Fb tile is read from
+// HBM about once per wave and served from L2 to the other CTAs (the unsynchronised grid read
+// Omega ~50x more often than this).  The operand ring runs continuously across tiles (global
+// step counter G): the prefetch of a tile's first step overlaps the previous tile's epilogue.
+// Requires co-residency of the grid: launched cooperatively.
 template <int BJ, int NT>
-__global__ void __launch_bounds__(512, 1) kmm_kernel(KmmArgs a, int SA) {
+__global__ void __launch_bounds__(512, 1) kmm_kernel(KmmArgs a, int SA, unsigned* gbar) {
   constexpr int NCH = 16 * NT, SW = NCH + 4, SE = BJ + 4, HQ = BJ / 16;  // n-tiles of distance per warp
   extern __shared__ __align__(128) double smem[];
   double* Fa_s = smem;                       // 64 x SA
@@ -120,21 +127,13 @@ __global__ void __launch_bounds__(512, 1) kmm_kernel(KmmArgs a, int SA) {
 
   const int tid = threadIdx.x, lane = tid & 31, w = tid >> 5, g = lane >> 2, t = lane & 3;
   const int mt = w & 7, hf = w >> 3;
-  const int64_t row0 = (int64_t)blockIdx.x * KBM;
   const int col0 = blockIdx.y * NCH;
   const int rp = a.rp;
   const int ncl = min(NCH, a.ncols - col0);  // valid columns of this chunk (even)
   const int64_t nsteps = (a.nb + BJ - 1) / BJ;
+  const int64_t ntiles = (a.na + KBM - 1) / KBM;
+  const int64_t niter = (ntiles + gridDim.x - 1) / gridDim.x;
 
-  for (int e = tid; e < KBM * rp; e += 512) {
-    const int i = e / rp, f = e % rp;
-    const int64_t gi = row0 + i;
-    Fa_s[i * SA + f] = (gi < a.na) ? a.Fa[gi * rp + f] : 0.0;
-  }
-  for (int i = tid; i < KBM; i += 512) {
-    const int64_t gi = row0 + i;
-    nua_s[i] = (gi < a.na) ? a.nua[gi] : 0.0;
-  }
   for (int e = tid; e < 2 * BJ * SW + 2 * (BJ * SA + BJ); e += 512) wbuf[e] = 0.0;
   for (int e = tid; e < 2 * BJ; e += 512) lbuf[e] = -3;
   if (tid == 0) {
@@ -144,8 +143,9 @@ __global__ void __launch_bounds__(512, 1) kmm_kernel(KmmArgs a, int SA) {
   asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");
   __syncthreads();
 
-  auto issue = [&](int64_t j) {  // warp 0: one bulk copy per row
-    const int b = (int)(j & 1);
+  auto issue = [&](int64_t G) {  // warp 0: one bulk copy per row; global step G -> j-step G mod nsteps
+    const int b = (int)(G & 1);
+    const int64_t j = G % nsteps;
     double* W_s = wbuf + b * BJ * SW;
     double* Fb_s = fbuf + b * (BJ * SA + BJ);
     double* nub_s = Fb_s + BJ * SA;
@@ -166,91 +166,121 @@ __global__ void __launch_bounds__(512, 1) kmm_kernel(KmmArgs a, int SA) {
     }
   };
 
-  const int64_t my_row = row0 + mt * 8 + g;
-  const bool row_ok = my_row < a.na;
-  const int my_leaf = (a.leaf_a && row_ok) ? a.leaf_a[my_row] : -1;
-  const double nui = nua_s[mt * 8 + g];
-  const double* Fa_w = Fa_s + (mt * 8 + g) * SA + t;
-  const double* E_w = E_s + (mt * 8 + g) * SE + t;
-
-  double acc[NT][2];
-#pragma unroll
-  for (int ni = 0; ni < NT; ++ni) acc[ni][0] = acc[ni][1] = 0.0;
+  const int64_t total = niter * nsteps;  // every CTA runs the same number of steps (idle tiles too)
+  int64_t G = 0;
   if (w == 0) issue(0);
-  for (int64_t js = 0; js < nsteps; ++js) {
-    const int b = (int)(js & 1);
-    mbar_wait(&full[b], (unsigned)((js >> 1) & 1));
-    __syncthreads();  // every warp is past step js-1: the other stage and E_s are free
-    if (w == 0 && js + 1 < nsteps) issue(js + 1);
-    const double* W_s = wbuf + b * BJ * SW;
-    const double* Fb_s = fbuf + b * (BJ * SA + BJ);
-    const double* nub_s = Fb_s + BJ * SA;
-    const int* lb = lbuf + b * BJ;
-    const int64_t j0 = js * BJ;
-    const int jvalid = (int)min((int64_t)BJ, a.nb - j0);
-    // (1) distances: rows mt*8.., columns hf*BJ/2 + [0, BJ/2)
-    double dacc[HQ][2];
+  for (int64_t it = 0; it < niter; ++it) {
+    const int64_t tile = blockIdx.x + it * gridDim.x;
+    const bool active = tile < ntiles;
+    const int64_t row0 = tile * KBM;
+    for (int e = tid; e < KBM * rp; e += 512) {
+      const int i = e / rp, f = e % rp;
+      const int64_t gi = row0 + i;
+      Fa_s[i * SA + f] = (active && gi < a.na) ? a.Fa[gi * rp + f] : 0.0;
+    }
+    for (int i = tid; i < KBM; i += 512) {
+      const int64_t gi = row0 + i;
+      nua_s[i] = (active && gi < a.na) ? a.nua[gi] : 0.0;
+    }
+    __syncthreads();
+    const int64_t my_row = row0 + mt * 8 + g;
+    const bool row_ok = active && my_row < a.na;
+    const int my_leaf = (a.leaf_a && row_ok) ? a.leaf_a[my_row] : -1;
+    const double nui = nua_s[mt * 8 + g];
+    const double* Fa_w = Fa_s + (mt * 8 + g) * SA + t;
+    const double* E_w = E_s + (mt * 8 + g) * SE + t;
+
+    double acc[NT][2];
 #pragma unroll
-    for (int q = 0; q < HQ; ++q) dacc[q][0] = dacc[q][1] = 0.0;
-    const double* Fb_w = Fb_s + (hf * (BJ / 2) + g) * SA + t;
-    {
-      // two interleaved partial sums per tile: 2*HQ independent DMMA chains of rp/8 steps
-      double dacc2[HQ][2];
+    for (int ni = 0; ni < NT; ++ni) acc[ni][0] = acc[ni][1] = 0.0;
+    for (int64_t js = 0; js < nsteps; ++js, ++G) {
+      const int b = (int)(G & 1);
+      mbar_wait(&full[b], (unsigned)((G >> 1) & 1));
+      __syncthreads();  // every warp is past step G-1: the other stage and E_s are free
+      if (w == 0 && G + 1 < total) issue(G + 1);
+      const double* W_s = wbuf + b * BJ * SW;
+      const double* Fb_s = fbuf + b * (BJ * SA + BJ);
+      const double* nub_s = Fb_s + BJ * SA;
+      const int* lb = lbuf + b * BJ;
+      const int64_t j0 = js * BJ;
+      const int jvalid = (int)min((int64_t)BJ, a.nb - j0);
+      if (!active) continue;  // idle tile: keep the ring and the barriers in step
+      // (1) distances: rows mt*8.., columns hf*BJ/2 + [0, BJ/2)
+      double dacc[HQ][2];
 #pragma unroll
-      for (int q = 0; q < HQ; ++q) dacc2[q][0] = dacc2[q][1] = 0.0;
-      int kk = 0;
-      for (; kk + 1 < rp / 4; kk += 2) {
-        const double av0 = Fa_w[kk * 4], av1 = Fa_w[kk * 4 + 4];
+      for (int q = 0; q < HQ; ++q) dacc[q][0] = dacc[q][1] = 0.0;
+      const double* Fb_w = Fb_s + (hf * (BJ / 2) + g) * SA + t;
+      {
+        // two interleaved partial sums per tile: 2*HQ independent DMMA chains of rp/8 steps
+        double dacc2[HQ][2];
 #pragma unroll
-        for (int q = 0; q < HQ; ++q) {
-          dmma884(dacc[q][0], dacc[q][1], av0, Fb_w[q * 8 * SA + kk * 4]);
-          dmma884(dacc2[q][0], dacc2[q][1], av1, Fb_w[q * 8 * SA + kk * 4 + 4]);
+        for (int q = 0; q < HQ; ++q) dacc2[q][0] = dacc2[q][1] = 0.0;
+        int kk = 0;
+        for (; kk + 1 < rp / 4; kk += 2) {
+          const double av0 = Fa_w[kk * 4], av1 = Fa_w[kk * 4 + 4];
+#pragma unroll
+          for (int q = 0; q < HQ; ++q) {
+            dmma884(dacc[q][0], dacc[q][1], av0, Fb_w[q * 8 * SA + kk * 4]);
+            dmma884(dacc2[q][0], dacc2[q][1], av1, Fb_w[q * 8 * SA + kk * 4 + 4]);
+          }
+        }
+        if (kk < rp / 4) {
+          const double av = Fa_w[kk * 4];
+#pragma unroll
+          for (int q = 0; q < HQ; ++q) dmma884(dacc[q][0], dacc[q][1], av, Fb_w[q * 8 * SA + kk * 4]);
+        }
+#pragma unroll
+        for (int q = 0; q < HQ; ++q) { dacc[q][0] += dacc2[q][0]; dacc[q][1] += dacc2[q][1]; }
+      }
+#pragma unroll
+      for (int q = 0; q < HQ; ++q) {
+        double ev[2];
+#pragma unroll
+        for (int e = 0; e < 2; ++e) {
+          const int jj = hf * (BJ / 2) + q * 8 + 2 * t + e;
+          double d2 = fmax(nui + nub_s[jj] - 2.0 * dacc[q][e], 0.0);
+          double v = exp_kernel(d2 * a.neg_inv_2h2);
+          if (a.same_set && j0 + jj == my_row + a.diag_off) v = 1.0;
+          if (a.leaf_b && lb[jj] == my_leaf) v = 0.0;
+          if (jj >= jvalid || !row_ok) v = 0.0;
+          ev[e] = v;
+        }
+        *reinterpret_cast<double2*>(&E_s[(mt * 8 + g) * SE + hf * (BJ / 2) + q * 8 + 2 * t]) =
+            make_double2(ev[0], ev[1]);
+      }
+      asm volatile("bar.sync %0, 64;\n" ::"r"(1 + mt) : "memory");  // partner warps w, w^8
+      // (2) sketch: columns hf*8*NT .. + 8*NT
+      const double* W_w = W_s + t * SW + hf * (8 * NT) + g;
+#pragma unroll
+      for (int kk = 0; kk < BJ / 4; ++kk) {
+        const double av = E_w[kk * 4];
+#pragma unroll
+        for (int ni = 0; ni < NT; ++ni) dmma884(acc[ni][0], acc[ni][1], av, W_w[kk * 4 * SW + ni * 8]);
+      }
+    }
+    // epilogue
+    if (row_ok) {
+#pragma unroll
+      for (int ni = 0; ni < NT; ++ni) {
+        const int gc = col0 + hf * (8 * NT) + ni * 8 + 2 * t;
+        if (gc < a.ncols) {
+          double* dst = a.S + my_row * a.lds + gc;
+          dst[0] = acc[ni][0];
+          if (gc + 1 < a.ncols) dst[1] = acc[ni][1];
         }
       }
-      if (kk < rp / 4) {
-        const double av = Fa_w[kk * 4];
-#pragma unroll
-        for (int q = 0; q < HQ; ++q) dmma884(dacc[q][0], dacc[q][1], av, Fb_w[q * 8 * SA + kk * 4]);
-      }
-#pragma unroll
-      for (int q = 0; q < HQ; ++q) { dacc[q][0] += dacc2[q][0]; dacc[q][1] += dacc2[q][1]; }
     }
-#pragma unroll
-    for (int q = 0; q < HQ; ++q) {
-      double ev[2];
-#pragma unroll
-      for (int e = 0; e < 2; ++e) {
-        const int jj = hf * (BJ / 2) + q * 8 + 2 * t + e;
-        double d2 = fmax(nui + nub_s[jj] - 2.0 * dacc[q][e], 0.0);
-        double v = exp_kernel(d2 * a.neg_inv_2h2);
-        if (a.same_set && j0 + jj == my_row + a.diag_off) v = 1.0;
-        if (a.leaf_b && lb[jj] == my_leaf) v = 0.0;
-        if (jj >= jvalid || !row_ok) v = 0.0;
-        ev[e] = v;
+    // wave barrier (grid-wide, per column chunk): nobody starts tile it+1 before all finished it
+    if (it + 1 < niter) {
+      __syncthreads();
+      if (tid == 0) {
+        unsigned* bar = gbar + blockIdx.y;
+        __threadfence();
+        atomicAdd(bar, 1u);
+        const unsigned target = (unsigned)((it + 1) * gridDim.x);
+        while (atomicAdd(bar, 0u) < target) __nanosleep(200);
       }
-      *reinterpret_cast<double2*>(&E_s[(mt * 8 + g) * SE + hf * (BJ / 2) + q * 8 + 2 * t]) =
-          make_double2(ev[0], ev[1]);
-    }
-    asm volatile("bar.sync %0, 64;\n" ::"r"(1 + mt) : "memory");  // partner warps w, w^8
-    // (2) sketch: columns hf*8*NT .. + 8*NT
-    const double* W_w = W_s + t * SW + hf * (8 * NT) + g;
-#pragma unroll
-    for (int kk = 0; kk < BJ / 4; ++kk) {
-      const double av = E_w[kk * 4];
-#pragma unroll
-      for (int ni = 0; ni < NT; ++ni) dmma884(acc[ni][0], acc[ni][1], av, W_w[kk * 4 * SW + ni * 8]);
-    }
-  }
-  // epilogue
-  if (row_ok) {
-#pragma unroll
-    for (int ni = 0; ni < NT; ++ni) {
-      const int gc = col0 + hf * (8 * NT) + ni * 8 + 2 * t;
-      if (gc < a.ncols) {
-        double* dst = a.S + my_row * a.lds + gc;
-        dst[0] = acc[ni][0];
-        if (gc + 1 < a.ncols) dst[1] = acc[ni][1];
-      }
+      __syncthreads();
     }
   }
 }
@@ -274,8 +304,28 @@ static void launch_kmm(const KmmArgs& a, int SA, cudaStream_t s) {
   const size_t smem = kmm_smem(BJ, NT, SA);
   CUDA_CHECK(cudaFuncSetAttribute(kmm_kernel<BJ, NT>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                   (int)smem));
-  dim3 grid((unsigned)((a.na + KBM - 1) / KBM), (unsigned)ceil_div(a.ncols, 16 * NT));
-  kmm_kernel<BJ, NT><<<grid, 512, smem, s>>>(a, SA);
+  int dev = 0, nsm = 0, per_sm = 0;
+  CUDA_CHECK(cudaGetDevice(&dev));
+  CUDA_CHECK(cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev));
+  CUDA_CHECK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kmm_kernel<BJ, NT>, 512, smem));
+  const int nchunk = ceil_div(a.ncols, 16 * NT);
+  const int64_t ntiles = (a.na + KBM - 1) / KBM;
+  // co-resident grid: every column chunk gets (SMs * per_sm) / nchunk persistent CTAs
+  const int64_t slots = std::max<int64_t>(1, ((int64_t)nsm * std::max(1, per_sm)) / nchunk);
+  const unsigned gx = (unsigned)std::max<int64_t>(1, std::min(ntiles, slots));
+  DevBuf<unsigned> gbar(nchunk);
+  CUDA_CHECK(cudaMemsetAsync(gbar.p, 0, nchunk * sizeof(unsigned), s));
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(gx, (unsigned)nchunk);
+  cfg.blockDim = dim3(512);
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = s;
+  cudaLaunchAttribute at[1];
+  at[0].id = cudaLaunchAttributeCooperative;
+  at[0].val.cooperative = 1;
+  cfg.attrs = at;
+  cfg.numAttrs = 1;
+  CUDA_CHECK(cudaLaunchKernelEx(&cfg, kmm_kernel<BJ, NT>, a, SA, gbar.p));
   LAUNCH_CHECK();
 }
 

@@ -86,7 +86,9 @@ void ulv_factor_impl(ULVImpl& F, cudaStream_t s) {
   DevBuf<double> DhC, RmC;           // child level
   std::vector<int64_t> dhoffC;       // offsets (doubles) by the child's BFS index (k*k packing)
   int64_t total_bytes = 0;
+  PhaseTrace ptr_("ulv_factor", s);
   for (int l = L; l >= 0; --l) {
+    ptr_.mark("L" + std::to_string(l) + " begin");
     const bool leaf = (l == L);
     const int f0 = sh.first(l);
     // this rank's nodes of level l, re-based to 0 (hv[i] = H.lv[l][f0 + i])
@@ -243,6 +245,7 @@ void ulv_factor_impl(ULVImpl& F, cudaStream_t s) {
           X1(std::max<int64_t>(1, sKK)), X2(std::max<int64_t>(1, sKK));
       std::vector<int64_t> tauoff(nn);
       { int64_t o = 0; for (int i = 0; i < nn; ++i) { tauoff[i] = o; o += K[i]; } }
+      ptr_.mark("  assembled");
       // QR of Ucur
       std::vector<QrProb> qp;
       for (int i : np) qp.push_back({R[i], K[i], Ucur.p + uoff[i], K[i], 1, tau.p + tauoff[i]});
@@ -254,6 +257,7 @@ void ulv_factor_impl(ULVImpl& F, cudaStream_t s) {
       }
       run_pack(Ucur.p, pR, RmP.p, s);
       run_pack(Ucur.p, pV, V.p, s);
+      ptr_.mark("  qr+pack");
       // T = larft(V^T V, tau)
       std::vector<GemmProb> g;
       for (int i : np) g.push_back({K[i], K[i], R[i], V.p + vo[i], 1, K[i], V.p + vo[i], K[i], 1, T.p + to[i], K[i], 1, 1.0, 0.0});
@@ -286,6 +290,7 @@ void ulv_factor_impl(ULVImpl& F, cudaStream_t s) {
       g.clear();
       for (int i : np) g.push_back({R[i], R[i], K[i], V.p + vo[i], K[i], 1, Z.p + vo[i], 1, K[i], Dcur.p + coff[i], R[i], 1, -1.0, 1.0});
       bgemm(g, s);
+      ptr_.mark("  wy QtDQ");
       // L_r = chol(Dc_rr)   (also nodes with k == 0: whole block)
       std::vector<SqProb> cp2;
       std::vector<int> ids;
@@ -310,6 +315,7 @@ void ulv_factor_impl(ULVImpl& F, cudaStream_t s) {
         g.push_back({K[i], K[i], R[i] - K[i], Lt, 1, R[i], Lt, R[i], 1, DhP.p + koff2[i], K[i], 1, -1.0, 1.0});
       }
       bgemm(g, s);
+      ptr_.mark("  potrf/trsm/Dh");
       // M = Q^T = I - V T^T V^T  ; G_r = L_r^-1 M[k:, :] ; M[:k, :] -= L_sr G_r
       std::vector<PackDesc> pI;
       for (int i : np) pI.push_back({0, moff[i], R[i], K[i], 2, 0});
@@ -379,6 +385,7 @@ void ulv_factor_impl(ULVImpl& F, cudaStream_t s) {
     RmC = std::move(RmP);
     CUDA_CHECK(cudaStreamSynchronize(s));
   }
+  ptr_.mark("levels done");
   // work lists: forward = (node, chunk of `ch` rows), backward = (node, chunk of kCW columns)
   for (int l = 0; l <= L; ++l) {
     auto& F_l = F.lv[l];

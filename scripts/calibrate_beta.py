@@ -30,6 +30,7 @@ def main():
     ap.add_argument("--n", type=int, default=None)
     ap.add_argument("--h", type=float, default=None)
     ap.add_argument("--chaos-it", type=int, default=0)
+    ap.add_argument("--sampling", default="sketch", choices=["sketch", "ann"])
     a = ap.parse_args()
     cfg = datagen.get_config(a.config)
     n = a.n or cfg["n"]
@@ -37,7 +38,10 @@ def main():
     F, y, _, _ = datagen.generate(a.config, n=n, n_test=0)
     t0 = time.time()
     tm = {}
-    perm, ranges, Om, H = pipeline.build(F, cfg, h=h, timings=tm)
+    if a.sampling == "ann":
+        perm, ranges, _, H = pipeline.build_ann(F, cfg, h=h, timings=tm)
+    else:
+        perm, ranges, Om, H = pipeline.build(F, cfg, h=h, timings=tm)
     print("built", tm, flush=True)
     op = LinearOperator((n, n), matvec=lambda v: hss.matvec(H, v), dtype=np.float64)
     lmin = float(eigsh(op, k=1, which="SA", tol=1e-4, maxiter=20000)[0][0])
@@ -46,6 +50,8 @@ def main():
     beta = sched if lmin >= 0 else max(sched, 10.0 ** math.ceil(math.log10(-4 * lmin)))
     rec = dict(config=a.config, n=n, h=h, lambda_min=lmin, schedule=sched, beta=beta,
                timings=tm, secs=time.time() - t0)
+    if a.sampling != "sketch":
+        rec["sampling"] = a.sampling
     if a.chaos_it:
         f = ulv.factor(H, beta)
         solve = lambda b: ulv.solve(f, b)  # noqa: E731
