@@ -374,6 +374,13 @@ def main():
                                "frac": ach_gbs / peaks["hbm_gbs"],
                                "work": "2 x factor_bytes + 64 n nC bytes per iteration"},
             "clocks": clocks}
+    if args.sampling == "ann":
+        # no dense sketch in HSS-ANN mode: the dominant kernel of the step is the ULV sweep pair
+        line["roofline_sketch_mode_only"] = line.pop("roofline")
+        line["roofline_sketch_mode_only"] = {"note": "HSS-ANN sampling: no K*Omega sketch in this step",
+                                             "ann_ms": line["phases_ms"]["sketch"]}
+        line["roofline"] = dict(line["roofline_solve"], traffic=None)
+        line["phases_ms"]["ann"] = line["phases_ms"].pop("sketch")
     if rank == 0 and world == 1 and not args.no_e2e and args.n is None:
         pin = lambda a: torch.from_numpy(a).pin_memory().numpy()  # noqa: E731
         Fh, yh, Fth = pin(F), pin(y), pin(Ft)

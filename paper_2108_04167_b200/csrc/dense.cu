@@ -32,8 +32,10 @@ __global__ void __launch_bounds__(256, 2) bgemm_kernel(const GemmProb* __restric
   const GemmProb P = probs[blockIdx.z];
   const int m0 = blockIdx.y * GBM, n0 = blockIdx.x * GBN;
   if (m0 >= P.m || n0 >= P.n) return;
-  __shared__ __align__(16) double As[2][GBK][GBM];
-  __shared__ __align__(16) double Bs[2][GBK][GBN];
+  // rows padded by 2 doubles: the transposing stores (8 consecutive threads -> 8 k-rows) hit
+  // 8 distinct bank pairs instead of one bank 8 times; double2 reads stay 16-byte aligned
+  __shared__ __align__(16) double As[2][GBK][GBM + 2];
+  __shared__ __align__(16) double Bs[2][GBK][GBN + 2];
   const int tid = threadIdx.x, tx = tid & 15, ty = tid >> 4;
   const bool a_rm = (P.acs == 1), b_rm = (P.bcs == 1);
   double acc[8][4];
