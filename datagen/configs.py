@@ -54,10 +54,8 @@ _CONFIGS = {
 #   cfg 1: lambda_min = -331.65  -> 1e4      cfg 2: lambda_min = -5185.1 -> 1e5
 #   cfg 4 (per h): 0.25: -7.09 -> 1e2; 0.5: -91.5 -> 1e3; 1: -476.3 -> 1e4; 2: -627.3 -> 1e4;
 #                  4: -206.7 -> 1e3
-#   cfg 3: PROVISIONAL 1e5 until the oracle's eigsh at n = 524288 finishes (scripts/calibrate_beta.py
-#          --config 3): the factorization of the same K~ (GPU, parity-tested against the oracle) breaks
-#          down at beta = 1e4, so lambda_min < -1e4 and the rule gives at least 10^ceil(log10 4e4) = 1e5.
-_BETA = {1: 1e4, 2: 1e5, 3: 1e5, 4: None}
+#   cfg 3: lambda_min = -62850.4 -> 1e6  (oracle at n = 524288: 8256 s of host compression + eigsh)
+_BETA = {1: 1e4, 2: 1e5, 3: 1e6, 4: None}
 _BETA_PER_H = {4: {0.25: 1e2, 0.5: 1e3, 1.0: 1e4, 2.0: 1e4, 4.0: 1e3}}
 
 # HSS-ANN sampling knobs (readings N1-N3): neighbours per point (the paper's

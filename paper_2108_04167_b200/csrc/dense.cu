@@ -294,8 +294,10 @@ inline size_t qr_smem(int m, int nb, int cb) {
   return ((size_t)m * nb + (size_t)m * cb + 2 * (size_t)nb * cb) * 8;
 }
 
+constexpr int QT = 512;  // threads of the QR kernel
+
 template <int NB>
-__global__ void __launch_bounds__(256) bgeqrf_kernel(const QrProb* __restrict__ probs, int cb) {
+__global__ void __launch_bounds__(QT) bgeqrf_kernel(const QrProb* __restrict__ probs, int cb) {
   const QrProb P = probs[blockIdx.x];
   const int m = P.m, n = P.n, tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
   extern __shared__ double sm[];
@@ -309,7 +311,7 @@ __global__ void __launch_bounds__(256) bgeqrf_kernel(const QrProb* __restrict__ 
 #define QA(i, j) P.A[(long long)(i) * P.rs + (long long)(j) * P.cs]
   for (int p0 = 0; p0 < n; p0 += NB) {
     const int pb = min(NB, n - p0), mr = m - p0;
-    for (int e = tid; e < mr * NB; e += 256) {
+    for (int e = tid; e < mr * NB; e += QT) {
       const int i = e / NB, j = e % NB;
       pan[e] = (j < pb) ? QA(p0 + i, p0 + j) : 0.0;
     }
@@ -317,7 +319,7 @@ __global__ void __launch_bounds__(256) bgeqrf_kernel(const QrProb* __restrict__ 
     // factor the panel in shared memory
     for (int j = 0; j < pb; ++j) {
       double part = 0.0;
-      for (int i = j + 1 + tid; i < mr; i += 256) { const double x = pan[i * NB + j]; part = fma(x, x, part); }
+      for (int i = j + 1 + tid; i < mr; i += QT) { const double x = pan[i * NB + j]; part = fma(x, x, part); }
       const double xs = block_sum(part, red);
       const double alpha = pan[j * NB + j];
       double tau, scal, beta;
@@ -328,12 +330,12 @@ __global__ void __launch_bounds__(256) bgeqrf_kernel(const QrProb* __restrict__ 
         scal = 1.0 / (alpha - beta);
       }
       if (tau != 0.0)
-        for (int i = j + 1 + tid; i < mr; i += 256) pan[i * NB + j] *= scal;
+        for (int i = j + 1 + tid; i < mr; i += QT) pan[i * NB + j] *= scal;
       __syncthreads();
       if (tid == 0) { pan[j * NB + j] = beta; tau_s[j] = tau; }
       // apply H_j to panel columns c > j: warp per column
       if (tau != 0.0) {
-        for (int c = j + 1 + wid; c < pb; c += 8) {
+        for (int c = j + 1 + wid; c < pb; c += QT / 32) {
           double w = 0.0;
           for (int i = j + lane; i < mr; i += 32) {
             const double vi = (i == j) ? 1.0 : pan[i * NB + j];
@@ -351,7 +353,7 @@ __global__ void __launch_bounds__(256) bgeqrf_kernel(const QrProb* __restrict__ 
     // T (pb x pb upper): T_jj = tau_j, T[0:j, j] = -tau_j T[0:j,0:j] (V[:,0:j]^T v_j)
     for (int j = 0; j < pb; ++j) {
       // s_i = V[:, i]^T v_j for i < j  (warp per i)
-      for (int i = wid; i < j; i += 8) {
+      for (int i = wid; i < j; i += QT / 32) {
         double a = 0.0;
         for (int r = j + lane; r < mr; r += 32) {
           const double vi = (r == i) ? 1.0 : (r > i ? pan[r * NB + i] : 0.0);
@@ -370,11 +372,11 @@ __global__ void __launch_bounds__(256) bgeqrf_kernel(const QrProb* __restrict__ 
       __syncthreads();
       if (tid < j) T[tid][j] = -tau_s[j] * red[tid];
       if (tid == 0) T[j][j] = tau_s[j];
-      for (int i = j + 1 + tid; i < NB; i += 256) T[i][j] = 0.0;
+      for (int i = j + 1 + tid; i < NB; i += QT) T[i][j] = 0.0;
       __syncthreads();
     }
     // write the panel back (R on/above the diagonal, V below) and tau
-    for (int e = tid; e < mr * pb; e += 256) {
+    for (int e = tid; e < mr * pb; e += QT) {
       const int i = e / pb, j = e % pb;
       QA(p0 + i, p0 + j) = pan[i * NB + j];
     }
@@ -385,12 +387,12 @@ __global__ void __launch_bounds__(256) bgeqrf_kernel(const QrProb* __restrict__ 
     // row order, w2 = T^T w, a_i -= sum_j v_ij w2_j in j order.
     for (int c0 = p0 + pb; c0 < n; c0 += cb) {
       const int nc = min(cb, n - c0);
-      for (int e = tid; e < mr * nc; e += 256) {
+      for (int e = tid; e < mr * nc; e += QT) {
         const int i = e / nc, c = e % nc;
         ablk[i * cb + c] = QA(p0 + i, c0 + c);
       }
       __syncthreads();
-      for (int e = tid; e < NB * nc; e += 256) {  // W[j][c] = V[:, j]^T a_c
+      for (int e = tid; e < NB * nc; e += QT) {  // W[j][c] = V[:, j]^T a_c
         const int j = e / nc, c = e % nc;
         double w = 0.0;
         if (j < pb) {
@@ -402,14 +404,14 @@ __global__ void __launch_bounds__(256) bgeqrf_kernel(const QrProb* __restrict__ 
         wsh[j * cb + c] = w;
       }
       __syncthreads();
-      for (int e = tid; e < NB * nc; e += 256) {  // W2 = T^T W (column c)
+      for (int e = tid; e < NB * nc; e += QT) {  // W2 = T^T W (column c)
         const int j = e / nc, c = e % nc;
         double a = 0.0;
         for (int q = 0; q <= j; ++q) a = fma(T[q][j], wsh[q * cb + c], a);
         w2sh[j * cb + c] = a;
       }
       __syncthreads();
-      for (int e = tid; e < mr * nc; e += 256) {  // a -= V W2
+      for (int e = tid; e < mr * nc; e += QT) {  // a -= V W2
         const int i = e / nc, c = e % nc;
         double a = ablk[i * cb + c];
 #pragma unroll
@@ -439,7 +441,7 @@ void bgeqr2(const std::vector<QrProb>& probs, cudaStream_t s) {
     if (smem > 200 * 1024) return false;
     if (smem > 48 * 1024)
       CUDA_CHECK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-    kern<<<(unsigned)probs.size(), 256, smem, s>>>(d, cb);
+    kern<<<(unsigned)probs.size(), QT, smem, s>>>(d, cb);
     return true;
   };
   if (launch(bgeqrf_kernel<16>, 16)) {}
