@@ -88,16 +88,19 @@ __global__ void __launch_bounds__(256, 2) bgemm_kernel(const GemmProb* __restric
 #pragma unroll
     for (int kk = 0; kk < GBK; ++kk) {
       const double2* ap = reinterpret_cast<const double2*>(&As[buf][kk][ty * 8]);
-      const double2* bp = reinterpret_cast<const double2*>(&Bs[buf][kk][tx * 4]);
-      double a[8], b[4];
+      // columns 2tx, 2tx+1, 32+2tx, 33+2tx: 8 consecutive threads read 128 contiguous bytes
+      const double2 b01 = *reinterpret_cast<const double2*>(&Bs[buf][kk][2 * tx]);
+      const double2 b23 = *reinterpret_cast<const double2*>(&Bs[buf][kk][32 + 2 * tx]);
+      double a[8];
 #pragma unroll
       for (int q = 0; q < 4; ++q) { const double2 v = ap[q]; a[2 * q] = v.x; a[2 * q + 1] = v.y; }
 #pragma unroll
-      for (int q = 0; q < 2; ++q) { const double2 v = bp[q]; b[2 * q] = v.x; b[2 * q + 1] = v.y; }
-#pragma unroll
-      for (int i = 0; i < 8; ++i)
-#pragma unroll
-        for (int j = 0; j < 4; ++j) acc[i][j] = fma(a[i], b[j], acc[i][j]);
+      for (int i = 0; i < 8; ++i) {
+        acc[i][0] = fma(a[i], b01.x, acc[i][0]);
+        acc[i][1] = fma(a[i], b01.y, acc[i][1]);
+        acc[i][2] = fma(a[i], b23.x, acc[i][2]);
+        acc[i][3] = fma(a[i], b23.y, acc[i][3]);
+      }
     }
     if (t + 1 < nk) store(buf ^ 1);
     __syncthreads();
@@ -108,7 +111,7 @@ __global__ void __launch_bounds__(256, 2) bgemm_kernel(const GemmProb* __restric
     if (gi >= P.m) continue;
 #pragma unroll
     for (int j = 0; j < 4; ++j) {
-      const int gj = n0 + tx * 4 + j;
+      const int gj = n0 + (j < 2 ? 2 * tx + j : 32 + 2 * tx + (j - 2));
       if (gj >= P.n) continue;
       double* c = P.C + (long long)gi * P.crs + (long long)gj * P.ccs;
       const double v = P.alpha * acc[i][j];

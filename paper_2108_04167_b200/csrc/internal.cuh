@@ -200,6 +200,22 @@ struct ULVImpl {
 
 void ulv_factor_impl(ULVImpl& F, cudaStream_t s);
 
+// one top level of the cooperative top-levels sweep kernel (ulv.cu)
+struct TopLv {
+  const SolveNode* nodes;
+  const SolveWork* work;
+  const SolveWork* bwork;
+  const double* M;
+  const double* fin;
+  double* fout;
+  double* yr;
+  const double* xin;
+  double* xout;
+  double* bpart;
+  unsigned* bcnt;
+  int nwork, nbwork, ch, pad;
+};
+
 // Solve workspace for nrhs right-hand sides (tree order in/out, this rank's points).
 struct SolveWS {
   int nrhs = 0;
@@ -219,13 +235,17 @@ struct SolveWS {
   // ADMM: the caller reads x of pass-through leaves from xout[L-1] and writes their next
   // right-hand side into fin[L-1] itself (via ptmap), so the two leaf copies are skipped.
   bool fused_leaf_io = false;
+  // top levels 0..lt run as one cooperative kernel (lt = -1: per-level kernels)
+  int lt = -1;
+  DevBuf<TopLv> top;
+  DevBuf<unsigned> topbar;
 };
 void solve_ws_alloc(const ULVImpl& F, int nrhs, SolveWS& ws);
 // x_tree = (K~+beta I)^-1 b_tree.  b is read from ws.fin[L] and x written to ws.xout[L].
 void ulv_solve_tree(const ULVImpl& F, SolveWS& ws, cudaStream_t s);
 // Pieces of the solve, for iterations that reorder / fuse levels (admm.cu).
 struct SolveStep {
-  enum Kind { FWD, BWD, FWD_LIST, BWD_LIST, EXCHANGE };
+  enum Kind { FWD, BWD, FWD_LIST, BWD_LIST, EXCHANGE, TOP };
   int kind = FWD, a = 0, b = 0;
   bool no_exchange = false;
   const SolveWork* work = nullptr;  // *_LIST: level a, this work list

@@ -435,6 +435,26 @@ void ulv_factor_impl(ULVImpl& F, cudaStream_t s) {
 
 // ------------------------------------------------------------------ solve sweeps
 // (device functions fwd_rows / bwd_cols: solve_dev.cuh)
+// Work-item bodies shared by the per-level kernels and the cooperative top-levels kernel
+// (same arithmetic either way).  All threads of the CTA take part; they end with a CTA barrier
+// so a CTA may run several items back to back.
+template <int NR>
+__device__ __forceinline__ void fwd_item(const SolveNode* __restrict__ nodes, SolveWork wk, int ch,
+                                         const double* __restrict__ M, const double* __restrict__ in,
+                                         double* __restrict__ out_up, double* __restrict__ out_yr, double* vsh) {
+  const SolveNode N = nodes[wk.node];
+  const int R = N.R, tid = threadIdx.x;
+  const int i0 = wk.chunk * ch, i1 = min(R, i0 + ch);
+  if (N.pt) {  // identity operator
+    for (int e = tid; e < (i1 - i0) * NR; e += 256) out_up[(N.koff + i0) * NR + e] = in[(N.roff + i0) * NR + e];
+  } else {
+    for (int e = tid; e < R * NR; e += 256) vsh[e] = in[N.roff * NR + e];
+    __syncthreads();
+    fwd_rows<NR>(M + N.moff, R, vsh, i0, i1, tid >> 5, 8, N.k, N.koff, N.yoff, out_up, out_yr);
+  }
+  __syncthreads();
+}
+
 template <int NR>
 __global__ void __launch_bounds__(256) ulv_fwd_kernel(const SolveNode* __restrict__ nodes,
                                                       const SolveWork* __restrict__ work, int ch,
@@ -442,18 +462,8 @@ __global__ void __launch_bounds__(256) ulv_fwd_kernel(const SolveNode* __restric
                                                       const double* __restrict__ in,
                                                       double* __restrict__ out_up,
                                                       double* __restrict__ out_yr) {
-  const SolveWork wk = work[blockIdx.x];
-  const SolveNode N = nodes[wk.node];
-  const int R = N.R, tid = threadIdx.x;
   extern __shared__ double vsh[];  // R * NR
-  const int i0 = wk.chunk * ch, i1 = min(R, i0 + ch);
-  if (N.pt) {  // identity operator
-    for (int e = tid; e < (i1 - i0) * NR; e += 256) out_up[(N.koff + i0) * NR + e] = in[(N.roff + i0) * NR + e];
-    return;
-  }
-  for (int e = tid; e < R * NR; e += 256) vsh[e] = in[N.roff * NR + e];
-  __syncthreads();
-  fwd_rows<NR>(M + N.moff, R, vsh, i0, i1, tid >> 5, 8, N.k, N.koff, N.yoff, out_up, out_yr);
+  fwd_item<NR>(nodes, work[blockIdx.x], ch, M, in, out_up, out_yr, vsh);
 }
 
 template <int NR>
@@ -487,15 +497,10 @@ __global__ void __launch_bounds__(kBW * 32) ulv_bwd_kernel(const SolveNode* __re
 // (node, cc) adds the row-chunk partials in rc order.  Used for levels l <= kSplitMaxLevel
 // (l < L-1), a rule of the global tree, so results stay P-invariant.
 template <int NR>
-__global__ void __launch_bounds__(kBW * 32) ulv_bwd_split_kernel(const SolveNode* __restrict__ nodes,
-                                                                 const SolveWork* __restrict__ work,
-                                                                 const double* __restrict__ M,
-                                                                 const double* __restrict__ in_s,
-                                                                 const double* __restrict__ in_r,
-                                                                 double* __restrict__ out,
-                                                                 double* __restrict__ part,
-                                                                 unsigned* __restrict__ cnt) {
-  const SolveWork wk = work[blockIdx.x];
+__device__ __forceinline__ void bwd_split_item(const SolveNode* __restrict__ nodes, SolveWork wk, int item,
+                                               const double* __restrict__ M, const double* __restrict__ in_s,
+                                               const double* __restrict__ in_r, double* __restrict__ out,
+                                               double* __restrict__ part, unsigned* __restrict__ cnt) {
   const SolveNode N = nodes[wk.node];
   const int R = N.R, tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
   const int nrc = (R + kRB - 1) / kRB, cc = wk.chunk / nrc, rc = wk.chunk % nrc;
@@ -505,6 +510,7 @@ __global__ void __launch_bounds__(kBW * 32) ulv_bwd_split_kernel(const SolveNode
       const int j1 = min(R, j0 + kCW);
       for (int e = tid; e < (j1 - j0) * NR; e += kBW * 32) out[(N.roff + j0) * NR + e] = in_s[(N.koff + j0) * NR + e];
     }
+    __syncthreads();
     return;
   }
   __shared__ double ush[kRB * NR];
@@ -549,7 +555,7 @@ __global__ void __launch_bounds__(kBW * 32) ulv_bwd_split_kernel(const SolveNode
     red[(wid * kCW + 32 + lane) * NR + c] = ab[c];
   }
   __syncthreads();
-  double* my = part + (int64_t)blockIdx.x * kCW * NR;
+  double* my = part + (int64_t)item * kCW * NR;
   for (int e = tid; e < kCW * NR; e += kBW * 32) {
     double t = red[e];
 #pragma unroll
@@ -559,19 +565,73 @@ __global__ void __launch_bounds__(kBW * 32) ulv_bwd_split_kernel(const SolveNode
   __shared__ bool last;
   __threadfence();
   __syncthreads();
-  const int g = blockIdx.x - rc;  // first work item of (node, cc)
+  const int g = item - rc;  // first work item of (node, cc)
   if (tid == 0) last = (atomicAdd(&cnt[g], 1u) == (unsigned)(nrc - 1));
   __syncthreads();
-  if (!last) return;
-  __threadfence();
-  for (int e = tid; e < kCW * NR; e += kBW * 32) {
-    const int jj = e / NR;
-    if (j0 + jj >= R) continue;
-    double t = 0.0;
-    for (int q = 0; q < nrc; ++q) t += part[((int64_t)(g + q) * kCW) * NR + e];
-    out[(N.roff + j0) * NR + e] = t;
+  if (last) {
+    __threadfence();
+    for (int e = tid; e < kCW * NR; e += kBW * 32) {
+      const int jj = e / NR;
+      if (j0 + jj >= R) continue;
+      double t = 0.0;
+      for (int q = 0; q < nrc; ++q) t += part[((int64_t)(g + q) * kCW) * NR + e];
+      out[(N.roff + j0) * NR + e] = t;
+    }
+    if (tid == 0) cnt[g] = 0u;
   }
-  if (tid == 0) cnt[g] = 0u;
+  __syncthreads();
+}
+
+template <int NR>
+__global__ void __launch_bounds__(kBW * 32) ulv_bwd_split_kernel(const SolveNode* __restrict__ nodes,
+                                                                 const SolveWork* __restrict__ work,
+                                                                 const double* __restrict__ M,
+                                                                 const double* __restrict__ in_s,
+                                                                 const double* __restrict__ in_r,
+                                                                 double* __restrict__ out,
+                                                                 double* __restrict__ part,
+                                                                 unsigned* __restrict__ cnt) {
+  bwd_split_item<NR>(nodes, work[blockIdx.x], blockIdx.x, M, in_s, in_r, out, part, cnt);
+}
+
+// The top levels (<= lt: few nodes, latency-bound) of BOTH sweeps in one cooperative launch:
+// forward lt..0 then backward 0..lt, a grid barrier between levels instead of a kernel
+// boundary.  Same item bodies as the per-level kernels.
+
+// grid barrier for a co-resident (cooperative) grid: bar[0] counts arrivals (monotone within a
+// launch), bar[1] counts finished blocks; the last block resets both for the next launch.
+__device__ __forceinline__ void grid_barrier(unsigned* bar, unsigned k) {
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    __threadfence();
+    atomicAdd(&bar[0], 1u);
+    const unsigned target = k * gridDim.x;
+    while (atomicAdd(&bar[0], 0u) < target) __nanosleep(64);
+    __threadfence();
+  }
+  __syncthreads();
+}
+
+template <int NR>
+__global__ void __launch_bounds__(256) ulv_top_kernel(const TopLv* __restrict__ lv, int lt, unsigned* bar) {
+  extern __shared__ double vsh[];
+  unsigned nb = 0;
+  for (int l = lt; l >= 0; --l) {
+    const TopLv T = lv[l];
+    for (int it = blockIdx.x; it < T.nwork; it += gridDim.x)
+      fwd_item<NR>(T.nodes, T.work[it], T.ch, T.M, T.fin, T.fout, T.yr, vsh);
+    grid_barrier(bar, ++nb);
+  }
+  for (int l = 0; l <= lt; ++l) {
+    const TopLv T = lv[l];
+    for (int it = blockIdx.x; it < T.nbwork; it += gridDim.x)
+      bwd_split_item<NR>(T.nodes, T.bwork[it], it, T.M, T.xin, T.yr, T.xout, T.bpart, T.bcnt);
+    if (l < lt) grid_barrier(bar, ++nb);
+  }
+  if (threadIdx.x == 0 && atomicAdd(&bar[1], 1u) == gridDim.x - 1) {
+    bar[0] = 0u;
+    bar[1] = 0u;
+  }
 }
 
 // pass-through leaves: fwd  fin_{L-1}[map[p]] = fin_L[p];  bwd  xout_L[p] = xout_{L-1}[map[p]]
@@ -607,7 +667,9 @@ void solve_ws_alloc(const ULVImpl& F, int nrhs, SolveWS& ws) {
   for (int l = L; l >= 1; --l) ws.fin[l - 1] = F.lv[l].allpt ? ws.fin[l] : mk(F.lv[l].sumK);
   for (int l = 0; l <= L; ++l) if (!F.lv[l].allpt) ws.yr[l] = mk(F.lv[l].sumY);
   ws.xout[0] = mk(F.lv[0].sumR);
+  for (int l = 1; l <= L; ++l) ws.xout[l] = F.lv[l].allpt ? ws.xout[l - 1] : mk(F.lv[l].sumR);
   ws.bpart.assign(L + 1, nullptr);
+  ws.lt = -1;
   ws.bcnt.assign(L + 1, nullptr);
   for (int l = 0; l <= L; ++l)
     if (F.lv[l].split && F.lv[l].nbwork > 0) {
@@ -616,7 +678,42 @@ void solve_ws_alloc(const ULVImpl& F, int nrhs, SolveWS& ws) {
       CUDA_CHECK(cudaMemsetAsync(ws.cnt_own.back().p, 0, F.lv[l].nbwork * sizeof(unsigned), g_alloc_stream));
       ws.bcnt[l] = ws.cnt_own.back().p;
     }
-  for (int l = 1; l <= L; ++l) ws.xout[l] = F.lv[l].allpt ? ws.xout[l - 1] : mk(F.lv[l].sumR);
+  // top levels 0..lt in one cooperative launch (split backward levels only, above the exchange).
+  // Off by default: measured at config 3 it is not faster (137.7 us for levels 0-5 of both sweeps
+  // vs ~140 us as 12 level kernels; 665 vs 681 it/s end to end) -- the levels are bound by their
+  // dependency chain, not by launches.  SVMHSS_TOP_MERGE=1 enables it (bitwise-identical results).
+  int lt = std::min(kSplitMaxLevel, L - 2);
+  if (H.sh.on()) lt = std::min(lt, H.sh.lg - 1);
+  const char* env = getenv("SVMHSS_TOP_MERGE");
+  if (!(env && env[0] == '1')) lt = -1;
+  if (lt >= 1) {
+    std::vector<TopLv> tv(lt + 1);
+    for (int l = 0; l <= lt; ++l) {
+      const auto& lv = F.lv[l];
+      require(lv.split, "internal: top levels must use the split backward sweep");
+      TopLv T{};
+      T.nodes = lv.nodes.p;
+      T.work = lv.work.p;
+      T.bwork = lv.bwork.p;
+      T.M = lv.M.p;
+      T.fin = ws.fin[l];
+      T.fout = l > 0 ? ws.fin[l - 1] : nullptr;
+      T.yr = ws.yr[l];
+      T.xin = l > 0 ? ws.xout[l - 1] : nullptr;
+      T.xout = ws.xout[l];
+      T.bpart = ws.bpart[l];
+      T.bcnt = ws.bcnt[l];
+      T.nwork = lv.allpt ? 0 : lv.nwork;
+      T.nbwork = lv.allpt ? 0 : lv.nbwork;
+      T.ch = lv.ch;
+      tv[l] = T;
+    }
+    ws.top = upload(tv, g_alloc_stream);
+    ws.topbar.alloc(2);
+    CUDA_CHECK(cudaMemsetAsync(ws.topbar.p, 0, 2 * sizeof(unsigned), g_alloc_stream));
+    CUDA_CHECK(cudaStreamSynchronize(g_alloc_stream));
+    ws.lt = lt;
+  }
 }
 
 template <int NR>
@@ -686,6 +783,38 @@ static void run_step(const ULVImpl& F, SolveWS& ws, const SolveStep& st, cudaStr
     case SolveStep::FWD_LIST: fwd_level<NR>(F, ws, st.a, st.work, st.nwork, s); break;
     case SolveStep::BWD_LIST: bwd_level<NR>(F, ws, st.a, st.work, st.nwork, s); break;
     case SolveStep::EXCHANGE: if (H.sh.on()) exchange_step<NR>(F, ws, s); break;
+    case SolveStep::TOP: {
+      int maxR = 0, items = 1;
+      for (int l = 0; l <= ws.lt; ++l) {
+        maxR = std::max(maxR, F.lv[l].maxR);
+        items = std::max(items, std::max(F.lv[l].nwork, F.lv[l].nbwork));
+      }
+      const size_t sm = (size_t)maxR * NR * sizeof(double);
+      static int nsm = 0;
+      if (!nsm) {
+        int dev = 0;
+        CUDA_CHECK(cudaGetDevice(&dev));
+        CUDA_CHECK(cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev));
+      }
+      if (sm > 48 * 1024)
+        CUDA_CHECK(cudaFuncSetAttribute(ulv_top_kernel<NR>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm));
+      int per_sm = 0;
+      CUDA_CHECK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, ulv_top_kernel<NR>, 256, sm));
+      const int grid = std::max(1, std::min(items, nsm * std::max(1, per_sm)));
+      cudaLaunchConfig_t cfg = {};
+      cfg.gridDim = dim3(grid);
+      cfg.blockDim = dim3(256);
+      cfg.dynamicSmemBytes = sm;
+      cfg.stream = s;
+      cudaLaunchAttribute at[1];
+      at[0].id = cudaLaunchAttributeCooperative;
+      at[0].val.cooperative = 1;
+      cfg.attrs = at;
+      cfg.numAttrs = 1;
+      CUDA_CHECK(cudaLaunchKernelEx(&cfg, ulv_top_kernel<NR>, (const TopLv*)ws.top.p, ws.lt, ws.topbar.p));
+      g_launches.fetch_add(1);
+      break;
+    }
   }
 }
 
@@ -716,7 +845,11 @@ void ulv_solve_steps(const ULVImpl& F, SolveWS& ws, const std::vector<SolveStep>
 
 void ulv_solve_tree(const ULVImpl& F, SolveWS& ws, cudaStream_t s) {
   const int L = F.H->L;
-  ulv_solve_steps(F, ws, {SolveStep{SolveStep::FWD, L, 0}, SolveStep{SolveStep::BWD, 0, L}}, s);
+  if (ws.lt >= 1)
+    ulv_solve_steps(F, ws, {SolveStep{SolveStep::FWD, L, ws.lt + 1}, SolveStep{SolveStep::TOP},
+                            SolveStep{SolveStep::BWD, ws.lt + 1, L}}, s);
+  else
+    ulv_solve_steps(F, ws, {SolveStep{SolveStep::FWD, L, 0}, SolveStep{SolveStep::BWD, 0, L}}, s);
 }
 
 

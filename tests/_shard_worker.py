@@ -4,7 +4,7 @@ torchrun, exchanging through a gloo group with the library's host-callback backe
 Runs build + factor + solve + mat-vec + ADMM (+ bias/objective) through the C-ABI and
 writes this rank's outputs to <out>/P<world>_r<rank>.npz.
 
-    torchrun --nproc-per-node P tests/_shard_worker.py OUTDIR CFG N [CAP] [BETA] [MAXIT]
+    torchrun --nproc-per-node P tests/_shard_worker.py OUTDIR CFG N [CAP] [BETA] [MAXIT] [sketch|ann]
 """
 import os
 import sys
@@ -22,6 +22,7 @@ def main():
     cap = int(sys.argv[4]) if len(sys.argv) > 4 else None
     beta = float(sys.argv[5]) if len(sys.argv) > 5 else 1e4
     max_it = int(sys.argv[6]) if len(sys.argv) > 6 else 60
+    sampling = sys.argv[7] if len(sys.argv) > 7 else "sketch"
     rank = int(os.environ.get("RANK", 0))
     world = int(os.environ.get("WORLD_SIZE", 1))
     import datagen
@@ -40,7 +41,9 @@ def main():
     h = cfg["h"][2] if isinstance(cfg["h"], list) else cfg["h"]
     H = P.hss_build(Fd, h, leaf_size=cfg["leaf"], rel_tol=cfg["rel_tol"], abs_tol=cfg["abs_tol"],
                     max_rank=cfg["cap"], oversample=cfg["s"] - cfg["cap"], omega_seed=cfg["seed_omega"],
-                    tree_seed=cfg["seed_tree"], comm=comm)
+                    tree_seed=cfg["seed_tree"], comm=comm, sampling=sampling,
+                    ann_neighbors=cfg["ann_neighbors"], ann_trees=cfg["ann_trees"], ann_leaf=cfg["ann_leaf"],
+                    ann_seed=cfg["ann_seed"])
     U = P.hss_ulv_factor(H, beta)
     g = np.random.default_rng(7)
     b = torch.from_numpy(g.standard_normal((n, 2))).to(dev)
