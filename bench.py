@@ -272,6 +272,8 @@ def main():
     if args.config == 4:
         return bench_grid(args, rank, world, dev)
     cfg = datagen.get_config(args.config)
+    if args.sampling == "ann":
+        cfg["beta"] = cfg["beta_ann"]  # AMB-9 calibrated on the ANN K~ (datagen/configs.py)
     if args.beta is not None:
         cfg["beta"] = args.beta
     n = args.n or cfg["n"]

@@ -57,6 +57,9 @@ _CONFIGS = {
 #   cfg 3: lambda_min = -62850.4 -> 1e6  (oracle at n = 524288: 8256 s of host compression + eigsh)
 _BETA = {1: 1e4, 2: 1e5, 3: 1e6, 4: None}
 _BETA_PER_H = {4: {0.25: 1e2, 0.5: 1e3, 1.0: 1e4, 2.0: 1e4, 4.0: 1e3}}
+# The same rule for the HSS-ANN K~ (sampling = "ann"; scripts/calibrate_beta.py --sampling ann):
+#   cfg 3: lambda_min = -4.43 -> schedule 1e3   (oracle ANN build at n = 524288: 629 s)
+_BETA_ANN = {3: 1e3}
 
 # HSS-ANN sampling knobs (readings N1-N3): neighbours per point (the paper's
 # Table 4 setting "hss_approximate_neighbors 64"), random-projection trees, their leaf
@@ -77,6 +80,7 @@ for _c, _cfg in _CONFIGS.items():
         _cfg["beta"] = b if b is not None else beta_schedule(_cfg["n"])
     if _c in _BETA_PER_H:
         _cfg["beta_per_h"] = dict(_BETA_PER_H[_c])
+    _cfg["beta_ann"] = _BETA_ANN.get(_c, beta_schedule(_cfg["n"]))
 
 CONFIGS = _CONFIGS
 
