@@ -296,13 +296,20 @@ def main():
         H = P.hss_build(Fd, h, **opts)
         U = P.hss_ulv_factor(H, cfg["beta"])
         res = P.admm_svm_train(U, yd, Cs, max_it, want_mu=False)
+        st = dict(res["stats"])
+        st["ms_predict"] = None
         if not args.no_predict and Ftd.shape[0] > 0:
             coef = (yd[:, None] * res["z"]).contiguous()
+            p0, p1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            p0.record(stream)
             P.svm_predict(Fd, coef, h, res["bias"], Ftd)
+            p1.record(stream)
+            p1.synchronize()
+            st["ms_predict"] = p0.elapsed_time(p1)
         hi, ui = H.info(), U.info()
         U.free()
         H.free()
-        return hi, ui, res["stats"]
+        return hi, ui, st
 
     dgemm_tf = measure_dgemm(dev)
     for _ in range(args.warmup):
@@ -357,7 +364,7 @@ def main():
             "phases_ms": {"tree": hi["ms_tree"], "omega": hi["ms_omega"], "sketch": hi["ms_sketch"],
                           "compress": hi["ms_compress"], "factor": ui["ms_factor"],
                           "admm_precompute": ast["ms_precompute"], "admm_loop": ast["ms_loop"],
-                          "bias": ast["ms_bias"]},
+                          "bias": ast["ms_bias"], "predict": ast["ms_predict"]},
             "hss": {"L": hi["L"], "max_rank": hi["max_rank_used"], "cap_hits": hi["cap_hits"],
                     "passthrough": hi["passthrough"], "generator_bytes": hi["generator_bytes"],
                     "factor_bytes": ui["factor_bytes"]},
@@ -375,6 +382,24 @@ def main():
                                "achieved": ach_gbs, "peak": peaks["hbm_gbs"], "unit": "GB/s",
                                "frac": ach_gbs / peaks["hbm_gbs"],
                                "work": "2 x factor_bytes + 64 n nC bytes per iteration"},
+            "roofline_factor": {"bound": "fp64 (DFMA)", "phase": "hss_ulv_factor (batched QR, WY GEMMs, POTRF, TRSM)",
+                                "achieved": ui["factor_flops"] / (ui["ms_factor"] / 1e3) / 1e12,
+                                "peak": fp64_peak, "unit": "TFLOP/s",
+                                "frac": ui["factor_flops"] / (ui["ms_factor"] / 1e3) / 1e12 / fp64_peak,
+                                "hbm_gbs": ui["factor_bytes"] / (ui["ms_factor"] / 1e3) / 1e9,
+                                "work": "sum over nodes 2Rk^2 + 8R^2k + (R-k)^3/3 + k(R-k)^2 + k^2(R-k) + 4k^3 "
+                                        "(SURVEY 8(d) a7), flops %.3e" % ui["factor_flops"]},
+            "roofline_predict": None if ast["ms_predict"] is None else {
+                "bound": "tensor", "phase": "svm_predict (kmm_kernel: K(Ftest, F) [y z | 0], 16 columns)",
+                "achieved": 2.0 * Ftd.shape[0] * n * (rp + 16) / (ast["ms_predict"] / 1e3) / 1e12,
+                "peak": fp64_peak, "unit": "TFLOP/s",
+                "frac": 2.0 * Ftd.shape[0] * n * (rp + 16) / (ast["ms_predict"] / 1e3) / 1e12 / fp64_peak,
+                "work": "2 m n (r_pad + 16) flops (incl. padding/norm/finish kernels in the time)"},
+            "roofline_bias": {"bound": "hbm", "phase": "bias + objective: one HSS mat-vec with 2 nC columns",
+                              "achieved": hi["generator_bytes"] / (ast["ms_bias"] / 1e3) / 1e9,
+                              "peak": peaks["hbm_gbs"], "unit": "GB/s",
+                              "frac": hi["generator_bytes"] / (ast["ms_bias"] / 1e3) / 1e9 / peaks["hbm_gbs"],
+                              "work": "generator bytes (D, U, B) read once"},
             "clocks": clocks}
     if args.sampling == "ann":
         # no dense sketch in HSS-ANN mode: the dominant kernel of the step is the ULV sweep pair

@@ -117,6 +117,7 @@ typedef struct {
   double beta;
   int64_t factor_bytes;    /* bytes of the per-node solve operators M_t */
   double ms_factor;
+  double factor_flops;     /* algorithmic flops of this rank's nodes (SURVEY §8(d) a7 count) */
 } ulv_stats;
 
 /* ---- build: tree + Omega + sketch + per-level ID compression (Alg.3 l.1) ----

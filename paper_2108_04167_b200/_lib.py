@@ -45,7 +45,8 @@ class HssStats(ct.Structure):
 
 
 class UlvStats(ct.Structure):
-    _fields_ = [("beta", ct.c_double), ("factor_bytes", ct.c_int64), ("ms_factor", ct.c_double)]
+    _fields_ = [("beta", ct.c_double), ("factor_bytes", ct.c_int64), ("ms_factor", ct.c_double),
+                ("factor_flops", ct.c_double)]
 
 
 class AdmmOpts(ct.Structure):

@@ -86,6 +86,9 @@ void ulv_factor_impl(ULVImpl& F, cudaStream_t s) {
   DevBuf<double> DhC, RmC;           // child level
   std::vector<int64_t> dhoffC;       // offsets (doubles) by the child's BFS index (k*k packing)
   int64_t total_bytes = 0;
+  // algorithmic flops (per non-pass-through node of R rows and rank k):
+  // 2Rk^2 + 8R^2k + (R-k)^3/3 + k(R-k)^2 + k^2(R-k) + 4k^3; root: R^3/3
+  double total_flops = 0.0;
   PhaseTrace ptr_("ulv_factor", s);
   for (int l = L; l >= 0; --l) {
     ptr_.mark("L" + std::to_string(l) + " begin");
@@ -159,6 +162,7 @@ void ulv_factor_impl(ULVImpl& F, cudaStream_t s) {
       F_l.nodes = upload(sn, s);
       F_l.sumR = Rn; F_l.sumK = 0; F_l.sumY = Rn; F_l.maxR = Rn; F_l.allpt = 0;
       total_bytes += 8LL * Rn * Rn;
+      total_flops += (double)Rn * Rn * Rn / 3.0;
       CUDA_CHECK(cudaStreamSynchronize(s));
       break;
     }
@@ -236,6 +240,11 @@ void ulv_factor_impl(ULVImpl& F, cudaStream_t s) {
     }
     F_l.M.alloc(std::max<int64_t>(1, sumM));
     total_bytes += 8 * sumM;
+    for (int i = 0; i < nn; ++i) {
+      if (PT[i]) continue;
+      const double r = R[i], k = K[i], e = r - k;
+      total_flops += 2 * r * k * k + 8 * r * r * k + e * e * e / 3 + k * e * e + k * k * e + 4 * k * k * k;
+    }
     if (!np.empty() || !nz.empty()) {
       std::vector<int64_t> vo(nn), to(nn);
       int64_t sRK = 0, sKK = 0;
@@ -430,6 +439,7 @@ void ulv_factor_impl(ULVImpl& F, cudaStream_t s) {
   }
   F.st.beta = beta;
   F.st.factor_bytes = total_bytes;
+  F.st.factor_flops = total_flops;
   F.st.ms_factor = tm.stop_ms();
 }
 
