@@ -144,6 +144,38 @@ def compress(Fp: np.ndarray, h: float, ranges, Omega_p: np.ndarray, *, ranks=Non
     return hss
 
 
+def unconverged(hss: HSS, s: int, p: int, cap) -> list:
+    """N2b: nodes whose rank ran into the sample budget: k > s - p while more rank was possible
+    (k < min(cap, rows))."""
+    bad = []
+    for t, k in hss.k.items():
+        lim = hss.rows[t] if cap is None else min(cap, hss.rows[t])
+        if k > s - p and k < lim:
+            bad.append(t)
+    return bad
+
+
+def compress_adaptive(Fp: np.ndarray, h: float, ranges, perm: np.ndarray, seed: int, *, s0: int, ds: int,
+                      s_max: int, p: int, rel_tol=0.0, abs_tol=0.0, cap=None):
+    """N2 (P:70 / P:184, adaptive randomized sampling; our reading):
+      N2a  start with s = min(s0, s_max) columns of Omega (R1-R3: column j of Omega does not
+           depend on s, so a larger s only appends columns);
+      N2b  compress (H1-H5); if any node is unconverged (its rank reached s - p while
+           min(cap, rows) allowed more), s = min(s + ds, s_max) and compress again from scratch;
+      N2c  stop when every node converged or s = s_max.
+    Returns (hss, s_final, rounds)."""
+    from .rng import omega
+    s = min(s0, s_max)
+    rounds = 0
+    while True:
+        rounds += 1
+        Om = omega(seed, perm, s)
+        H = compress(Fp, h, ranges, Om, rel_tol=rel_tol, abs_tol=abs_tol, cap=cap)
+        if s >= s_max or not unconverged(H, s, p, cap):
+            return H, s, rounds
+        s = min(s + ds, s_max)
+
+
 def matvec(hss: HSS, V: np.ndarray) -> np.ndarray:
     """M: K~ V in tree order (upward U^T sweep, B coupling, downward U sweep, leaf D)."""
     V = np.asarray(V, dtype=np.float64)

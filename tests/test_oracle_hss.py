@@ -134,3 +134,35 @@ def test_ulv_breakdown_names_node():
         ulv.factor(H, 1e-6)
     assert isinstance(ei.value.node, int)
     ulv.factor(H, -4 * lmin)   # a shift past -lambda_min succeeds
+
+
+# ------------------------------------------------------------------ N2: adaptive sampling
+def test_adaptive_with_full_budget_is_the_plain_compression():
+    F, perm, ranges, Fp, Om = _setup(600, 5, 40, 96, 1.0)
+    H1 = hss.compress(Fp, 1.0, ranges, Om, rel_tol=1e-3, cap=80)
+    H2, s, rounds = hss.compress_adaptive(Fp, 1.0, ranges, perm, 22, s0=96, ds=16, s_max=96, p=16,
+                                          rel_tol=1e-3, cap=80)
+    assert s == 96 and rounds == 1
+    assert all(H1.k[t] == H2.k[t] for t in H1.k)
+    assert np.array_equal(hss.assemble_dense(H1), hss.assemble_dense(H2))
+
+
+def test_adaptive_grows_until_converged_and_meets_tolerance():
+    # near-exact tolerance, small start: the loop must grow s, end with every node converged
+    # (or at the budget), and the compressed K~ must meet the tolerance (E6 shape)
+    F, perm, ranges, Fp, _ = _setup(700, 3, 64, 16, 1.5)
+    H, s, rounds = hss.compress_adaptive(Fp, 1.5, ranges, perm, 0, s0=24, ds=24, s_max=400, p=16,
+                                         rel_tol=1e-6)
+    assert rounds > 1 and s > 24
+    assert s == 400 or not hss.unconverged(H, s, 16, None)
+    K = np.exp(-((Fp[:, None, :] - Fp[None, :, :]) ** 2).sum(-1) / (2 * 1.5 ** 2))
+    assert np.linalg.norm(hss.assemble_dense(H) - K, 2) <= 1e-6 * np.linalg.norm(K, 2)
+
+
+def test_unconverged_rule():
+    H = hss.HSS(n=0, L=1, ranges=[], Fp=np.zeros((0, 1)), h=1.0)
+    H.k = {1: 40, 2: 30, 3: 50}
+    H.rows = {1: 100, 2: 100, 3: 50}
+    # s = 48, p = 16: k > 32 and k < min(cap, rows) -> node 1 only (node 3 is full rank)
+    assert hss.unconverged(H, 48, 16, None) == [1]
+    assert hss.unconverged(H, 48, 16, 40) == []     # node 1 at the cap
