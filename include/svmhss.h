@@ -99,6 +99,11 @@ typedef struct {
   int32_t sampling;
   int32_t ann_neighbors, ann_trees, ann_leaf;
   uint64_t ann_seed;
+  /* Adaptive randomized sampling (readings N2a-c; sketch sampling only):
+   * adaptive_s0 > 0 starts with s = min(adaptive_s0, max_rank + oversample) columns of Omega and,
+   * while some node's rank k > s - oversample with k < min(max_rank, rows), rebuilds with
+   * s += adaptive_ds (> 0), up to max_rank + oversample.  0 = fixed s = max_rank + oversample. */
+  int32_t adaptive_s0, adaptive_ds;
 } hss_opts;
 enum { HSS_SAMPLING_SKETCH = 0, HSS_SAMPLING_ANN = 1 };
 
@@ -111,6 +116,7 @@ typedef struct {
   int32_t passthrough;     /* nodes with k_t == rows_t */
   int64_t generator_bytes; /* bytes of D, U, B (fp64) */
   double ms_tree, ms_omega, ms_sketch, ms_compress; /* phase device times (CUDA events) */
+  int32_t s_used, sample_rounds;   /* sketch columns of the final build, builds (adaptive: >= 1) */
 } hss_stats;
 
 typedef struct {

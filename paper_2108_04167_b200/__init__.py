@@ -236,8 +236,9 @@ SAMPLING = {"sketch": 0, "ann": 1}
 
 def make_opts(leaf_size, rel_tol=0.0, abs_tol=0.0, max_rank=64, oversample=16, omega_seed=0,
               tree_seed=0, ranks=None, comm=None, sampling="sketch", ann_neighbors=64, ann_trees=4,
-              ann_leaf=256, ann_seed=0):
+              ann_leaf=256, ann_seed=0, adaptive_s0=0, adaptive_ds=0):
     o = HssOpts()
+    o.adaptive_s0, o.adaptive_ds = int(adaptive_s0), int(adaptive_ds)
     o.comm = comm.handle if comm is not None else None
     o.sampling = SAMPLING[sampling]
     o.ann_neighbors, o.ann_trees, o.ann_leaf, o.ann_seed = int(ann_neighbors), int(ann_trees), int(ann_leaf), int(ann_seed)
@@ -253,14 +254,14 @@ def make_opts(leaf_size, rel_tol=0.0, abs_tol=0.0, max_rank=64, oversample=16, o
 
 def hss_build(F, h, leaf_size, rel_tol=0.0, abs_tol=0.0, max_rank=64, oversample=16, omega_seed=0,
               tree_seed=0, ranks=None, comm=None, sampling="sketch", ann_neighbors=64, ann_trees=4,
-              ann_leaf=256, ann_seed=0, stream=None) -> HSS:
+              ann_leaf=256, ann_seed=0, adaptive_s0=0, adaptive_ds=0, stream=None) -> HSS:
     """hss_build (Alg. 3 line 1): F is a CUDA float64 (n, r) tensor, original order
     (all n points on every rank when `comm` shards the tree).  sampling="ann" selects HSS-ANN
     column sampling instead of the randomized sketch."""
     _cuda_f64(F, "F")
     n, r = F.shape
     o, keep = make_opts(leaf_size, rel_tol, abs_tol, max_rank, oversample, omega_seed, tree_seed, ranks, comm,
-                        sampling, ann_neighbors, ann_trees, ann_leaf, ann_seed)
+                        sampling, ann_neighbors, ann_trees, ann_leaf, ann_seed, adaptive_s0, adaptive_ds)
     hdl = ct.c_void_p()
     check(_L.hss_build(ptr(F), n, r, float(h), ct.byref(o), _stream(stream), ct.byref(hdl)))
     del keep

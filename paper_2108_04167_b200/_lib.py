@@ -29,7 +29,8 @@ class HssOpts(ct.Structure):
                 ("max_rank", ct.c_int32), ("oversample", ct.c_int32), ("omega_seed", ct.c_uint64),
                 ("tree_seed", ct.c_uint64), ("ranks", ct.POINTER(ct.c_int32)), ("comm", ct.c_void_p),
                 ("sampling", ct.c_int32), ("ann_neighbors", ct.c_int32), ("ann_trees", ct.c_int32),
-                ("ann_leaf", ct.c_int32), ("ann_seed", ct.c_uint64)]
+                ("ann_leaf", ct.c_int32), ("ann_seed", ct.c_uint64),
+                ("adaptive_s0", ct.c_int32), ("adaptive_ds", ct.c_int32)]
 
 
 # int (*hss_allgather_fn)(void* ctx, const void* send, void* recv, size_t bytes)
@@ -41,7 +42,7 @@ class HssStats(ct.Structure):
                 ("leaf_size", ct.c_int32), ("max_rank_used", ct.c_int32), ("cap_hits", ct.c_int32),
                 ("passthrough", ct.c_int32), ("generator_bytes", ct.c_int64),
                 ("ms_tree", ct.c_double), ("ms_omega", ct.c_double), ("ms_sketch", ct.c_double),
-                ("ms_compress", ct.c_double)]
+                ("ms_compress", ct.c_double), ("s_used", ct.c_int32), ("sample_rounds", ct.c_int32)]
 
 
 class UlvStats(ct.Structure):

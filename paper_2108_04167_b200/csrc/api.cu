@@ -83,6 +83,35 @@ static bool held(const HSSImpl& H, int l, int i) {
   return i >= H.sh.first(l) && i < H.sh.last(l);
 }
 
+// hss_build with the adaptive sampling loop (N2a-c) when opt.adaptive_s0 > 0
+static HSSImpl* build_adaptive(const double* F, int64_t n, int r, double h, const hss_opts& o,
+                               std::shared_ptr<Comm> comm, cudaStream_t s) {
+  const int s_max = o.max_rank + o.oversample;
+  int s_cur = (o.adaptive_s0 > 0) ? std::min(o.adaptive_s0, s_max) : s_max;
+  if (s_cur % 2) ++s_cur;  // the sketch kernel needs an even column count
+  s_cur = std::min(s_cur, s_max);
+  double ms[4] = {0, 0, 0, 0};
+  for (int round = 1;; ++round) {
+    auto* H = new HSSImpl();
+    try {
+      hss_build_impl(*H, F, n, r, h, o, comm, s, s_cur);
+    } catch (...) {
+      delete H;
+      throw;
+    }
+    ms[0] += H->st.ms_tree; ms[1] += H->st.ms_omega; ms[2] += H->st.ms_sketch; ms[3] += H->st.ms_compress;
+    const bool done = o.adaptive_s0 <= 0 || s_cur >= s_max || !hss_unconverged(*H, o.oversample, o.max_rank);
+    if (done) {
+      H->st.s_used = s_cur;
+      H->st.sample_rounds = round;
+      H->st.ms_tree = ms[0]; H->st.ms_omega = ms[1]; H->st.ms_sketch = ms[2]; H->st.ms_compress = ms[3];
+      return H;
+    }
+    delete H;
+    s_cur = std::min(s_max, s_cur + o.adaptive_ds + (o.adaptive_ds % 2));
+  }
+}
+
 static void release_hss(HSSImpl* H) {
   if (H && H->refs.fetch_sub(1) == 1) delete H;
 }
@@ -100,6 +129,10 @@ static void validate_opts(const hss_opts* o, int64_t n, int32_t r, double h) {
   require(s % 2 == 0, "hss_build: s = max_rank + oversample must be even");
   require(o->rel_tol >= 0 && o->abs_tol >= 0, "hss_build: tolerances must be >= 0");
   require(o->sampling == HSS_SAMPLING_SKETCH || o->sampling == HSS_SAMPLING_ANN, "hss_build: unknown sampling");
+  if (o->adaptive_s0 > 0) {
+    require(o->sampling == HSS_SAMPLING_SKETCH, "hss_build: adaptive sampling needs the sketch sampling");
+    require(o->adaptive_ds > 0, "hss_build: adaptive_ds must be > 0");
+  }
   if (o->sampling == HSS_SAMPLING_ANN) {
     require(o->ann_neighbors >= 1 && o->ann_trees >= 1 && o->ann_leaf >= 2 && o->ann_leaf <= 256,
             "hss_build: ANN needs ann_neighbors >= 1, ann_trees >= 1, 2 <= ann_leaf <= 256");
@@ -133,14 +166,7 @@ int hss_build(const double* F, int64_t n, int32_t r, double h, const hss_opts* o
     StreamScope ss__((cudaStream_t)stream);
     require(out != nullptr && F != nullptr, "hss_build: NULL pointer");
     validate_opts(opt, n, r, h);
-    auto* H = new HSSImpl();
-    try {
-      hss_build_impl(*H, F, n, r, h, *opt, comm_of(opt), (cudaStream_t)stream);
-    } catch (...) {
-      delete H;
-      throw;
-    }
-    *out = new hss_s{H};
+    *out = new hss_s{build_adaptive(F, n, r, h, *opt, comm_of(opt), (cudaStream_t)stream)};
   });
 }
 
@@ -334,9 +360,8 @@ int svm_train_predict_host(const double* F, const double* y, int64_t n, int32_t 
     h2d(dy.p, y, n, s);
     if (labels_out && m > 0) h2d(dFt.p, Ftest, (size_t)m * r, s);
     CUDA_CHECK(cudaEventRecord(ev[1], s));
-    HSSImpl* H = new HSSImpl();
+    HSSImpl* H = build_adaptive(dF.p, n, r, h, *opt, comm_of(opt), s);
     struct HG { HSSImpl* h; ~HG() { release_hss(h); } } hg{H};
-    hss_build_impl(*H, dF.p, n, r, h, *opt, comm_of(opt), s);
     CUDA_CHECK(cudaEventRecord(ev[2], s));
     ULVImpl Fz;
     Fz.H = H;

@@ -72,13 +72,13 @@ struct RootRec {
 };
 
 void hss_build_impl(HSSImpl& H, const double* F, int64_t n, int r, double h, const hss_opts& o,
-                    std::shared_ptr<Comm> comm, cudaStream_t s) {
+                    std::shared_ptr<Comm> comm, cudaStream_t s, int s_cols) {
   H.n = n;
   H.r = r;
   H.rp = (r + 3) / 4 * 4;
   H.h = h;
   H.m = o.leaf_size;
-  H.s = o.max_rank + o.oversample;
+  H.s = s_cols > 0 ? s_cols : o.max_rank + o.oversample;
   H.L = num_levels(n, H.m);
   const int rp = H.rp, S = H.s, L = H.L;
   // ---- shard plan: rank g owns node g of level lg = log2 P
@@ -400,6 +400,28 @@ void hss_build_impl(HSSImpl& H, const double* F, int64_t n, int r, double h, con
   H.st.passthrough = npt + sub_pt;
   H.st.generator_bytes = sub_bytes + top_bytes;
   CUDA_CHECK(cudaStreamSynchronize(s));
+}
+
+// N2b: does some node of this build have its rank at the sample budget (k > s - p) while
+// min(cap, rows) allowed more?  Global over ranks (an allgather of one flag).
+bool hss_unconverged(const HSSImpl& H, int p, int cap) {
+  int bad = 0;
+  for (int l = 1; l <= H.L && !bad; ++l)
+    for (int i = H.sh.first(l); i < H.sh.last(l); ++i) {
+      const auto& nd = H.lv[l][i];
+      if (nd.k > H.s - p && nd.k < std::min(cap, nd.rows)) { bad = 1; break; }
+    }
+  if (H.sh.on()) {
+    DevBuf<int> one(1), all(H.sh.P);
+    CUDA_CHECK(cudaMemcpy(one.p, &bad, sizeof(int), cudaMemcpyHostToDevice));
+    H.sh.comm->allgather(one.p, all.p, sizeof(int), g_alloc_stream);
+    std::vector<int> h(H.sh.P);
+    d2h(h.data(), all.p, H.sh.P, g_alloc_stream);
+    CUDA_CHECK(cudaStreamSynchronize(g_alloc_stream));
+    bad = 0;
+    for (int v : h) bad |= v;
+  }
+  return bad != 0;
 }
 
 // ------------------------------------------------------------------ mat-vec (M)

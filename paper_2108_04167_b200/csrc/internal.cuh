@@ -115,8 +115,10 @@ struct HSSImpl {
   int node_id(int l, int i) const { return (1 << l) - 1 + i; }
 };
 
+// s_cols > 0: sketch with s_cols columns instead of max_rank + oversample (adaptive sampling)
 void hss_build_impl(HSSImpl& H, const double* F, int64_t n, int r, double h,
-                    const hss_opts& o, std::shared_ptr<Comm> comm, cudaStream_t s);
+                    const hss_opts& o, std::shared_ptr<Comm> comm, cudaStream_t s, int s_cols = -1);
+bool hss_unconverged(const HSSImpl& H, int p, int cap);
 // K~ V in TREE order on this rank's points: V/out nloc x nrhs point-major (device),
 // rows [lo_g, hi_g) of the tree order.
 void hss_matvec_tree(const HSSImpl& H, const double* V, double* out, int nrhs, cudaStream_t s);
