@@ -249,6 +249,7 @@ def main():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-predict", action="store_true")
+    ap.add_argument("--no-variants", action="store_true", help="skip the HSS-ANN variant sub-line")
     ap.add_argument("--sampling", default="sketch", choices=["sketch", "ann"],
                     help="compression sampling: the randomized sketch (north star, default) or HSS-ANN "
                          "column sampling (SURVEY 8(f) N1)")
@@ -420,6 +421,33 @@ def main():
                        "timings_ms": e["timings_ms"],
                        "note": "svm_train_predict_host on pinned host buffers: h2d + build + factor + "
                                "ADMM + bias + predict + d2h; iterations / total call time"}
+    if world == 1 and args.sampling == "sketch" and not args.no_variants and args.n is None:
+        # the same step with HSS-ANN compression (the paper's P:186-187 construction),
+        # its own calibrated beta; one warm-up + one timed step, device-timed like the main line
+        opts_a = cfg_opts(cfg, "ann")
+        beta_a = cfg["beta_ann"]
+
+        def step_ann():
+            H = P.hss_build(Fd, h, **opts_a)
+            U = P.hss_ulv_factor(H, beta_a)
+            res = P.admm_svm_train(U, yd, Cs, max_it, want_mu=False)
+            hi_a, ui_a = H.info(), U.info()
+            U.free()
+            H.free()
+            return hi_a, ui_a, res["stats"]
+
+        step_ann()
+        hi_a, ui_a, st_a = step_ann()
+        line["variants"] = {"ann": {
+            "sampling": "ann", "beta": beta_a, "admm_iters_per_s": max_it * len(Cs) / (st_a["ms_loop"] / 1e3),
+            "hss_build_ulv_s": (hi_a["ms_tree"] + hi_a["ms_sketch"] + hi_a["ms_compress"] + ui_a["ms_factor"]) / 1e3,
+            "phases_ms": {"tree": hi_a["ms_tree"], "ann": hi_a["ms_sketch"], "compress": hi_a["ms_compress"],
+                          "factor": ui_a["ms_factor"], "admm_loop": st_a["ms_loop"]},
+            "solve_gbs": (2.0 * ui_a["factor_bytes"] + 64.0 * n * len(Cs)) * max_it / (st_a["ms_loop"] / 1e3) / 1e9,
+            "ranks_max": hi_a["max_rank_used"], "passthrough": hi_a["passthrough"],
+            "factor_bytes": ui_a["factor_bytes"],
+            "note": "HSS-ANN sampling (ann_neighbors/trees/leaf from datagen/configs.py); not the north-star "
+                    "dense sketch - reported beside it"}}
     if rank == 0 and world == 1 and not args.no_cpu_baseline and args.n is None:
         r = oracle_sample(args.config, args.ref_n, args.ref_iters)
         line["cpu_baseline"] = {"value": r["value"], "unit": "iters/s", "cores": r["cores"], "kind": "oracle",

@@ -340,9 +340,12 @@ void kernel_matmul(const KmmArgs& a, cudaStream_t s) {
   const int SA = pad_stride(a.rp);
   const int NT = pick_nt(a.ncols);
   const size_t lim = 227 * 1024;
-  const int BJ = (kmm_smem(32, NT, SA) <= lim) ? 32 : 16;
+  // narrow right-hand sides (prediction: 16 columns): 64-point steps, so each warp runs 4
+  // distance tiles (8 independent DMMA chains) per step and the per-step barriers amortise
+  const int BJ = (NT <= 5 && kmm_smem(64, NT, SA) <= lim) ? 64 : (kmm_smem(32, NT, SA) <= lim) ? 32 : 16;
   require(kmm_smem(BJ, NT, SA) <= lim, "kernel_matmul: feature dimension too large for shared memory");
 #define KMM_CASE(bj, nt) if (BJ == bj && NT == nt) { launch_kmm<bj, nt>(a, SA, s); return; }
+  KMM_CASE(64, 1) KMM_CASE(64, 5)
   KMM_CASE(32, 1) KMM_CASE(32, 5) KMM_CASE(32, 9) KMM_CASE(32, 17)
   KMM_CASE(16, 1) KMM_CASE(16, 5) KMM_CASE(16, 9) KMM_CASE(16, 17)
 #undef KMM_CASE
