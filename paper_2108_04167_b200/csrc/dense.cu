@@ -9,6 +9,7 @@
 //  blarft  : compact-WY T factor (Q = I - V T V^T).
 //  bcpqr   : column-pivoted Householder QR of Y^T with the AMB-10 rank rule (H3): exact
 //            trailing column norms recomputed in the update pass; argmax ties -> lowest index.
+#include <cstdlib>
 #include "dense.cuh"
 
 namespace svmhss {
@@ -120,6 +121,100 @@ __global__ void __launch_bounds__(256, 2) bgemm_kernel(const GemmProb* __restric
   }
 }
 
+// 128 x 128 x 8 tiles, 256 threads, 8 x 8 outputs per thread (rows 8ty.., columns
+// {4tx.., 64+4tx..}): 64 independent FMA chains per k and 8 FMAs per 16-byte shared load; one
+// CTA per SM (registers).  Same per-element k order as bgemm_kernel.
+constexpr int HBM_ = 128, HBN = 128;
+
+__global__ void __launch_bounds__(256, 1) bgemm_big_kernel(const GemmProb* __restrict__ probs) {
+  const GemmProb P = probs[blockIdx.z];
+  const int m0 = blockIdx.y * HBM_, n0 = blockIdx.x * HBN;
+  if (m0 >= P.m || n0 >= P.n) return;
+  __shared__ __align__(16) double As[2][GBK][HBM_ + 2];
+  __shared__ __align__(16) double Bs[2][GBK][HBN + 2];
+  const int tid = threadIdx.x, tx = tid & 15, ty = tid >> 4;
+  const bool a_rm = (P.acs == 1), b_rm = (P.bcs == 1);
+  double acc[8][8];
+#pragma unroll
+  for (int i = 0; i < 8; ++i)
+#pragma unroll
+    for (int j = 0; j < 8; ++j) acc[i][j] = 0.0;
+  double ra[4], rb[4];
+  auto load = [&](int k0) {
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {
+      const int e = tid + 256 * q;
+      int i, kk;
+      if (a_rm) { i = e >> 3; kk = e & 7; } else { i = e & 127; kk = e >> 7; }
+      const int gi = m0 + i, gk = k0 + kk;
+      ra[q] = (gi < P.m && gk < P.k) ? P.A[(long long)gi * P.ars + (long long)gk * P.acs] : 0.0;
+    }
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {
+      const int e = tid + 256 * q;
+      int j, kk;
+      if (b_rm) { kk = e >> 7; j = e & 127; } else { j = e >> 3; kk = e & 7; }
+      const int gj = n0 + j, gk = k0 + kk;
+      rb[q] = (gj < P.n && gk < P.k) ? P.B[(long long)gk * P.brs + (long long)gj * P.bcs] : 0.0;
+    }
+  };
+  auto store = [&](int buf) {
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {
+      const int e = tid + 256 * q;
+      int i, kk;
+      if (a_rm) { i = e >> 3; kk = e & 7; } else { i = e & 127; kk = e >> 7; }
+      As[buf][kk][i] = ra[q];
+    }
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {
+      const int e = tid + 256 * q;
+      int j, kk;
+      if (b_rm) { kk = e >> 7; j = e & 127; } else { j = e >> 3; kk = e & 7; }
+      Bs[buf][kk][j] = rb[q];
+    }
+  };
+  const int nk = (P.k + GBK - 1) / GBK;
+  load(0);
+  store(0);
+  __syncthreads();
+  for (int t = 0; t < nk; ++t) {
+    const int buf = t & 1;
+    if (t + 1 < nk) load((t + 1) * GBK);
+#pragma unroll
+    for (int kk = 0; kk < GBK; ++kk) {
+      const double2* ap = reinterpret_cast<const double2*>(&As[buf][kk][ty * 8]);
+      double a[8], b[8];
+#pragma unroll
+      for (int q = 0; q < 4; ++q) { const double2 v = ap[q]; a[2 * q] = v.x; a[2 * q + 1] = v.y; }
+#pragma unroll
+      for (int q = 0; q < 4; ++q) {  // columns 32q + 2tx, +1: 8 consecutive threads read 128 bytes
+        const double2 v = *reinterpret_cast<const double2*>(&Bs[buf][kk][32 * q + 2 * tx]);
+        b[2 * q] = v.x; b[2 * q + 1] = v.y;
+      }
+#pragma unroll
+      for (int i = 0; i < 8; ++i)
+#pragma unroll
+        for (int j = 0; j < 8; ++j) acc[i][j] = fma(a[i], b[j], acc[i][j]);
+    }
+    if (t + 1 < nk) store(buf ^ 1);
+    __syncthreads();
+  }
+#pragma unroll
+  for (int i = 0; i < 8; ++i) {
+    const int gi = m0 + ty * 8 + i;
+    if (gi >= P.m) continue;
+#pragma unroll
+    for (int j = 0; j < 8; ++j) {
+      const int gj = n0 + 32 * (j >> 1) + 2 * tx + (j & 1);
+      if (gj >= P.n) continue;
+      double* c = P.C + (long long)gi * P.crs + (long long)gj * P.ccs;
+      const double v = P.alpha * acc[i][j];
+      *c = (P.beta == 0.0) ? v : fma(P.beta, *c, v);
+    }
+  }
+}
+
 void bgemm(const std::vector<GemmProb>& probs_in, cudaStream_t s) {
   std::vector<GemmProb> probs;
   int maxm = 0, maxn = 0;
@@ -134,8 +229,13 @@ void bgemm(const std::vector<GemmProb>& probs_in, cudaStream_t s) {
     std::vector<GemmProb> chunk(probs.begin() + b0,
                                 probs.begin() + std::min(probs.size(), b0 + 65535));
     GemmProb* d = upload_probs(chunk, s);
-    dim3 grid(ceil_div(maxn, GBN), ceil_div(maxm, GBM), (unsigned)chunk.size());
-    bgemm_kernel<<<grid, 256, 0, s>>>(d);
+    if (maxm >= 256 && maxn >= 256 && !getenv("SVMHSS_GEMM_SMALL")) {  // big batched GEMMs (factor)
+      dim3 grid(ceil_div(maxn, HBN), ceil_div(maxm, HBM_), (unsigned)chunk.size());
+      bgemm_big_kernel<<<grid, 256, 0, s>>>(d);
+    } else {
+      dim3 grid(ceil_div(maxn, GBN), ceil_div(maxm, GBM), (unsigned)chunk.size());
+      bgemm_kernel<<<grid, 256, 0, s>>>(d);
+    }
     LAUNCH_CHECK();
     free_probs(d, s);
   }
