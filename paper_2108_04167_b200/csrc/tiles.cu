@@ -123,7 +123,8 @@ __global__ void __launch_bounds__(512, 1) kmm_kernel(KmmArgs a, int SA, unsigned
   double* wbuf = E_s + KBM * SE;             // 2 x BJ x SW
   double* fbuf = wbuf + 2 * BJ * SW;         // 2 x (BJ x SA + BJ)
   int* lbuf = (int*)(fbuf + 2 * (BJ * SA + BJ));  // 2 x BJ
-  __shared__ __align__(8) uint64_t full[2];
+  __shared__ __align__(8) uint64_t full[2];   // stage filled (TMA transaction count)
+  __shared__ __align__(8) uint64_t empty[2];  // stage released by all 16 warps
 
   const int tid = threadIdx.x, lane = tid & 31, w = tid >> 5, g = lane >> 2, t = lane & 3;
   const int mt = w & 7, hf = w >> 3;
@@ -138,6 +139,7 @@ __global__ void __launch_bounds__(512, 1) kmm_kernel(KmmArgs a, int SA, unsigned
   for (int e = tid; e < 2 * BJ; e += 512) lbuf[e] = -3;
   if (tid == 0) {
     mbar_init(&full[0], 1); mbar_init(&full[1], 1);
+    mbar_init(&empty[0], 16); mbar_init(&empty[1], 16);
     asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
   }
   asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");
@@ -196,15 +198,22 @@ __global__ void __launch_bounds__(512, 1) kmm_kernel(KmmArgs a, int SA, unsigned
     for (int64_t js = 0; js < nsteps; ++js, ++G) {
       const int b = (int)(G & 1);
       mbar_wait(&full[b], (unsigned)((G >> 1) & 1));
-      __syncthreads();  // every warp is past step G-1: the other stage and E_s are free
-      if (w == 0 && G + 1 < total) issue(G + 1);
+      if (w == 0 && G + 1 < total) {
+        // the other stage held step G-1: refill it once all 16 warps released it
+        if (G >= 1) mbar_wait(&empty[b ^ 1], (unsigned)(((G - 1) >> 1) & 1));
+        issue(G + 1);
+      }
       const double* W_s = wbuf + b * BJ * SW;
       const double* Fb_s = fbuf + b * (BJ * SA + BJ);
       const double* nub_s = Fb_s + BJ * SA;
       const int* lb = lbuf + b * BJ;
       const int64_t j0 = js * BJ;
       const int jvalid = (int)min((int64_t)BJ, a.nb - j0);
-      if (!active) continue;  // idle tile: keep the ring and the barriers in step
+      if (!active) {  // idle tile: keep the ring in step
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&empty[b]);
+        continue;
+      }
       // (1) distances: rows mt*8.., columns hf*BJ/2 + [0, BJ/2)
       double dacc[HQ][2];
 #pragma unroll
@@ -232,6 +241,8 @@ __global__ void __launch_bounds__(512, 1) kmm_kernel(KmmArgs a, int SA, unsigned
 #pragma unroll
         for (int q = 0; q < HQ; ++q) { dacc[q][0] += dacc2[q][0]; dacc[q][1] += dacc2[q][1]; }
       }
+      // the partner warp (same m-tile) has finished reading E_s of the previous step
+      asm volatile("bar.sync %0, 64;\n" ::"r"(1 + mt) : "memory");
 #pragma unroll
       for (int q = 0; q < HQ; ++q) {
         double ev[2];
@@ -257,6 +268,8 @@ __global__ void __launch_bounds__(512, 1) kmm_kernel(KmmArgs a, int SA, unsigned
 #pragma unroll
         for (int ni = 0; ni < NT; ++ni) dmma884(acc[ni][0], acc[ni][1], av, W_w[kk * 4 * SW + ni * 8]);
       }
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&empty[b]);  // this warp is done with stage b
     }
     // epilogue
     if (row_ok) {
