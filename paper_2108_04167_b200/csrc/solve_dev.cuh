@@ -2,7 +2,7 @@
 // (ulv.cu) and the fused bottom-level ADMM kernel (admm.cu), so both produce bitwise-identical
 // values.  Forward sweep t = M_t b (rows i < k -> the parent's input "up", rows >= k -> y_r);
 // backward sweep x = M_t^T [x_s; y_r], both streaming the same stored M_t (no transposed copy):
-//  - fwd_rows: one warp per row (two rows in flight), lane-strided partial sums + butterfly;
+//  - fwd_rows: one warp per row (2-4 rows in flight), lane-strided partial sums + butterfly;
 //  - bwd_cols: a CTA of kBW warps owns kCW consecutive columns (lane l -> columns j0 + l and
 //    j0 + 32 + l: fully coalesced row segments); warp w accumulates rows w, w + kBW, ... in
 //    order; the kBW warp partials are summed in warp order.
@@ -64,8 +64,19 @@ __device__ __forceinline__ void row_store(double (&acc)[NR], int i, int k, int64
 template <int NR>
 __device__ __forceinline__ void fwd_rows(const double* __restrict__ M, int R, const double* __restrict__ vsh,
                                          int i0, int i1, int wid, int nw, int k, int64_t koff, int64_t yoff,
-                                         double* __restrict__ out_up, double* __restrict__ out_yr) {
+                                         double* __restrict__ out_up, double* __restrict__ out_yr,
+                                         bool four = false) {
   int i = i0 + wid;
+  if (NR <= 2 && four) {  // four rows in flight (16 independent loads per lane)
+    for (; i + 3 * nw < i1; i += 4 * nw) {
+      const double* Mr[4] = {M + (int64_t)i * R, M + (int64_t)(i + nw) * R, M + (int64_t)(i + 2 * nw) * R,
+                             M + (int64_t)(i + 3 * nw) * R};
+      double acc[4][NR];
+      row_partials<NR, 4>(Mr, R, vsh, acc);
+#pragma unroll
+      for (int u = 0; u < 4; ++u) row_store<NR>(acc[u], i + u * nw, k, koff, yoff, out_up, out_yr);
+    }
+  }
   for (; i + nw < i1; i += 2 * nw) {
     const double* Mr[2] = {M + (int64_t)i * R, M + (int64_t)(i + nw) * R};
     double acc[2][NR];

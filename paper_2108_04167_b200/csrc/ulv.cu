@@ -451,7 +451,8 @@ void ulv_factor_impl(ULVImpl& F, cudaStream_t s) {
 template <int NR>
 __device__ __forceinline__ void fwd_item(const SolveNode* __restrict__ nodes, SolveWork wk, int ch,
                                          const double* __restrict__ M, const double* __restrict__ in,
-                                         double* __restrict__ out_up, double* __restrict__ out_yr, double* vsh) {
+                                         double* __restrict__ out_up, double* __restrict__ out_yr, double* vsh,
+                                         bool four = false) {
   const SolveNode N = nodes[wk.node];
   const int R = N.R, tid = threadIdx.x;
   const int i0 = wk.chunk * ch, i1 = min(R, i0 + ch);
@@ -460,7 +461,7 @@ __device__ __forceinline__ void fwd_item(const SolveNode* __restrict__ nodes, So
   } else {
     for (int e = tid; e < R * NR; e += 256) vsh[e] = in[N.roff * NR + e];
     __syncthreads();
-    fwd_rows<NR>(M + N.moff, R, vsh, i0, i1, tid >> 5, 8, N.k, N.koff, N.yoff, out_up, out_yr);
+    fwd_rows<NR>(M + N.moff, R, vsh, i0, i1, tid >> 5, 8, N.k, N.koff, N.yoff, out_up, out_yr, four);
   }
   __syncthreads();
 }
@@ -471,9 +472,9 @@ __global__ void __launch_bounds__(256) ulv_fwd_kernel(const SolveNode* __restric
                                                       const double* __restrict__ M,
                                                       const double* __restrict__ in,
                                                       double* __restrict__ out_up,
-                                                      double* __restrict__ out_yr) {
+                                                      double* __restrict__ out_yr, int four) {
   extern __shared__ double vsh[];  // R * NR
-  fwd_item<NR>(nodes, work[blockIdx.x], ch, M, in, out_up, out_yr, vsh);
+  fwd_item<NR>(nodes, work[blockIdx.x], ch, M, in, out_up, out_yr, vsh, four != 0);
 }
 
 template <int NR>
@@ -731,8 +732,10 @@ static void fwd_level(const ULVImpl& F, SolveWS& ws, int l, const SolveWork* wor
   const auto& lv = F.lv[l];
   if (nwork <= 0) return;
   const size_t sm = (size_t)lv.maxR * NR * sizeof(double);
+  // four rows in flight per warp (A/B on one box: 673 vs 657 it/s); SVMHSS_FWD_ROWS=2 for two
+  static const int four = [] { const char* e = getenv("SVMHSS_FWD_ROWS"); return (e && e[0] == '2') ? 0 : 1; }();
   ulv_fwd_kernel<NR><<<nwork, 256, sm, s>>>(lv.nodes.p, work, lv.ch, lv.M.p, ws.fin[l], l > 0 ? ws.fin[l - 1] : nullptr,
-                                            ws.yr[l]);
+                                            ws.yr[l], four);
   g_launches.fetch_add(1);
 }
 
