@@ -344,7 +344,7 @@ def main():
     value = max_it * len(Cs) / (loop_ms / 1e3)  # iterations of the whole (sharded) problem
     peaks, peak_src = _peaks()
     rp = (cfg["r"] + 3) // 4 * 4
-    sk_flops = 2.0 * n * n * (rp + cfg["s"])
+    sk_flops = 2.0 * n * n * (rp + cfg["s"]) / world  # this rank's rows of the sketch (n / world)
     fp64_derived = peaks["bf16_tflops_sustained"] * FP64_NOMINAL_TF / BF16_NOMINAL_TF
     fp64_peak = max(dgemm_tf, fp64_derived)
     ach_tf = sk_flops / (sketch_ms / 1e3) / 1e12
@@ -378,7 +378,7 @@ def main():
                                          "profiles/traffic.json)",
                          "peak_source": "max(cuBLAS fp64 DGEMM 8192^3 measured in this run = %.2f, %s bf16_tflops_sustained x FP64/BF16 nominal %g/%g = %.2f)" % (
                              dgemm_tf, peak_src, FP64_NOMINAL_TF, BF16_NOMINAL_TF, fp64_derived),
-                         "work": "2 n^2 (r_pad + s) flops per launch"},
+                         "work": "2 (n / n_gpus) n (r_pad + s) flops per launch (this rank's rows)"},
             "roofline_solve": {"bound": "hbm", "kernel": "ulv_fwd_kernel + ulv_bwd_kernel (+ epilogue)",
                                "achieved": ach_gbs, "peak": peaks["hbm_gbs"], "unit": "GB/s",
                                "frac": ach_gbs / peaks["hbm_gbs"],
