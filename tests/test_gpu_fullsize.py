@@ -1,5 +1,5 @@
-"""Full-size (BASELINE.json config 3, n = 524,288 / 131,072 test points) checks of the CUDA path in
-the configuration bench.py times, on outputs the oracle can compute one by one or on properties
+"""Full-size (BASELINE.json config 3, n = 524,288 / 131,072 test points, with the sketch and with
+HSS-ANN sampling; config 2, n = 131,072) checks of the CUDA path in the configuration bench.py times, on outputs the oracle can compute one by one or on properties
 that hold at any size (the oracle's full HSS at this n takes hours on the host):
 
   - tree: the permutation equals the oracle's PCA bisection (T1-T4) bit for bit;
@@ -19,7 +19,6 @@ from oracle import svm as o_svm
 from oracle import tree as o_tree
 
 pytestmark = pytest.mark.gpu
-CFG = 3
 
 
 def _t(a):
@@ -27,14 +26,20 @@ def _t(a):
     return torch.from_numpy(np.ascontiguousarray(a)).to("cuda")
 
 
-@pytest.fixture(scope="module")
-def full(gpu_lib):
+# (config, sampling): config 3 with both compressions, config 2 (n = 131072, r = 123 binary)
+@pytest.fixture(scope="module", params=[(3, "sketch"), (3, "ann"), (2, "sketch")],
+                ids=["cfg3-sketch", "cfg3-ann", "cfg2-sketch"])
+def full(gpu_lib, request):
     P = gpu_lib
-    cfg = datagen.get_config(CFG)
-    F, y, Ft, yt = datagen.generate(CFG, n=cfg["n"], n_test=cfg["n_test"])
+    c, sampling = request.param
+    cfg = datagen.get_config(c)
+    if sampling == "ann":
+        cfg["beta"] = cfg["beta_ann"]
+    F, y, Ft, yt = datagen.generate(c, n=cfg["n"], n_test=cfg["n_test"])
     H = P.hss_build(_t(F), cfg["h"], leaf_size=cfg["leaf"], rel_tol=cfg["rel_tol"], abs_tol=cfg["abs_tol"],
                     max_rank=cfg["cap"], oversample=cfg["s"] - cfg["cap"], omega_seed=cfg["seed_omega"],
-                    tree_seed=cfg["seed_tree"])
+                    tree_seed=cfg["seed_tree"], sampling=sampling, ann_neighbors=cfg["ann_neighbors"],
+                    ann_trees=cfg["ann_trees"], ann_leaf=cfg["ann_leaf"], ann_seed=cfg["ann_seed"])
     U = P.hss_ulv_factor(H, cfg["beta"])
     yield dict(P=P, cfg=cfg, F=F, y=y, Ft=Ft, H=H, U=U)
     U.free()
