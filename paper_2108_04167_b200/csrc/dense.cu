@@ -10,9 +10,11 @@
 //  bcpqr   : column-pivoted Householder QR of Y^T with the AMB-10 rank rule (H3): exact
 //            trailing column norms recomputed in the update pass; argmax ties -> lowest index.
 #include <cstdlib>
+#include <cooperative_groups.h>
 #include "dense.cuh"
 
 namespace svmhss {
+namespace cg = cooperative_groups;
 
 template <typename P>
 static P* upload_probs(const std::vector<P>& v, cudaStream_t s) {
@@ -741,12 +743,264 @@ __global__ void __launch_bounds__(CP_THREADS) bcpqr_kernel(const CpqrProb* __res
   if (tid == 0) { *P.k_out = k; if (P.cap_hit) *P.cap_hit = hit; }
 }
 
+// Column-pivoted QR of one node on an 8-CTA cluster: position c (a column of W^T, i.e. a row of
+// W) lives in the shared memory of CTA c % 8, so the whole node stays on chip (distributed
+// shared memory) for all its pivot steps instead of streaming through L2 once per step.  Per
+// step: local argmax -> candidates to CTA 0 (DSMEM) -> cluster barrier -> every CTA picks the
+// same winner (max norm, lowest index) -> swap through DSMEM -> the owner of position j forms
+// the Householder vector (block_sum over its 512 threads, as bcpqr_kernel) and writes it into
+// every CTA -> cluster barrier -> each CTA updates its own columns (warp per column, the same
+// lane partition as bcpqr_kernel).  Bitwise the same pivots, ranks and R as bcpqr_kernel.
+constexpr int CPQ_CL = 8;
+
+template <int MAXPL>
+__global__ void __launch_bounds__(CP_THREADS) bcpqr_cluster_kernel(const CpqrProb* __restrict__ probs,
+                                                                   double rel_tol, double abs_tol, int cap,
+                                                                   int slots_max) {
+  cg::cluster_group cl = cg::this_cluster();
+  const int q = (int)cl.block_rank();
+  const CpqrProb P = probs[blockIdx.x / CPQ_CL];
+  const int rows = P.rows, s = P.s;
+  const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5, nw = CP_THREADS / 32;
+  extern __shared__ double sm[];
+  double* cols = sm;                                   // slots_max x s: position q + CPQ_CL*m at slot m
+  double* v = cols + (size_t)slots_max * s;            // s: Householder vector of the current step
+  double* tmp = v + s;                                 // s: swap staging
+  double* norm2 = tmp + s;                             // slots_max
+  int* piv = (int*)(norm2 + slots_max);                // slots_max
+  __shared__ double red[32];
+  __shared__ double rv[32];
+  __shared__ int ri[32];
+  __shared__ double cand_v[CPQ_CL];                    // used in CTA 0
+  __shared__ int cand_i[CPQ_CL];
+  __shared__ double sc[4];                             // tau, rjj, stop, tmp norm (written by the owner)
+  __shared__ double tmpn;
+  __shared__ int tmpp;
+  const int nslot = (rows - q + CPQ_CL - 1) / CPQ_CL;  // positions q, q+8, ... < rows
+  double* W = P.W;
+  for (int e = tid; e < nslot * s; e += CP_THREADS) {
+    const int m = e / s, i = e % s;
+    cols[(size_t)m * s + i] = W[(long long)(q + CPQ_CL * m) * s + i];
+  }
+  for (int m = tid; m < nslot; m += CP_THREADS) piv[m] = q + CPQ_CL * m;
+  __syncthreads();
+  for (int m = wid; m < nslot; m += nw) {
+    double a = 0.0;
+    for (int i = lane; i < s; i += 32) { const double x = cols[(size_t)m * s + i]; a = fma(x, x, a); }
+    a = warp_sum(a);
+    if (lane == 0) norm2[m] = a;
+  }
+  __syncthreads();
+  const bool adaptive = P.kfixed < 0;
+  const int kmax = adaptive ? min(min(cap, rows), s) : min(min(P.kfixed, rows), s);
+  double thr = 0.0;
+  int k = 0;
+  double* cand_v0 = cl.map_shared_rank(cand_v, 0);
+  int* cand_i0 = cl.map_shared_rank(cand_i, 0);
+  for (int j = 0; j < kmax; ++j) {
+    // (1) argmax over this CTA's positions >= j
+    double bv = -1.0;
+    int bi = 0x7fffffff;
+    for (int m = tid; m < nslot; m += CP_THREADS) {
+      const int c = q + CPQ_CL * m;
+      if (c >= j && norm2[m] > bv) { bv = norm2[m]; bi = c; }   // increasing c per thread
+    }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+      const double ov = __shfl_xor_sync(0xffffffffu, bv, o);
+      const int oi = __shfl_xor_sync(0xffffffffu, bi, o);
+      if (ov > bv || (ov == bv && oi < bi)) { bv = ov; bi = oi; }
+    }
+    if (lane == 0) { rv[wid] = bv; ri[wid] = bi; }
+    __syncthreads();
+    if (tid == 0) {
+      double b = rv[0];
+      int ix = ri[0];
+      for (int w = 1; w < nw; ++w)
+        if (rv[w] > b || (rv[w] == b && ri[w] < ix)) { b = rv[w]; ix = ri[w]; }
+      cand_v0[q] = b;
+      cand_i0[q] = ix;
+    }
+    cl.sync();
+    // (2) the winner, computed identically by every CTA
+    double b = cand_v0[0];
+    int p = cand_i0[0];
+    for (int r = 1; r < CPQ_CL; ++r) {
+      const double vb = cand_v0[r];
+      const int ib = cand_i0[r];
+      if (vb > b || (vb == b && ib < p)) { b = vb; p = ib; }
+    }
+    const int oj = j % CPQ_CL, op = p % CPQ_CL, mj = j / CPQ_CL, mp = p / CPQ_CL;
+    // (3) swap positions j and p (column data, norm, original index)
+    if (p != j && oj == op) {  // both positions in one CTA: local swap
+      if (q == oj) {
+        double* a = cols + (size_t)mj * s;
+        double* c2 = cols + (size_t)mp * s;
+        for (int i = tid; i < s; i += CP_THREADS) { const double t = a[i]; a[i] = c2[i]; c2[i] = t; }
+        if (tid == 0) {
+          const double t = norm2[mj]; norm2[mj] = norm2[mp]; norm2[mp] = t;
+          const int pp = piv[mj]; piv[mj] = piv[mp]; piv[mp] = pp;
+        }
+        __syncthreads();
+      }
+    } else if (p != j) {
+      if (q == oj) {  // fetch column p
+        const double* src = cl.map_shared_rank(cols, op) + (size_t)mp * s;
+        for (int i = tid; i < s; i += CP_THREADS) tmp[i] = src[i];
+        if (tid == 0) { tmpn = cl.map_shared_rank(norm2, op)[mp]; tmpp = cl.map_shared_rank(piv, op)[mp]; }
+      } else if (q == op) {  // fetch column j
+        const double* src = cl.map_shared_rank(cols, oj) + (size_t)mj * s;
+        for (int i = tid; i < s; i += CP_THREADS) tmp[i] = src[i];
+        if (tid == 0) { tmpn = cl.map_shared_rank(norm2, oj)[mj]; tmpp = cl.map_shared_rank(piv, oj)[mj]; }
+      }
+      cl.sync();
+      if (q == oj || q == op) {
+        const int m = (q == oj) ? mj : mp;
+        for (int i = tid; i < s; i += CP_THREADS) cols[(size_t)m * s + i] = tmp[i];
+        if (tid == 0) { norm2[m] = tmpn; piv[m] = tmpp; }
+      }
+      __syncthreads();
+    }
+    // (4) Householder of position j (owner), broadcast to every CTA
+    if (q == oj) {
+      double* cj = cols + (size_t)mj * s;
+      double part = 0.0;
+      for (int i = j + 1 + tid; i < s; i += CP_THREADS) { const double x = cj[i]; part = fma(x, x, part); }
+      const double xs = block_sum(part, red);
+      const double alpha = cj[j];
+      const double rjj = sqrt(alpha * alpha + xs);
+      double stop = 0.0;
+      if (adaptive) {
+        if (j == 0) thr = fmax(rel_tol * rjj, abs_tol * sqrt((double)s));
+        if (!(rjj > thr)) stop = 1.0;
+      }
+      double tau = 0.0, scal = 0.0, beta = alpha;
+      if (stop == 0.0 && xs != 0.0) {
+        beta = -copysign(rjj, alpha);
+        tau = (beta - alpha) / beta;
+        scal = 1.0 / (alpha - beta);
+      }
+      if (stop == 0.0) {
+        for (int i = j + 1 + tid; i < s; i += CP_THREADS) {
+          const double x = (tau == 0.0) ? cj[i] : cj[i] * scal;
+          cj[i] = x;
+        }
+        __syncthreads();
+        if (tid == 0) cj[j] = beta;
+      }
+      __syncthreads();
+      for (int r = 0; r < CPQ_CL; ++r) {
+        double* vr = cl.map_shared_rank(v, r);
+        for (int i = j + tid; i < s; i += CP_THREADS) vr[i] = (i == j) ? 1.0 : cj[i];
+        if (tid == 0) {
+          double* sr = cl.map_shared_rank(sc, r);
+          sr[0] = tau; sr[1] = thr; sr[2] = stop;
+        }
+      }
+    }
+    cl.sync();
+    if (sc[2] != 0.0) break;  // tolerance met (every CTA sees the same flag)
+    thr = sc[1];
+    const double tau = sc[0];
+    // (5) update this CTA's positions c > j (warp per column) + exact trailing norms
+    for (int m = wid; m < nslot; m += nw) {
+      const int c = q + CPQ_CL * m;
+      if (c <= j) continue;
+      double x[MAXPL];
+      double* col = cols + (size_t)m * s;
+      double dot = 0.0;
+#pragma unroll
+      for (int qq = 0; qq < MAXPL; ++qq) {
+        const int i = j + lane + 32 * qq;
+        x[qq] = (i < s) ? col[i] : 0.0;
+        if (i < s) dot = fma(v[i], x[qq], dot);
+      }
+      dot = warp_sum(dot) * tau;
+      double nn = 0.0;
+#pragma unroll
+      for (int qq = 0; qq < MAXPL; ++qq) {
+        const int i = j + lane + 32 * qq;
+        if (i < s) {
+          const double yv = fma(-dot, v[i], x[qq]);
+          col[i] = yv;
+          if (i > j) nn = fma(yv, yv, nn);
+        }
+      }
+      nn = warp_sum(nn);
+      if (lane == 0) norm2[m] = nn;
+    }
+    __syncthreads();
+    k = j + 1;
+  }
+  // cap hit: tolerance unmet at the cap iff the next pivot's |R_kk| exceeds the threshold
+  int hit = 0;
+  if (adaptive && k == kmax && k == cap && k < rows && k < s) {
+    double bv = 0.0;
+    for (int m = tid; m < nslot; m += CP_THREADS)
+      if (q + CPQ_CL * m >= k) bv = fmax(bv, norm2[m]);
+    for (int o = 16; o > 0; o >>= 1) bv = fmax(bv, __shfl_xor_sync(0xffffffffu, bv, o));
+    if (lane == 0) red[wid] = bv;
+    __syncthreads();
+    if (tid == 0) {
+      double b = 0.0;
+      for (int w = 0; w < nw; ++w) b = fmax(b, red[w]);
+      cand_v0[q] = b;
+    }
+    cl.sync();
+    double b = 0.0;
+    for (int r = 0; r < CPQ_CL; ++r) b = fmax(b, cand_v0[r]);
+    hit = (sqrt(b) > thr) ? 1 : 0;
+  }
+  // write back this CTA's columns and pivots
+  for (int e = tid; e < nslot * s; e += CP_THREADS) {
+    const int m = e / s, i = e % s;
+    W[(long long)(q + CPQ_CL * m) * s + i] = cols[(size_t)m * s + i];
+  }
+  for (int m = tid; m < nslot; m += CP_THREADS) P.piv[q + CPQ_CL * m] = piv[m];
+  if (q == 0 && tid == 0) { *P.k_out = k; if (P.cap_hit) *P.cap_hit = hit; }
+  cl.sync();  // no CTA exits while others may still read its shared memory
+}
+
 void bcpqr(const std::vector<CpqrProb>& probs, double rel_tol, double abs_tol, int cap,
            cudaStream_t s) {
   if (probs.empty()) return;
   int maxr = 0, maxs = 0;
   for (auto& p : probs) { maxr = std::max(maxr, p.rows); maxs = std::max(maxs, p.s); }
   CpqrProb* d = upload_probs(probs, s);
+  // cluster version when a node's columns fit the 8 CTAs' shared memory
+  const int slots = (maxr + CPQ_CL - 1) / CPQ_CL;
+  const size_t csm = ((size_t)slots * maxs + 2 * (size_t)maxs + slots) * sizeof(double) + (size_t)slots * sizeof(int) + 16;
+  // default: levels with few nodes (one CTA per node would leave most SMs idle); env 0 = never,
+  // 1 = every level that fits
+  const char* env = getenv("SVMHSS_CPQR_CLUSTER");
+  const int mode = env ? atoi(env) : 2;
+  const bool use = csm <= 200 * 1024 && (mode == 1 || (mode == 2 && probs.size() * CPQ_CL <= 2 * 148));
+  if (use) {
+    auto launchc = [&](auto kern) {
+      CUDA_CHECK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)csm));
+      cudaLaunchConfig_t cfg = {};
+      cfg.gridDim = dim3((unsigned)(probs.size() * CPQ_CL));
+      cfg.blockDim = dim3(CP_THREADS);
+      cfg.dynamicSmemBytes = csm;
+      cfg.stream = s;
+      cudaLaunchAttribute at[1];
+      at[0].id = cudaLaunchAttributeClusterDimension;
+      at[0].val.clusterDim.x = CPQ_CL;
+      at[0].val.clusterDim.y = 1;
+      at[0].val.clusterDim.z = 1;
+      cfg.attrs = at;
+      cfg.numAttrs = 1;
+      CUDA_CHECK(cudaLaunchKernelEx(&cfg, kern, (const CpqrProb*)d, rel_tol, abs_tol, cap, slots));
+    };
+    if (maxs <= 96) launchc(bcpqr_cluster_kernel<3>);
+    else if (maxs <= 160) launchc(bcpqr_cluster_kernel<5>);
+    else if (maxs <= 288) launchc(bcpqr_cluster_kernel<9>);
+    else if (maxs <= 576) launchc(bcpqr_cluster_kernel<18>);
+    else launchc(bcpqr_cluster_kernel<36>);
+    LAUNCH_CHECK();
+    free_probs(d, s);
+    return;
+  }
   size_t smem = (size_t)maxr * (sizeof(double) + sizeof(int)) + (size_t)maxs * sizeof(double) + 16;
   auto launch = [&](auto kern) {
     if (smem > 48 * 1024)
