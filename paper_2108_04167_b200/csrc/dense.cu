@@ -217,6 +217,130 @@ __global__ void __launch_bounds__(256, 1) bgemm_big_kernel(const GemmProb* __res
   }
 }
 
+// FP64 tensor-core (DMMA m8n8k4) batched GEMM.  8 warps as 2 (m) x 4 (n); warp tile
+// (8 MT) x (8 NT), CTA tile (16 MT) x (32 NT), k in 16-wide shared-memory tiles, register
+// prefetch of the next tile (double buffered).  Operands are stored [row][k] (A) and [col][k]
+// (B) with row stride 20 = 4 (mod 16) doubles, so every fragment load (row g, k t) is bank-
+// conflict free.  Every tile shape runs the same per-element sequence of DMMAs (k = 0, 4, 8,
+// ... in order, zero padded), so a node's result does not depend on which shape its batch
+// used (bitwise P-invariance of the sharded build).
+constexpr int DBK = 16, DSK = 20;
+
+__device__ __forceinline__ void dmma884_(double& d0, double& d1, double a, double b) {
+  asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};\n"
+               : "+d"(d0), "+d"(d1) : "d"(a), "d"(b));
+}
+
+__device__ __forceinline__ void cp_async8_(double* smem, const double* gmem, bool pred) {
+  const unsigned sa = (unsigned)__cvta_generic_to_shared(smem);
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 8, %2;\n" ::"r"(sa), "l"(gmem), "r"(pred ? 8 : 0));
+}
+
+template <int MT, int NT>
+__global__ void __launch_bounds__(256) bgemm_dmma_kernel(const GemmProb* __restrict__ probs) {
+  constexpr int BM = 16 * MT, BN = 32 * NT;
+  constexpr int LA = BM * DBK / 256, LB = BN * DBK / 256;  // elements per thread per tile
+  const GemmProb P = probs[blockIdx.z];
+  const int m0 = blockIdx.y * BM, n0 = blockIdx.x * BN;
+  if (m0 >= P.m || n0 >= P.n) return;
+  extern __shared__ __align__(16) double dsm[];
+  double* As = dsm;                       // 2 x BM x DSK
+  double* Bs = dsm + 2 * BM * DSK;        // 2 x BN x DSK
+  const int tid = threadIdx.x, lane = tid & 31, w = tid >> 5, g = lane >> 2, t = lane & 3;
+  const int wm = (w >> 2) * (8 * MT), wn = (w & 3) * (8 * NT);
+  const bool a_k = (P.acs == 1), b_n = (P.bcs == 1);
+  double acc[MT][NT][2];
+#pragma unroll
+  for (int i = 0; i < MT; ++i)
+#pragma unroll
+    for (int j = 0; j < NT; ++j) acc[i][j][0] = acc[i][j][1] = 0.0;
+  // per-thread element (i0 + q di, k0 + kq0 + q dk) of the A tile, (j0 + q dj, k0 + kb0 + q dkb) of B:
+  // consecutive threads walk the operand's unit-stride dimension (coalesced loads); the tiles
+  // go global -> shared by 8-byte cp.async (zero fill outside the matrix), two stages
+  int ai0, ak0, adi, adk, bj0, bk0, bdj, bdk;
+  if (a_k) { ai0 = tid / DBK; ak0 = tid % DBK; adi = 256 / DBK; adk = 0; }
+  else { ai0 = tid % BM; ak0 = tid / BM; adi = 0; adk = 256 / BM; }
+  if (b_n) { bj0 = tid % BN; bk0 = tid / BN; bdj = 0; bdk = 256 / BN; }
+  else { bj0 = tid / DBK; bk0 = tid % DBK; bdj = 256 / DBK; bdk = 0; }
+  const long long astep = (long long)adi * P.ars + (long long)adk * P.acs;
+  const long long bstep = (long long)bdk * P.brs + (long long)bdj * P.bcs;
+  const double* Ab = P.A + (long long)(m0 + ai0) * P.ars + (long long)ak0 * P.acs;
+  const double* Bb = P.B + (long long)bk0 * P.brs + (long long)(n0 + bj0) * P.bcs;
+  auto issue = [&](int kt, int buf) {
+    const int k0 = kt * DBK;
+    const double* pa = Ab + (long long)k0 * P.acs;
+    double* sa = As + (buf * BM + ai0) * DSK + ak0;
+#pragma unroll
+    for (int q = 0; q < LA; ++q) {
+      const bool ok = (m0 + ai0 + q * adi < P.m) && (k0 + ak0 + q * adk < P.k);
+      cp_async8_(sa + q * (adi * DSK + adk), ok ? pa + q * astep : P.A, ok);
+    }
+    const double* pb = Bb + (long long)k0 * P.brs;
+    double* sb = Bs + (buf * BN + bj0) * DSK + bk0;
+#pragma unroll
+    for (int q = 0; q < LB; ++q) {
+      const bool ok = (n0 + bj0 + q * bdj < P.n) && (k0 + bk0 + q * bdk < P.k);
+      cp_async8_(sb + q * (bdj * DSK + bdk), ok ? pb + q * bstep : P.B, ok);
+    }
+    asm volatile("cp.async.commit_group;\n" ::);
+  };
+  const int nk = (P.k + DBK - 1) / DBK;
+  issue(0, 0);
+  for (int kt = 0; kt < nk; ++kt) {
+    const int buf = kt & 1;
+    if (kt + 1 < nk) {
+      issue(kt + 1, buf ^ 1);
+      asm volatile("cp.async.wait_group 1;\n" ::);
+    } else {
+      asm volatile("cp.async.wait_group 0;\n" ::);
+    }
+    __syncthreads();
+    const double* Aw = As + (buf * BM + wm + g) * DSK + t;
+    const double* Bw = Bs + (buf * BN + wn + g) * DSK + t;
+#pragma unroll
+    for (int ks = 0; ks < DBK / 4; ++ks) {
+      double a[MT], b[NT];
+#pragma unroll
+      for (int i = 0; i < MT; ++i) a[i] = Aw[i * 8 * DSK + ks * 4];
+#pragma unroll
+      for (int j = 0; j < NT; ++j) b[j] = Bw[j * 8 * DSK + ks * 4];
+#pragma unroll
+      for (int i = 0; i < MT; ++i)
+#pragma unroll
+        for (int j = 0; j < NT; ++j) dmma884_(acc[i][j][0], acc[i][j][1], a[i], b[j]);
+    }
+    __syncthreads();
+  }
+#pragma unroll
+  for (int i = 0; i < MT; ++i) {
+    const int gi = m0 + wm + i * 8 + g;
+    if (gi >= P.m) continue;
+#pragma unroll
+    for (int j = 0; j < NT; ++j)
+#pragma unroll
+      for (int e = 0; e < 2; ++e) {
+        const int gj = n0 + wn + j * 8 + 2 * t + e;
+        if (gj >= P.n) continue;
+        double* c = P.C + (long long)gi * P.crs + (long long)gj * P.ccs;
+        const double v = P.alpha * acc[i][j][e];
+        *c = (P.beta == 0.0) ? v : fma(P.beta, *c, v);
+      }
+  }
+}
+
+template <int MT, int NT>
+static void launch_dmma(const GemmProb* d, int maxm, int maxn, unsigned nb, cudaStream_t s) {
+  constexpr int BM = 16 * MT, BN = 32 * NT;
+  const size_t smem = (size_t)2 * (BM + BN) * DSK * sizeof(double);
+  static bool attr = false;
+  if (!attr) {
+    CUDA_CHECK(cudaFuncSetAttribute(bgemm_dmma_kernel<MT, NT>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    attr = true;
+  }
+  dim3 grid(ceil_div(maxn, BN), ceil_div(maxm, BM), nb);
+  bgemm_dmma_kernel<MT, NT><<<grid, 256, smem, s>>>(d);
+}
+
 void bgemm(const std::vector<GemmProb>& probs_in, cudaStream_t s) {
   std::vector<GemmProb> probs;
   int maxm = 0, maxn = 0;
@@ -231,7 +355,12 @@ void bgemm(const std::vector<GemmProb>& probs_in, cudaStream_t s) {
     std::vector<GemmProb> chunk(probs.begin() + b0,
                                 probs.begin() + std::min(probs.size(), b0 + 65535));
     GemmProb* d = upload_probs(chunk, s);
-    if (maxm >= 256 && maxn >= 256 && !getenv("SVMHSS_GEMM_SMALL")) {  // big batched GEMMs (factor)
+    static const int dfma = [] { const char* e = getenv("SVMHSS_GEMM_DFMA"); return (e && e[0] == '1') ? 1 : 0; }();
+    if (!dfma) {
+      // FP64 tensor cores: 128 x 128 CTA tiles for the big factor GEMMs, 64 x 64 otherwise
+      if (maxm >= 256 && maxn >= 256) launch_dmma<8, 4>(d, maxm, maxn, (unsigned)chunk.size(), s);
+      else launch_dmma<4, 2>(d, maxm, maxn, (unsigned)chunk.size(), s);
+    } else if (maxm >= 256 && maxn >= 256 && !getenv("SVMHSS_GEMM_SMALL")) {  // big batched GEMMs (factor)
       dim3 grid(ceil_div(maxn, HBN), ceil_div(maxm, HBM_), (unsigned)chunk.size());
       bgemm_big_kernel<<<grid, 256, 0, s>>>(d);
     } else {

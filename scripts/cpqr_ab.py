@@ -1,4 +1,4 @@
-"""A/B of the column-pivoted QR variants on config 3 (n = 524288): builds the HSS with the
+"""A/B of build/factor variants (env knobs) on config 3 (n = 524288): builds the HSS with the
 SVMHSS_CPQR_CLUSTER mode given on the command line, prints the build time and a digest of the
 compressed generators (must match across modes bit for bit).
     SVMHSS_TRACE=1 python scripts/cpqr_ab.py MODE [sketch|ann]"""
@@ -37,4 +37,12 @@ b = torch.from_numpy(np.random.default_rng(3).standard_normal((cfg["n"], 1))).cu
 mv = H.matvec(b).cpu().numpy()
 dig = hashlib.sha1(mv.tobytes() + info["ranks"].tobytes() + info["skeletons"].tobytes()).hexdigest()[:16]
 st = {k: info[k] for k in ("kmax", "s_used") if k in info}
-print(f"mode={sys.argv[1]} sampling={sampling} build_s={dt:.3f} digest={dig} {st}")
+beta = cfg["beta_ann"] if sampling == "ann" else cfg["beta"]
+torch.cuda.synchronize()
+t = time.perf_counter()
+U = P.hss_ulv_factor(H, beta)
+torch.cuda.synchronize()
+ft = time.perf_counter() - t
+x = U.solve(b).cpu().numpy()
+fd = hashlib.sha1(x.tobytes()).hexdigest()[:16]
+print(f"mode={sys.argv[1]} sampling={sampling} build_s={dt:.3f} digest={dig} {st} factor_s={ft:.3f} solve_digest={fd}")
