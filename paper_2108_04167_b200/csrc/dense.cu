@@ -662,11 +662,234 @@ __global__ void __launch_bounds__(QT) bgeqrf_kernel(const QrProb* __restrict__ p
 #undef QA
 }
 
+// Householder QR with tensor-core trailing updates, one CTA (16 warps) per node, m <= 16 * 32.
+// Panels of NB = 16 columns: warp w keeps panel column w in registers (rows lane + 32 q);
+// step j: warp j forms its reflector (dlarfg convention) and publishes v_j to shared memory,
+// one CTA barrier, warps c > j apply H_j to their own column -- one barrier per column.  Then
+// T (compact WY, NB x NB) from G = V^T V, and the trailing columns, in blocks of QCB = 16
+// staged in shared memory, get A -= V (T^T (V^T A)) on DMMA: W = V^T A as 2 x 2 output tiles
+// with the row range split in 4 quarters (16 warps), the quarters summed in a fixed order;
+// the update D = A + V (-T^T W) as (m/8) x 2 tiles.  Arithmetic order depends on m and n only.
+constexpr int QNB = 16, QCB = 16, QRPL = 16, QMAX = 32 * QRPL;
+constexpr int QSP = 520;   // panel column stride (= 8 mod 32: conflict-free A-fragments of V W2)
+constexpr int QSB = 24;    // trailing block row stride (= 24 mod 32: conflict-free B-fragments)
+
+__global__ void __launch_bounds__(512, 1) bgeqrf_tc_kernel(const QrProb* __restrict__ probs) {
+  const QrProb P = probs[blockIdx.x];
+  const int m = P.m, n = P.n, tid = threadIdx.x, lane = tid & 31, w = tid >> 5, g = lane >> 2, t = lane & 3;
+  extern __shared__ __align__(16) double qsm[];
+  double* pv = qsm;                         // QNB x QSP: v_j (unit diagonal, zeros above), local rows
+  double* ab = pv + QNB * QSP;              // QMAX x QSB: trailing column block
+  double* wp = ab + QMAX * QSB;             // 4 x QNB x QCB: W partials (row quarters)
+  double* w2 = wp + 4 * QNB * QCB;          // QNB x QCB: -T^T W
+  __shared__ double Tm[QNB][QNB + 1];
+  __shared__ double Gm[QNB][QNB + 1];
+  __shared__ double taus[QNB];
+#define QA(i, j) P.A[(long long)(i) * P.rs + (long long)(j) * P.cs]
+  for (int p0 = 0; p0 < n; p0 += QNB) {
+    const int pb = min(QNB, n - p0), mr = m - p0;
+    // ---- panel: warp w owns column p0 + w
+    double x[QRPL];
+    const bool own = w < pb;
+#pragma unroll
+    for (int q = 0; q < QRPL; ++q) {
+      const int i = lane + 32 * q;
+      x[q] = (own && i < mr) ? QA(p0 + i, p0 + w) : 0.0;
+    }
+    double rjj = 0.0;
+    for (int j = 0; j < pb; ++j) {
+      if (w == j) {
+        double xs = 0.0;
+#pragma unroll
+        for (int q = 0; q < QRPL; ++q) {
+          const int i = lane + 32 * q;
+          if (i > j && i < mr) xs = fma(x[q], x[q], xs);
+        }
+        xs = warp_sum(xs);
+        const double alpha = __shfl_sync(0xffffffffu, x[0], j);  // row j < QNB <= 32: q = 0
+        double tau = 0.0, scal = 1.0, beta = alpha;
+        if (xs != 0.0) {
+          beta = -copysign(sqrt(alpha * alpha + xs), alpha);
+          tau = (beta - alpha) / beta;
+          scal = 1.0 / (alpha - beta);
+        }
+#pragma unroll
+        for (int q = 0; q < QRPL; ++q) {
+          const int i = lane + 32 * q;
+          if (i < mr) {
+            double v = 0.0;
+            if (i == j) v = 1.0;
+            else if (i > j) { if (tau != 0.0) x[q] *= scal; v = x[q]; }
+            pv[j * QSP + i] = v;
+          }
+        }
+        rjj = beta;
+        if (lane == 0) taus[j] = tau;
+      }
+      __syncthreads();
+      if (w > j && w < pb) {
+        const double tau = taus[j];
+        double d = 0.0;
+#pragma unroll
+        for (int q = 0; q < QRPL; ++q) {
+          const int i = lane + 32 * q;
+          if (i >= j && i < mr) d = fma(pv[j * QSP + i], x[q], d);
+        }
+        d = warp_sum(d) * tau;
+#pragma unroll
+        for (int q = 0; q < QRPL; ++q) {
+          const int i = lane + 32 * q;
+          if (i >= j && i < mr) x[q] = fma(-d, pv[j * QSP + i], x[q]);
+        }
+      }
+    }
+    // write the panel back: R above / on the diagonal, v below; zero-pad pv past pb and mr
+    if (own) {
+#pragma unroll
+      for (int q = 0; q < QRPL; ++q) {
+        const int i = lane + 32 * q;
+        if (i < mr) QA(p0 + i, p0 + w) = (i == w) ? rjj : x[q];
+      }
+      if (lane == 0) P.tau[p0 + w] = taus[w];
+    }
+    for (int e = tid; e < QNB * QSP; e += 512) {
+      const int j = e / QSP, i = e % QSP;
+      if (j >= pb || i >= mr) pv[e] = 0.0;
+    }
+    __syncthreads();
+    // ---- G = V^T V (upper), warp c: G[i][c], i <= c
+    if (w < pb) {
+      for (int i = 0; i <= w; ++i) {
+        double d = 0.0;
+#pragma unroll
+        for (int q = 0; q < QRPL; ++q) {
+          const int r = lane + 32 * q;
+          if (r < mr) d = fma(pv[i * QSP + r], pv[w * QSP + r], d);
+        }
+        d = warp_sum(d);
+        if (lane == 0) Gm[i][w] = d;
+      }
+    }
+    __syncthreads();
+    // ---- T (upper): T_jj = tau_j, T[0:j, j] = -tau_j T[0:j, 0:j] G[0:j, j]  (warp 0)
+    if (w == 0) {
+      for (int j = 0; j < QNB; ++j) {
+        double a = 0.0;
+        if (lane < j && j < pb)
+          for (int p = lane; p < j; ++p) a = fma(Tm[lane][p], Gm[p][j], a);
+        __syncwarp();
+        if (lane < QNB) {
+          if (j >= pb) Tm[lane][j] = 0.0;
+          else if (lane < j) Tm[lane][j] = -taus[j] * a;
+          else Tm[lane][j] = (lane == j) ? taus[j] : 0.0;
+        }
+        __syncwarp();
+      }
+    }
+    __syncthreads();
+    // ---- trailing columns in blocks of QCB; the next block's loads are issued into registers
+    // before the current block's arithmetic (global latency hidden under the DMMAs)
+    const int mr8 = (mr + 7) & ~7;
+    const int quarter = ((mr8 / 4 + 3) / 4) * 4;   // k range per W-partial, multiple of 4
+    constexpr int PF = QMAX * QCB / 512;            // prefetch registers per thread
+    double nx[PF];
+    auto fetch = [&](int c0) {
+      const int nc = min(QCB, n - c0);
+#pragma unroll
+      for (int q = 0; q < PF; ++q) {
+        const int e = tid + 512 * q, i = e / QCB, c = e % QCB;
+        nx[q] = (i < mr && c < nc) ? QA(p0 + i, c0 + c) : 0.0;
+      }
+    };
+    auto stage = [&]() {
+#pragma unroll
+      for (int q = 0; q < PF; ++q) {
+        const int e = tid + 512 * q, i = e / QCB, c = e % QCB;
+        if (i < mr8) ab[i * QSB + c] = nx[q];
+      }
+    };
+    if (p0 + pb < n) { fetch(p0 + pb); stage(); }
+    __syncthreads();
+    for (int c0 = p0 + pb; c0 < n; c0 += QCB) {
+      const int nc = min(QCB, n - c0);
+      const bool more = c0 + QCB < n;
+      if (more) fetch(c0 + QCB);
+      {  // W partial: tile (mt, nt) = (w & 1, (w >> 1) & 1), rows quarter w >> 2
+        const int mt = w & 1, nt = (w >> 1) & 1, qr = w >> 2;
+        const int k0 = qr * quarter, k1 = min(mr8, k0 + quarter);
+        double a0 = 0.0, a1 = 0.0, b0 = 0.0, b1 = 0.0;
+        int k = k0;
+        for (; k + 8 <= k1; k += 8) {
+          dmma884_(a0, a1, pv[(mt * 8 + g) * QSP + k + t], ab[(k + t) * QSB + nt * 8 + g]);
+          dmma884_(b0, b1, pv[(mt * 8 + g) * QSP + k + 4 + t], ab[(k + 4 + t) * QSB + nt * 8 + g]);
+        }
+        for (; k < k1; k += 4)
+          dmma884_(a0, a1, pv[(mt * 8 + g) * QSP + k + t], ab[(k + t) * QSB + nt * 8 + g]);
+        double* dst = wp + qr * QNB * QCB + (mt * 8 + g) * QCB + nt * 8 + 2 * t;
+        dst[0] = a0 + b0;
+        dst[1] = a1 + b1;
+      }
+      __syncthreads();
+      if (tid < QNB * QCB) {  // W = sum of quarters (fixed order); w2 = -T^T W
+        const int j = tid / QCB, c = tid % QCB;
+        double a = 0.0;
+        for (int q = 0; q <= j; ++q) {
+          const int o = q * QCB + c;
+          const double wv = ((wp[o] + wp[QNB * QCB + o]) + wp[2 * QNB * QCB + o]) + wp[3 * QNB * QCB + o];
+          a = fma(Tm[q][j], wv, a);
+        }
+        w2[j * QCB + c] = -a;
+      }
+      __syncthreads();
+      {  // update: tiles (mi, ni), mi < mr8 / 8, ni < 2; warp w takes mi = w, w + 16, ...
+        double bf[2][QNB / 4];
+#pragma unroll
+        for (int ni = 0; ni < 2; ++ni)
+#pragma unroll
+          for (int ks = 0; ks < QNB / 4; ++ks) bf[ni][ks] = w2[(ks * 4 + t) * QCB + ni * 8 + g];
+        for (int mi = w; mi < mr8 / 8; mi += 16) {
+          const int r = mi * 8 + g;
+          double af[QNB / 4];
+#pragma unroll
+          for (int ks = 0; ks < QNB / 4; ++ks) af[ks] = pv[(ks * 4 + t) * QSP + mi * 8 + g];
+#pragma unroll
+          for (int ni = 0; ni < 2; ++ni) {
+            const int c = ni * 8 + 2 * t;
+            double d0 = ab[r * QSB + c], d1 = ab[r * QSB + c + 1];
+#pragma unroll
+            for (int ks = 0; ks < QNB / 4; ++ks) dmma884_(d0, d1, af[ks], bf[ni][ks]);
+            if (r < mr) {
+              if (c < nc) QA(p0 + r, c0 + c) = d0;
+              if (c + 1 < nc) QA(p0 + r, c0 + c + 1) = d1;
+            }
+          }
+        }
+      }
+      __syncthreads();
+      if (more) { stage(); __syncthreads(); }
+    }
+  }
+#undef QA
+}
+
 void bgeqr2(const std::vector<QrProb>& probs, cudaStream_t s) {
   if (probs.empty()) return;
   int maxm = 0;
   for (auto& p : probs) maxm = std::max(maxm, p.m);
   QrProb* d = upload_probs(probs, s);
+  static const int tc = [] { const char* e = getenv("SVMHSS_QR_TC"); return (e && e[0] == '0') ? 0 : 1; }();
+  if (tc && maxm <= QMAX) {
+    const size_t smem = ((size_t)QNB * QSP + (size_t)QMAX * QSB + 5 * QNB * QCB) * sizeof(double);
+    static bool attr = false;
+    if (!attr) {
+      CUDA_CHECK(cudaFuncSetAttribute(bgeqrf_tc_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+      attr = true;
+    }
+    bgeqrf_tc_kernel<<<(unsigned)probs.size(), 512, smem, s>>>(d);
+    LAUNCH_CHECK();
+    free_probs(d, s);
+    return;
+  }
   // panel width NB and trailing column block cb: the largest that fit 200 KB for the tallest problem
   auto launch = [&](auto kern, int nb) -> bool {
     int cb = 32;
