@@ -25,6 +25,11 @@ static P* upload_probs(const std::vector<P>& v, cudaStream_t s) {
 }
 static void free_probs(void* d, cudaStream_t s) { CUDA_CHECK(cudaFreeAsync(d, s)); }
 
+__device__ __forceinline__ void dmma884_(double& d0, double& d1, double a, double b) {
+  asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};\n"
+               : "+d"(d0), "+d"(d1) : "d"(a), "d"(b));
+}
+
 // ------------------------------------------------------------------ GEMM
 // 128 x 64 x 8 tiles, 256 threads, 8 x 4 outputs per thread (DFMA), register-prefetched
 // double-buffered shared-memory tiles; any operand strides (coalesced load mapping chosen
@@ -226,10 +231,6 @@ __global__ void __launch_bounds__(256, 1) bgemm_big_kernel(const GemmProb* __res
 // used (bitwise P-invariance of the sharded build).
 constexpr int DBK = 16, DSK = 20;
 
-__device__ __forceinline__ void dmma884_(double& d0, double& d1, double a, double b) {
-  asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};\n"
-               : "+d"(d0), "+d"(d1) : "d"(a), "d"(b));
-}
 
 __device__ __forceinline__ void cp_async8_(double* smem, const double* gmem, bool pred) {
   const unsigned sa = (unsigned)__cvta_generic_to_shared(smem);
@@ -415,11 +416,128 @@ __global__ void __launch_bounds__(256) bpotrf_kernel(const SqProb* __restrict__ 
   }
 }
 
+// Right-looking blocked Cholesky on tensor cores, one CTA (16 warps) per node.  Per panel of
+// CNB = 16 columns (already updated by the previous panels): the panel rows are staged in
+// shared memory, warp 0 factors the 16 x 16 diagonal block, every thread solves one row of
+// L21 = A21 L11^-T (forward substitution), and the trailing lower triangle gets
+// A22 -= L21 L21^T as 8 x 8 DMMA tiles (k = 16) read and written in place.  The first
+// non-positive pivot stops the factorization (info = its index + 1), as bpotrf_kernel.
+constexpr int CNB = 16, CPS = 20, CMAX = 1024;
+
+__global__ void __launch_bounds__(512, 1) bpotrf_tc_kernel(const SqProb* __restrict__ probs, int* info) {
+  const SqProb P = probs[blockIdx.x];
+  const int n = P.n, tid = threadIdx.x, lane = tid & 31, w = tid >> 5, g = lane >> 2, t = lane & 3;
+  extern __shared__ __align__(16) double csm[];
+  double* pl = csm;                       // CMAX x CPS: panel rows (row-major)
+  __shared__ int fail;
+  if (tid == 0) fail = 0;
+  for (int p0 = 0; p0 < n; p0 += CNB) {
+    const int pb = min(CNB, n - p0), mr = n - p0;
+    for (int e = tid; e < mr * CNB; e += 512) {
+      const int i = e / CNB, j = e % CNB;
+      pl[i * CPS + j] = (j < pb) ? AT(P, p0 + i, p0 + j) : 0.0;
+    }
+    __syncthreads();
+    if (w == 0) {  // diagonal block: lane i holds row i
+      for (int j = 0; j < pb; ++j) {
+        double d = 0.0;
+        if (lane == j) {
+          d = pl[j * CPS + j];
+          if (d > 0.0) pl[j * CPS + j] = d = sqrt(d);
+        }
+        d = __shfl_sync(0xffffffffu, d, j);
+        if (!(d > 0.0)) {
+          if (lane == 0) fail = p0 + j + 1;
+          break;
+        }
+        if (lane > j && lane < pb) pl[lane * CPS + j] /= d;
+        __syncwarp();
+        if (lane > j && lane < pb) {
+          const double l = pl[lane * CPS + j];
+          for (int k = j + 1; k <= lane; ++k) pl[lane * CPS + k] = fma(-l, pl[k * CPS + j], pl[lane * CPS + k]);
+        }
+        __syncwarp();
+      }
+    }
+    __syncthreads();
+    if (fail) break;
+    for (int i = pb + tid; i < mr; i += 512) {  // L21 row i: forward substitution against L11^T
+      double* r = pl + i * CPS;
+      for (int j = 0; j < pb; ++j) {
+        double a = r[j];
+        for (int k = 0; k < j; ++k) a = fma(-r[k], pl[j * CPS + k], a);
+        r[j] = a / pl[j * CPS + j];
+      }
+    }
+    __syncthreads();
+    for (int e = tid; e < mr * CNB; e += 512) {  // write the panel back (lower part)
+      const int i = e / CNB, j = e % CNB;
+      if (j < pb && j <= i) AT(P, p0 + i, p0 + j) = pl[i * CPS + j];
+    }
+    // trailing: rows / columns pb .. mr-1 (panel-local); tiles (mi, ci), ci <= mi
+    const int nt = (mr - pb + 7) / 8, ntile = nt * (nt + 1) / 2;
+    constexpr int U = 4;  // tiles in flight per warp
+    for (int base = w * U; base < ntile; base += 16 * U) {
+      double d[U][2];
+      int rr[U], cc[U], ra[U], rb[U];
+#pragma unroll
+      for (int u = 0; u < U; ++u) {
+        const int tI = base + u;
+        int mi = (int)((sqrtf(8.0f * tI + 1.0f) - 1.0f) * 0.5f);
+        while ((mi + 1) * (mi + 2) / 2 <= tI) ++mi;
+        while (mi * (mi + 1) / 2 > tI) --mi;
+        const int ci = tI - mi * (mi + 1) / 2;
+        rr[u] = (tI < ntile) ? pb + mi * 8 + g : mr;
+        cc[u] = pb + ci * 8 + 2 * t;
+        ra[u] = pb + mi * 8 + g;
+        rb[u] = pb + ci * 8 + g;
+        d[u][0] = (rr[u] < mr && cc[u] < mr) ? AT(P, p0 + rr[u], p0 + cc[u]) : 0.0;
+        d[u][1] = (rr[u] < mr && cc[u] + 1 < mr) ? AT(P, p0 + rr[u], p0 + cc[u] + 1) : 0.0;
+      }
+#pragma unroll
+      for (int ks = 0; ks < CNB / 4; ++ks)
+#pragma unroll
+        for (int u = 0; u < U; ++u) {
+          const double av = (ra[u] < mr) ? -pl[ra[u] * CPS + ks * 4 + t] : 0.0;
+          const double bv = (rb[u] < mr) ? pl[rb[u] * CPS + ks * 4 + t] : 0.0;
+          dmma884_(d[u][0], d[u][1], av, bv);
+        }
+#pragma unroll
+      for (int u = 0; u < U; ++u) {
+        if (rr[u] < mr) {
+          if (cc[u] < mr) AT(P, p0 + rr[u], p0 + cc[u]) = d[u][0];
+          if (cc[u] + 1 < mr) AT(P, p0 + rr[u], p0 + cc[u] + 1) = d[u][1];
+        }
+      }
+    }
+    __syncthreads();
+  }
+  if (tid == 0 && info) info[blockIdx.x] = fail;
+  if (fail) return;
+  for (long long e = tid; e < (long long)n * n; e += 512) {
+    const int i = (int)(e / n), j = (int)(e % n);
+    if (j > i) AT(P, i, j) = 0.0;
+  }
+}
+
 void bpotrf(const std::vector<SqProb>& probs, int* d_info, cudaStream_t s) {
   if (probs.empty()) return;
   int maxn = 0;
   for (auto& p : probs) maxn = std::max(maxn, p.n);
   SqProb* d = upload_probs(probs, s);
+  static const int tc = [] { const char* e = getenv("SVMHSS_POTRF_TC"); return (e && e[0] == '0') ? 0 : 1; }();
+  if (tc && maxn <= CMAX) {
+    const size_t smem = (size_t)CMAX * CPS * sizeof(double);
+    static bool attr = false;
+    if (!attr) {
+      CUDA_CHECK(cudaFuncSetAttribute(bpotrf_tc_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+      attr = true;
+    }
+    bpotrf_tc_kernel<<<(unsigned)probs.size(), 512, smem, s>>>(d, d_info);
+    LAUNCH_CHECK();
+    free_probs(d, s);
+    return;
+  }
   size_t smem = (size_t)std::max(1, maxn) * sizeof(double);
   if (smem > 48 * 1024)
     CUDA_CHECK(cudaFuncSetAttribute(bpotrf_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
@@ -934,6 +1052,64 @@ __global__ void __launch_bounds__(256) blarft_kernel(const SqProb* __restrict__ 
   }
 }
 
+// Blocked larft: block columns of LNB = 16.  With S = V^T V on input (in place), for block
+// column J: the diagonal block T_JJ by the column recurrence (warp 0), Y = S[0:J, J] T_JJ,
+// and T[0:J, J] = -T[0:J, 0:J] Y (Q = Q_1 Q_2: T = [T1, -T1 V1^T V2 T2; 0, T2]); the block
+// columns before J are final when J starts.  Thread (i, c) owns output row i, column c.
+constexpr int LNB = 16, LMAX = 512;
+
+__global__ void __launch_bounds__(512) blarft_blk_kernel(const SqProb* __restrict__ probs,
+                                                         const double* const* __restrict__ taus) {
+  const SqProb P = probs[blockIdx.x];
+  const double* tau = taus[blockIdx.x];
+  const int n = P.n, tid = threadIdx.x, lane = tid & 31, w = tid >> 5;
+  extern __shared__ __align__(16) double lsm[];
+  double* Sb = lsm;                  // LMAX x LNB: S[0:j1, J-block]
+  double* Y = Sb + LMAX * LNB;       // LMAX x LNB
+  __shared__ double Tjj[LNB][LNB + 1];
+  for (int j0 = 0; j0 < n; j0 += LNB) {
+    const int jb = min(LNB, n - j0), j1 = j0 + jb;
+    for (int e = tid; e < j1 * LNB; e += 512) {
+      const int i = e / LNB, c = e % LNB;
+      Sb[e] = (c < jb) ? AT(P, i, j0 + c) : 0.0;
+    }
+    __syncthreads();
+    if (w == 0) {  // T_JJ: T[r][c] = -tau_c sum_{p=r}^{c-1} T[r][p] S[j0+p][j0+c]
+      for (int c = 0; c < LNB; ++c) {
+        double a = 0.0;
+        if (lane < c && c < jb)
+          for (int q = lane; q < c; ++q) a = fma(Tjj[lane][q], Sb[(j0 + q) * LNB + c], a);
+        __syncwarp();
+        if (lane < LNB) {
+          if (c >= jb) Tjj[lane][c] = 0.0;
+          else if (lane < c) Tjj[lane][c] = -tau[j0 + c] * a;
+          else Tjj[lane][c] = (lane == c) ? tau[j0 + c] : 0.0;
+        }
+        __syncwarp();
+      }
+    }
+    __syncthreads();
+    for (int e = tid; e < j0 * LNB; e += 512) {  // Y = S[0:j0, J] T_JJ
+      const int i = e / LNB, c = e % LNB;
+      double a = 0.0;
+      for (int q = 0; q <= c; ++q) a = fma(Sb[i * LNB + q], Tjj[q][c], a);
+      Y[e] = a;
+    }
+    __syncthreads();
+    for (int e = tid; e < j0 * LNB; e += 512) {  // T[i, J] = -T[i, i:j0] Y[i:j0, :]
+      const int i = e / LNB, c = e % LNB;
+      double a = 0.0;
+      for (int p = i; p < j0; ++p) a = fma(AT(P, i, p), Y[p * LNB + c], a);
+      if (c < jb) AT(P, i, j0 + c) = -a;
+    }
+    for (int e = tid; e < (n - j0) * LNB; e += 512) {  // diagonal block and zeros below it
+      const int i = j0 + e / LNB, c = e % LNB;
+      if (c < jb) AT(P, i, j0 + c) = (i < j1) ? Tjj[i - j0][c] : 0.0;
+    }
+    __syncthreads();
+  }
+}
+
 void blarft(const std::vector<SqProb>& probs, const std::vector<const double*>& taus,
             cudaStream_t s) {
   if (probs.empty()) return;
@@ -941,6 +1117,20 @@ void blarft(const std::vector<SqProb>& probs, const std::vector<const double*>& 
   for (auto& p : probs) maxn = std::max(maxn, p.n);
   SqProb* d = upload_probs(probs, s);
   const double** dt = upload_probs(taus, s);
+  static const int blk = [] { const char* e = getenv("SVMHSS_LARFT_BLK"); return (e && e[0] == '0') ? 0 : 1; }();
+  if (blk && maxn <= LMAX) {
+    const size_t sm2 = (size_t)2 * LMAX * LNB * sizeof(double);
+    static bool attr = false;
+    if (!attr) {
+      CUDA_CHECK(cudaFuncSetAttribute(blarft_blk_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm2));
+      attr = true;
+    }
+    blarft_blk_kernel<<<(unsigned)probs.size(), 512, sm2, s>>>(d, dt);
+    LAUNCH_CHECK();
+    free_probs(d, s);
+    free_probs((void*)dt, s);
+    return;
+  }
   size_t smem = (size_t)std::max(1, maxn) * sizeof(double);
   if (smem > 48 * 1024)
     CUDA_CHECK(cudaFuncSetAttribute(blarft_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
