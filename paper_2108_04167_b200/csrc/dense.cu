@@ -237,8 +237,8 @@ __device__ __forceinline__ void cp_async8_(double* smem, const double* gmem, boo
   asm volatile("cp.async.ca.shared.global [%0], [%1], 8, %2;\n" ::"r"(sa), "l"(gmem), "r"(pred ? 8 : 0));
 }
 
-template <int MT, int NT>
-__global__ void __launch_bounds__(256) bgemm_dmma_kernel(const GemmProb* __restrict__ probs) {
+template <int MT, int NT, int MINB>
+__global__ void __launch_bounds__(256, MINB) bgemm_dmma_kernel(const GemmProb* __restrict__ probs) {
   constexpr int BM = 16 * MT, BN = 32 * NT;
   constexpr int LA = BM * DBK / 256, LB = BN * DBK / 256;  // elements per thread per tile
   const GemmProb P = probs[blockIdx.z];
@@ -329,17 +329,17 @@ __global__ void __launch_bounds__(256) bgemm_dmma_kernel(const GemmProb* __restr
   }
 }
 
-template <int MT, int NT>
+template <int MT, int NT, int MINB>
 static void launch_dmma(const GemmProb* d, int maxm, int maxn, unsigned nb, cudaStream_t s) {
   constexpr int BM = 16 * MT, BN = 32 * NT;
   const size_t smem = (size_t)2 * (BM + BN) * DSK * sizeof(double);
   static bool attr = false;
   if (!attr) {
-    CUDA_CHECK(cudaFuncSetAttribute(bgemm_dmma_kernel<MT, NT>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    CUDA_CHECK(cudaFuncSetAttribute(bgemm_dmma_kernel<MT, NT, MINB>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
     attr = true;
   }
   dim3 grid(ceil_div(maxn, BN), ceil_div(maxm, BM), nb);
-  bgemm_dmma_kernel<MT, NT><<<grid, 256, smem, s>>>(d);
+  bgemm_dmma_kernel<MT, NT, MINB><<<grid, 256, smem, s>>>(d);
 }
 
 void bgemm(const std::vector<GemmProb>& probs_in, cudaStream_t s) {
@@ -359,8 +359,14 @@ void bgemm(const std::vector<GemmProb>& probs_in, cudaStream_t s) {
     static const int dfma = [] { const char* e = getenv("SVMHSS_GEMM_DFMA"); return (e && e[0] == '1') ? 1 : 0; }();
     if (!dfma) {
       // FP64 tensor cores: 128 x 128 CTA tiles for the big factor GEMMs, 64 x 64 otherwise
-      if (maxm >= 256 && maxn >= 256) launch_dmma<8, 4>(d, maxm, maxn, (unsigned)chunk.size(), s);
-      else launch_dmma<4, 2>(d, maxm, maxn, (unsigned)chunk.size(), s);
+      static const int tile = [] { const char* e = getenv("SVMHSS_GEMM_TILE"); return e ? atoi(e) : 44; }();
+      if (maxm >= 256 && maxn >= 256) {
+        if (tile == 84) launch_dmma<8, 4, 1>(d, maxm, maxn, (unsigned)chunk.size(), s);
+        else if (tile == 82) launch_dmma<8, 2, 2>(d, maxm, maxn, (unsigned)chunk.size(), s);
+        else launch_dmma<4, 4, 2>(d, maxm, maxn, (unsigned)chunk.size(), s);
+      } else {
+        launch_dmma<4, 2, 2>(d, maxm, maxn, (unsigned)chunk.size(), s);
+      }
     } else if (maxm >= 256 && maxn >= 256 && !getenv("SVMHSS_GEMM_SMALL")) {  // big batched GEMMs (factor)
       dim3 grid(ceil_div(maxn, HBN), ceil_div(maxm, HBM_), (unsigned)chunk.size());
       bgemm_big_kernel<<<grid, 256, 0, s>>>(d);
@@ -617,16 +623,151 @@ __global__ void __launch_bounds__(256) btrsm_kernel(const TrsmProb* __restrict__
 #undef XX
 }
 
+// Triangular solve on tensor cores: one CTA (8 warps) per (problem, 16 right-hand-side
+// columns).  The 16 x 16 diagonal blocks are inverted first (lane c: column c of the block
+// inverse, by substitution); then block by block (top down for lower, bottom up for upper):
+// X_b = D_b^-1 X_b (DMMA, 2 x 2 tiles) and the not-yet-solved rows get X_i -= T_ib X_b (DMMA,
+// k = 16), with X resident in shared memory and T fragments read through L1.
+constexpr int SW_ = 16, SXS = 24, SDS = 20, SMAXN = 512;
+
+template <bool LOWER>
+__global__ void __launch_bounds__(256) btrsm_tc_kernel(const TrsmProb* __restrict__ probs) {
+  const TrsmProb P = probs[blockIdx.y];
+  const int c0 = blockIdx.x * SW_;
+  if (c0 >= P.nrhs || P.n == 0) return;
+  const int n = P.n, nc = min(SW_, P.nrhs - c0), nb = (n + 15) / 16;
+  const int tid = threadIdx.x, lane = tid & 31, w = tid >> 5, g = lane >> 2, t = lane & 3;
+  extern __shared__ __align__(16) double tsm[];
+  double* Xs = tsm;                               // n8 x SXS
+  double* Di = tsm + (size_t)((n + 7) & ~7) * SXS;  // nb x 16 x SDS
+#define TT(i, j) __ldg(P.T + (long long)(i) * P.trs + (long long)(j) * P.tcs)
+#define XX(i, j) P.X[(long long)(i) * P.xrs + (long long)(j) * P.xcs]
+  auto blk = [&](int bi, int& r0, int& r1) {
+    if (LOWER) { r0 = bi * 16; r1 = min(n, r0 + 16); }
+    else { r1 = n - bi * 16; r0 = max(0, r1 - 16); }
+  };
+  for (int e = tid; e < ((n + 7) & ~7) * SW_; e += 256) {
+    const int i = e / SW_, c = e % SW_;
+    Xs[i * SXS + c] = (i < n && c < nc) ? XX(i, c0 + c) : 0.0;
+  }
+  for (int bi = w; bi < nb; bi += 8) {  // diagonal block inverses, zero padded to 16 x 16
+    int r0, r1;
+    blk(bi, r0, r1);
+    const int bs = r1 - r0;
+    double* D = Di + (size_t)bi * 16 * SDS;
+    if (lane < 16) {
+      const int c = lane;
+      double z[16];
+#pragma unroll
+      for (int j = 0; j < 16; ++j) z[j] = 0.0;
+      if (c < bs) {
+        if (LOWER) {
+#pragma unroll
+          for (int j = 0; j < 16; ++j) {
+            if (j < c || j >= bs) continue;
+            double a = (j == c) ? 1.0 : 0.0;
+            for (int p = c; p < j; ++p) a = fma(-TT(r0 + j, r0 + p), z[p], a);
+            z[j] = a / TT(r0 + j, r0 + j);
+          }
+        } else {
+#pragma unroll
+          for (int jj = 15; jj >= 0; --jj) {
+            if (jj > c) continue;
+            double a = (jj == c) ? 1.0 : 0.0;
+            for (int p = jj + 1; p <= c; ++p) a = fma(-TT(r0 + jj, r0 + p), z[p], a);
+            z[jj] = a / TT(r0 + jj, r0 + jj);
+          }
+        }
+      }
+#pragma unroll
+      for (int j = 0; j < 16; ++j) D[j * SDS + c] = z[j];
+    }
+  }
+  __syncthreads();
+  for (int bi = 0; bi < nb; ++bi) {
+    int r0, r1;
+    blk(bi, r0, r1);
+    const int bs = r1 - r0;
+    const double* D = Di + (size_t)bi * 16 * SDS;
+    double y0 = 0.0, y1 = 0.0;
+    const int mt = w & 1, nt = (w >> 1) & 1;
+    if (w < 4) {  // X_b = D^-1 X_b, tile (mt, nt)
+#pragma unroll
+      for (int ks = 0; ks < 4; ++ks) {
+        const int k = ks * 4 + t;
+        const double bv = (k < bs) ? Xs[(r0 + k) * SXS + nt * 8 + g] : 0.0;
+        dmma884_(y0, y1, D[(mt * 8 + g) * SDS + k], bv);
+      }
+    }
+    __syncthreads();
+    if (w < 4 && mt * 8 + g < bs) {
+      Xs[(r0 + mt * 8 + g) * SXS + nt * 8 + 2 * t] = y0;
+      Xs[(r0 + mt * 8 + g) * SXS + nt * 8 + 2 * t + 1] = y1;
+    }
+    __syncthreads();
+    // X_i -= T[i, r0:r1] X_b for the unsolved rows: lower [r1, n), upper [0, r0)
+    const int u0 = LOWER ? r1 : 0, u1 = LOWER ? n : r0;
+    double bf[2][4];
+#pragma unroll
+    for (int q = 0; q < 2; ++q)
+#pragma unroll
+      for (int ks = 0; ks < 4; ++ks) {
+        const int k = ks * 4 + t;
+        bf[q][ks] = (k < bs) ? Xs[(r0 + k) * SXS + q * 8 + g] : 0.0;
+      }
+    const int nt8 = (u1 - u0 + 7) / 8;
+    for (int mi = w; mi < nt8; mi += 8) {
+      const int ra = u0 + mi * 8 + g;
+      double af[4];
+#pragma unroll
+      for (int ks = 0; ks < 4; ++ks) {
+        const int k = ks * 4 + t;
+        af[ks] = (ra < u1 && k < bs) ? -TT(ra, r0 + k) : 0.0;
+      }
+#pragma unroll
+      for (int q = 0; q < 2; ++q) {
+        double* xr = Xs + ra * SXS + q * 8 + 2 * t;
+        double d0 = (ra < u1) ? xr[0] : 0.0, d1 = (ra < u1) ? xr[1] : 0.0;
+#pragma unroll
+        for (int ks = 0; ks < 4; ++ks) dmma884_(d0, d1, af[ks], bf[q][ks]);
+        if (ra < u1) { xr[0] = d0; xr[1] = d1; }
+      }
+    }
+    __syncthreads();
+  }
+  for (int e = tid; e < n * SW_; e += 256) {
+    const int i = e / SW_, c = e % SW_;
+    if (c < nc) XX(i, c0 + c) = Xs[i * SXS + c];
+  }
+#undef TT
+#undef XX
+}
+
 void btrsm(const std::vector<TrsmProb>& probs_in, bool lower, cudaStream_t s) {
   std::vector<TrsmProb> probs;
-  int maxr = 0;
+  int maxr = 0, maxn = 0;
   for (auto& p : probs_in)
-    if (p.n > 0 && p.nrhs > 0) { probs.push_back(p); maxr = std::max(maxr, p.nrhs); }
+    if (p.n > 0 && p.nrhs > 0) { probs.push_back(p); maxr = std::max(maxr, p.nrhs); maxn = std::max(maxn, p.n); }
   if (probs.empty()) return;
   for (size_t b0 = 0; b0 < probs.size(); b0 += 65535) {
     std::vector<TrsmProb> chunk(probs.begin() + b0,
                                 probs.begin() + std::min(probs.size(), b0 + 65535));
     TrsmProb* d = upload_probs(chunk, s);
+    static const int tc = [] { const char* e = getenv("SVMHSS_TRSM_TC"); return (e && e[0] == '0') ? 0 : 1; }();
+    if (tc && maxn <= SMAXN) {
+      const size_t smem = ((size_t)((maxn + 7) & ~7) * SXS + (size_t)((maxn + 15) / 16) * 16 * SDS) * sizeof(double);
+      dim3 grid(ceil_div(maxr, SW_), (unsigned)chunk.size());
+      if (lower) {
+        CUDA_CHECK(cudaFuncSetAttribute(btrsm_tc_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+        btrsm_tc_kernel<true><<<grid, 256, smem, s>>>(d);
+      } else {
+        CUDA_CHECK(cudaFuncSetAttribute(btrsm_tc_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+        btrsm_tc_kernel<false><<<grid, 256, smem, s>>>(d);
+      }
+      LAUNCH_CHECK();
+      free_probs(d, s);
+      continue;
+    }
     dim3 grid(ceil_div(maxr, TC), (unsigned)chunk.size());
     if (lower) btrsm_kernel<true><<<grid, 256, 0, s>>>(d);
     else btrsm_kernel<false><<<grid, 256, 0, s>>>(d);
