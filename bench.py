@@ -340,7 +340,12 @@ def main():
     if world > 1:
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
     ms_total, loop_ms, build_ms, sketch_ms = t.tolist()
-    hi, ui, ast = recs[-1]
+    hi, ui, ast = (dict(d) for d in recs[-1])
+    # phase times: per-phase medians over the timed steps (one step can hit a memory-pool growth)
+    for j, d in enumerate((hi, ui, ast)):
+        for k in list(d):
+            if k.startswith("ms_") and all(r[j].get(k) is not None for r in recs):
+                d[k] = float(np.median([r[j][k] for r in recs]))
     value = max_it * len(Cs) / (loop_ms / 1e3)  # iterations of the whole (sharded) problem
     peaks, peak_src = _peaks()
     rp = (cfg["r"] + 3) // 4 * 4

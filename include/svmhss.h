@@ -129,7 +129,11 @@ typedef struct {
 /* ---- build: tree + Omega + sketch + per-level ID compression (Alg.3 l.1) ----
  * F: n x r row-major features (device).  h > 0 kernel width.
  * Returns HSS_EINVAL if n < 1, r < 1, h <= 0, leaf_size < 1, max_rank < 1, oversample < 0,
- * or s = max_rank + oversample > 2^20 (RNG column field, R1). */
+ * or s = max_rank + oversample > 2^20 (RNG column field, R1).
+ * Memory: device buffers come from the device's default stream-ordered pool (release threshold
+ * kept at max, so freed memory stays reserved for the next call).  Before the first build of a
+ * given size the pool is grown once to about 24 n (s + r) 8 bytes (at most half the free memory;
+ * SVMHSS_POOL_RESERVE_GB overrides, 0 disables) so later phases do not map memory mid-call. */
 int hss_build(const double* F, int64_t n, int32_t r, double h, const hss_opts* opt,
               void* stream, hss_t* out);
 

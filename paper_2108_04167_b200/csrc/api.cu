@@ -20,6 +20,28 @@ void init_mem_pool() {
   }
   done_dev = dev;
 }
+// Memory-pool reservation ahead of a build: one physical chunk of about the problem's peak
+// footprint (sketch operands, generators, factor and its per-level temporaries ~ 24 n (s + r) 8
+// bytes), capped at half the free memory, so the stream-ordered allocations of build / factor /
+// ADMM sub-allocate from it instead of growing the pool (mapping GBs) in the middle of a
+// factorization.  SVMHSS_POOL_RESERVE_GB overrides the estimate (0 disables).
+static void pool_reserve(int64_t n, int r, int s_cols, cudaStream_t st) {
+  static thread_local size_t reserved = 0;
+  const char* e = getenv("SVMHSS_POOL_RESERVE_GB");
+  double want = e ? atof(e) * 1e9 : 24.0 * (double)n * (double)(s_cols + r) * 8.0;
+  size_t fr = 0, tot = 0;
+  if (cudaMemGetInfo(&fr, &tot) != cudaSuccess) { cudaGetLastError(); return; }
+  want = std::min(want, 0.5 * (double)fr + (double)reserved);
+  if (want <= (double)reserved + 64e6) return;
+  void* p = nullptr;
+  if (cudaMallocAsync(&p, (size_t)want, st) == cudaSuccess) {
+    cudaFreeAsync(p, st);
+    reserved = (size_t)want;
+  } else {
+    cudaGetLastError();
+  }
+}
+
 void set_last_error(const std::string& s) { g_last_error = s; }
 
 double PhaseTrace::now_ms() {
@@ -166,6 +188,7 @@ int hss_build(const double* F, int64_t n, int32_t r, double h, const hss_opts* o
     StreamScope ss__((cudaStream_t)stream);
     require(out != nullptr && F != nullptr, "hss_build: NULL pointer");
     validate_opts(opt, n, r, h);
+    pool_reserve(n, r, opt->max_rank + opt->oversample, (cudaStream_t)stream);
     *out = new hss_s{build_adaptive(F, n, r, h, *opt, comm_of(opt), (cudaStream_t)stream)};
   });
 }
