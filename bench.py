@@ -396,11 +396,11 @@ def main():
                                 "work": "sum over nodes 2Rk^2 + 8R^2k + (R-k)^3/3 + k(R-k)^2 + k^2(R-k) + 4k^3 "
                                         "(SURVEY 8(d) a7), flops %.3e" % ui["factor_flops"]},
             "roofline_predict": None if ast["ms_predict"] is None else {
-                "bound": "tensor", "phase": "svm_predict (kmm_kernel: K(Ftest, F) [y z | 0], 16 columns)",
-                "achieved": 2.0 * Ftd.shape[0] * n * (rp + 16) / (ast["ms_predict"] / 1e3) / 1e12,
+                "bound": "tensor", "phase": "svm_predict (predict_kernel: distance DMMA + exp + coefficient sums)",
+                "achieved": 2.0 * Ftd.shape[0] * n * (rp + len(Cs)) / (ast["ms_predict"] / 1e3) / 1e12,
                 "peak": fp64_peak, "unit": "TFLOP/s",
-                "frac": 2.0 * Ftd.shape[0] * n * (rp + 16) / (ast["ms_predict"] / 1e3) / 1e12 / fp64_peak,
-                "work": "2 m n (r_pad + 16) flops (incl. padding/norm/finish kernels in the time)"},
+                "frac": 2.0 * Ftd.shape[0] * n * (rp + len(Cs)) / (ast["ms_predict"] / 1e3) / 1e12 / fp64_peak,
+                "work": "2 m n (r_pad + nC) flops + m n exp (incl. padding/norm/finish kernels in the time)"},
             "roofline_bias": {"bound": "hbm", "phase": "bias + objective: one HSS mat-vec with 2 nC columns",
                               "achieved": hi["generator_bytes"] / (ast["ms_bias"] / 1e3) / 1e9,
                               "peak": peaks["hbm_gbs"], "unit": "GB/s",

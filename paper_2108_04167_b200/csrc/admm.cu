@@ -608,22 +608,17 @@ void predict_impl(const double* Ftrain, const double* coef, int64_t n, int r, do
                   const double* bias_host, int nC, const double* Ftest, int64_t m, double* dv,
                   int8_t* lab, cudaStream_t s) {
   const int rp = (r + 3) / 4 * 4;
-  const int ld = 16;
-  DevBuf<double> Ftr((size_t)n * rp), Fte((size_t)std::max<int64_t>(1, m) * rp), nutr(n + kNormPad),
-      nute(std::max<int64_t>(1, m) + kNormPad), W((size_t)n * ld), S((size_t)std::max<int64_t>(1, m) * ld), b(nC);
-  pad_rows(Ftrain, n, r, rp, Ftr.p, s);
-  pad_rows(Ftest, m, r, rp, Fte.p, s);
-  row_norms(Ftr.p, n, rp, nutr.p, s);
-  row_norms(Fte.p, m, rp, nute.p, s);
+  const int SA = predict_stride(rp);
+  const int ld = nC <= 1 ? 1 : nC <= 2 ? 2 : nC <= 4 ? 4 : nC <= 8 ? 8 : 16;
+  DevBuf<double> Ftr((size_t)n * SA), Fte((size_t)std::max<int64_t>(1, m) * SA), nutr(n + kNormPad),
+      nute(std::max<int64_t>(1, m) + kNormPad), W((size_t)n * ld + 2), S((size_t)std::max<int64_t>(1, m) * ld), b(nC);
+  pad_rows(Ftrain, n, r, SA, Ftr.p, s);
+  pad_rows(Ftest, m, r, SA, Fte.p, s);
+  row_norms(Ftr.p, n, SA, nutr.p, s);
+  row_norms(Fte.p, m, SA, nute.p, s);
   pad_coef_kernel<<<ceil_div(n * ld, 256), 256, 0, s>>>(coef, n, nC, ld, W.p);
   LAUNCH_CHECK();
-  KmmArgs a{};
-  a.Fa = Fte.p; a.nua = nute.p; a.na = m;
-  a.Fb = Ftr.p; a.nub = nutr.p; a.nb = n;
-  a.rp = rp; a.W = W.p; a.ldw = ld; a.ncols = ld; a.S = S.p; a.lds = ld;
-  a.neg_inv_2h2 = -1.0 / (2.0 * h * h);
-  a.same_set = 0; a.leaf_a = nullptr; a.leaf_b = nullptr;
-  kernel_matmul(a, s);
+  predict_sums(Fte.p, nute.p, m, Ftr.p, nutr.p, W.p, n, rp, SA, ld, -1.0 / (2.0 * h * h), S.p, s);
   h2d(b.p, bias_host, nC, s);
   predict_finish_kernel<<<ceil_div(m * nC, 256), 256, 0, s>>>(S.p, m, nC, ld, b.p, dv, lab);
   LAUNCH_CHECK();

@@ -25,6 +25,12 @@ struct KmmArgs {
 constexpr int kNormPad = 2, kLeafPad = 4;
 // S = K(Fa, Fb) W via DMMA distance GEMM -> exp -> DMMA GEMM (H1).
 void kernel_matmul(const KmmArgs& a, cudaStream_t s);
+// Prediction sums S (na x NC) = K(Fa, Fb) coef (a11): Fa / Fb with row stride SA =
+// predict_stride(rp) (zero padded), nub and coef (nb x NC) with >= 2 doubles of padding.
+int predict_stride(int rp);
+void predict_sums(const double* Fa, const double* nua, int64_t na, const double* Fb, const double* nub,
+                  const double* coef, int64_t nb, int rp, int SA, int NC, double neg_inv_2h2, double* S,
+                  cudaStream_t s);
 // Which kernel_matmul configuration serves (rp, ncols); for reporting.
 int kmm_chunk_cols(int rp, int ncols);
 

@@ -365,6 +365,145 @@ void kernel_matmul(const KmmArgs& a, cudaStream_t s) {
   throw Error(HSS_EINVAL, "kernel_matmul: no kernel configuration");
 }
 
+// ------------------------------------------------------------------ prediction (a11)
+// dv_t = sum_i coef_i K(f_i, t) for nC <= 16 coefficient columns.  One CTA = 128 test
+// points (16 warps x one 8-row m-tile); the warp keeps its rows' A-fragments in registers for the
+// whole sweep, so a step needs only the B-fragments of the 64 training points.  Per step:
+// distance tile 8 x 64 on DMMA (8 independent chains of rp/4), exp, and the coefficient-weighted
+// sums accumulated in registers (a GEMV: no second DMMA, no shared-memory exchange).  Training
+// tiles (features with row stride PSA = 4 mod 16, norms, coefficients) stream through a
+// 3-stage TMA bulk-copy ring.  Per-thread sums run in training-point order; the 4 lanes of a
+// row are combined by a fixed butterfly.
+constexpr int PBJ = 64, PST = 3;
+
+// NKM: register A-fragments per thread (rp <= 4 NKM); NW warps per CTA (rows = 8 NW).
+template <int NC, int NKM, int NW>
+__global__ void __launch_bounds__(NW * 32, 1) predict_kernel(const double* __restrict__ Fa, const double* __restrict__ nua,
+                                                         int64_t na, const double* __restrict__ Fb,
+                                                         const double* __restrict__ nub, const double* __restrict__ coef,
+                                                         int64_t nb, int rp, int SA, double neg_inv_2h2,
+                                                         double* __restrict__ S, int nst) {
+  extern __shared__ __align__(128) double psm[];
+  const int cpad = (PBJ * NC + 1) & ~1;
+  const int stage_d = PBJ * SA + PBJ + cpad;          // doubles per stage (16-byte multiples)
+  __shared__ __align__(8) uint64_t full[PST];
+  __shared__ __align__(8) uint64_t empty[PST];
+  const int tid = threadIdx.x, lane = tid & 31, w = tid >> 5, g = lane >> 2, t = lane & 3;
+  const int64_t row0 = (int64_t)blockIdx.x * (8 * NW);
+  const int64_t nsteps = (nb + PBJ - 1) / PBJ;
+  if (tid == 0) {
+    for (int b = 0; b < nst; ++b) { mbar_init(&full[b], 1); mbar_init(&empty[b], NW); }
+    asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
+  }
+  __syncthreads();
+  auto issue = [&](int64_t js) {
+    const int b = (int)(js % nst);
+    double* Fs = psm + (size_t)b * stage_d;
+    double* ns = Fs + PBJ * SA;
+    double* cs = ns + PBJ;
+    const int64_t j0 = js * PBJ;
+    const int jv = (int)min((int64_t)PBJ, nb - j0);
+    const unsigned fb = (unsigned)jv * SA * 8, nbv = (unsigned)((jv * 8 + 15) & ~15),
+                   cb = (unsigned)((jv * NC * 8 + 15) & ~15);
+    mbar_expect_tx(&full[b], fb + nbv + cb);
+    bulk_g2s(Fs, Fb + j0 * SA, fb, &full[b]);
+    bulk_g2s(ns, nub + j0, nbv, &full[b]);
+    bulk_g2s(cs, coef + j0 * NC, cb, &full[b]);
+  };
+  if (tid == 0)
+    for (int64_t js = 0; js < min((int64_t)nst, nsteps); ++js) issue(js);
+  // this warp's rows: A-fragments (row g, k = 4 kk + t) in registers for the whole sweep
+  const int64_t my_row = row0 + w * 8 + g;
+  const bool row_ok = my_row < na;
+  double fa[NKM];
+#pragma unroll
+  for (int kk = 0; kk < NKM; ++kk)
+    fa[kk] = (row_ok && 4 * kk < rp) ? Fa[my_row * SA + 4 * kk + t] : 0.0;
+  const double nui = row_ok ? nua[my_row] : 0.0;
+  double acc[NC];
+#pragma unroll
+  for (int c = 0; c < NC; ++c) acc[c] = 0.0;
+  const int nk = rp / 4;
+  for (int64_t js = 0; js < nsteps; ++js) {
+    const int b = (int)(js % nst);
+    mbar_wait(&full[b], (unsigned)((js / nst) & 1));
+    // refill the stage of step js-1 (released by every warp by now, in the common case)
+    if (tid == 0 && js >= 1 && js - 1 + nst < nsteps) {
+      const int pb = (int)((js - 1) % nst);
+      mbar_wait(&empty[pb], (unsigned)(((js - 1) / nst) & 1));
+      issue(js - 1 + nst);
+    }
+    const double* Fs = psm + (size_t)b * stage_d;
+    const double* ns = Fs + PBJ * SA;
+    const double* cs = ns + PBJ;
+    const int jv = (int)min((int64_t)PBJ, nb - js * PBJ);
+    double d[8][2];
+#pragma unroll
+    for (int q = 0; q < 8; ++q) d[q][0] = d[q][1] = 0.0;
+    const double* Fw = Fs + g * SA + t;
+#pragma unroll
+    for (int kk = 0; kk < NKM; ++kk) {
+      if (kk < nk) {
+#pragma unroll
+        for (int q = 0; q < 8; ++q) dmma884(d[q][0], d[q][1], fa[kk], Fw[q * 8 * SA + 4 * kk]);
+      }
+    }
+#pragma unroll
+    for (int q = 0; q < 8; ++q)
+#pragma unroll
+      for (int e = 0; e < 2; ++e) {
+        const int jj = q * 8 + 2 * t + e;
+        const double d2 = fmax(nui + ns[jj] - 2.0 * d[q][e], 0.0);
+        double v = exp_kernel(d2 * neg_inv_2h2);
+        if (jj >= jv) v = 0.0;
+#pragma unroll
+        for (int c = 0; c < NC; ++c) acc[c] = fma(v, cs[jj * NC + c], acc[c]);
+      }
+    __syncwarp();
+    if (lane == 0) mbar_arrive(&empty[b]);
+  }
+#pragma unroll
+  for (int c = 0; c < NC; ++c) {
+    acc[c] += __shfl_xor_sync(0xffffffffu, acc[c], 1);
+    acc[c] += __shfl_xor_sync(0xffffffffu, acc[c], 2);
+  }
+  if (row_ok && t == 0)
+#pragma unroll
+    for (int c = 0; c < NC; ++c) S[my_row * NC + c] = acc[c];
+}
+
+int predict_stride(int rp) { return pad_stride(rp); }
+
+template <int NC, int NKM, int NW>
+static void launch_predict(const double* Fa, const double* nua, int64_t na, const double* Fb, const double* nub,
+                           const double* coef, int64_t nb, int rp, int SA, double c, double* S, cudaStream_t s) {
+  const size_t stage = (size_t)(PBJ * SA + PBJ + ((PBJ * NC + 1) & ~1)) * sizeof(double);
+  const int nst = (PST * stage <= 220 * 1024) ? PST : 2;   // 3-stage ring, 2 for wide features
+  const size_t smem = nst * stage;
+  require(smem <= 220 * 1024, "predict: feature dimension too large for shared memory");
+  CUDA_CHECK(cudaFuncSetAttribute(predict_kernel<NC, NKM, NW>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+  const unsigned grid = (unsigned)((na + 8 * NW - 1) / (8 * NW));
+  predict_kernel<NC, NKM, NW><<<grid, NW * 32, smem, s>>>(Fa, nua, na, Fb, nub, coef, nb, rp, SA, c, S, nst);
+  LAUNCH_CHECK();
+}
+
+void predict_sums(const double* Fa, const double* nua, int64_t na, const double* Fb, const double* nub,
+                  const double* coef, int64_t nb, int rp, int SA, int NC, double neg_inv_2h2, double* S,
+                  cudaStream_t s) {
+  if (na <= 0) return;
+  require(rp % 4 == 0 && rp <= 128, "predict: padded feature count must be a multiple of 4 and <= 128");
+#define PRED_CASE(nc)                                                                                       \
+  if (NC == nc) {                                                                                          \
+    if (rp <= 32) launch_predict<nc, 8, 16>(Fa, nua, na, Fb, nub, coef, nb, rp, SA, neg_inv_2h2, S, s);     \
+    else if (rp <= 64) launch_predict<nc, 16, 16>(Fa, nua, na, Fb, nub, coef, nb, rp, SA, neg_inv_2h2, S, s); \
+    else launch_predict<nc, 32, 8>(Fa, nua, na, Fb, nub, coef, nb, rp, SA, neg_inv_2h2, S, s);              \
+    return;                                                                                                \
+  }
+  PRED_CASE(1) PRED_CASE(2) PRED_CASE(4) PRED_CASE(8) PRED_CASE(16)
+#undef PRED_CASE
+  throw Error(HSS_EINVAL, "predict: NC must be 1, 2, 4, 8 or 16");
+}
+
 // ------------------------------------------------------------------ Omega (R1-R3)
 __global__ void omega_kernel(uint64_t key, const int64_t* __restrict__ idx, int64_t rows, int s,
                              double* __restrict__ out) {
