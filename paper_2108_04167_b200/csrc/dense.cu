@@ -229,7 +229,7 @@ __global__ void __launch_bounds__(256, 1) bgemm_big_kernel(const GemmProb* __res
 // conflict free.  Every tile shape runs the same per-element sequence of DMMAs (k = 0, 4, 8,
 // ... in order, zero padded), so a node's result does not depend on which shape its batch
 // used (bitwise P-invariance of the sharded build).
-constexpr int DBK = 16, DSK = 20;
+constexpr int DBK = 16, DSK = 20, DNS = 3;
 
 
 __device__ __forceinline__ void cp_async8_(double* smem, const double* gmem, bool pred) {
@@ -245,8 +245,8 @@ __global__ void __launch_bounds__(256, MINB) bgemm_dmma_kernel(const GemmProb* _
   const int m0 = blockIdx.y * BM, n0 = blockIdx.x * BN;
   if (m0 >= P.m || n0 >= P.n) return;
   extern __shared__ __align__(16) double dsm[];
-  double* As = dsm;                       // 2 x BM x DSK
-  double* Bs = dsm + 2 * BM * DSK;        // 2 x BN x DSK
+  double* As = dsm;                       // DNS x BM x DSK
+  double* Bs = dsm + DNS * BM * DSK;      // DNS x BN x DSK
   const int tid = threadIdx.x, lane = tid & 31, w = tid >> 5, g = lane >> 2, t = lane & 3;
   const int wm = (w >> 2) * (8 * MT), wn = (w & 3) * (8 * NT);
   const bool a_k = (P.acs == 1), b_n = (P.bcs == 1);
@@ -257,7 +257,7 @@ __global__ void __launch_bounds__(256, MINB) bgemm_dmma_kernel(const GemmProb* _
     for (int j = 0; j < NT; ++j) acc[i][j][0] = acc[i][j][1] = 0.0;
   // per-thread element (i0 + q di, k0 + kq0 + q dk) of the A tile, (j0 + q dj, k0 + kb0 + q dkb) of B:
   // consecutive threads walk the operand's unit-stride dimension (coalesced loads); the tiles
-  // go global -> shared by 8-byte cp.async (zero fill outside the matrix), two stages
+  // go global -> shared by 8-byte cp.async (zero fill outside the matrix)
   int ai0, ak0, adi, adk, bj0, bk0, bdj, bdk;
   if (a_k) { ai0 = tid / DBK; ak0 = tid % DBK; adi = 256 / DBK; adk = 0; }
   else { ai0 = tid % BM; ak0 = tid / BM; adi = 0; adk = 256 / BM; }
@@ -285,17 +285,20 @@ __global__ void __launch_bounds__(256, MINB) bgemm_dmma_kernel(const GemmProb* _
     }
     asm volatile("cp.async.commit_group;\n" ::);
   };
+  // DNS-stage ring, one barrier per k-tile: tile kt + DNS - 1 goes into the buffer of tile
+  // kt - 1, which every warp has finished once it passes this iteration's barrier
   const int nk = (P.k + DBK - 1) / DBK;
-  issue(0, 0);
+#pragma unroll
+  for (int st = 0; st < DNS - 1; ++st) {
+    if (st < nk) issue(st, st);
+    else asm volatile("cp.async.commit_group;\n" ::);
+  }
   for (int kt = 0; kt < nk; ++kt) {
-    const int buf = kt & 1;
-    if (kt + 1 < nk) {
-      issue(kt + 1, buf ^ 1);
-      asm volatile("cp.async.wait_group 1;\n" ::);
-    } else {
-      asm volatile("cp.async.wait_group 0;\n" ::);
-    }
+    const int buf = kt % DNS;
+    asm volatile("cp.async.wait_group %0;\n" ::"n"(DNS - 2));
     __syncthreads();
+    if (kt + DNS - 1 < nk) issue(kt + DNS - 1, (kt + DNS - 1) % DNS);
+    else asm volatile("cp.async.commit_group;\n" ::);
     const double* Aw = As + (buf * BM + wm + g) * DSK + t;
     const double* Bw = Bs + (buf * BN + wn + g) * DSK + t;
 #pragma unroll
@@ -310,7 +313,6 @@ __global__ void __launch_bounds__(256, MINB) bgemm_dmma_kernel(const GemmProb* _
 #pragma unroll
         for (int j = 0; j < NT; ++j) dmma884_(acc[i][j][0], acc[i][j][1], a[i], b[j]);
     }
-    __syncthreads();
   }
 #pragma unroll
   for (int i = 0; i < MT; ++i) {
@@ -332,7 +334,7 @@ __global__ void __launch_bounds__(256, MINB) bgemm_dmma_kernel(const GemmProb* _
 template <int MT, int NT, int MINB>
 static void launch_dmma(const GemmProb* d, int maxm, int maxn, unsigned nb, cudaStream_t s) {
   constexpr int BM = 16 * MT, BN = 32 * NT;
-  const size_t smem = (size_t)2 * (BM + BN) * DSK * sizeof(double);
+  const size_t smem = (size_t)DNS * (BM + BN) * DSK * sizeof(double);
   static bool attr = false;
   if (!attr) {
     CUDA_CHECK(cudaFuncSetAttribute(bgemm_dmma_kernel<MT, NT, MINB>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
