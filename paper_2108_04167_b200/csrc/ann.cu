@@ -283,32 +283,56 @@ void ann_sample_level(const HSSImpl& H, int l, const int64_t* act, const int64_t
 }
 
 // N3: Y_t = K(A_t, C_t) for every node of the level: W[(roff + i) * S + c] = K(act[roff + i], C[q*S + c])
-// (direct differences, as kblock_kernel; columns with C = -1 are zero).  One CTA per (node, 16 rows).
+// (direct differences summed in feature order, as kblock_kernel; columns with C = -1 are zero).
+// One CTA per (node, 32 rows): the rows' features and 64 sampled columns' features at a time are
+// staged in shared memory (odd row stride: conflict-free per-column reads); thread (c, i0) owns
+// column c and rows i0, i0 + 4, ... (8 independent distance chains).
+constexpr int AYR = 32, AYC = 64;
+
 __global__ void __launch_bounds__(256) ann_y_kernel(const SampNode* __restrict__ nodes, const double* __restrict__ F,
                                                     int rp, int r, double neg_inv_2h2, int S,
                                                     const int64_t* __restrict__ act, const int64_t* __restrict__ C,
                                                     double* __restrict__ W) {
   const SampNode N = nodes[blockIdx.y];
-  const int i0 = blockIdx.x * 16;
+  const int i0 = blockIdx.x * AYR;
   if (i0 >= N.rows) return;
-  extern __shared__ double xa[];  // 16 x r
-  const int nr = min(16, N.rows - i0);
-  for (int e = threadIdx.x; e < nr * r; e += blockDim.x) xa[e] = F[act[N.roff + i0 + e / r] * rp + e % r];
-  __syncthreads();
+  const int rs = r | 1;                      // odd stride
+  extern __shared__ double ysm[];
+  double* xa = ysm;                          // AYR x rs
+  double* xc = ysm + AYR * rs;               // AYC x rs
+  const int nr = min(AYR, N.rows - i0);
+  for (int e = threadIdx.x; e < AYR * r; e += blockDim.x) {
+    const int i = e / r, f = e % r;
+    xa[i * rs + f] = (i < nr) ? F[act[N.roff + i0 + i] * rp + f] : 0.0;
+  }
   const int64_t* Cq = C + (int64_t)blockIdx.y * S;
-  for (int e = threadIdx.x; e < nr * S; e += blockDim.x) {
-    const int i = e / S, c = e % S;
-    const int64_t q = Cq[c];
-    double v = 0.0;
-    if (q >= 0) {
-      double d = 0.0;
-      for (int f = 0; f < r; ++f) {
-        const double t = xa[i * r + f] - F[q * rp + f];
-        d = fma(t, t, d);
-      }
-      v = exp(d * neg_inv_2h2);
+  const int c = threadIdx.x % AYC, ib = threadIdx.x / AYC;   // rows ib + 4 u
+  for (int c0 = 0; c0 < S; c0 += AYC) {
+    __syncthreads();
+    for (int e = threadIdx.x; e < AYC * r; e += blockDim.x) {
+      const int cc = e / r, f = e % r;
+      const int64_t q = (c0 + cc < S) ? Cq[c0 + cc] : -1;
+      xc[cc * rs + f] = (q >= 0) ? F[q * rp + f] : 0.0;
     }
-    W[(N.roff + i0 + i) * (int64_t)S + c] = v;
+    __syncthreads();
+    if (c0 + c >= S) continue;
+    const bool valid = Cq[c0 + c] >= 0;
+    double d[AYR / 4];
+#pragma unroll
+    for (int u = 0; u < AYR / 4; ++u) d[u] = 0.0;
+    for (int f = 0; f < r; ++f) {
+      const double xv = xc[c * rs + f];
+#pragma unroll
+      for (int u = 0; u < AYR / 4; ++u) {
+        const double t = xa[(ib + 4 * u) * rs + f] - xv;
+        d[u] = fma(t, t, d[u]);
+      }
+    }
+#pragma unroll
+    for (int u = 0; u < AYR / 4; ++u) {
+      const int i = ib + 4 * u;
+      if (i < nr) W[(N.roff + i0 + i) * (int64_t)S + c0 + c] = valid ? exp(d[u] * neg_inv_2h2) : 0.0;
+    }
   }
 }
 
@@ -322,9 +346,11 @@ void ann_y_level(const HSSImpl& H, int l, const int64_t* act, const int64_t* C, 
     maxr = std::max(maxr, nd.rows);
   }
   auto dsn = upload(sn, s);
-  dim3 grid(ceil_div(maxr, 16), nn);
-  ann_y_kernel<<<grid, 256, 16 * (size_t)H.r * sizeof(double), s>>>(dsn.p, H.Fp.p, H.rp, H.r, -1.0 / (2.0 * H.h * H.h),
-                                                                    H.s, act, C, W);
+  dim3 grid(ceil_div(maxr, AYR), nn);
+  const size_t smem = (size_t)(AYR + AYC) * (H.r | 1) * sizeof(double);
+  if (smem > 48 * 1024)
+    CUDA_CHECK(cudaFuncSetAttribute(ann_y_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+  ann_y_kernel<<<grid, 256, smem, s>>>(dsn.p, H.Fp.p, H.rp, H.r, -1.0 / (2.0 * H.h * H.h), H.s, act, C, W);
   LAUNCH_CHECK();
   CUDA_CHECK(cudaStreamSynchronize(s));
 }
