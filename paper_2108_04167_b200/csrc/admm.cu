@@ -91,6 +91,8 @@ __global__ void __launch_bounds__(256) admm_epilogue_kernel(EpiArgs A, const int
                                                             double* __restrict__ part, double* __restrict__ out,
                                                             unsigned* __restrict__ counter) {
   extern __shared__ double cs[];  // chunk sums: nch x nC
+  pdl_trigger();
+  pdl_wait();
   const int leaf = leaves ? leaves[blockIdx.x] : (int)blockIdx.x;
   const int64_t i0 = leaf_lo[leaf], i1 = leaf_lo[leaf + 1];
   const int nch = (int)((i1 - i0 + 31) / 32);
@@ -470,8 +472,8 @@ AdmmResult admm_train_impl(const ULVImpl& F, const double* y_orig, const std::ve
   auto iteration = [&](cudaStream_t st) {
     if (!bottom) {
       ulv_solve_tree(F, ws, st);
-      admm_epilogue_kernel<<<nleaf, 256, epi_smem, st>>>(EA, H.leaf_lo.p, nullptr, nleaf, part.p, epi_out, counter.p);
-      LAUNCH_CHECK();
+      launch_pdl(admm_epilogue_kernel, dim3(nleaf), dim3(256), epi_smem, st, EA, H.leaf_lo.p, (const int*)nullptr,
+                 nleaf, part.p, epi_out, counter.p);
       return;
     }
     std::vector<SolveStep> top;

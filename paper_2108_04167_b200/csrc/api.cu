@@ -42,6 +42,11 @@ static void pool_reserve(int64_t n, int r, int s_cols, cudaStream_t st) {
   }
 }
 
+bool pdl_enabled() {
+  static const bool on = [] { const char* e = getenv("SVMHSS_PDL"); return !(e && e[0] == '0'); }();
+  return on;
+}
+
 void set_last_error(const std::string& s) { g_last_error = s; }
 
 double PhaseTrace::now_ms() {

@@ -13,7 +13,9 @@
 namespace svmhss {
 
 // one row's lane-partial dot product: lane sums j = lane, lane + 32, ... in order
-template <int NR, int RU>
+// QN loads per row in flight (lane-strided, 32 QN columns per pass); the per-element order
+// (j = lane, lane + 32, ... sequentially) does not depend on RU or QN
+template <int NR, int RU, int QN = 4>
 __device__ __forceinline__ void row_partials(const double* const (&Mr)[RU], int R, const double* __restrict__ vsh,
                                              double (&acc)[RU][NR]) {
   const int lane = threadIdx.x & 31;
@@ -22,16 +24,16 @@ __device__ __forceinline__ void row_partials(const double* const (&Mr)[RU], int 
 #pragma unroll
     for (int c = 0; c < NR; ++c) acc[u][c] = 0.0;
   int j = lane;
-  for (; j + 96 < R; j += 128) {
-    double m[RU][4];
+  for (; j + 32 * (QN - 1) < R; j += 32 * QN) {
+    double m[RU][QN];
 #pragma unroll
     for (int u = 0; u < RU; ++u)
 #pragma unroll
-      for (int q = 0; q < 4; ++q) m[u][q] = Mr[u][j + 32 * q];
+      for (int q = 0; q < QN; ++q) m[u][q] = Mr[u][j + 32 * q];
 #pragma unroll
     for (int u = 0; u < RU; ++u)
 #pragma unroll
-      for (int q = 0; q < 4; ++q)
+      for (int q = 0; q < QN; ++q)
 #pragma unroll
         for (int c = 0; c < NR; ++c) acc[u][c] = fma(m[u][q], vsh[(j + 32 * q) * NR + c], acc[u][c]);
   }
@@ -60,13 +62,43 @@ __device__ __forceinline__ void row_store(double (&acc)[NR], int i, int k, int64
   }
 }
 
-// rows i0 + wid, i0 + wid + nw, ... < i1; two rows per warp in flight (8 loads per lane)
+// rows i0 + wid, i0 + wid + nw, ... < i1; two rows per warp in flight (8 loads per lane).
+// mode (NR <= 2): 1 = four rows x 4 loads, 2 = two rows x 8 loads, 3 = one row x 16 loads,
+// 4 = four rows x 8 loads; the results are identical for every mode.
 template <int NR>
 __device__ __forceinline__ void fwd_rows(const double* __restrict__ M, int R, const double* __restrict__ vsh,
                                          int i0, int i1, int wid, int nw, int k, int64_t koff, int64_t yoff,
                                          double* __restrict__ out_up, double* __restrict__ out_yr,
-                                         bool four = false) {
+                                         int mode = 0) {
   int i = i0 + wid;
+  const bool four = mode == 1;
+  if (NR <= 2 && mode == 2) {
+    for (; i + nw < i1; i += 2 * nw) {
+      const double* Mr[2] = {M + (int64_t)i * R, M + (int64_t)(i + nw) * R};
+      double acc[2][NR];
+      row_partials<NR, 2, 8>(Mr, R, vsh, acc);
+      row_store<NR>(acc[0], i, k, koff, yoff, out_up, out_yr);
+      row_store<NR>(acc[1], i + nw, k, koff, yoff, out_up, out_yr);
+    }
+  }
+  if (NR <= 2 && mode == 3) {
+    for (; i < i1; i += nw) {
+      const double* Mr[1] = {M + (int64_t)i * R};
+      double acc[1][NR];
+      row_partials<NR, 1, 16>(Mr, R, vsh, acc);
+      row_store<NR>(acc[0], i, k, koff, yoff, out_up, out_yr);
+    }
+  }
+  if (NR <= 2 && mode == 4) {
+    for (; i + 3 * nw < i1; i += 4 * nw) {
+      const double* Mr[4] = {M + (int64_t)i * R, M + (int64_t)(i + nw) * R, M + (int64_t)(i + 2 * nw) * R,
+                             M + (int64_t)(i + 3 * nw) * R};
+      double acc[4][NR];
+      row_partials<NR, 4, 8>(Mr, R, vsh, acc);
+#pragma unroll
+      for (int u = 0; u < 4; ++u) row_store<NR>(acc[u], i + u * nw, k, koff, yoff, out_up, out_yr);
+    }
+  }
   if (NR <= 2 && four) {  // four rows in flight (16 independent loads per lane)
     for (; i + 3 * nw < i1; i += 4 * nw) {
       const double* Mr[4] = {M + (int64_t)i * R, M + (int64_t)(i + nw) * R, M + (int64_t)(i + 2 * nw) * R,

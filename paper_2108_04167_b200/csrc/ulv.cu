@@ -404,7 +404,8 @@ void ulv_factor_impl(ULVImpl& F, cudaStream_t s) {
     // rows per CTA: enough CTAs to fill the chip (>= ~8 per SM), at most 32
     int64_t rows = 0;
     for (auto& nd : sn) if (!(l == L && nd.pt)) rows += nd.R;
-    int ch = 32;
+    static const int chmax = [] { const char* e = getenv("SVMHSS_FWD_CH"); return e ? atoi(e) : 32; }();
+    int ch = chmax;
     while (ch > 8 && rows / ch < 148 * 8) ch /= 2;
     F_l.ch = ch;
     std::vector<SolveWork> wk, bk;
@@ -452,7 +453,7 @@ template <int NR>
 __device__ __forceinline__ void fwd_item(const SolveNode* __restrict__ nodes, SolveWork wk, int ch,
                                          const double* __restrict__ M, const double* __restrict__ in,
                                          double* __restrict__ out_up, double* __restrict__ out_yr, double* vsh,
-                                         bool four = false) {
+                                         int four = 0) {
   const SolveNode N = nodes[wk.node];
   const int R = N.R, tid = threadIdx.x;
   const int i0 = wk.chunk * ch, i1 = min(R, i0 + ch);
@@ -474,7 +475,20 @@ __global__ void __launch_bounds__(256) ulv_fwd_kernel(const SolveNode* __restric
                                                       double* __restrict__ out_up,
                                                       double* __restrict__ out_yr, int four) {
   extern __shared__ double vsh[];  // R * NR
-  fwd_item<NR>(nodes, work[blockIdx.x], ch, M, in, out_up, out_yr, vsh, four != 0);
+  pdl_trigger();
+  if (four & 2) {  // L2 prefetch of this CTA's rows of M (static data) ahead of the dependency wait
+    const SolveWork wk = work[blockIdx.x];
+    const SolveNode N = nodes[wk.node];
+    if (!N.pt) {
+      const int i0 = wk.chunk * ch, i1 = min(N.R, i0 + ch);
+      const char* base = reinterpret_cast<const char*>(M + N.moff + (int64_t)i0 * N.R);
+      const int64_t bytes = (int64_t)(i1 - i0) * N.R * 8;
+      for (int64_t o = (int64_t)threadIdx.x * 128; o < bytes; o += 256 * 128)
+        asm volatile("prefetch.global.L2 [%0];\n" ::"l"(base + o));
+    }
+  }
+  pdl_wait();
+  fwd_item<NR>(nodes, work[blockIdx.x], ch, M, in, out_up, out_yr, vsh, four >> 2);
 }
 
 template <int NR>
@@ -484,6 +498,8 @@ __global__ void __launch_bounds__(kBW * 32) ulv_bwd_kernel(const SolveNode* __re
                                                            const double* __restrict__ in_s,
                                                            const double* __restrict__ in_r,
                                                            double* __restrict__ out) {
+  pdl_trigger();
+  pdl_wait();
   const SolveWork wk = work[blockIdx.x];
   const SolveNode N = nodes[wk.node];
   const int R = N.R, tid = threadIdx.x;
@@ -602,6 +618,8 @@ __global__ void __launch_bounds__(kBW * 32) ulv_bwd_split_kernel(const SolveNode
                                                                  double* __restrict__ out,
                                                                  double* __restrict__ part,
                                                                  unsigned* __restrict__ cnt) {
+  pdl_trigger();
+  pdl_wait();
   bwd_split_item<NR>(nodes, work[blockIdx.x], blockIdx.x, M, in_s, in_r, out, part, cnt);
 }
 
@@ -649,6 +667,8 @@ __global__ void __launch_bounds__(256) ulv_top_kernel(const TopLv* __restrict__ 
 template <int NR>
 __global__ void leaf_pt_copy_kernel(const int64_t* __restrict__ map, int64_t n, int bwd,
                                     const double* __restrict__ src, double* __restrict__ dst) {
+  pdl_trigger();
+  pdl_wait();
   const int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
   if (e >= n * NR) return;
   const int64_t p = e / NR;
@@ -732,10 +752,18 @@ static void fwd_level(const ULVImpl& F, SolveWS& ws, int l, const SolveWork* wor
   const auto& lv = F.lv[l];
   if (nwork <= 0) return;
   const size_t sm = (size_t)lv.maxR * NR * sizeof(double);
-  // four rows in flight per warp (A/B on one box: 673 vs 657 it/s); SVMHSS_FWD_ROWS=2 for two
-  static const int four = [] { const char* e = getenv("SVMHSS_FWD_ROWS"); return (e && e[0] == '2') ? 0 : 1; }();
-  ulv_fwd_kernel<NR><<<nwork, 256, sm, s>>>(lv.nodes.p, work, lv.ch, lv.M.p, ws.fin[l], l > 0 ? ws.fin[l - 1] : nullptr,
-                                            ws.yr[l], four);
+  // load pattern of the forward GEMV: SVMHSS_FWD_MODE (solve_dev.cuh fwd_rows); SVMHSS_FWD_ROWS=2: mode 0
+  static const int four = [] {
+    const char* e = getenv("SVMHSS_FWD_ROWS");
+    const char* p = getenv("SVMHSS_FWD_PREFETCH");
+    const char* m = getenv("SVMHSS_FWD_MODE");
+    // default: one row x 16 loads per warp (4 KB contiguous per round trip); A/B at config 3:
+    // 1.439 ms/iteration vs 1.543 (four rows x 4 loads) and 1.501 (two rows x 4), same results
+    const int mode = m ? atoi(m) : ((e && e[0] == '2') ? 0 : 3);
+    return (mode << 2) | ((p && p[0] == '1') ? 2 : 0);
+  }();
+  launch_pdl(ulv_fwd_kernel<NR>, dim3(nwork), dim3(256), sm, s, lv.nodes.p, work, lv.ch, lv.M.p, ws.fin[l],
+             l > 0 ? ws.fin[l - 1] : nullptr, ws.yr[l], four);
   g_launches.fetch_add(1);
 }
 
@@ -744,14 +772,14 @@ static void bwd_level(const ULVImpl& F, SolveWS& ws, int l, const SolveWork* wor
   const auto& lv = F.lv[l];
   if (nwork <= 0) return;
   if (lv.split) {
-    ulv_bwd_split_kernel<NR><<<nwork, kBW * 32, 0, s>>>(lv.nodes.p, work, lv.M.p, l > 0 ? ws.xout[l - 1] : nullptr,
-                                                        ws.yr[l], ws.xout[l], ws.bpart[l], ws.bcnt[l]);
+    launch_pdl(ulv_bwd_split_kernel<NR>, dim3(nwork), dim3(kBW * 32), 0, s, lv.nodes.p, work, lv.M.p,
+               l > 0 ? ws.xout[l - 1] : nullptr, ws.yr[l], ws.xout[l], ws.bpart[l], ws.bcnt[l]);
     g_launches.fetch_add(1);
     return;
   }
   const size_t sm = ((size_t)lv.maxR + (size_t)kBW * kCW) * NR * sizeof(double);
-  ulv_bwd_kernel<NR><<<nwork, kBW * 32, sm, s>>>(lv.nodes.p, work, lv.M.p, l > 0 ? ws.xout[l - 1] : nullptr, ws.yr[l],
-                                                 ws.xout[l]);
+  launch_pdl(ulv_bwd_kernel<NR>, dim3(nwork), dim3(kBW * 32), sm, s, lv.nodes.p, work, lv.M.p,
+             l > 0 ? ws.xout[l - 1] : nullptr, ws.yr[l], ws.xout[l]);
   g_launches.fetch_add(1);
 }
 
@@ -774,7 +802,8 @@ static void run_step(const ULVImpl& F, SolveWS& ws, const SolveStep& st, cudaStr
         const auto& lv = F.lv[l];
         if (!lv.allpt) {
           if (l == L && F.nleafpt > 0 && !ws.fused_leaf_io) {
-            leaf_pt_copy_kernel<NR><<<ceil_div(n * NR, 256), 256, 0, s>>>(F.ptmap.p, n, 0, ws.fin[L], ws.fin[L - 1]);
+            launch_pdl(leaf_pt_copy_kernel<NR>, dim3(ceil_div(n * NR, 256)), dim3(256), 0, s, F.ptmap.p, n, 0,
+                       ws.fin[L], ws.fin[L - 1]);
             g_launches.fetch_add(1);
           }
           fwd_level<NR>(F, ws, l, lv.work.p, lv.nwork, s);
@@ -788,7 +817,8 @@ static void run_step(const ULVImpl& F, SolveWS& ws, const SolveStep& st, cudaStr
         if (lv.allpt) continue;
         bwd_level<NR>(F, ws, l, lv.bwork.p, lv.nbwork, s);
         if (l == L && F.nleafpt > 0 && !ws.fused_leaf_io) {
-          leaf_pt_copy_kernel<NR><<<ceil_div(n * NR, 256), 256, 0, s>>>(F.ptmap.p, n, 1, ws.xout[L - 1], ws.xout[L]);
+          launch_pdl(leaf_pt_copy_kernel<NR>, dim3(ceil_div(n * NR, 256)), dim3(256), 0, s, F.ptmap.p, n, 1,
+                     ws.xout[L - 1], ws.xout[L]);
           g_launches.fetch_add(1);
         }
       }
