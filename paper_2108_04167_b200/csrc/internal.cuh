@@ -221,7 +221,9 @@ struct TopLv {
   double* xout;
   double* bpart;
   unsigned* bcnt;
-  int nwork, nbwork, ch, pad;
+  unsigned* fdone;   // dataflow: per node, finished forward chunks
+  unsigned* bdone;   // dataflow: per node, finalized backward column chunks
+  int nwork, nbwork, ch, nnodes;
 };
 
 // Solve workspace for nrhs right-hand sides (tree order in/out, this rank's points).
@@ -247,6 +249,7 @@ struct SolveWS {
   int lt = -1;
   DevBuf<TopLv> top;
   DevBuf<unsigned> topbar;
+  int top_mode = 0, top_items = 0;   // top levels: 1 grid barriers, 2 dataflow queue
 };
 void solve_ws_alloc(const ULVImpl& F, int nrhs, SolveWS& ws);
 // x_tree = (K~+beta I)^-1 b_tree.  b is read from ws.fin[L] and x written to ws.xout[L].

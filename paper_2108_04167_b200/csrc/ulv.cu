@@ -449,7 +449,11 @@ void ulv_factor_impl(ULVImpl& F, cudaStream_t s) {
 // Work-item bodies shared by the per-level kernels and the cooperative top-levels kernel
 // (same arithmetic either way).  All threads of the CTA take part; they end with a CTA barrier
 // so a CTA may run several items back to back.
-template <int NR>
+// ld(): inputs written by other CTAs of the same launch (dataflow top kernel) are read L2-coherent
+template <bool CG>
+__device__ __forceinline__ double ld_in(const double* p) { return CG ? __ldcg(p) : *p; }
+
+template <int NR, bool CG = false>
 __device__ __forceinline__ void fwd_item(const SolveNode* __restrict__ nodes, SolveWork wk, int ch,
                                          const double* __restrict__ M, const double* __restrict__ in,
                                          double* __restrict__ out_up, double* __restrict__ out_yr, double* vsh,
@@ -458,9 +462,9 @@ __device__ __forceinline__ void fwd_item(const SolveNode* __restrict__ nodes, So
   const int R = N.R, tid = threadIdx.x;
   const int i0 = wk.chunk * ch, i1 = min(R, i0 + ch);
   if (N.pt) {  // identity operator
-    for (int e = tid; e < (i1 - i0) * NR; e += 256) out_up[(N.koff + i0) * NR + e] = in[(N.roff + i0) * NR + e];
+    for (int e = tid; e < (i1 - i0) * NR; e += 256) out_up[(N.koff + i0) * NR + e] = ld_in<CG>(in + (N.roff + i0) * NR + e);
   } else {
-    for (int e = tid; e < R * NR; e += 256) vsh[e] = in[N.roff * NR + e];
+    for (int e = tid; e < R * NR; e += 256) vsh[e] = ld_in<CG>(in + N.roff * NR + e);
     __syncthreads();
     fwd_rows<NR>(M + N.moff, R, vsh, i0, i1, tid >> 5, 8, N.k, N.koff, N.yoff, out_up, out_yr, four);
   }
@@ -523,11 +527,12 @@ __global__ void __launch_bounds__(kBW * 32) ulv_bwd_kernel(const SolveNode* __re
 // i0 + w, i0 + w + kBW, ... in order; warps in order) into a partial slab, and the last CTA of
 // (node, cc) adds the row-chunk partials in rc order.  Used for levels l <= kSplitMaxLevel
 // (l < L-1), a rule of the global tree, so results stay P-invariant.
-template <int NR>
+template <int NR, bool CG = false>
 __device__ __forceinline__ void bwd_split_item(const SolveNode* __restrict__ nodes, SolveWork wk, int item,
                                                const double* __restrict__ M, const double* __restrict__ in_s,
                                                const double* __restrict__ in_r, double* __restrict__ out,
-                                               double* __restrict__ part, unsigned* __restrict__ cnt) {
+                                               double* __restrict__ part, unsigned* __restrict__ cnt,
+                                               unsigned* __restrict__ done = nullptr) {
   const SolveNode N = nodes[wk.node];
   const int R = N.R, tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
   const int nrc = (R + kRB - 1) / kRB, cc = wk.chunk / nrc, rc = wk.chunk % nrc;
@@ -535,7 +540,12 @@ __device__ __forceinline__ void bwd_split_item(const SolveNode* __restrict__ nod
   if (N.pt) {  // identity operator (row chunk 0 copies)
     if (rc == 0) {
       const int j1 = min(R, j0 + kCW);
-      for (int e = tid; e < (j1 - j0) * NR; e += kBW * 32) out[(N.roff + j0) * NR + e] = in_s[(N.koff + j0) * NR + e];
+      for (int e = tid; e < (j1 - j0) * NR; e += kBW * 32) out[(N.roff + j0) * NR + e] = ld_in<CG>(in_s + (N.koff + j0) * NR + e);
+      if (done) {
+        __threadfence();
+        __syncthreads();
+        if (tid == 0) atomicAdd(done + wk.node, 1u);
+      }
     }
     __syncthreads();
     return;
@@ -544,7 +554,7 @@ __device__ __forceinline__ void bwd_split_item(const SolveNode* __restrict__ nod
   __shared__ double red[kBW * kCW * NR];
   for (int e = tid; e < (i1 - i0) * NR; e += kBW * 32) {
     const int i = i0 + e / NR, c = e % NR;
-    ush[e] = (i < N.k) ? in_s[(N.koff + i) * NR + c] : in_r[(N.yoff + i - N.k) * NR + c];
+    ush[e] = (i < N.k) ? ld_in<CG>(in_s + (N.koff + i) * NR + c) : ld_in<CG>(in_r + (N.yoff + i - N.k) * NR + c);
   }
   __syncthreads();
   const int ja = j0 + lane, jb = j0 + 32 + lane;
@@ -601,10 +611,15 @@ __device__ __forceinline__ void bwd_split_item(const SolveNode* __restrict__ nod
       const int jj = e / NR;
       if (j0 + jj >= R) continue;
       double t = 0.0;
-      for (int q = 0; q < nrc; ++q) t += part[((int64_t)(g + q) * kCW) * NR + e];
+      for (int q = 0; q < nrc; ++q) t += ld_in<CG>(part + ((int64_t)(g + q) * kCW) * NR + e);
       out[(N.roff + j0) * NR + e] = t;
     }
     if (tid == 0) cnt[g] = 0u;
+    if (done) {  // dataflow: this (node, column chunk) is final
+      __threadfence();
+      __syncthreads();
+      if (tid == 0) atomicAdd(done + wk.node, 1u);
+    }
   }
   __syncthreads();
 }
@@ -663,6 +678,85 @@ __global__ void __launch_bounds__(256) ulv_top_kernel(const TopLv* __restrict__ 
   }
 }
 
+// Dataflow variant of the top levels: one persistent launch walks a queue of work items (forward
+// items of levels lt..0, then backward items of levels 0..lt; every dependency points to an
+// earlier item, so the CTA holding the oldest unfinished item can always proceed).  Instead of a
+// grid barrier per level, an item waits only for what it reads: a forward item of node t at level
+// l < lt for all forward items of t's two children (fdone[l+1][child] == their chunk count), a
+// backward item for all column chunks of its parent (bdone[l-1][parent]) or, at the root, for the
+// root's forward items.  Same item bodies (same arithmetic) as the per-level kernels; inputs
+// written in this launch are read L2-coherent (ld.global.cg).  dq[0] = queue head, dq[1] = exits.
+__device__ __forceinline__ void df_wait(const unsigned* flag, unsigned target) {
+  if (threadIdx.x == 0) {
+    while (true) {
+      unsigned v;
+      asm volatile("ld.acquire.gpu.global.u32 %0, [%1];\n" : "=r"(v) : "l"(flag) : "memory");
+      if (v >= target) break;
+      __nanosleep(32);
+    }
+    __threadfence();
+  }
+  __syncthreads();
+}
+
+template <int NR>
+__global__ void __launch_bounds__(256) ulv_top_df_kernel(const TopLv* __restrict__ lv, int lt, int nitems,
+                                                         unsigned* __restrict__ dq) {
+  extern __shared__ double vsh[];
+  __shared__ int s_item;
+  pdl_trigger();
+  pdl_wait();
+  int nf = 0;
+  for (int l = 0; l <= lt; ++l) nf += lv[l].nwork;
+  while (true) {
+    if (threadIdx.x == 0) s_item = (int)atomicAdd(&dq[0], 1u);
+    __syncthreads();
+    int q = s_item;
+    __syncthreads();
+    if (q >= nitems) break;
+    if (q < nf) {  // forward: levels lt, lt-1, ..., 0
+      int l = lt;
+      while (q >= lv[l].nwork) { q -= lv[l].nwork; --l; }
+      const TopLv T = lv[l];
+      const SolveWork wk = T.work[q];
+      if (l < lt) {
+        const TopLv C = lv[l + 1];
+        for (int c = 0; c < 2; ++c) {
+          const int ch = 2 * wk.node + c;
+          df_wait(C.fdone + ch, (unsigned)((C.nodes[ch].R + C.ch - 1) / C.ch));
+        }
+      }
+      fwd_item<NR, true>(T.nodes, wk, T.ch, T.M, T.fin, T.fout, T.yr, vsh);
+      __threadfence();
+      __syncthreads();
+      if (threadIdx.x == 0) atomicAdd(T.fdone + wk.node, 1u);
+    } else {       // backward: levels 0, 1, ..., lt
+      q -= nf;
+      int l = 0;
+      while (q >= lv[l].nbwork) { q -= lv[l].nbwork; ++l; }
+      const TopLv T = lv[l];
+      const SolveWork wk = T.bwork[q];
+      if (l == 0) {
+        df_wait(T.fdone + wk.node, (unsigned)((T.nodes[wk.node].R + T.ch - 1) / T.ch));
+      } else {
+        const TopLv Pp = lv[l - 1];
+        const int pn = wk.node >> 1;
+        df_wait(Pp.bdone + pn, (unsigned)((Pp.nodes[pn].R + kCW - 1) / kCW));
+      }
+      bwd_split_item<NR, true>(T.nodes, wk, q, T.M, T.xin, T.yr, T.xout, T.bpart, T.bcnt, T.bdone);
+    }
+  }
+  // the last CTA out resets the queue and the level counters for the next launch
+  __shared__ bool last;
+  if (threadIdx.x == 0) last = (atomicAdd(&dq[1], 1u) == gridDim.x - 1);
+  __syncthreads();
+  if (last) {
+    for (int l = 0; l <= lt; ++l)
+      for (int i = threadIdx.x; i < lv[l].nnodes; i += blockDim.x) { lv[l].fdone[i] = 0u; lv[l].bdone[i] = 0u; }
+    if (threadIdx.x == 0) { dq[0] = 0u; dq[1] = 0u; }
+  }
+}
+
 // pass-through leaves: fwd  fin_{L-1}[map[p]] = fin_L[p];  bwd  xout_L[p] = xout_{L-1}[map[p]]
 template <int NR>
 __global__ void leaf_pt_copy_kernel(const int64_t* __restrict__ map, int64_t n, int bwd,
@@ -701,6 +795,8 @@ void solve_ws_alloc(const ULVImpl& F, int nrhs, SolveWS& ws) {
   for (int l = 1; l <= L; ++l) ws.xout[l] = F.lv[l].allpt ? ws.xout[l - 1] : mk(F.lv[l].sumR);
   ws.bpart.assign(L + 1, nullptr);
   ws.lt = -1;
+  ws.top_items = 0;
+  ws.top_mode = 0;
   ws.bcnt.assign(L + 1, nullptr);
   for (int l = 0; l <= L; ++l)
     if (F.lv[l].split && F.lv[l].nbwork > 0) {
@@ -716,7 +812,10 @@ void solve_ws_alloc(const ULVImpl& F, int nrhs, SolveWS& ws) {
   int lt = std::min(kSplitMaxLevel, L - 2);
   if (H.sh.on()) lt = std::min(lt, H.sh.lg - 1);
   const char* env = getenv("SVMHSS_TOP_MERGE");
-  if (!(env && env[0] == '1')) lt = -1;
+  const int tmode = env ? atoi(env) : 0;   // 0 per-level kernels, 1 grid barriers, 2 dataflow
+  if (tmode != 1 && tmode != 2) lt = -1;
+  for (int l = 0; l <= lt && lt >= 0; ++l)
+    if (F.lv[l].allpt) lt = -1;   // dataflow counters assume every top level has its own items
   if (lt >= 1) {
     std::vector<TopLv> tv(lt + 1);
     for (int l = 0; l <= lt; ++l) {
@@ -737,8 +836,16 @@ void solve_ws_alloc(const ULVImpl& F, int nrhs, SolveWS& ws) {
       T.nwork = lv.allpt ? 0 : lv.nwork;
       T.nbwork = lv.allpt ? 0 : lv.nbwork;
       T.ch = lv.ch;
+      T.nnodes = lv.nnodes;
+      ws.cnt_own.emplace_back((size_t)std::max(1, 2 * lv.nnodes));
+      CUDA_CHECK(cudaMemsetAsync(ws.cnt_own.back().p, 0, (size_t)std::max(1, 2 * lv.nnodes) * sizeof(unsigned),
+                                 g_alloc_stream));
+      T.fdone = ws.cnt_own.back().p;
+      T.bdone = T.fdone + lv.nnodes;
       tv[l] = T;
+      ws.top_items += T.nwork + T.nbwork;
     }
+    ws.top_mode = tmode;
     ws.top = upload(tv, g_alloc_stream);
     ws.topbar.alloc(2);
     CUDA_CHECK(cudaMemsetAsync(ws.topbar.p, 0, 2 * sizeof(unsigned), g_alloc_stream));
@@ -827,6 +934,26 @@ static void run_step(const ULVImpl& F, SolveWS& ws, const SolveStep& st, cudaStr
     case SolveStep::BWD_LIST: bwd_level<NR>(F, ws, st.a, st.work, st.nwork, s); break;
     case SolveStep::EXCHANGE: if (H.sh.on()) exchange_step<NR>(F, ws, s); break;
     case SolveStep::TOP: {
+      if (ws.top_mode == 2) {
+        int maxR = 0;
+        for (int l = 0; l <= ws.lt; ++l) maxR = std::max(maxR, F.lv[l].maxR);
+        const size_t sm = (size_t)maxR * NR * sizeof(double);
+        static int nsm = 0;
+        if (!nsm) {
+          int dev = 0;
+          CUDA_CHECK(cudaGetDevice(&dev));
+          CUDA_CHECK(cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev));
+        }
+        if (sm > 48 * 1024)
+          CUDA_CHECK(cudaFuncSetAttribute(ulv_top_df_kernel<NR>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm));
+        int per_sm = 0;
+        CUDA_CHECK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, ulv_top_df_kernel<NR>, 256, sm));
+        const int grid = std::max(1, std::min(ws.top_items, nsm * std::max(1, per_sm)));
+        launch_pdl(ulv_top_df_kernel<NR>, dim3(grid), dim3(256), sm, s, (const TopLv*)ws.top.p, ws.lt,
+                   ws.top_items, ws.topbar.p);
+        g_launches.fetch_add(1);
+        break;
+      }
       int maxR = 0, items = 1;
       for (int l = 0; l <= ws.lt; ++l) {
         maxR = std::max(maxR, F.lv[l].maxR);

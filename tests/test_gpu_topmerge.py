@@ -1,6 +1,7 @@
-"""The optional cooperative top-levels sweep (SVMHSS_TOP_MERGE=1: levels 0..5 of both ULV sweeps
-in one launch with grid barriers) must give bitwise the same solve and ADMM iterates as the
-per-level kernels: it runs the same item bodies."""
+"""The optional top-levels sweeps (levels 0..5 of both ULV sweeps in one launch: SVMHSS_TOP_MERGE=1
+with grid barriers between levels, =2 as a dataflow queue with per-node dependency counters) must
+give bitwise the same solve and ADMM iterates as the per-level kernels: they run the same item
+bodies."""
 import os
 
 import numpy as np
@@ -13,7 +14,7 @@ pytestmark = pytest.mark.gpu
 
 def _run(P, F, y, cfg, merge):
     import torch
-    os.environ["SVMHSS_TOP_MERGE"] = "1" if merge else "0"
+    os.environ["SVMHSS_TOP_MERGE"] = str(merge)
     try:
         H = P.hss_build(torch.from_numpy(F).cuda(), cfg["h"], leaf_size=cfg["leaf"], rel_tol=cfg["rel_tol"],
                         max_rank=cfg["cap"], oversample=cfg["s"] - cfg["cap"], omega_seed=cfg["seed_omega"],
@@ -27,11 +28,12 @@ def _run(P, F, y, cfg, merge):
         os.environ.pop("SVMHSS_TOP_MERGE", None)
 
 
+@pytest.mark.parametrize("mode", [1, 2])
 @pytest.mark.parametrize("n", [5000, 20000])
-def test_top_merge_bitwise(gpu_lib, n):
+def test_top_merge_bitwise(gpu_lib, n, mode):
     cfg = datagen.get_config(3)
     F, y, _, _ = datagen.generate(3, n=n, n_test=0)
-    a = _run(gpu_lib, F, y, cfg, True)
-    b = _run(gpu_lib, F, y, cfg, False)
+    a = _run(gpu_lib, F, y, cfg, mode)
+    b = _run(gpu_lib, F, y, cfg, 0)
     for u, v in zip(a, b):
         assert np.array_equal(u, v)
