@@ -113,8 +113,17 @@ __device__ __forceinline__ void bulk_g2s(void* dst, const void* src, unsigned by
 // Omega ~50x more often than this).  The operand ring runs continuously across tiles (global
 // step counter G): the prefetch of a tile's first step overlaps the previous tile's epilogue.
 // Requires co-residency of the grid: launched cooperatively.
+__device__ __forceinline__ unsigned long long gtimer() {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
+  return t;
+}
+
 template <int BJ, int NT>
-__global__ void __launch_bounds__(512, 1) kmm_kernel(KmmArgs a, int SA, unsigned* gbar) {
+__global__ void __launch_bounds__(512, 1) kmm_kernel(KmmArgs a, int SA, unsigned* gbar,
+                                                     unsigned long long* probe) {
+  const unsigned long long t_start = probe ? gtimer() : 0ull;
+  unsigned long long t_wait = 0ull;
   constexpr int NCH = 16 * NT, SW = NCH + 4, SE = BJ + 4, HQ = BJ / 16;  // n-tiles of distance per warp
   extern __shared__ __align__(128) double smem[];
   double* Fa_s = smem;                       // 64 x SA
@@ -287,14 +296,21 @@ __global__ void __launch_bounds__(512, 1) kmm_kernel(KmmArgs a, int SA, unsigned
     if (it + 1 < niter) {
       __syncthreads();
       if (tid == 0) {
+        const unsigned long long t0 = probe ? gtimer() : 0ull;
         unsigned* bar = gbar + blockIdx.y;
         __threadfence();
         atomicAdd(bar, 1u);
         const unsigned target = (unsigned)((it + 1) * gridDim.x);
         while (atomicAdd(bar, 0u) < target) __nanosleep(200);
+        if (probe) t_wait += gtimer() - t0;
       }
       __syncthreads();
     }
+  }
+  if (probe && tid == 0) {  // diagnostics (SVMHSS_KMM_PROBE=1): barrier wait and total time per CTA
+    const int b = blockIdx.y * gridDim.x + blockIdx.x;
+    probe[2 * b] = t_wait;
+    probe[2 * b + 1] = gtimer() - t_start;
   }
 }
 
@@ -338,8 +354,20 @@ static void launch_kmm(const KmmArgs& a, int SA, cudaStream_t s) {
   at[0].val.cooperative = 1;
   cfg.attrs = at;
   cfg.numAttrs = 1;
-  CUDA_CHECK(cudaLaunchKernelEx(&cfg, kmm_kernel<BJ, NT>, a, SA, gbar.p));
+  static const bool probe_on = [] { const char* e = getenv("SVMHSS_KMM_PROBE"); return e && e[0] == '1'; }();
+  const int nb = (int)gx * nchunk;
+  DevBuf<unsigned long long> probe(probe_on ? 2 * (size_t)nb : 0);
+  CUDA_CHECK(cudaLaunchKernelEx(&cfg, kmm_kernel<BJ, NT>, a, SA, gbar.p, probe_on ? probe.p : (unsigned long long*)nullptr));
   LAUNCH_CHECK();
+  if (probe_on) {
+    std::vector<unsigned long long> h(2 * (size_t)nb);
+    d2h(h.data(), probe.p, h.size(), s);
+    CUDA_CHECK(cudaStreamSynchronize(s));
+    double w = 0, tmax = 0, wmax = 0;
+    for (int b = 0; b < nb; ++b) { w += h[2 * b]; tmax = std::max(tmax, (double)h[2 * b + 1]); wmax = std::max(wmax, (double)h[2 * b]); }
+    fprintf(stderr, "[kmm probe] na=%lld nb=%lld grid=%dx%d: mean barrier wait %.3f ms (max %.3f) of %.3f ms\n",
+            (long long)a.na, (long long)a.nb, (int)gx, nchunk, w / nb / 1e6, wmax / 1e6, tmax / 1e6);
+  }
 }
 
 void kernel_matmul(const KmmArgs& a, cudaStream_t s) {
