@@ -206,6 +206,58 @@ __global__ void __launch_bounds__(256) samp_take_kernel(const SampNode* __restri
 // Sampled columns for the nodes [f, e) of level l: C (nn x s tree positions, sorted; entries past
 // the node's count are filled randomly (N2) or -1 if the complement is exhausted).
 // act: row-packed active tree positions of the level (roff per node).
+// Global radix formulation of the per-node column choice (same result as sorting each node's
+// segment): key1 = node << QB | q (q = n for excluded pairs) -> radix sort (node, q); per
+// (node, q) run the minimum d; key2 = bits of dmin (+inf for non-first / excluded) -> stable radix
+// sort by dmin, then stable by node -> every node's segment ordered by (dmin, q).
+__global__ void samp_keys_kernel(const SampNode* __restrict__ nodes, int kappa, const int64_t* __restrict__ act,
+                                 const int64_t* __restrict__ ann_pos, const double* __restrict__ ann_d, int qb,
+                                 int64_t n, uint64_t* __restrict__ key, double* __restrict__ pd) {
+  const SampNode N = nodes[blockIdx.x];
+  const int64_t tot = (int64_t)N.rows * kappa;
+  for (int64_t e = threadIdx.x; e < tot; e += blockDim.x) {
+    const int64_t a = act[N.roff + e / kappa];
+    const int c = (int)(e % kappa);
+    const int64_t q = ann_pos[a * kappa + c];
+    const bool ok = q >= 0 && (q < N.lo || q >= N.hi);
+    pd[N.roff * kappa + e] = ok ? ann_d[a * kappa + c] : INFINITY;
+    key[N.roff * kappa + e] = ((uint64_t)blockIdx.x << qb) | (uint64_t)(ok ? q : n);
+  }
+}
+
+// sorted by (node, q): run starts carry min d of the run; others +inf with q = n (node kept)
+__global__ void samp_runmin_kernel(int64_t np, int qb, int64_t n, const uint64_t* __restrict__ key,
+                                   const double* __restrict__ d, uint64_t* __restrict__ dkey,
+                                   uint64_t* __restrict__ val) {
+  const int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (e >= np) return;
+  const uint64_t k = key[e];
+  const uint64_t mask = (1ull << qb) - 1ull;
+  const bool valid = (int64_t)(k & mask) != n;
+  const bool first = valid && (e == 0 || key[e - 1] != k);
+  double m = INFINITY;
+  if (first) {
+    m = d[e];
+    for (int64_t f = e + 1; f < np && key[f] == k; ++f) m = fmin(m, d[f]);
+  }
+  dkey[e] = __double_as_longlong(m);            // non-negative doubles: bit order = value order
+  val[e] = first ? k : ((k & ~mask) | (uint64_t)n);
+}
+
+__global__ void samp_nodekey_kernel(int64_t np, int qb, const uint64_t* __restrict__ val, unsigned* __restrict__ nk) {
+  const int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (e < np) nk[e] = (unsigned)(val[e] >> qb);
+}
+
+__global__ void samp_q_kernel(int64_t np, int qb, int64_t n, const uint64_t* __restrict__ val, int64_t* __restrict__ q) {
+  const int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (e >= np) return;
+  const int64_t v = (int64_t)(val[e] & ((1ull << qb) - 1ull));
+  q[e] = (v == n) ? INT64_MAX : v;
+}
+
+static int bits_for(uint64_t v) { int b = 0; while (b < 63 && (1ull << b) <= v) ++b; return b; }
+
 void ann_sample_level(const HSSImpl& H, int l, const int64_t* act, const int64_t* ann_pos, const double* ann_d,
                       int kappa, uint64_t seed, int64_t* C, cudaStream_t s) {
   const int f = H.sh.first(l), e = H.sh.last(l), nn = e - f, S = H.s;
@@ -218,32 +270,37 @@ void ann_sample_level(const HSSImpl& H, int l, const int64_t* act, const int64_t
   }
   const int64_t np = std::max<int64_t>(1, sumR * kappa);
   auto dsn = upload(sn, s);
+  const int64_t nall = H.n;
+  const int qb = bits_for((uint64_t)nall);          // q in [0, n], n = excluded
+  const int nb = bits_for((uint64_t)std::max(1, nn - 1));
+  require(qb + nb <= 63, "ann_sample_level: key overflow");
+  DevBuf<uint64_t> k1(np), k2(np), v1(np), v2(np);
   DevBuf<double> d1(np), d2(np);
-  DevBuf<int64_t> q1(np), q2(np);
-  samp_pairs_kernel<<<nn, 256, 0, s>>>(dsn.p, kappa, act, ann_pos, ann_d, d1.p, q1.p);
+  DevBuf<unsigned> nk1(np), nk2(np);
+  DevBuf<int64_t> q1(np);
+  if (sumR * kappa < np) {  // no rows (empty level): keep the tail defined
+    CUDA_CHECK(cudaMemsetAsync(k1.p, 0, np * sizeof(uint64_t), s));
+    CUDA_CHECK(cudaMemsetAsync(d1.p, 0, np * sizeof(double), s));
+  }
+  samp_keys_kernel<<<nn, 256, 0, s>>>(dsn.p, kappa, act, ann_pos, ann_d, qb, nall, k1.p, d1.p);
   LAUNCH_CHECK();
-  std::vector<int> off(nn + 1);
-  for (int q = 0; q < nn; ++q) off[q] = (int)(sn[q].roff * kappa);
-  off[nn] = (int)(sumR * kappa);
-  // segments must tile [off[0], off[nn]) without gaps: they do (row packing)
-  auto doff = upload(off, s);
-  size_t tb = 0, tb2 = 0;
-  CUDA_CHECK(cub::DeviceSegmentedSort::StableSortPairs(nullptr, tb, d1.p, d2.p, q1.p, q2.p, (int)np, nn, doff.p,
-                                                       doff.p + 1, s));
-  CUDA_CHECK(cub::DeviceSegmentedSort::StableSortPairs(nullptr, tb2, q2.p, q1.p, d2.p, d1.p, (int)np, nn, doff.p,
-                                                       doff.p + 1, s));
-  DevBuf<unsigned char> tmp(std::max(tb, tb2) + 16);
-  // (q, d) order: stable by d, then stable by q
-  CUDA_CHECK(cub::DeviceSegmentedSort::StableSortPairs(tmp.p, tb, d1.p, d2.p, q1.p, q2.p, (int)np, nn, doff.p,
-                                                       doff.p + 1, s));
-  CUDA_CHECK(cub::DeviceSegmentedSort::StableSortPairs(tmp.p, tb2, q2.p, q1.p, d2.p, d1.p, (int)np, nn, doff.p,
-                                                       doff.p + 1, s));
-  // d1/q1 sorted by (q, d); first of each q run -> (dmin, q) in d2/q2
-  samp_unique_kernel<<<nn, 256, 0, s>>>(dsn.p, kappa, d2.p, q2.p, d1.p, q1.p);
+  size_t t1 = 0, t2 = 0, t3 = 0;
+  CUDA_CHECK(cub::DeviceRadixSort::SortPairs(nullptr, t1, k1.p, k2.p, d1.p, d2.p, np, 0, qb + nb, s));
+  CUDA_CHECK(cub::DeviceRadixSort::SortPairs(nullptr, t2, k1.p, k2.p, v1.p, v2.p, np, 0, 64, s));
+  CUDA_CHECK(cub::DeviceRadixSort::SortPairs(nullptr, t3, nk1.p, nk2.p, v2.p, v1.p, np, 0, std::max(1, nb), s));
+  DevBuf<unsigned char> tmp(std::max(t1, std::max(t2, t3)) + 16);
+  // (node, q) order
+  CUDA_CHECK(cub::DeviceRadixSort::SortPairs(tmp.p, t1, k1.p, k2.p, d1.p, d2.p, np, 0, qb + nb, s));
+  const unsigned g = (unsigned)((np + 255) / 256);
+  samp_runmin_kernel<<<g, 256, 0, s>>>(np, qb, nall, k2.p, d2.p, k1.p, v1.p);
   LAUNCH_CHECK();
-  // stable sort by dmin (q order kept within equal dmin) -> d1/q1
-  CUDA_CHECK(cub::DeviceSegmentedSort::StableSortPairs(tmp.p, tb, d2.p, d1.p, q2.p, q1.p, (int)np, nn, doff.p,
-                                                       doff.p + 1, s));
+  // stable by dmin, then stable by node: (node, dmin, q)
+  CUDA_CHECK(cub::DeviceRadixSort::SortPairs(tmp.p, t2, k1.p, k2.p, v1.p, v2.p, np, 0, 64, s));
+  samp_nodekey_kernel<<<g, 256, 0, s>>>(np, qb, v2.p, nk1.p);
+  LAUNCH_CHECK();
+  CUDA_CHECK(cub::DeviceRadixSort::SortPairs(tmp.p, t3, nk1.p, nk2.p, v2.p, v1.p, np, 0, std::max(1, nb), s));
+  samp_q_kernel<<<g, 256, 0, s>>>(np, qb, nall, v1.p, q1.p);
+  LAUNCH_CHECK();
   DevBuf<int> cnt(nn);
   samp_take_kernel<<<nn, 256, (size_t)S * sizeof(int64_t), s>>>(dsn.p, kappa, S, q1.p, C, cnt.p);
   LAUNCH_CHECK();
