@@ -182,6 +182,14 @@ __global__ void gather_key_kernel(const uint64_t* __restrict__ key, const int* _
   if (i < n) out[i] = key[order[i]];
 }
 
+__global__ void node_key_kernel(const int* __restrict__ node_of_pos, const int* __restrict__ order, int64_t n,
+                                unsigned* __restrict__ out) {
+  const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (i < n) out[i] = (unsigned)node_of_pos[order[i]];
+}
+
+static int bits_for(uint64_t v) { int b = 0; while (b < 63 && (1ull << b) <= v) ++b; return b; }
+
 __global__ void permute_kernel(const double* __restrict__ F, const int64_t* __restrict__ idx,
                                const int* __restrict__ order, int64_t n, int rp,
                                double* __restrict__ F2, int64_t* __restrict__ idx2) {
@@ -213,6 +221,7 @@ void build_tree(const double* Fpad, int64_t n, int r, int rp, int m, uint64_t tr
   const uint64_t key = splitmix64(tree_seed);
   DevBuf<uint64_t> k1(n), k2(n);
   DevBuf<int> p1(n), p2(n), node_of(n);
+  DevBuf<unsigned> nk1(n), nk2(n);
   DevBuf<int64_t> ik(n);
   for (int l = 0; l < L; ++l) {
     const auto& nodes = rg[l];
@@ -220,22 +229,18 @@ void build_tree(const double* Fpad, int64_t n, int r, int rp, int m, uint64_t tr
     std::vector<Chunk> ch;
     std::vector<int> cb(nn), ce(nn), nof(n);
     std::vector<int64_t> cnt(nn);
-    std::vector<int> segb(nn), sege(nn);
     for (int i = 0; i < nn; ++i) {
       cb[i] = (int)ch.size();
       for (int64_t lo = nodes[i].first; lo < nodes[i].second; lo += TREE_CHUNK)
         ch.push_back({i, lo, std::min(nodes[i].second, lo + TREE_CHUNK)});
       ce[i] = (int)ch.size();
       cnt[i] = nodes[i].second - nodes[i].first;
-      segb[i] = (int)nodes[i].first;
-      sege[i] = (int)nodes[i].second;
       for (int64_t p = nodes[i].first; p < nodes[i].second; ++p) nof[p] = i;
     }
     auto d_ch = upload(ch, s);
     auto d_cb = upload(cb, s), d_ce = upload(ce, s);
     auto d_cnt = upload(cnt, s);
     auto d_nof = upload(nof, s);
-    auto d_sb = upload(segb, s), d_se = upload(sege, s);
     if (rp_tree_index >= 0) {  // N1: random-projection tree
       rp_project_kernel<<<ceil_div(n, 256), 256, 0, s>>>(Fa.p, rp, r, n, d_nof.p,
                                                          splitmix64(tree_seed + (uint64_t)rp_tree_index),
@@ -262,23 +267,30 @@ void build_tree(const double* Fpad, int64_t n, int r, int rp, int m, uint64_t tr
     project_kernel<<<ceil_div(n, 256), 256, 0, s>>>(Fa.p, rp, r, n, d_nof.p, mean.p, dir.p, k1.p, p1.p);
     LAUNCH_CHECK();
     }
-    // pass 1: stable sort positions by original index within each node
-    size_t tb1 = 0, tb2 = 0;
-    CUDA_CHECK(cub::DeviceSegmentedSort::StableSortPairs(nullptr, tb1, ia.p, ik.p, p1.p, p2.p,
-                                                         (int)n, nn, d_sb.p, d_se.p, s));
-    CUDA_CHECK(cub::DeviceSegmentedSort::StableSortPairs(nullptr, tb2, k2.p, k1.p, p2.p, p1.p,
-                                                         (int)n, nn, d_sb.p, d_se.p, s));
-    DevBuf<unsigned char> tmp(std::max(tb1, tb2) + 16);
+    // order of positions within each node by (projection key, original index), as three global
+    // stable radix sorts instead of per-node segmented sorts: by original index, by projection
+    // key, then by node (node ranges are contiguous and in node order, so each node's positions
+    // land in its own range)
+    const int qb = std::max(1, bits_for((uint64_t)std::max<int64_t>(1, n - 1)));
+    const int nbits = std::max(1, bits_for((uint64_t)std::max(1, nn - 1)));
+    size_t tb1 = 0, tb2 = 0, tb3 = 0;
+    const uint64_t* iak = reinterpret_cast<const uint64_t*>(ia.p);
+    uint64_t* ikk = reinterpret_cast<uint64_t*>(ik.p);
+    CUDA_CHECK(cub::DeviceRadixSort::SortPairs(nullptr, tb1, iak, ikk, p1.p, p2.p, (int)n, 0, qb, s));
+    CUDA_CHECK(cub::DeviceRadixSort::SortPairs(nullptr, tb2, k1.p, k2.p, p2.p, p1.p, (int)n, 0, 64, s));
+    CUDA_CHECK(cub::DeviceRadixSort::SortPairs(nullptr, tb3, nk1.p, nk2.p, p1.p, p2.p, (int)n, 0, nbits, s));
+    DevBuf<unsigned char> tmp(std::max(tb1, std::max(tb2, tb3)) + 16);
     // keys1 (the projection keys) must survive pass 1: keep a copy in k2 for the gather
     CUDA_CHECK(cudaMemcpyAsync(k2.p, k1.p, n * sizeof(uint64_t), cudaMemcpyDeviceToDevice, s));
-    CUDA_CHECK(cub::DeviceSegmentedSort::StableSortPairs(tmp.p, tb1, ia.p, ik.p, p1.p, p2.p,
-                                                         (int)n, nn, d_sb.p, d_se.p, s));
+    CUDA_CHECK(cub::DeviceRadixSort::SortPairs(tmp.p, tb1, iak, ikk, p1.p, p2.p, (int)n, 0, qb, s));
     // p2 = positions ordered by original index; gather their projection keys
     gather_key_kernel<<<ceil_div(n, 256), 256, 0, s>>>(k2.p, p2.p, n, k1.p);
     LAUNCH_CHECK();
-    // pass 2: stable sort by projection key -> final order of positions in p1
-    CUDA_CHECK(cub::DeviceSegmentedSort::StableSortPairs(tmp.p, tb2, k1.p, k2.p, p2.p, p1.p,
-                                                         (int)n, nn, d_sb.p, d_se.p, s));
+    CUDA_CHECK(cub::DeviceRadixSort::SortPairs(tmp.p, tb2, k1.p, k2.p, p2.p, p1.p, (int)n, 0, 64, s));
+    node_key_kernel<<<ceil_div(n, 256), 256, 0, s>>>(d_nof.p, p1.p, n, nk1.p);
+    LAUNCH_CHECK();
+    CUDA_CHECK(cub::DeviceRadixSort::SortPairs(tmp.p, tb3, nk1.p, nk2.p, p1.p, p2.p, (int)n, 0, nbits, s));
+    std::swap(p1, p2);   // final order of positions in p1
     permute_kernel<<<ceil_div(n * rp, 256), 256, 0, s>>>(Fa.p, ia.p, p1.p, n, rp, Fb.p, ib.p);
     LAUNCH_CHECK();
     std::swap(Fa, Fb);
