@@ -1290,7 +1290,7 @@ constexpr int CP_THREADS = 512;
 template <int MAXPL>
 __global__ void __launch_bounds__(CP_THREADS) bcpqr_kernel(const CpqrProb* __restrict__ probs,
                                                            double rel_tol, double abs_tol,
-                                                           int cap) {
+                                                           int cap, int cpqr_prefetch) {
   const CpqrProb P = probs[blockIdx.x];
   const int rows = P.rows, s = P.s;
   const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5, nw = CP_THREADS / 32;
@@ -1383,6 +1383,9 @@ __global__ void __launch_bounds__(CP_THREADS) bcpqr_kernel(const CpqrProb* __res
     for (int c = j + 1 + wid; c < rows; c += nw) {
       double x[MAXPL];
       double* col = W + (long long)c * s;
+      // L2 prefetch of this warp's next column (its DRAM latency overlaps this column's work)
+      if (cpqr_prefetch && c + nw < rows && 16 * lane < s - j)
+        asm volatile("prefetch.global.L2 [%0];\n" ::"l"(W + (long long)(c + nw) * s + j + 16 * lane));
       double dot = 0.0;
 #pragma unroll
       for (int q = 0; q < MAXPL; ++q) {
@@ -1690,7 +1693,8 @@ void bcpqr(const std::vector<CpqrProb>& probs, double rel_tol, double abs_tol, i
   auto launch = [&](auto kern) {
     if (smem > 48 * 1024)
       CUDA_CHECK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-    kern<<<(unsigned)probs.size(), CP_THREADS, smem, s>>>(d, rel_tol, abs_tol, cap);
+    static const int pf = [] { const char* e = getenv("SVMHSS_CPQR_PREFETCH"); return (e && e[0] == '0') ? 0 : 1; }();
+    kern<<<(unsigned)probs.size(), CP_THREADS, smem, s>>>(d, rel_tol, abs_tol, cap, pf);
   };
   if (maxs <= 96) launch(bcpqr_kernel<3>);
   else if (maxs <= 160) launch(bcpqr_kernel<5>);
