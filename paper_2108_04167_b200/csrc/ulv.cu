@@ -463,6 +463,30 @@ __device__ __forceinline__ void fwd_item(const SolveNode* __restrict__ nodes, So
   const int i0 = wk.chunk * ch, i1 = min(R, i0 + ch);
   if (N.pt) {  // identity operator
     for (int e = tid; e < (i1 - i0) * NR; e += 256) out_up[(N.koff + i0) * NR + e] = ld_in<CG>(in + (N.roff + i0) * NR + e);
+  } else if (four == 3 && NR <= 2 && R <= 512 && i1 - i0 <= 8) {
+    // one row per warp (small chunks: the top levels): the row's 16 loads are issued before the
+    // input vector is staged, so the two latencies overlap; same per-row FMA order as fwd_rows
+    const int lane = tid & 31, i = i0 + (tid >> 5);
+    const double* Mr = M + N.moff + (int64_t)i * R;
+    double m[16];
+#pragma unroll
+    for (int q = 0; q < 16; ++q) m[q] = (i < i1 && lane + 32 * q < R) ? Mr[lane + 32 * q] : 0.0;
+    for (int e = tid; e < R * NR; e += 256) vsh[e] = ld_in<CG>(in + N.roff * NR + e);
+    __syncthreads();
+    if (i < i1) {
+      double acc[NR];
+#pragma unroll
+      for (int c = 0; c < NR; ++c) acc[c] = 0.0;
+#pragma unroll
+      for (int q = 0; q < 16; ++q) {
+        const int j = lane + 32 * q;
+        if (j < R) {
+#pragma unroll
+          for (int c = 0; c < NR; ++c) acc[c] = fma(m[q], vsh[j * NR + c], acc[c]);
+        }
+      }
+      row_store<NR>(acc, i, N.k, N.koff, N.yoff, out_up, out_yr);
+    }
   } else {
     for (int e = tid; e < R * NR; e += 256) vsh[e] = ld_in<CG>(in + N.roff * NR + e);
     __syncthreads();
@@ -552,11 +576,6 @@ __device__ __forceinline__ void bwd_split_item(const SolveNode* __restrict__ nod
   }
   __shared__ double ush[kRB * NR];
   __shared__ double red[kBW * kCW * NR];
-  for (int e = tid; e < (i1 - i0) * NR; e += kBW * 32) {
-    const int i = i0 + e / NR, c = e % NR;
-    ush[e] = (i < N.k) ? ld_in<CG>(in_s + (N.koff + i) * NR + c) : ld_in<CG>(in_r + (N.yoff + i - N.k) * NR + c);
-  }
-  __syncthreads();
   const int ja = j0 + lane, jb = j0 + 32 + lane;
   const bool va = ja < R, vb = jb < R;
   const double* Mn = M + N.moff;
@@ -566,6 +585,7 @@ __device__ __forceinline__ void bwd_split_item(const SolveNode* __restrict__ nod
   {  // this warp's rows i0 + wid + q*kBW (q < kRB/kBW): all loads in flight, then FMAs in row order
     constexpr int NQ = kRB / kBW;
     double ma[NQ], mb[NQ];
+    // M (static) first: its loads overlap the input-vector load and the barrier below
 #pragma unroll
     for (int q = 0; q < NQ; ++q) {
       const int i = i0 + wid + q * kBW;
@@ -573,6 +593,11 @@ __device__ __forceinline__ void bwd_split_item(const SolveNode* __restrict__ nod
       ma[q] = (i < i1 && va) ? Mr[ja] : 0.0;
       mb[q] = (i < i1 && vb) ? Mr[jb] : 0.0;
     }
+    for (int e = tid; e < (i1 - i0) * NR; e += kBW * 32) {
+      const int i = i0 + e / NR, c = e % NR;
+      ush[e] = (i < N.k) ? ld_in<CG>(in_s + (N.koff + i) * NR + c) : ld_in<CG>(in_r + (N.yoff + i - N.k) * NR + c);
+    }
+    __syncthreads();
 #pragma unroll
     for (int q = 0; q < NQ; ++q) {
       const int i = i0 + wid + q * kBW;
