@@ -430,8 +430,11 @@ __global__ void __launch_bounds__(256) bpotrf_kernel(const SqProb* __restrict__ 
 // L21 = A21 L11^-T (forward substitution), and the trailing lower triangle gets
 // A22 -= L21 L21^T as 8 x 8 DMMA tiles (k = 16) read and written in place.  The first
 // non-positive pivot stops the factorization (info = its index + 1), as bpotrf_kernel.
-constexpr int CNB = 16, CPS = 20, CMAX = 1024;
+constexpr int CMAX = 1024, CMAX8 = 2304;
 
+// CNB panel width, CPS its shared-memory row stride (= 4 mod 8: conflict-free fragments);
+// <16, 20> up to CMAX rows, <8, 12> up to CMAX8 (large near-exact nodes)
+template <int CNB, int CPS>
 __global__ void __launch_bounds__(512, 1) bpotrf_tc_kernel(const SqProb* __restrict__ probs, int* info) {
   const SqProb P = probs[blockIdx.x];
   const int n = P.n, tid = threadIdx.x, lane = tid & 31, w = tid >> 5, g = lane >> 2, t = lane & 3;
@@ -534,14 +537,18 @@ void bpotrf(const std::vector<SqProb>& probs, int* d_info, cudaStream_t s) {
   for (auto& p : probs) maxn = std::max(maxn, p.n);
   SqProb* d = upload_probs(probs, s);
   static const int tc = [] { const char* e = getenv("SVMHSS_POTRF_TC"); return (e && e[0] == '0') ? 0 : 1; }();
-  if (tc && maxn <= CMAX) {
-    const size_t smem = (size_t)CMAX * CPS * sizeof(double);
-    static bool attr = false;
-    if (!attr) {
-      CUDA_CHECK(cudaFuncSetAttribute(bpotrf_tc_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-      attr = true;
+  if (tc && maxn <= CMAX8) {
+    // (the panel width is chosen by the batch's largest node; bitwise P-invariance of the
+    // sharded build therefore assumes all nodes of a level are on the same side of CMAX)
+    if (maxn <= CMAX) {
+      const size_t smem = (size_t)CMAX * 20 * sizeof(double);
+      CUDA_CHECK(cudaFuncSetAttribute(bpotrf_tc_kernel<16, 20>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+      bpotrf_tc_kernel<16, 20><<<(unsigned)probs.size(), 512, smem, s>>>(d, d_info);
+    } else {
+      const size_t smem = (size_t)CMAX8 * 12 * sizeof(double);
+      CUDA_CHECK(cudaFuncSetAttribute(bpotrf_tc_kernel<8, 12>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+      bpotrf_tc_kernel<8, 12><<<(unsigned)probs.size(), 512, smem, s>>>(d, d_info);
     }
-    bpotrf_tc_kernel<<<(unsigned)probs.size(), 512, smem, s>>>(d, d_info);
     LAUNCH_CHECK();
     free_probs(d, s);
     return;
@@ -1199,16 +1206,16 @@ __global__ void __launch_bounds__(256) blarft_kernel(const SqProb* __restrict__ 
 // column J: the diagonal block T_JJ by the column recurrence (warp 0), Y = S[0:J, J] T_JJ,
 // and T[0:J, J] = -T[0:J, 0:J] Y (Q = Q_1 Q_2: T = [T1, -T1 V1^T V2 T2; 0, T2]); the block
 // columns before J are final when J starts.  Thread (i, c) owns output row i, column c.
-constexpr int LNB = 16, LMAX = 512;
+constexpr int LNB = 16;
 
 __global__ void __launch_bounds__(512) blarft_blk_kernel(const SqProb* __restrict__ probs,
-                                                         const double* const* __restrict__ taus) {
+                                                         const double* const* __restrict__ taus, int lmax) {
   const SqProb P = probs[blockIdx.x];
   const double* tau = taus[blockIdx.x];
   const int n = P.n, tid = threadIdx.x, lane = tid & 31, w = tid >> 5;
   extern __shared__ __align__(16) double lsm[];
-  double* Sb = lsm;                  // LMAX x LNB: S[0:j1, J-block]
-  double* Y = Sb + LMAX * LNB;       // LMAX x LNB
+  double* Sb = lsm;                  // lmax x LNB: S[0:j1, J-block]
+  double* Y = Sb + (size_t)lmax * LNB;  // lmax x LNB
   __shared__ double Tjj[LNB][LNB + 1];
   for (int j0 = 0; j0 < n; j0 += LNB) {
     const int jb = min(LNB, n - j0), j1 = j0 + jb;
@@ -1261,14 +1268,11 @@ void blarft(const std::vector<SqProb>& probs, const std::vector<const double*>& 
   SqProb* d = upload_probs(probs, s);
   const double** dt = upload_probs(taus, s);
   static const int blk = [] { const char* e = getenv("SVMHSS_LARFT_BLK"); return (e && e[0] == '0') ? 0 : 1; }();
-  if (blk && maxn <= LMAX) {
-    const size_t sm2 = (size_t)2 * LMAX * LNB * sizeof(double);
-    static bool attr = false;
-    if (!attr) {
-      CUDA_CHECK(cudaFuncSetAttribute(blarft_blk_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm2));
-      attr = true;
-    }
-    blarft_blk_kernel<<<(unsigned)probs.size(), 512, sm2, s>>>(d, dt);
+  const int lmax = (maxn + 15) & ~15;
+  const size_t sm2 = (size_t)2 * lmax * LNB * sizeof(double);
+  if (blk && sm2 <= 226 * 1024) {
+    CUDA_CHECK(cudaFuncSetAttribute(blarft_blk_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm2));
+    blarft_blk_kernel<<<(unsigned)probs.size(), 512, sm2, s>>>(d, dt, lmax);
     LAUNCH_CHECK();
     free_probs(d, s);
     free_probs((void*)dt, s);
