@@ -623,6 +623,12 @@ __global__ void pad_coef_kernel(const double* __restrict__ coef, int64_t n, int 
   out[e] = (c < nC) ? coef[i * nC + c] : 0.0;
 }
 
+__global__ void copy_cols_kernel(const double* __restrict__ src, int64_t m, int lds, int ldd, double* __restrict__ dst) {
+  const int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (e >= m * ldd) return;
+  dst[e] = src[(e / ldd) * lds + e % ldd];
+}
+
 void predict_impl(const double* Ftrain, const double* coef, int64_t n, int r, double h,
                   const double* bias_host, int nC, const double* Ftest, int64_t m, double* dv,
                   int8_t* lab, cudaStream_t s) {
@@ -637,7 +643,27 @@ void predict_impl(const double* Ftrain, const double* coef, int64_t n, int r, do
   row_norms(Fte.p, m, SA, nute.p, s);
   pad_coef_kernel<<<ceil_div(n * ld, 256), 256, 0, s>>>(coef, n, nC, ld, W.p);
   LAUNCH_CHECK();
-  predict_sums(Fte.p, nute.p, m, Ftr.p, nutr.p, W.p, n, rp, SA, ld, -1.0 / (2.0 * h * h), S.p, s);
+  if (rp <= 128) {
+    predict_sums(Fte.p, nute.p, m, Ftr.p, nutr.p, W.p, n, rp, SA, ld, -1.0 / (2.0 * h * h), S.p, s);
+  } else {
+    // wide features (r > 128): the sketch kernel's shared-memory tiling (rows at stride rp),
+    // with the coefficients as a 16-column right-hand side
+    DevBuf<double> Ftr2((size_t)n * rp), Fte2((size_t)std::max<int64_t>(1, m) * rp), W16((size_t)n * 16 + 2),
+        S16((size_t)std::max<int64_t>(1, m) * 16);
+    pad_rows(Ftrain, n, r, rp, Ftr2.p, s);
+    pad_rows(Ftest, m, r, rp, Fte2.p, s);
+    pad_coef_kernel<<<ceil_div(n * 16, 256), 256, 0, s>>>(coef, n, nC, 16, W16.p);
+    LAUNCH_CHECK();
+    KmmArgs a{};
+    a.Fa = Fte2.p; a.nua = nute.p; a.na = m;
+    a.Fb = Ftr2.p; a.nub = nutr.p; a.nb = n;
+    a.rp = rp; a.W = W16.p; a.ldw = 16; a.ncols = 16; a.S = S16.p; a.lds = 16;
+    a.neg_inv_2h2 = -1.0 / (2.0 * h * h);
+    a.same_set = 0; a.leaf_a = nullptr; a.leaf_b = nullptr;
+    kernel_matmul(a, s);
+    copy_cols_kernel<<<ceil_div(std::max<int64_t>(1, m) * ld, 256), 256, 0, s>>>(S16.p, m, 16, ld, S.p);
+    LAUNCH_CHECK();
+  }
   h2d(b.p, bias_host, nC, s);
   predict_finish_kernel<<<ceil_div(m * nC, 256), 256, 0, s>>>(S.p, m, nC, ld, b.p, dv, lab);
   LAUNCH_CHECK();

@@ -1,7 +1,7 @@
 """svm_predict (a11: dv_t = sum_i coef_i K(f_i, t) + b, label = sign with 0 -> +1) on
 the GPU against the oracle's exact decision values, across the predict kernel's shapes: feature
 counts that select each A-fragment register width (r = 8 -> rp 8, r = 54 -> rp 56, r = 123 ->
-rp 124 with 8-warp CTAs), coefficient widths nC = 1, 3 (padded to 4) and 16, and ragged sizes
+rp 124 with 8-warp CTAs) and the wide-feature path (r > 128), coefficient widths nC = 1, 3 (padded to 4) and 16, and ragged sizes
 (test points not a multiple of the 128 / 64-row CTA tile, training points not a multiple of the
 64-point step, a single test point, fewer training points than one step)."""
 import numpy as np
@@ -25,6 +25,8 @@ def _t(a):
     (50, 70, 22, 2, 0.5),
     (2050, 65, 123, 1, 2.0),
     (513, 200, 123, 16, 3.0),
+    (700, 150, 150, 1, 4.0),      # r > 128: the wide-feature path (sketch kernel tiling)
+    (300, 77, 203, 3, 5.0),
 ])
 def test_predict_matches_oracle(gpu_lib, n, m, r, nC, h):
     P = gpu_lib
