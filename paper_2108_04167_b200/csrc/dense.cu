@@ -335,11 +335,8 @@ template <int MT, int NT, int MINB>
 static void launch_dmma(const GemmProb* d, int maxm, int maxn, unsigned nb, cudaStream_t s) {
   constexpr int BM = 16 * MT, BN = 32 * NT;
   const size_t smem = (size_t)DNS * (BM + BN) * DSK * sizeof(double);
-  static bool attr = false;
-  if (!attr) {
-    CUDA_CHECK(cudaFuncSetAttribute(bgemm_dmma_kernel<MT, NT, MINB>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-    attr = true;
-  }
+  // (set per launch: the attribute belongs to the current device's context)
+  CUDA_CHECK(cudaFuncSetAttribute(bgemm_dmma_kernel<MT, NT, MINB>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
   dim3 grid(ceil_div(maxn, BN), ceil_div(maxm, BM), nb);
   bgemm_dmma_kernel<MT, NT, MINB><<<grid, 256, smem, s>>>(d);
 }
@@ -1148,11 +1145,7 @@ void bgeqr2(const std::vector<QrProb>& probs, cudaStream_t s) {
   static const int tc = [] { const char* e = getenv("SVMHSS_QR_TC"); return (e && e[0] == '0') ? 0 : 1; }();
   if (tc && maxm <= QMAX) {
     const size_t smem = ((size_t)QNB * QSP + (size_t)QMAX * QSB + 5 * QNB * QCB) * sizeof(double);
-    static bool attr = false;
-    if (!attr) {
-      CUDA_CHECK(cudaFuncSetAttribute(bgeqrf_tc_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-      attr = true;
-    }
+    CUDA_CHECK(cudaFuncSetAttribute(bgeqrf_tc_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
     bgeqrf_tc_kernel<<<(unsigned)probs.size(), 512, smem, s>>>(d);
     LAUNCH_CHECK();
     free_probs(d, s);
