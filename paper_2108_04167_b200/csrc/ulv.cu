@@ -275,30 +275,57 @@ void ulv_factor_impl(ULVImpl& F, cudaStream_t s) {
       std::vector<const double*> taus;
       for (int i : np) { tp.push_back({K[i], T.p + to[i], K[i], 1}); taus.push_back(tau.p + tauoff[i]); }
       blarft(tp, taus, s);
+      // Q^T D Q.  Default: M = Q^T = I - (V T^T) V^T formed first (needed for the solve operator
+      // anyway), then Y = D M^T and D' = M Y (two R x R x R GEMMs, 13% fewer flops than the
+      // compact-WY form and fewer, larger launches).  SVMHSS_FACTOR_QDQ=0: compact WY
+      // (D' = D - Z V^T - V Z^T, Z = D V T - 1/2 V T^T V^T D V T).
+      static const int mfirst = [] { const char* e = getenv("SVMHSS_FACTOR_QDQ"); return (e && e[0] == '0') ? 0 : 1; }();
+      if (mfirst) {
+        std::vector<PackDesc> pI0;
+        for (int i : np) pI0.push_back({0, moff[i], R[i], K[i], 2, 0});
+        run_pack(nullptr, pI0, F_l.M.p, s);
+        g.clear();
+        for (int i : np) g.push_back({R[i], K[i], K[i], V.p + vo[i], K[i], 1, T.p + to[i], 1, K[i], Wt.p + vo[i], K[i], 1, 1.0, 0.0});
+        bgemm(g, s);  // Wt := V T^T
+        g.clear();
+        for (int i : np) g.push_back({R[i], R[i], K[i], Wt.p + vo[i], K[i], 1, V.p + vo[i], 1, K[i], F_l.M.p + moff[i], R[i], 1, -1.0, 1.0});
+        bgemm(g, s);  // M = I - Wt V^T = Q^T
+        int64_t sumR2np = 0;
+        std::vector<int64_t> yo(nn, 0);
+        for (int i : np) { yo[i] = sumR2np; sumR2np += (int64_t)R[i] * R[i]; }
+        DevBuf<double> Yq(std::max<int64_t>(1, sumR2np));
+        g.clear();
+        for (int i : np) g.push_back({R[i], R[i], R[i], Dcur.p + coff[i], R[i], 1, F_l.M.p + moff[i], 1, R[i], Yq.p + yo[i], R[i], 1, 1.0, 0.0});
+        bgemm(g, s);  // Y = D M^T
+        g.clear();
+        for (int i : np) g.push_back({R[i], R[i], R[i], F_l.M.p + moff[i], R[i], 1, Yq.p + yo[i], R[i], 1, Dcur.p + coff[i], R[i], 1, 1.0, 0.0});
+        bgemm(g, s);  // D' = M Y = Q^T D Q
+      } else {
       // W = Dcur V ; Mk = V^T W ; X1 = Mk T ; X2 = T^T X1 ; Z = W T - 1/2 V X2
-      g.clear();
-      for (int i : np) g.push_back({R[i], K[i], R[i], Dcur.p + coff[i], R[i], 1, V.p + vo[i], K[i], 1, Wt.p + vo[i], K[i], 1, 1.0, 0.0});
-      bgemm(g, s);
-      g.clear();
-      for (int i : np) g.push_back({K[i], K[i], R[i], V.p + vo[i], 1, K[i], Wt.p + vo[i], K[i], 1, Mk.p + to[i], K[i], 1, 1.0, 0.0});
-      for (int i : np) g.push_back({R[i], K[i], K[i], Wt.p + vo[i], K[i], 1, T.p + to[i], K[i], 1, Z.p + vo[i], K[i], 1, 1.0, 0.0});
-      bgemm(g, s);
-      g.clear();
-      for (int i : np) g.push_back({K[i], K[i], K[i], Mk.p + to[i], K[i], 1, T.p + to[i], K[i], 1, X1.p + to[i], K[i], 1, 1.0, 0.0});
-      bgemm(g, s);
-      g.clear();
-      for (int i : np) g.push_back({K[i], K[i], K[i], T.p + to[i], 1, K[i], X1.p + to[i], K[i], 1, X2.p + to[i], K[i], 1, 1.0, 0.0});
-      bgemm(g, s);
-      g.clear();
-      for (int i : np) g.push_back({R[i], K[i], K[i], V.p + vo[i], K[i], 1, X2.p + to[i], K[i], 1, Z.p + vo[i], K[i], 1, -0.5, 1.0});
-      bgemm(g, s);
-      // Dc = Dcur - Z V^T - V Z^T
-      g.clear();
-      for (int i : np) g.push_back({R[i], R[i], K[i], Z.p + vo[i], K[i], 1, V.p + vo[i], 1, K[i], Dcur.p + coff[i], R[i], 1, -1.0, 1.0});
-      bgemm(g, s);
-      g.clear();
-      for (int i : np) g.push_back({R[i], R[i], K[i], V.p + vo[i], K[i], 1, Z.p + vo[i], 1, K[i], Dcur.p + coff[i], R[i], 1, -1.0, 1.0});
-      bgemm(g, s);
+        g.clear();
+        for (int i : np) g.push_back({R[i], K[i], R[i], Dcur.p + coff[i], R[i], 1, V.p + vo[i], K[i], 1, Wt.p + vo[i], K[i], 1, 1.0, 0.0});
+        bgemm(g, s);
+        g.clear();
+        for (int i : np) g.push_back({K[i], K[i], R[i], V.p + vo[i], 1, K[i], Wt.p + vo[i], K[i], 1, Mk.p + to[i], K[i], 1, 1.0, 0.0});
+        for (int i : np) g.push_back({R[i], K[i], K[i], Wt.p + vo[i], K[i], 1, T.p + to[i], K[i], 1, Z.p + vo[i], K[i], 1, 1.0, 0.0});
+        bgemm(g, s);
+        g.clear();
+        for (int i : np) g.push_back({K[i], K[i], K[i], Mk.p + to[i], K[i], 1, T.p + to[i], K[i], 1, X1.p + to[i], K[i], 1, 1.0, 0.0});
+        bgemm(g, s);
+        g.clear();
+        for (int i : np) g.push_back({K[i], K[i], K[i], T.p + to[i], 1, K[i], X1.p + to[i], K[i], 1, X2.p + to[i], K[i], 1, 1.0, 0.0});
+        bgemm(g, s);
+        g.clear();
+        for (int i : np) g.push_back({R[i], K[i], K[i], V.p + vo[i], K[i], 1, X2.p + to[i], K[i], 1, Z.p + vo[i], K[i], 1, -0.5, 1.0});
+        bgemm(g, s);
+        // Dc = Dcur - Z V^T - V Z^T
+        g.clear();
+        for (int i : np) g.push_back({R[i], R[i], K[i], Z.p + vo[i], K[i], 1, V.p + vo[i], 1, K[i], Dcur.p + coff[i], R[i], 1, -1.0, 1.0});
+        bgemm(g, s);
+        g.clear();
+        for (int i : np) g.push_back({R[i], R[i], K[i], V.p + vo[i], K[i], 1, Z.p + vo[i], 1, K[i], Dcur.p + coff[i], R[i], 1, -1.0, 1.0});
+        bgemm(g, s);
+      }
       ptr_.mark("  wy QtDQ");
       // L_r = chol(Dc_rr)   (also nodes with k == 0: whole block)
       std::vector<SqProb> cp2;
@@ -325,17 +352,19 @@ void ulv_factor_impl(ULVImpl& F, cudaStream_t s) {
       }
       bgemm(g, s);
       ptr_.mark("  potrf/trsm/Dh");
-      // M = Q^T = I - V T^T V^T  ; G_r = L_r^-1 M[k:, :] ; M[:k, :] -= L_sr G_r
+      // M = Q^T = I - V T^T V^T (unless formed above) ; G_r = L_r^-1 M[k:, :] ; M[:k, :] -= L_sr G_r
       std::vector<PackDesc> pI;
-      for (int i : np) pI.push_back({0, moff[i], R[i], K[i], 2, 0});
+      if (!mfirst) for (int i : np) pI.push_back({0, moff[i], R[i], K[i], 2, 0});
       for (int i : nz) pI.push_back({0, moff[i], R[i], K[i], 2, 0});
       run_pack(nullptr, pI, F_l.M.p, s);
-      g.clear();
-      for (int i : np) g.push_back({R[i], K[i], K[i], V.p + vo[i], K[i], 1, T.p + to[i], 1, K[i], Wt.p + vo[i], K[i], 1, 1.0, 0.0});
-      bgemm(g, s);  // Wt := V T^T (reuse)
-      g.clear();
-      for (int i : np) g.push_back({R[i], R[i], K[i], Wt.p + vo[i], K[i], 1, V.p + vo[i], 1, K[i], F_l.M.p + moff[i], R[i], 1, -1.0, 1.0});
-      bgemm(g, s);
+      if (!mfirst) {
+        g.clear();
+        for (int i : np) g.push_back({R[i], K[i], K[i], V.p + vo[i], K[i], 1, T.p + to[i], 1, K[i], Wt.p + vo[i], K[i], 1, 1.0, 0.0});
+        bgemm(g, s);  // Wt := V T^T (reuse)
+        g.clear();
+        for (int i : np) g.push_back({R[i], R[i], K[i], Wt.p + vo[i], K[i], 1, V.p + vo[i], 1, K[i], F_l.M.p + moff[i], R[i], 1, -1.0, 1.0});
+        bgemm(g, s);
+      }
       tr.clear();
       for (int i : np)
         tr.push_back({R[i] - K[i], R[i], Dcur.p + coff[i] + (int64_t)K[i] * R[i] + K[i], R[i], 1,
