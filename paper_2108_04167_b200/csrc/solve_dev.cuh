@@ -64,7 +64,8 @@ __device__ __forceinline__ void row_store(double (&acc)[NR], int i, int k, int64
 
 // rows i0 + wid, i0 + wid + nw, ... < i1; two rows per warp in flight (8 loads per lane).
 // mode (NR <= 2): 1 = four rows x 4 loads, 2 = two rows x 8 loads, 3 = one row x 16 loads,
-// 4 = four rows x 8 loads; the results are identical for every mode.
+// 4 = four rows x 8 loads, 5 = mode 3 + L2 prefetch of the next row; the results are identical
+// for every mode.
 template <int NR>
 __device__ __forceinline__ void fwd_rows(const double* __restrict__ M, int R, const double* __restrict__ vsh,
                                          int i0, int i1, int wid, int nw, int k, int64_t koff, int64_t yoff,
@@ -81,9 +82,12 @@ __device__ __forceinline__ void fwd_rows(const double* __restrict__ M, int R, co
       row_store<NR>(acc[1], i + nw, k, koff, yoff, out_up, out_yr);
     }
   }
-  if (NR <= 2 && mode == 3) {
+  if (NR <= 2 && (mode == 3 || mode == 5)) {
     for (; i < i1; i += nw) {
       const double* Mr[1] = {M + (int64_t)i * R};
+      // mode 5: L2 prefetch of this warp's next row (one 128-byte line per lane) ahead of this row
+      if (mode == 5 && i + nw < i1 && 16 * (threadIdx.x & 31) < R)
+        asm volatile("prefetch.global.L2 [%0];\n" ::"l"(M + (int64_t)(i + nw) * R + 16 * (threadIdx.x & 31)));
       double acc[1][NR];
       row_partials<NR, 1, 16>(Mr, R, vsh, acc);
       row_store<NR>(acc[0], i, k, koff, yoff, out_up, out_yr);

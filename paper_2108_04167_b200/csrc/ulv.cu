@@ -492,7 +492,7 @@ __device__ __forceinline__ void fwd_item(const SolveNode* __restrict__ nodes, So
   const int i0 = wk.chunk * ch, i1 = min(R, i0 + ch);
   if (N.pt) {  // identity operator
     for (int e = tid; e < (i1 - i0) * NR; e += 256) out_up[(N.koff + i0) * NR + e] = ld_in<CG>(in + (N.roff + i0) * NR + e);
-  } else if (four == 3 && NR <= 2 && R <= 512 && i1 - i0 <= 8) {
+  } else if ((four == 3 || four == 5) && NR <= 2 && R <= 512 && i1 - i0 <= 8) {
     // one row per warp (small chunks: the top levels): the row's 16 loads are issued before the
     // input vector is staged, so the two latencies overlap; same per-row FMA order as fwd_rows
     const int lane = tid & 31, i = i0 + (tid >> 5);
@@ -918,9 +918,10 @@ static void fwd_level(const ULVImpl& F, SolveWS& ws, int l, const SolveWork* wor
     const char* e = getenv("SVMHSS_FWD_ROWS");
     const char* p = getenv("SVMHSS_FWD_PREFETCH");
     const char* m = getenv("SVMHSS_FWD_MODE");
-    // default: one row x 16 loads per warp (4 KB contiguous per round trip); A/B at config 3:
-    // 1.439 ms/iteration vs 1.543 (four rows x 4 loads) and 1.501 (two rows x 4), same results
-    const int mode = m ? atoi(m) : ((e && e[0] == '2') ? 0 : 3);
+    // default: one row x 16 loads per warp (4 KB contiguous per round trip) plus an L2 prefetch
+    // of the warp's next row (mode 5); A/B at config 3: 1.439 ms/iteration (mode 3) vs 1.543
+    // (four rows x 4 loads) and 1.501 (two rows x 4); mode 5 vs 3: 1.431 vs 1.443; same results
+    const int mode = m ? atoi(m) : ((e && e[0] == '2') ? 0 : 5);
     return (mode << 2) | ((p && p[0] == '1') ? 2 : 0);
   }();
   launch_pdl(ulv_fwd_kernel<NR>, dim3(nwork), dim3(256), sm, s, lv.nodes.p, work, lv.ch, lv.M.p, ws.fin[l],
