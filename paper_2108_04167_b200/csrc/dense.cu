@@ -636,8 +636,51 @@ __global__ void __launch_bounds__(256) btrsm_kernel(const TrsmProb* __restrict__
 // k = 16), with X resident in shared memory and T fragments read through L1.
 constexpr int SW_ = 16, SXS = 24, SDS = 20, SMAXN = 512;
 
+// The 16 x 16 diagonal-block inverses of every problem, once (warp per block, lane c: column c
+// by substitution), into dg (problem p at dg + doff[p], block bi at 256 bi, row-major 16 x 16).
 template <bool LOWER>
-__global__ void __launch_bounds__(256) btrsm_tc_kernel(const TrsmProb* __restrict__ probs) {
+__global__ void __launch_bounds__(256) trsm_dinv_kernel(const TrsmProb* __restrict__ probs,
+                                                        const long long* __restrict__ doff, double* __restrict__ dg) {
+  const TrsmProb P = probs[blockIdx.y];
+  const int n = P.n, nb = (n + 15) / 16, lane = threadIdx.x & 31;
+  const int bi = blockIdx.x * 8 + (threadIdx.x >> 5);
+  if (bi >= nb || lane >= 16) return;
+  int r0, r1;
+  if (LOWER) { r0 = bi * 16; r1 = min(n, r0 + 16); }
+  else { r1 = n - bi * 16; r0 = max(0, r1 - 16); }
+  const int bs = r1 - r0, c = lane;
+#define TD(i, j) __ldg(P.T + (long long)(i) * P.trs + (long long)(j) * P.tcs)
+  double z[16];
+#pragma unroll
+  for (int j = 0; j < 16; ++j) z[j] = 0.0;
+  if (c < bs) {
+    if (LOWER) {
+#pragma unroll
+      for (int j = 0; j < 16; ++j) {
+        if (j < c || j >= bs) continue;
+        double a = (j == c) ? 1.0 : 0.0;
+        for (int p = c; p < j; ++p) a = fma(-TD(r0 + j, r0 + p), z[p], a);
+        z[j] = a / TD(r0 + j, r0 + j);
+      }
+    } else {
+#pragma unroll
+      for (int jj = 15; jj >= 0; --jj) {
+        if (jj > c) continue;
+        double a = (jj == c) ? 1.0 : 0.0;
+        for (int p = jj + 1; p <= c; ++p) a = fma(-TD(r0 + jj, r0 + p), z[p], a);
+        z[jj] = a / TD(r0 + jj, r0 + jj);
+      }
+    }
+  }
+#undef TD
+  double* D = dg + doff[blockIdx.y] + (long long)bi * 256;
+#pragma unroll
+  for (int j = 0; j < 16; ++j) D[j * 16 + c] = z[j];
+}
+
+template <bool LOWER>
+__global__ void __launch_bounds__(256) btrsm_tc_kernel(const TrsmProb* __restrict__ probs,
+                                                        const long long* __restrict__ doff, const double* __restrict__ dg) {
   const TrsmProb P = probs[blockIdx.y];
   const int c0 = blockIdx.x * SW_;
   if (c0 >= P.nrhs || P.n == 0) return;
@@ -656,38 +699,9 @@ __global__ void __launch_bounds__(256) btrsm_tc_kernel(const TrsmProb* __restric
     const int i = e / SW_, c = e % SW_;
     Xs[i * SXS + c] = (i < n && c < nc) ? XX(i, c0 + c) : 0.0;
   }
-  for (int bi = w; bi < nb; bi += 8) {  // diagonal block inverses, zero padded to 16 x 16
-    int r0, r1;
-    blk(bi, r0, r1);
-    const int bs = r1 - r0;
-    double* D = Di + (size_t)bi * 16 * SDS;
-    if (lane < 16) {
-      const int c = lane;
-      double z[16];
-#pragma unroll
-      for (int j = 0; j < 16; ++j) z[j] = 0.0;
-      if (c < bs) {
-        if (LOWER) {
-#pragma unroll
-          for (int j = 0; j < 16; ++j) {
-            if (j < c || j >= bs) continue;
-            double a = (j == c) ? 1.0 : 0.0;
-            for (int p = c; p < j; ++p) a = fma(-TT(r0 + j, r0 + p), z[p], a);
-            z[j] = a / TT(r0 + j, r0 + j);
-          }
-        } else {
-#pragma unroll
-          for (int jj = 15; jj >= 0; --jj) {
-            if (jj > c) continue;
-            double a = (jj == c) ? 1.0 : 0.0;
-            for (int p = jj + 1; p <= c; ++p) a = fma(-TT(r0 + jj, r0 + p), z[p], a);
-            z[jj] = a / TT(r0 + jj, r0 + jj);
-          }
-        }
-      }
-#pragma unroll
-      for (int j = 0; j < 16; ++j) D[j * SDS + c] = z[j];
-    }
+  {  // diagonal block inverses (trsm_dinv_kernel), zero padded to 16 x 16
+    const double* dsrc = dg + doff[blockIdx.y];
+    for (int e = tid; e < nb * 256; e += 256) Di[(size_t)(e >> 8) * 16 * SDS + ((e >> 4) & 15) * SDS + (e & 15)] = dsrc[e];
   }
   __syncthreads();
   for (int bi = 0; bi < nb; ++bi) {
@@ -763,12 +777,20 @@ void btrsm(const std::vector<TrsmProb>& probs_in, bool lower, cudaStream_t s) {
     if (tc && maxn <= SMAXN) {
       const size_t smem = ((size_t)((maxn + 7) & ~7) * SXS + (size_t)((maxn + 15) / 16) * 16 * SDS) * sizeof(double);
       dim3 grid(ceil_div(maxr, SW_), (unsigned)chunk.size());
+      std::vector<long long> doff(chunk.size());
+      long long tot = 0;
+      for (size_t q = 0; q < chunk.size(); ++q) { doff[q] = tot; tot += (long long)((chunk[q].n + 15) / 16) * 256; }
+      auto ddoff = upload(doff, s);
+      DevBuf<double> dg((size_t)std::max<long long>(1, tot));
+      dim3 gdi(ceil_div((maxn + 15) / 16, 8), (unsigned)chunk.size());
       if (lower) {
+        trsm_dinv_kernel<true><<<gdi, 256, 0, s>>>(d, ddoff.p, dg.p);
         CUDA_CHECK(cudaFuncSetAttribute(btrsm_tc_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-        btrsm_tc_kernel<true><<<grid, 256, smem, s>>>(d);
+        btrsm_tc_kernel<true><<<grid, 256, smem, s>>>(d, ddoff.p, dg.p);
       } else {
+        trsm_dinv_kernel<false><<<gdi, 256, 0, s>>>(d, ddoff.p, dg.p);
         CUDA_CHECK(cudaFuncSetAttribute(btrsm_tc_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-        btrsm_tc_kernel<false><<<grid, 256, smem, s>>>(d);
+        btrsm_tc_kernel<false><<<grid, 256, smem, s>>>(d, ddoff.p, dg.p);
       }
       LAUNCH_CHECK();
       free_probs(d, s);
