@@ -33,32 +33,35 @@ __global__ void leaf_dcur_kernel(const double* __restrict__ D, const int64_t* __
 struct PackDesc { int64_t src, dst; int R, k, mode, pad; };
 // mode 0: extract R (k x k upper of A (R x k)) ; mode 1: extract V (unit lower trapezoidal R x k)
 // mode 2: identity (R x R) ; mode 3: blockdiag(Ra, Rb) with Ra at src (ka = k) and Rb at dst2
+// grid (row blocks of 8, problems): each CTA writes 8 rows of one problem (coalesced columns)
 __global__ void pack_kernel(const double* __restrict__ A, const PackDesc* __restrict__ pd,
                             double* __restrict__ out) {
-  const PackDesc P = pd[blockIdx.x];
-  if (P.mode == 0) {
-    for (int64_t e = threadIdx.x; e < (int64_t)P.k * P.k; e += blockDim.x) {
-      const int i = (int)(e / P.k), j = (int)(e % P.k);
-      out[P.dst + e] = (j >= i) ? A[P.src + (int64_t)i * P.k + j] : 0.0;
-    }
-  } else if (P.mode == 1) {
-    for (int64_t e = threadIdx.x; e < (int64_t)P.R * P.k; e += blockDim.x) {
-      const int i = (int)(e / P.k), j = (int)(e % P.k);
-      out[P.dst + e] = (i > j) ? A[P.src + e] : (i == j ? 1.0 : 0.0);
-    }
-  } else {
-    for (int64_t e = threadIdx.x; e < (int64_t)P.R * P.R; e += blockDim.x) {
-      const int i = (int)(e / P.R), j = (int)(e % P.R);
-      out[P.dst + e] = (i == j) ? 1.0 : 0.0;
-    }
+  const PackDesc P = pd[blockIdx.y];
+  const int rows = (P.mode == 0) ? P.k : P.R, cols = (P.mode == 2) ? P.R : P.k;
+  const int i0 = blockIdx.x * 8;
+  if (i0 >= rows) return;
+  for (int e = threadIdx.x; e < 8 * cols; e += blockDim.x) {
+    const int i = i0 + e / cols, j = e % cols;
+    if (i >= rows) break;
+    const int64_t o = (int64_t)i * cols + j;
+    double v;
+    if (P.mode == 0) v = (j >= i) ? A[P.src + o] : 0.0;
+    else if (P.mode == 1) v = (i > j) ? A[P.src + o] : (i == j ? 1.0 : 0.0);
+    else v = (i == j) ? 1.0 : 0.0;
+    out[P.dst + o] = v;
   }
 }
 
 static void run_pack(const double* A, const std::vector<PackDesc>& pd, double* out, cudaStream_t s) {
   if (pd.empty()) return;
+  int maxrows = 1;
+  for (auto& q : pd) maxrows = std::max(maxrows, q.mode == 0 ? q.k : q.R);
   auto d = upload(pd, s);
-  pack_kernel<<<(unsigned)pd.size(), 256, 0, s>>>(A, d.p, out);
-  LAUNCH_CHECK();
+  for (size_t b0 = 0; b0 < pd.size(); b0 += 65535) {
+    const unsigned nb = (unsigned)std::min<size_t>(65535, pd.size() - b0);
+    pack_kernel<<<dim3((unsigned)ceil_div(maxrows, 8), nb), 256, 0, s>>>(A, d.p + b0, out);
+    LAUNCH_CHECK();
+  }
   CUDA_CHECK(cudaStreamSynchronize(s));
 }
 
