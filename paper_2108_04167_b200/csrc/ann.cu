@@ -53,19 +53,113 @@ __device__ void warp_topk(double (&cd)[kAnnMaxC], int64_t (&cj)[kAnnMaxC], int k
   }
 }
 
+// warp: the kappa smallest (d, j) among DISTINCT lane-held candidates (no repeated j), sorted,
+// padded with +inf / -1 -- the same output as warp_topk.  The kappa-th smallest distance T is
+// found by a radix select over the bits of d (non-negative doubles order as their bit patterns),
+// candidates with d < T are taken, ties at T by increasing j, and the selected <= 64 pairs are
+// ordered by a bitonic sort in shared memory (scratch: 64 (d, j) pairs per warp).
+__device__ void warp_topk_select(double (&cd)[kAnnMaxC], int64_t (&cj)[kAnnMaxC], int kappa,
+                                 double* __restrict__ out_d, int64_t* __restrict__ out_j,
+                                 double* __restrict__ sd, int64_t* __restrict__ sj) {
+  const int lane = threadIdx.x & 31;
+  unsigned long long key[kAnnMaxC];
+  int nv = 0;
+#pragma unroll
+  for (int c = 0; c < kAnnMaxC; ++c) {
+    key[c] = (cj[c] >= 0) ? (unsigned long long)__double_as_longlong(cd[c]) : ~0ull;
+    nv += (cj[c] >= 0) ? 1 : 0;
+  }
+  const int nvalid = __reduce_add_sync(0xffffffffu, (unsigned)nv);
+  const int K = min(kappa, nvalid);
+  int taken = 0;
+  if (K > 0) {
+    unsigned long long prefix = 0ull;
+    int rem = K;
+    for (int b = 62; b >= 0; --b) {   // bit 63 (sign) is 0 for every valid key
+      const unsigned long long hi = ~((2ull << b) - 1ull);   // bits above b
+      int cnt = 0;
+#pragma unroll
+      for (int c = 0; c < kAnnMaxC; ++c)
+        cnt += (cj[c] >= 0 && (key[c] & hi) == prefix && !((key[c] >> b) & 1ull)) ? 1 : 0;
+      cnt = (int)__reduce_add_sync(0xffffffffu, (unsigned)cnt);
+      if (rem > cnt) { prefix |= (1ull << b); rem -= cnt; }
+    }
+    // prefix = T (the K-th smallest key); rem = how many candidates equal to T to take
+    int pos = 0;   // compaction: this lane's selected entries go after the lower lanes' ones
+    int mine = 0;
+#pragma unroll
+    for (int c = 0; c < kAnnMaxC; ++c) mine += (cj[c] >= 0 && key[c] < prefix) ? 1 : 0;
+    pos = mine;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const int v = __shfl_up_sync(0xffffffffu, pos, o);
+      if (lane >= o) pos += v;
+    }
+    pos -= mine;
+    const int nless = __shfl_sync(0xffffffffu, pos + mine, 31);
+#pragma unroll
+    for (int c = 0; c < kAnnMaxC; ++c)
+      if (cj[c] >= 0 && key[c] < prefix) { sd[pos] = cd[c]; sj[pos] = cj[c]; ++pos; }
+    // ties at T: the rem smallest j (rare: usually rem = 1)
+    int64_t last = -1;
+    for (int q = 0; q < rem; ++q) {
+      int64_t bj = INT64_MAX;
+#pragma unroll
+      for (int c = 0; c < kAnnMaxC; ++c)
+        if (cj[c] >= 0 && key[c] == prefix && cj[c] > last && cj[c] < bj) bj = cj[c];
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) {
+        const int64_t oj = __shfl_xor_sync(0xffffffffu, bj, o);
+        bj = oj < bj ? oj : bj;
+      }
+      if (lane == 0) { sd[nless + q] = __longlong_as_double((long long)prefix); sj[nless + q] = bj; }
+      last = bj;
+    }
+    taken = K;
+  }
+  __syncwarp();
+  // bitonic sort of the first `taken` entries (padded to 64 with +inf) by (d, j)
+  for (int e = lane; e < 64; e += 32)
+    if (e >= taken) { sd[e] = INFINITY; sj[e] = INT64_MAX; }
+  __syncwarp();
+  for (int size = 2; size <= 64; size <<= 1) {
+    for (int stride = size >> 1; stride > 0; stride >>= 1) {
+      for (int e = lane; e < 64; e += 32) {
+        const int partner = e ^ stride;
+        if (partner > e) {
+          const bool up = (e & size) == 0;
+          const double d0 = sd[e], d1 = sd[partner];
+          const int64_t j0 = sj[e], j1 = sj[partner];
+          const bool gt = lex_less(d1, j1, d0, j0);   // (d0, j0) > (d1, j1)
+          if (gt == up) { sd[e] = d1; sd[partner] = d0; sj[e] = j1; sj[partner] = j0; }
+        }
+      }
+      __syncwarp();
+    }
+  }
+  for (int q = lane; q < kappa; q += 32) {
+    out_d[q] = (q < taken) ? sd[q] : INFINITY;
+    out_j[q] = (q < taken) ? sj[q] : -1;
+  }
+  __syncwarp();
+}
+
 // Phase A (one tree): one CTA per leaf.  Ft: features in this tree's order (stride rp),
 // perm: tree position -> original index.  cand rows are ORIGINAL indices.
-__global__ void __launch_bounds__(256) ann_leaf_kernel(const double* __restrict__ Ft, int rp, int r,
+__global__ void __launch_bounds__(512) ann_leaf_kernel(const double* __restrict__ Ft, int rp, int r,
                                                        const int64_t* __restrict__ perm,
                                                        const int64_t* __restrict__ leaf_lo,
                                                        int kappa, double* __restrict__ cand_d,
-                                                       int64_t* __restrict__ cand_j) {
-  extern __shared__ double xs[];  // m x r
+                                                       int64_t* __restrict__ cand_j, int xs_rows) {
+  extern __shared__ double xs[];  // m x r, then 16 warps x 64 (d, j) selection scratch
   const int64_t lo = leaf_lo[blockIdx.x], hi = leaf_lo[blockIdx.x + 1];
   const int m = (int)(hi - lo), lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  double* scr_d = xs + (size_t)xs_rows * r;
+  int64_t* scr_j = reinterpret_cast<int64_t*>(scr_d + 16 * 64);
   for (int e = threadIdx.x; e < m * r; e += blockDim.x) xs[e] = Ft[(lo + e / r) * rp + e % r];
   __syncthreads();
-  for (int i = wid; i < m; i += 8) {
+  const int nw = blockDim.x >> 5;
+  for (int i = wid; i < m; i += nw) {
     double cd[kAnnMaxC];
     int64_t cj[kAnnMaxC];
 #pragma unroll
@@ -84,7 +178,10 @@ __global__ void __launch_bounds__(256) ann_leaf_kernel(const double* __restrict_
       }
     }
     const int64_t oi = perm[lo + i];
-    warp_topk(cd, cj, kappa, cand_d + oi * kappa, cand_j + oi * kappa);
+    if (kappa <= 64)
+      warp_topk_select(cd, cj, kappa, cand_d + oi * kappa, cand_j + oi * kappa, scr_d + wid * 64, scr_j + wid * 64);
+    else
+      warp_topk(cd, cj, kappa, cand_d + oi * kappa, cand_j + oi * kappa);
   }
 }
 
@@ -117,7 +214,7 @@ void ann_build(const double* Fpad, int64_t n, int r, int rp, int kappa, int tree
   require(kappa >= 1 && trees >= 1 && leaf >= 2, "ann: kappa, trees >= 1 and leaf >= 2");
   require(leaf <= 32 * kAnnMaxC, "ann: ann_leaf must be <= 256");
   require((int64_t)trees * kappa <= 32 * kAnnMaxC, "ann: ann_trees * ann_neighbors must be <= 256");
-  const size_t smem = (size_t)leaf * r * sizeof(double);
+  const size_t smem = ((size_t)leaf * r + 16 * 64 * 2) * sizeof(double);
   require(smem <= 227 * 1024, "ann: ann_leaf * features too large for shared memory (lower ann_leaf)");
   const int L = num_levels(n, leaf);
   std::vector<std::vector<std::pair<int64_t, int64_t>>> rg;
@@ -133,8 +230,8 @@ void ann_build(const double* Fpad, int64_t n, int r, int rp, int kappa, int tree
     CUDA_CHECK(cudaFuncSetAttribute(ann_leaf_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
   for (int t = 0; t < trees; ++t) {
     build_tree(Fpad, n, r, rp, leaf, seed, perm.p, Ft.p, s, t);
-    ann_leaf_kernel<<<nleaf, 256, smem, s>>>(Ft.p, rp, r, perm.p, d_llo.p, kappa, cd.p + (size_t)t * n * kappa,
-                                             cj.p + (size_t)t * n * kappa);
+    ann_leaf_kernel<<<nleaf, 512, smem, s>>>(Ft.p, rp, r, perm.p, d_llo.p, kappa, cd.p + (size_t)t * n * kappa,
+                                             cj.p + (size_t)t * n * kappa, leaf);
     LAUNCH_CHECK();
   }
   ann_merge_kernel<<<ceil_div(n, 8), 256, 0, s>>>(n, trees, kappa, cd.p, cj.p, d_out, idx_out);
