@@ -433,10 +433,12 @@ void ulv_factor_impl(ULVImpl& F, cudaStream_t s) {
     std::vector<SolveNode> sn(F_l.nnodes);
     d2h(sn.data(), F_l.nodes.p, sn.size(), s);
     CUDA_CHECK(cudaStreamSynchronize(s));
-    // rows per CTA: enough CTAs to fill the chip (>= ~8 per SM), at most 32
+    // rows per CTA: enough CTAs to fill the chip (>= ~8 per SM)
     int64_t rows = 0;
     for (auto& nd : sn) if (!(l == L && nd.pt)) rows += nd.R;
-    static const int chmax = [] { const char* e = getenv("SVMHSS_FWD_CH"); return e ? atoi(e) : 32; }();
+    // rows per forward CTA, at most 64 (A/B with the mode-5 forward GEMV at config 3: 1.406 ms per
+    // iteration vs 1.426 with 32 and 1.41-1.42 with 128; the per-row arithmetic does not depend on it)
+    static const int chmax = [] { const char* e = getenv("SVMHSS_FWD_CH"); return e ? atoi(e) : 64; }();
     int ch = chmax;
     while (ch > 8 && rows / ch < 148 * 8) ch /= 2;
     F_l.ch = ch;
