@@ -10,6 +10,12 @@
 #pragma once
 #include "internal.cuh"
 
+// rows in flight per warp in the backward column GEMV (A/B at config 3: 8 -> 1.405 ms per ADMM
+// iteration, 4 -> 1.425, 16 -> 1.447)
+#ifndef BWD_BQ
+#define BWD_BQ 8
+#endif
+
 namespace svmhss {
 
 // one row's lane-partial dot product: lane sums j = lane, lane + 32, ... in order
@@ -140,16 +146,19 @@ __device__ __forceinline__ void bwd_cols(const double* __restrict__ M, int R, co
 #pragma unroll
   for (int c = 0; c < NR; ++c) aa[c] = ab[c] = 0.0;
   int i = wid;
-  for (; i + 7 * kBW < R; i += 8 * kBW) {
-    double ma[8], mb[8];
+  // BQ rows in flight per warp (16 loads / lane at BQ = 8); the per-column order (rows i, i + kBW,
+  // ... sequentially) does not depend on BQ
+  constexpr int BQ = BWD_BQ;
+  for (; i + (BQ - 1) * kBW < R; i += BQ * kBW) {
+    double ma[BQ], mb[BQ];
 #pragma unroll
-    for (int q = 0; q < 8; ++q) {
+    for (int q = 0; q < BQ; ++q) {
       const double* Mr = M + (int64_t)(i + q * kBW) * R;
       ma[q] = va ? Mr[ja] : 0.0;
       mb[q] = vb ? Mr[jb] : 0.0;
     }
 #pragma unroll
-    for (int q = 0; q < 8; ++q)
+    for (int q = 0; q < BQ; ++q)
 #pragma unroll
       for (int c = 0; c < NR; ++c) {
         const double u = ush[(i + q * kBW) * NR + c];
