@@ -134,6 +134,150 @@ def cfg_opts(cfg, sampling="sketch"):
     return o
 
 
+def node_shapes(ranks, n, leaf):
+    """(level, R_t, k_t) of every non-root node from the exported ranks (level-major BFS) and the
+    uniform T1 split: R = leaf size at the leaves, the children's k above."""
+    L = 0
+    while leaf * (1 << L) < n:
+        L += 1
+    sizes = [n]
+    for _ in range(L):
+        sizes = [x for v in sizes for x in (v // 2, v - v // 2)]
+    k = {}
+    out = []
+    for lvl in range(L, 0, -1):
+        for i in range(1 << lvl):
+            t = (1 << lvl) - 1 + i
+            R = sizes[i] if lvl == L else k[2 * t + 1] + k[2 * t + 2]
+            k[t] = int(ranks[t])
+            out.append((lvl, R, k[t]))
+    root_R = k[1] + k[2] if L > 0 else n
+    return out, root_R
+
+
+def solve_algorithmic_bytes(shapes, root_R, n, nC):
+    """one ULV solve reads each compressing node's compact factor twice (forward and
+    backward): V (R k - k(k-1)/2, unit-diagonal Householder vectors), T (k(k+1)/2), L_r
+    ((R-k)(R-k+1)/2), L_sr (k (R-k)); the root's Cholesky triangle R0(R0+1)/2; plus 8 n-vectors of
+    nC columns (rhs, solution, y, w, z, mu and the epilogue's q / next rhs)."""
+    per = 0
+    for _, R, k in shapes:
+        if k >= R:
+            continue  # pass-through: no transform
+        e = R - k
+        per += R * k - k * (k - 1) // 2 + k * (k + 1) // 2 + e * (e + 1) // 2 + k * e
+    per += root_R * (root_R + 1) // 2
+    return 2.0 * 8.0 * per + 64.0 * n * nC
+
+
+def compress_work(shapes, s):
+    """per CPQR'd node 4 s R k + 4 k^2 s flops (pivoted Householder on the s x R
+    sample block, R11^-1 R12, Omega' = U^T Omega^); algorithmic bytes: the node's sample block read
+    and written once (16 R s)."""
+    fl = sum(4.0 * s * R * k + 4.0 * k * k * s for _, R, k in shapes)
+    by = sum(16.0 * R * s for _, R, k in shapes)
+    return fl, by
+
+
+def host_info():
+    """CPU model, host DGEMM GFLOP/s (numpy 2048^3) and a STREAM-like copy GB/s (256 MB) on the
+    cores the oracle uses: the denominators of the CPU baseline."""
+    model = "unknown"
+    try:
+        for line in open("/proc/cpuinfo"):
+            if line.startswith("model name"):
+                model = line.split(":", 1)[1].strip()
+                break
+    except OSError:
+        pass
+    a = np.random.default_rng(0).standard_normal((2048, 2048))
+    a @ a
+    t = time.perf_counter()
+    for _ in range(3):
+        a @ a
+    gf = 3 * 2.0 * 2048 ** 3 / (time.perf_counter() - t) / 1e9
+    x = np.ones(1 << 25)
+    y = np.empty_like(x)
+    np.copyto(y, x)
+    t = time.perf_counter()
+    for _ in range(5):
+        np.copyto(y, x)
+    gbs = 5 * 2.0 * x.nbytes / (time.perf_counter() - t) / 1e9
+    return {"cpu_model": model, "cores": len(os.sched_getaffinity(0)), "host_dgemm_gflops": gf,
+            "host_copy_gbs": gbs}
+
+
+def oracle_offline(cfg_id):
+    """The oracle's MEASURED full-size phase times, from the committed golden run
+    (scripts/make_fullsize_goldens.py: oracle only, on the dev container's host)."""
+    p = os.path.join(ROOT, "tests", "golden", f"cfg{cfg_id}_full.json")
+    if not os.path.exists(p):
+        return None
+    d = json.load(open(p))
+    t = d.get("oracle_timings_s", {})
+    return {"n": d["n"], "host": d.get("host"), "tree_s": t.get("tree"), "sketch_s": t.get("sketch"),
+            "compress_after_sketch_s": t.get("compress_after_sketch"), "factor_s": t.get("factor"),
+            "admm_per_iter_s": t.get("admm_per_iter"), "admm_iters_per_s": 1.0 / t["admm_per_iter"]
+            if t.get("admm_per_iter") else None, "bias_objective_s": t.get("bias_objective"),
+            "predict_1024_s": t.get("predict_1024"),
+            "note": "measured at the full config size by the oracle-only golden script (not on this box)"}
+
+
+def oracle_phases(cfg_id, n_sample, iters, sketch_rows=512):
+    """The oracle (as it stands) timed per phase on this box's cores, on bounded samples of the
+    config: HSS build + ULV of an n_sample-point draw (same knobs) and `iters` ADMM iterations on it
+    (an iteration is linear in n at fixed node shapes: projected by n / n_sample), and `sketch_rows`
+    full-length rows of the sketch S = K Omega (projected by n / sketch_rows).  Every projected
+    number is labelled as such."""
+    import datagen
+    from oracle import admm, kernel, pipeline, rng, svm, ulv
+    cfg = datagen.get_config(cfg_id)
+    n = cfg["n"]
+    F, y, Ft, _ = datagen.generate(cfg_id, n=n_sample, n_test=256)
+    tm = {}
+    t0 = time.perf_counter()
+    perm, ranges, Om, H = pipeline.build(F, cfg, timings=tm)
+    t1 = time.perf_counter()
+    fac = ulv.factor(H, cfg["beta"])
+    t2 = time.perf_counter()
+    yp = y[perm]
+    solve = lambda b: ulv.solve(fac, b)  # noqa: E731
+    t3 = time.perf_counter()
+    out = admm.run(solve, yp, cfg["C"][0], cfg["beta"], iters)
+    t4 = time.perf_counter()
+    mv = lambda v: __import__("oracle").hss.matvec(H, v)  # noqa: E731
+    b = svm.bias(mv, out["z"], yp, cfg["C"][0])
+    t5 = time.perf_counter()
+    # sketch rows at the full size (the dominant phase): rows of K(F, F) Omega over all n points
+    Ff, _, _, _ = datagen.generate(cfg_id)
+    idx = np.arange(sketch_rows)
+    Omf = rng.omega(cfg["seed_omega"], np.arange(n), cfg["s"])
+    t6 = time.perf_counter()
+    kernel.sketch_rows(Ff, cfg["h"], Omf, idx)
+    t7 = time.perf_counter()
+    del Ff, Omf
+    inv = np.empty_like(perm)
+    inv[perm] = np.arange(n_sample)
+    t8 = time.perf_counter()
+    svm.decision_values(F, y * out["z"][inv], cfg["h"], b, Ft)
+    t9 = time.perf_counter()
+    per_it = (t4 - t3) / iters
+    sc = n / n_sample
+    return {
+        "admm_iters_per_s_projected": 1.0 / (per_it * sc),
+        "phases_s_projected": {
+            "sketch": (t7 - t6) * n / sketch_rows,
+            "compress_excl_sketch": (t1 - t0 - tm.get("tree", 0.0)) * sc,
+            "factor": (t2 - t1) * sc,
+            "admm_per_iter": per_it * sc,
+            "bias_objective": (t5 - t4) * sc,
+            "predict_per_test_point": (t9 - t8) / Ft.shape[0] * sc},
+        "sample": (f"oracle (NumPy/SciPy fp64): HSS build + ULV + {iters} ADMM iterations + bias on an "
+                   f"n={n_sample} config-{cfg_id} draw (same leaf/cap/s/tol/seeds; times x n/n_sample = "
+                   f"{sc:.1f}: per-node shapes equal the full config's), {sketch_rows} full-length sketch "
+                   f"rows (x n/{sketch_rows}), 256 test points; all PROJECTED to n={n}")}
+
+
 # ----------------------------------------------------------------------------- reference arm
 def oracle_sample(cfg_id, n_sample, iters, steps=1, warmup=0):
     """Time the CPU oracle (as it stands) on a bounded sample of the workload: build + factor
@@ -172,6 +316,7 @@ def run_reference(args, rank, world):
     import datagen
     cfg = datagen.get_config(args.config)
     r = oracle_sample(args.config, args.ref_n, args.ref_iters, steps=args.steps, warmup=args.warmup)
+    hinfo = host_info()
     line = {"metric": METRIC, "value": r["value"], "unit": "iters/s", "n_gpus": world, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": 1e3 * float(np.median(r["times"])),
             "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
@@ -179,7 +324,8 @@ def run_reference(args, rank, world):
             "config": {"workload": cfg["name"], "n": cfg["n"], "r": cfg["r"], "max_it": cfg["max_it"],
                        "leaf": cfg["leaf"], "cap": cfg["cap"], "s": cfg["s"], "sample_n": args.ref_n},
             "cpu_baseline": {"value": r["value"], "unit": "iters/s", "cores": r["cores"], "kind": "oracle",
-                             "sample": r["sample"]},
+                             "sample": r["sample"], "projected": True, **hinfo,
+                             "offline_full_size": oracle_offline(args.config)},
             "e2e": {"value": r["value"], "unit": "iters/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
             "hss_build_ulv_s_sample": r["build_ulv_s_sample"]}
     print(json.dumps(line), flush=True)
@@ -269,6 +415,11 @@ def main():
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
     if world > 1:
+        # NCCL's communicator-init lines (rank count, transports, NVLS) on stderr, init only, so the
+        # driver can see N ranks; the JSON line stays the only stdout line of rank 0
+        os.environ.setdefault("NCCL_DEBUG", "INFO")
+        os.environ.setdefault("NCCL_DEBUG_SUBSYS", "INIT")
+        os.environ.setdefault("NCCL_DEBUG_FILE", "/dev/stderr")
         dist.init_process_group("nccl", device_id=dev)
     if args.config == 4:
         return bench_grid(args, rank, world, dev)
@@ -300,10 +451,9 @@ def main():
         st = dict(res["stats"])
         st["ms_predict"] = None
         if not args.no_predict and Ftd.shape[0] > 0:
-            coef = (yd[:, None] * res["z"]).contiguous()
             p0, p1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
             p0.record(stream)
-            P.svm_predict(Fd, coef, h, res["bias"], Ftd)
+            P.svm_predict(Fd, yd, res["z"], h, res["bias"], Ftd)
             p1.record(stream)
             p1.synchronize()
             st["ms_predict"] = p0.elapsed_time(p1)
@@ -353,8 +503,13 @@ def main():
     fp64_derived = peaks["bf16_tflops_sustained"] * FP64_NOMINAL_TF / BF16_NOMINAL_TF
     fp64_peak = max(dgemm_tf, fp64_derived)
     ach_tf = sk_flops / (sketch_ms / 1e3) / 1e12
-    solve_bytes = 2.0 * ui["factor_bytes"] + 64.0 * n * len(Cs)
-    ach_gbs = solve_bytes * max_it / (loop_ms / 1e3) / 1e9
+    shapes, root_R = node_shapes(hi["ranks"], n, cfg["leaf"])
+    solve_alg = solve_algorithmic_bytes(shapes, root_R, n, len(Cs))
+    solve_expl = 2.0 * ui["factor_bytes"] + 64.0 * n * len(Cs)
+    ach_gbs = solve_alg * max_it / (loop_ms / 1e3) / 1e9
+    cf_flops, cf_bytes = compress_work(shapes, cfg["s"])
+    tree_bytes = 3.0 * hi["L"] * 8.0 * n * cfg["r"]
+    solve_traffic = _traffic("admm_iteration", cfg["name"]) if args.n is None else None
     line = {"metric": METRIC, "value": value, "unit": "iters/s", "n_gpus": world, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": ms_total / args.steps, "higher_is_better": True,
             "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
@@ -387,8 +542,31 @@ def main():
             "roofline_solve": {"bound": "hbm", "kernel": "ulv_fwd_kernel + ulv_bwd_kernel (+ epilogue)",
                                "achieved": ach_gbs, "peak": peaks["hbm_gbs"], "unit": "GB/s",
                                "frac": ach_gbs / peaks["hbm_gbs"],
-                               "work": "2 x factor_bytes + 64 n nC bytes per iteration"},
-            "roofline_factor": {"bound": "fp64 (DFMA)", "phase": "hss_ulv_factor (batched QR, WY GEMMs, POTRF, TRSM)",
+                               "algorithmic_bytes_per_iter": solve_alg,
+                               "explicit_operator_bytes_per_iter": solve_expl,
+                               "explicit_over_algorithmic": solve_expl / solve_alg,
+                               "dram_bytes_per_iter_ncu": solve_traffic,
+                               "work": "SURVEY 8(d) a9 algorithmic bytes: 2 x sum over compressing nodes 8[Rk - "
+                                       "k(k-1)/2 + k(k+1)/2 + (R-k)(R-k+1)/2 + k(R-k)] + 2 x 8 R0(R0+1)/2 (root) "
+                                       "+ 64 n nC per iteration; the library streams explicit R x R operators "
+                                       "(explicit_operator_bytes_per_iter), ncu DRAM bytes beside it"},
+            "roofline_compress": {"bound": "fp64 (CPQR: FP64 ALU) / hbm",
+                                  "phase": "per-level ID (a6): blocked CPQR + R11^-1 R12 + U^T Omega + B + sibling update",
+                                  "achieved": cf_flops / (hi["ms_compress"] / 1e3) / 1e12, "peak": fp64_peak,
+                                  "unit": "TFLOP/s",
+                                  "frac": cf_flops / (hi["ms_compress"] / 1e3) / 1e12 / fp64_peak,
+                                  "hbm_achieved_gbs": cf_bytes / (hi["ms_compress"] / 1e3) / 1e9,
+                                  "hbm_frac": cf_bytes / (hi["ms_compress"] / 1e3) / 1e9 / peaks["hbm_gbs"],
+                                  "cpqr_dram_bytes_ncu": _traffic("cpqr_level_sum", cfg["name"]) if args.n is None else None,
+                                  "work": "SURVEY 8(d) a6: sum over CPQR'd nodes 4sRk + 4k^2 s flops = %.3e; "
+                                          "algorithmic bytes 16 R s per node (sample block read + written once) "
+                                          "= %.3e" % (cf_flops, cf_bytes)},
+            "roofline_tree": {"bound": "hbm", "phase": "cluster tree (a2): per level mean, covariance, power "
+                                                      "iteration, projections, stable sorts",
+                              "achieved": tree_bytes / (hi["ms_tree"] / 1e3) / 1e9, "peak": peaks["hbm_gbs"],
+                              "unit": "GB/s", "frac": tree_bytes / (hi["ms_tree"] / 1e3) / 1e9 / peaks["hbm_gbs"],
+                              "work": "SURVEY 8(d) a2: 3 passes over F per level, 3 L 8 n r = %.3e bytes" % tree_bytes},
+            "roofline_factor": {"bound": "fp64 (DMMA)", "phase": "hss_ulv_factor (batched QR, WY GEMMs, POTRF, TRSM)",
                                 "achieved": ui["factor_flops"] / (ui["ms_factor"] / 1e3) / 1e12,
                                 "peak": fp64_peak, "unit": "TFLOP/s",
                                 "frac": ui["factor_flops"] / (ui["ms_factor"] / 1e3) / 1e12 / fp64_peak,
@@ -454,9 +632,12 @@ def main():
             "note": "HSS-ANN sampling (ann_neighbors/trees/leaf from datagen/configs.py); not the north-star "
                     "dense sketch - reported beside it"}}
     if rank == 0 and world == 1 and not args.no_cpu_baseline and args.n is None:
-        r = oracle_sample(args.config, args.ref_n, args.ref_iters)
-        line["cpu_baseline"] = {"value": r["value"], "unit": "iters/s", "cores": r["cores"], "kind": "oracle",
-                                "sample": r["sample"], "build_ulv_s_sample": r["build_ulv_s_sample"]}
+        r = oracle_phases(args.config, args.ref_n, args.ref_iters)
+        hinfo = host_info()
+        line["cpu_baseline"] = {"value": r["admm_iters_per_s_projected"], "unit": "iters/s",
+                                "cores": hinfo["cores"], "kind": "oracle", "projected": True,
+                                "sample": r["sample"], **hinfo, "phases_s_projected": r["phases_s_projected"],
+                                "offline_full_size": oracle_offline(args.config)}
     if rank == 0:
         print(json.dumps(line), flush=True)
     if world > 1:

@@ -104,6 +104,18 @@ typedef struct {
    * while some node's rank k > s - oversample with k < min(max_rank, rows), rebuilds with
    * s += adaptive_ds (> 0), up to max_rank + oversample.  0 = fixed s = max_rank + oversample. */
   int32_t adaptive_s0, adaptive_ds;
+  /* Parity imports (sketch sampling, no adaptive rounds):
+   * perm: HOST pointer, nullable.  n int64 tree position -> original index (a bijection of
+   *   0..n-1, e.g. the oracle's T1-T4 output); replaces the tree construction (T1-T4).  Node
+   *   ranges stay the uniform split of T1.  HSS_EINVAL if it is not a permutation.
+   * skeletons: HOST pointer, nullable; needs `ranks`.  Fixed-skeleton diagnostic mode (AMB-12):
+   *   the skeleton J_t of every non-root node, in hss_info's skel_out layout (levels 1..L,
+   *   nodes in BFS order, k_t tree positions each, in pivot order).  The CPQR of Y_t^T then
+   *   takes these columns as its first k_t pivots, in this order, instead of the norm argmax;
+   *   U_t = P[I; (R11^-1 R12)^T] as usual.  Every J_t must be k_t distinct active rows of t
+   *   (its points at the leaves, its children's skeletons above), else HSS_EINVAL. */
+  const int64_t* perm;
+  const int64_t* skeletons;
 } hss_opts;
 enum { HSS_SAMPLING_SKETCH = 0, HSS_SAMPLING_ANN = 1 };
 
@@ -130,9 +142,11 @@ typedef struct {
  * F: n x r row-major features (device).  h > 0 kernel width.
  * Returns HSS_EINVAL if n < 1, r < 1, h <= 0, leaf_size < 1, max_rank < 1, oversample < 0,
  * or s = max_rank + oversample > 2^20 (RNG column field, R1).
- * Memory: device buffers come from the device's default stream-ordered pool (release threshold
- * kept at max, so freed memory stays reserved for the next call).  Before the first build of a
- * given size the pool is grown once to about 24 n (s + r) 8 bytes (at most half the free memory;
+ * Memory: device buffers come from the library's OWN stream-ordered pool on the current device
+ * (cudaMemPoolCreate; never the device's default pool, so torch's allocator is not affected).
+ * The pool keeps freed memory reserved while any hss_t / ulv_t of the device is alive and is
+ * trimmed to zero when the last one is freed.  Before the first build of a given size the pool
+ * is grown once to about 24 n (s + r) 8 bytes (at most half the free memory;
  * SVMHSS_POOL_RESERVE_GB overrides, 0 disables) so later phases do not map memory mid-call. */
 int hss_build(const double* F, int64_t n, int32_t r, double h, const hss_opts* opt,
               void* stream, hss_t* out);
@@ -154,13 +168,18 @@ int hss_matvec(hss_t H, const double* v, double* out, int32_t nrhs, void* stream
 int hss_ulv_factor(hss_t H, double beta, void* stream, ulv_t* out);
 int ulv_info(ulv_t U, ulv_stats* st);
 
-/* x = (K~ + beta I)^-1 b (readings S); b, x: n x nrhs, original order; may alias. */
+/* x = (K~ + beta I)^-1 b (readings S); b, x: n x nrhs, original order; may alias.
+ * nrhs >= 1 (the sweep kernels take up to 8 columns at a time; more run in groups of 8). */
 int ulv_solve(ulv_t U, const double* b, double* x, int32_t nrhs, void* stream);
 
 /* ---- ADMM training (Alg. 2; Alg. 3 lines 4-13; AMB-1) ----
- * y: n labels, exactly +-1.0 (original order).  C: nC box bounds > 0 (HOST pointer).
+ * y: n labels, exactly +-1.0 (original order).  C: nC box bounds > 0 (HOST pointer), nC >= 1.
  * The nC problems advance together as nC right-hand sides of one solve per iteration
- * (factorization reused across C).  max_it >= 1 iterations exactly.
+ * (factorization reused across C); nC > 8 runs in groups of 8 (the sweep kernels'
+ * widest right-hand side), each group an independent ADMM over its C values.
+ * HSS_EW1 if w1 = e^T (K~+beta I)^-1 e <= 0.  Test hook: with the environment variable
+ * SVMHSS_FAULT_W1=1 the computed w1 is negated before that check (the error path is otherwise
+ * unreachable once the factorization succeeded: a successful ULV makes K~+beta I SPD).  max_it >= 1 iterations exactly.
  * Outputs (device, n x nC point-major, original order): z_out (required), mu_out (nullable).
  * bias_out, obj_out: nC HOST doubles, nullable: bias per AMB-2/AMB-3 via one HSS mat-vec
  * (P:196-200), objective f~(z) of Eq. (8).
@@ -186,12 +205,18 @@ int admm_svm_train(ulv_t U, const double* y, const double* C, int32_t nC, int32_
                    double* obj_out, admm_stats* st, void* stream);
 
 /* ---- prediction (Alg. 3; AMB-15, AMB-19: exact kernel) ----
- * dv[t*nC + c] = sum_i coef[i*nC + c] K(Ftrain_i, Ftest_t) + bias[c]; label = +1 if dv >= 0.
- * Ftrain: n x r, Ftest: m x r row-major; coef: n x nC (device, e.g. y*z); bias: nC HOST.
- * dv_out: m x nC device (nullable); label_out: m x nC int8 device (nullable).  nC <= 16. */
-int svm_predict(const double* Ftrain, const double* coef, int64_t n, int32_t r, double h,
-                const double* bias, int32_t nC, const double* Ftest, int64_t m,
-                double* dv_out, int8_t* label_out, void* stream);
+ * dv[t*nC + c] = sum_i y_i z[i*nC + c] K(Ftrain_i, Ftest_t) + bias[c]; label = +1 if dv >= 0.
+ * The coefficients z_y = y o z are formed inside the library.
+ * Ftrain: n x r, Ftest: m x r row-major (device); y: n labels (device); z: n x nC (device,
+ * admm_svm_train's z_out); bias: nC HOST doubles.  dv_out: m x nC device (nullable);
+ * label_out: m x nC int8 device (nullable).  1 <= nC <= 16.
+ * comm: nullable.  With a communicator of P ranks every rank passes the same full inputs; rank
+ * g evaluates test points [floor(m g / P), floor(m (g+1) / P)) and one allgather of the decision
+ * values gives every rank the full dv_out / label_out (bitwise the same as P = 1: each test
+ * point's sum does not depend on P). */
+int svm_predict(const double* Ftrain, const double* y, const double* z, int64_t n, int32_t r,
+                double h, const double* bias, int32_t nC, const double* Ftest, int64_t m,
+                double* dv_out, int8_t* label_out, hss_comm_t comm, void* stream);
 
 /* ---- end-to-end on HOST buffers (Alg. 3): host->device copies of F, y,
  * Ftest, the full build + factor + ADMM + bias + predict, device->host copies of z and
@@ -234,8 +259,14 @@ int hss_node(hss_t H, int32_t node, int32_t* rows, int32_t* k, double* U, double
  * used by bench.py to report gpu_launches. */
 int64_t hss_launch_count(void);
 
+/* Handles are freed on the device they were created on (the caller's current device is kept).
+ * Freeing the device's last hss_t / ulv_t trims the library's memory pool to zero. */
 void hss_free(hss_t H);
 void ulv_free(ulv_t U);
+/* Release the memory the library's pool keeps reserved on the current device (e.g. after
+ * svm_train_predict_host, which keeps its buffers' memory for the next call).  Synchronizes
+ * the device.  Memory of live handles is not affected. */
+int hss_pool_trim(void);
 const char* hss_last_error(void);
 const char* hss_version(void);
 

@@ -59,6 +59,27 @@ def run(solve, y, C, beta, max_it, *, trace_every=0, z0=None, mu0=None):
     return dict(z=z, mu=mu, x=x, trace=trace, w=w, w1=w1, lam=lam)
 
 
+def run_multi(solve, y, Cs, beta, max_it, *, trace_every=0):
+    """A1-A4 for several box bounds C_c at once (the factorization is shared across C):
+    the nC problems are independent and advance together, column c of z / mu being problem c
+    (solve takes an n x nC right-hand side).  Same arithmetic per column as run()."""
+    y = np.asarray(y, dtype=np.float64)
+    Cs = np.asarray(Cs, dtype=np.float64)
+    n, nC = y.shape[0], Cs.shape[0]
+    w, w1 = precompute(solve, y)
+    z, mu, x = np.zeros((n, nC)), np.zeros((n, nC)), np.zeros((n, nC))
+    trace = []
+    for it in range(1, max_it + 1):
+        q = 1.0 + mu + beta * z
+        v = solve(y[:, None] * q)
+        x = y[:, None] * v - np.outer(w, (w @ q) / w1)
+        z = np.clip(x - mu / beta, 0.0, Cs[None, :])
+        mu = mu - beta * (x - z)
+        if trace_every and (it % trace_every == 0 or it == max_it):
+            trace.append((it, z.copy(), mu.copy()))
+    return dict(z=z, mu=mu, x=x, trace=trace, w=w, w1=w1)
+
+
 def dense_solver(K, beta):
     """Dense oracle: Cholesky of K + beta I (equivalently of Y(K+beta I)Y = YKY + beta I,
     since Y^2 = I); returns b -> (K + beta I)^-1 b."""

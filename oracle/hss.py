@@ -82,8 +82,14 @@ def choose_rank(rdiag: np.ndarray, rows: int, s: int, *, fixed_rank=None,
 
 
 def compress(Fp: np.ndarray, h: float, ranges, Omega_p: np.ndarray, *, ranks=None,
-             rel_tol=0.0, abs_tol=0.0, cap=None, S=None) -> HSS:
-    """H1-H5.  `ranks` (dict or array indexed by BFS node id) selects fixed-rank mode."""
+             rel_tol=0.0, abs_tol=0.0, cap=None, S=None, skeletons=None) -> HSS:
+    """H1-H5.  `ranks` (dict or array indexed by BFS node id) selects fixed-rank mode.
+
+    `skeletons` (dict: node id -> tree positions J_t in pivot order, every non-root node)
+    selects the fixed-skeleton diagnostic mode (AMB-12): in H3 the pivots are J_t's local
+    indices followed by the other active rows in increasing order, the QR of Y_t^T is taken
+    WITHOUT pivoting in that column order, k = len(J_t), and U, J, Y_sk, Omega' follow as usual
+    (U[piv[k:]] = (R11^-1 R12)^T, the interpolation coefficients of the given skeleton)."""
     n, s = Omega_p.shape
     L = len(ranges) - 1
     hss = HSS(n=n, L=L, ranges=ranges, Fp=Fp, h=h)
@@ -110,6 +116,31 @@ def compress(Fp: np.ndarray, h: float, ranges, Omega_p: np.ndarray, *, ranks=Non
             Yt = Y[t]
             rows = Yt.shape[0]
             hss.rows[t] = rows
+            if skeletons is not None:                             # H3, fixed skeleton
+                Jt = np.asarray(skeletons[t], dtype=np.int64)
+                where = {int(a): q for q, a in enumerate(act[t])}
+                loc = [where[int(a)] for a in Jt]
+                if len(set(loc)) != len(loc):
+                    raise ValueError(f"skeleton of node {t} repeats an active row")
+                rest = [q for q in range(rows) if q not in set(loc)]
+                piv = np.array(loc + rest, dtype=np.int64)
+                k = len(loc)
+                R = sla.qr(Yt.T[:, piv], mode="r")[0] if rows else np.zeros((0, 0))
+                rd = np.abs(np.diag(R)) if R.size else np.zeros(0)
+                hss.Rdiag[t], hss.cap_hit[t], hss.k[t] = rd, False, k
+                if k == rows:
+                    if list(loc) != list(range(rows)):
+                        raise ValueError(f"pass-through node {t}: skeleton must be its active rows in order")
+                    hss.U[t], hss.Jloc[t], hss.J[t] = None, np.arange(rows), act[t]
+                else:
+                    T = sla.solve_triangular(R[:k, :k], R[:k, k:], lower=False)
+                    U = np.zeros((rows, k))
+                    U[piv[:k]] = np.eye(k)
+                    U[piv[k:]] = T.T
+                    hss.U[t], hss.Jloc[t], hss.J[t] = U, piv[:k].copy(), act[t][piv[:k]]
+                    Y[t] = Yt[piv[:k]]
+                    Om[t] = U.T @ Om[t]
+                continue
             if rows == 0:
                 _Q, R, piv = None, np.zeros((0, 0)), np.zeros(0, dtype=np.int64)
             else:                                                 # H3
@@ -142,6 +173,29 @@ def compress(Fp: np.ndarray, h: float, ranges, Omega_p: np.ndarray, *, ranks=Non
     else:
         hss.D[0] = gaussian_block(Fp, Fp, h)
     return hss
+
+
+def skeletons_from_flat(flat, ranks, ranges, s):
+    """The flat skeleton layout of the C-ABI (hss_info's skel_out, hss_opts.skeletons: levels
+    1..L, nodes in BFS order, k_t tree positions each) -> dict node id -> J_t.  k_t follows the
+    fixed-rank rule min(ranks[t], rows_t, s), rows_t = leaf size or the children's k."""
+    L = len(ranges) - 1
+    k = {}
+    for lvl in range(L, 0, -1):
+        for i, (lo, hi) in enumerate(ranges[lvl]):
+            t = (1 << lvl) - 1 + i
+            rows = hi - lo if lvl == L else k[2 * t + 1] + k[2 * t + 2]
+            k[t] = int(max(0, min(int(ranks[t]), rows, s)))
+    out, off = {}, 0
+    flat = np.asarray(flat, dtype=np.int64)
+    for lvl in range(1, L + 1):
+        for i in range(len(ranges[lvl])):
+            t = (1 << lvl) - 1 + i
+            out[t] = flat[off:off + k[t]]
+            off += k[t]
+    if off != flat.size:
+        raise ValueError(f"flat skeleton array has {flat.size} entries, the ranks need {off}")
+    return out
 
 
 def unconverged(hss: HSS, s: int, p: int, cap) -> list:

@@ -8,10 +8,11 @@ package loads the library and raises if it is missing (no CPU fallback).
     H = hss_build(F, h=..., leaf_size=..., rel_tol=..., max_rank=..., ...)
     U = hss_ulv_factor(H, beta)
     out = admm_svm_train(U, y, C=[...], max_it=...)
-    dv, labels = svm_predict(F, y[:, None] * out["z"], h, out["bias"], Ftest)
+    dv, labels = svm_predict(F, y, out["z"], h, out["bias"], Ftest)
 """
 from __future__ import annotations
 
+import contextlib
 import ctypes as ct
 
 import numpy as np
@@ -22,6 +23,7 @@ from ._lib import ALLGATHER_FN, AdmmOpts, AdmmStats, HssError, HssOpts, HssStats
 _L = _lib.load()
 
 __all__ = ["Comm", "hss_build", "hss_ulv_factor", "admm_svm_train", "svm_predict", "svm_train_predict_host",
+           "hss_pool_trim",
            "hss_omega", "hss_tree", "hss_kernel_matmul", "hss_kernel_block", "HSS", "ULV", "HssError",
            "version"]
 
@@ -120,16 +122,34 @@ def _cuda_f64(t, name):
     return t
 
 
-def _stream(stream):
-    return _lib.stream_handle(stream)
+def _shape(cond, msg):
+    if not cond:
+        raise ValueError(msg)
+
+
+def _on_device(*tensors):
+    """Every call runs with the tensors' device current (kernels, stream and the library's pool
+    of that device); all tensor arguments must share it."""
+    import torch
+    devs = {t.device for t in tensors if isinstance(t, torch.Tensor)}
+    _shape(len(devs) <= 1, f"tensor arguments on different devices: {sorted(map(str, devs))}")
+    if not devs:
+        return contextlib.nullcontext(), None
+    d = devs.pop()
+    return torch.cuda.device(d), d
+
+
+def _stream(stream, device=None):
+    return _lib.stream_handle(stream, device)
 
 
 class HSS:
     """Handle of a compressed kernel K~ (hss_t)."""
 
-    def __init__(self, handle, n, r, h):
+    def __init__(self, handle, n, r, h, device=None):
         self._h = handle
         self.n, self.r, self.h = n, r, h
+        self.device = device
 
     @property
     def handle(self):
@@ -176,9 +196,13 @@ class HSS:
     def matvec(self, v, stream=None):
         import torch
         _cuda_f64(v, "v")
+        _shape(v.dim() in (1, 2) and v.shape[0] == self.n, f"v must have {self.n} rows (got {tuple(v.shape)})")
+        _shape(self.device is None or v.device == self.device, "v is not on the HSS handle's device")
         nrhs = 1 if v.dim() == 1 else v.shape[1]
         out = torch.empty_like(v)
-        check(_L.hss_matvec(self.handle, ptr(v), ptr(out), nrhs, _stream(stream)))
+        ctx, d = _on_device(v)
+        with ctx:
+            check(_L.hss_matvec(self.handle, ptr(v), ptr(out), nrhs, _stream(stream, d)))
         return out
 
     def free(self):
@@ -214,9 +238,14 @@ class ULV:
     def solve(self, b, stream=None):
         import torch
         _cuda_f64(b, "b")
+        n = self.hss.n
+        _shape(b.dim() in (1, 2) and b.shape[0] == n, f"b must have {n} rows (got {tuple(b.shape)})")
+        _shape(self.hss.device is None or b.device == self.hss.device, "b is not on the ULV handle's device")
         nrhs = 1 if b.dim() == 1 else b.shape[1]
         x = torch.empty_like(b)
-        check(_L.ulv_solve(self.handle, ptr(b), ptr(x), nrhs, _stream(stream)))
+        ctx, d = _on_device(b)
+        with ctx:
+            check(_L.ulv_solve(self.handle, ptr(b), ptr(x), nrhs, _stream(stream, d)))
         return x
 
     def free(self):
@@ -236,7 +265,7 @@ SAMPLING = {"sketch": 0, "ann": 1}
 
 def make_opts(leaf_size, rel_tol=0.0, abs_tol=0.0, max_rank=64, oversample=16, omega_seed=0,
               tree_seed=0, ranks=None, comm=None, sampling="sketch", ann_neighbors=64, ann_trees=4,
-              ann_leaf=256, ann_seed=0, adaptive_s0=0, adaptive_ds=0):
+              ann_leaf=256, ann_seed=0, adaptive_s0=0, adaptive_ds=0, perm=None, skeletons=None):
     o = HssOpts()
     o.adaptive_s0, o.adaptive_ds = int(adaptive_s0), int(adaptive_ds)
     o.comm = comm.handle if comm is not None else None
@@ -245,35 +274,55 @@ def make_opts(leaf_size, rel_tol=0.0, abs_tol=0.0, max_rank=64, oversample=16, o
     o.leaf_size, o.rel_tol, o.abs_tol = int(leaf_size), float(rel_tol), float(abs_tol)
     o.max_rank, o.oversample = int(max_rank), int(oversample)
     o.omega_seed, o.tree_seed = int(omega_seed), int(tree_seed)
-    keep = None
+    keep = []
     if ranks is not None:
-        keep = np.ascontiguousarray(np.asarray(ranks, dtype=np.int32))
-        o.ranks = keep.ctypes.data_as(ct.POINTER(ct.c_int32))
+        kr = np.ascontiguousarray(np.asarray(ranks, dtype=np.int32))
+        o.ranks = kr.ctypes.data_as(ct.POINTER(ct.c_int32))
+        keep.append(kr)
+    if perm is not None:
+        kp = np.ascontiguousarray(np.asarray(perm, dtype=np.int64))
+        o.perm = kp.ctypes.data_as(ct.POINTER(ct.c_int64))
+        keep.append(kp)
+    if skeletons is not None:
+        ks = np.ascontiguousarray(np.asarray(skeletons, dtype=np.int64))
+        o.skeletons = ks.ctypes.data_as(ct.POINTER(ct.c_int64))
+        keep.append(ks)
     return o, keep
 
 
 def hss_build(F, h, leaf_size, rel_tol=0.0, abs_tol=0.0, max_rank=64, oversample=16, omega_seed=0,
               tree_seed=0, ranks=None, comm=None, sampling="sketch", ann_neighbors=64, ann_trees=4,
-              ann_leaf=256, ann_seed=0, adaptive_s0=0, adaptive_ds=0, stream=None) -> HSS:
+              ann_leaf=256, ann_seed=0, adaptive_s0=0, adaptive_ds=0, perm=None, skeletons=None,
+              stream=None) -> HSS:
     """hss_build (Alg. 3 line 1): F is a CUDA float64 (n, r) tensor, original order
     (all n points on every rank when `comm` shards the tree).  sampling="ann" selects HSS-ANN
-    column sampling instead of the randomized sketch."""
+    column sampling instead of the randomized sketch.  perm / skeletons (host
+    arrays) import a tree / fixed skeletons (parity modes; include/svmhss.h)."""
     _cuda_f64(F, "F")
+    _shape(F.dim() == 2, "F must be (n, r)")
     n, r = F.shape
+    if perm is not None:
+        _shape(np.asarray(perm).shape == (n,), f"perm must have {n} entries")
     o, keep = make_opts(leaf_size, rel_tol, abs_tol, max_rank, oversample, omega_seed, tree_seed, ranks, comm,
-                        sampling, ann_neighbors, ann_trees, ann_leaf, ann_seed, adaptive_s0, adaptive_ds)
+                        sampling, ann_neighbors, ann_trees, ann_leaf, ann_seed, adaptive_s0, adaptive_ds,
+                        perm, skeletons)
     hdl = ct.c_void_p()
-    check(_L.hss_build(ptr(F), n, r, float(h), ct.byref(o), _stream(stream), ct.byref(hdl)))
+    ctx, d = _on_device(F)
+    with ctx:
+        check(_L.hss_build(ptr(F), n, r, float(h), ct.byref(o), _stream(stream, d), ct.byref(hdl)))
     del keep
-    H = HSS(hdl.value, n, r, h)
+    H = HSS(hdl.value, n, r, h, F.device)
     H.comm = comm  # keep the Python object alive with the handle
     return H
 
 
 def hss_ulv_factor(H: HSS, beta, stream=None) -> ULV:
     """hss_ulv_factor (P:188, P:209-210)."""
+    import torch
     hdl = ct.c_void_p()
-    check(_L.hss_ulv_factor(H.handle, float(beta), _stream(stream), ct.byref(hdl)))
+    ctx = torch.cuda.device(H.device) if H.device is not None else contextlib.nullcontext()
+    with ctx:
+        check(_L.hss_ulv_factor(H.handle, float(beta), _stream(stream, H.device), ct.byref(hdl)))
     return ULV(hdl.value, H, beta)
 
 
@@ -283,7 +332,9 @@ def admm_svm_train(U: ULV, y, C, max_it, trace_every=0, margin_eps_rel=0.0, want
     Returns dict(z (n, nC), mu, bias[nC], obj[nC], stats, trace_z, trace_mu)."""
     import torch
     _cuda_f64(y, "y")
-    n = y.shape[0]
+    n = U.hss.n
+    _shape(y.dim() == 1 and y.shape[0] == n, f"y must have shape ({n},) (got {tuple(y.shape)})")
+    _shape(U.hss.device is None or y.device == U.hss.device, "y is not on the ULV handle's device")
     Cs = np.ascontiguousarray(np.atleast_1d(np.asarray(C, dtype=np.float64)))
     nC = Cs.shape[0]
     z = torch.empty((n, nC), dtype=torch.float64, device=y.device)
@@ -299,27 +350,42 @@ def admm_svm_train(U: ULV, y, C, max_it, trace_every=0, margin_eps_rel=0.0, want
         tm = torch.empty_like(tz)
         opts.trace_every, opts.trace_z, opts.trace_mu = int(trace_every), ptr(tz), ptr(tm)
     st = AdmmStats()
-    check(_L.admm_svm_train(U.handle, ptr(y), Cs.ctypes.data, nC, int(max_it), ct.byref(opts), ptr(z),
-                            ptr(mu), bias.ctypes.data, obj.ctypes.data, ct.byref(st), _stream(stream)))
+    ctx, d = _on_device(y)
+    with ctx:
+        check(_L.admm_svm_train(U.handle, ptr(y), Cs.ctypes.data, nC, int(max_it), ct.byref(opts), ptr(z),
+                                ptr(mu), bias.ctypes.data, obj.ctypes.data, ct.byref(st), _stream(stream, d)))
     return dict(z=z, mu=mu, bias=bias, obj=obj, trace_z=tz, trace_mu=tm,
                 stats={f: getattr(st, f) for f, _ in AdmmStats._fields_})
 
 
-def svm_predict(Ftrain, coef, h, bias, Ftest, stream=None):
-    """svm_predict (P:29-32, P:229): dv = K(Ftest, Ftrain) coef + bias; labels = sign (0 -> +1)."""
+def svm_predict(Ftrain, y, z, h, bias, Ftest, comm=None, stream=None):
+    """svm_predict: dv = K(Ftest, Ftrain) (y o z) + bias; labels = sign (0 -> +1).
+    y: (n,) labels, z: (n,) or (n, nC) dual variables (admm_svm_train's z), bias: nC values.
+    comm: shard the test points over its ranks (every rank gets the full outputs)."""
     import torch
-    _cuda_f64(Ftrain, "Ftrain")
-    _cuda_f64(coef, "coef")
-    _cuda_f64(Ftest, "Ftest")
+    for t, nm in ((Ftrain, "Ftrain"), (y, "y"), (z, "z"), (Ftest, "Ftest")):
+        _cuda_f64(t, nm)
+    _shape(Ftrain.dim() == 2 and Ftest.dim() == 2, "Ftrain and Ftest must be 2-D")
     n, r = Ftrain.shape
     m = Ftest.shape[0]
-    nC = 1 if coef.dim() == 1 else coef.shape[1]
+    _shape(Ftest.shape[1] == r, f"Ftest must have {r} columns (got {Ftest.shape[1]})")
+    _shape(y.dim() == 1 and y.shape[0] == n, f"y must have shape ({n},)")
+    _shape(z.dim() in (1, 2) and z.shape[0] == n, f"z must have {n} rows")
+    nC = 1 if z.dim() == 1 else z.shape[1]
     b = np.ascontiguousarray(np.atleast_1d(np.asarray(bias, dtype=np.float64)))
+    _shape(b.shape == (nC,), f"bias must have {nC} entries (got {b.shape[0]})")
     dv = torch.empty((m, nC), dtype=torch.float64, device=Ftrain.device)
     lab = torch.empty((m, nC), dtype=torch.int8, device=Ftrain.device)
-    check(_L.svm_predict(ptr(Ftrain), ptr(coef), n, r, float(h), b.ctypes.data, nC, ptr(Ftest), m,
-                         ptr(dv), ptr(lab), _stream(stream)))
+    ctx, d = _on_device(Ftrain, y, z, Ftest)
+    with ctx:
+        check(_L.svm_predict(ptr(Ftrain), ptr(y), ptr(z), n, r, float(h), b.ctypes.data, nC, ptr(Ftest), m,
+                             ptr(dv), ptr(lab), comm.handle if comm is not None else None, _stream(stream, d)))
     return dv, lab
+
+
+def hss_pool_trim():
+    """Release the memory the library keeps reserved in its pool on the current device."""
+    check(_L.hss_pool_trim())
 
 
 def svm_train_predict_host(F, y, h, beta, C, max_it, Ftest=None, **opt_kw):
@@ -328,8 +394,11 @@ def svm_train_predict_host(F, y, h, beta, C, max_it, Ftest=None, **opt_kw):
     F = np.ascontiguousarray(F, dtype=np.float64)
     y = np.ascontiguousarray(y, dtype=np.float64)
     n, r = F.shape
+    _shape(y.shape == (n,), f"y must have shape ({n},)")
     Cs = np.ascontiguousarray(np.atleast_1d(np.asarray(C, dtype=np.float64)))
     nC = Cs.shape[0]
+    if Ftest is not None:
+        _shape(np.asarray(Ftest).ndim == 2 and np.asarray(Ftest).shape[1] == r, f"Ftest must have {r} columns")
     o, keep = make_opts(**opt_kw)
     z = np.zeros((n, nC))
     bias, obj = np.zeros(nC), np.zeros(nC)
@@ -385,8 +454,11 @@ def hss_kernel_matmul(Fa, Fb, h, W, same_set=False, stream=None):
     for t, nm in ((Fa, "Fa"), (Fb, "Fb"), (W, "W")):
         _cuda_f64(t, nm)
     S = torch.empty((Fa.shape[0], W.shape[1]), dtype=torch.float64, device=Fa.device)
-    check(_L.hss_kernel_matmul(ptr(Fa), Fa.shape[0], ptr(Fb), Fb.shape[0], Fa.shape[1], float(h), ptr(W),
-                               W.shape[1], int(bool(same_set)), ptr(S), _stream(stream)))
+    _shape(Fb.shape[1] == Fa.shape[1] and W.shape[0] == Fb.shape[0], "hss_kernel_matmul: shape mismatch")
+    ctx, d = _on_device(Fa, Fb, W)
+    with ctx:
+        check(_L.hss_kernel_matmul(ptr(Fa), Fa.shape[0], ptr(Fb), Fb.shape[0], Fa.shape[1], float(h), ptr(W),
+                                   W.shape[1], int(bool(same_set)), ptr(S), _stream(stream, d)))
     return S
 
 

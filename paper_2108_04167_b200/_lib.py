@@ -30,7 +30,8 @@ class HssOpts(ct.Structure):
                 ("tree_seed", ct.c_uint64), ("ranks", ct.POINTER(ct.c_int32)), ("comm", ct.c_void_p),
                 ("sampling", ct.c_int32), ("ann_neighbors", ct.c_int32), ("ann_trees", ct.c_int32),
                 ("ann_leaf", ct.c_int32), ("ann_seed", ct.c_uint64),
-                ("adaptive_s0", ct.c_int32), ("adaptive_ds", ct.c_int32)]
+                ("adaptive_s0", ct.c_int32), ("adaptive_ds", ct.c_int32),
+                ("perm", ct.POINTER(ct.c_int64)), ("skeletons", ct.POINTER(ct.c_int64))]
 
 
 # int (*hss_allgather_fn)(void* ctx, const void* send, void* recv, size_t bytes)
@@ -65,7 +66,7 @@ EXPORTS = ["hss_build", "hss_info", "hss_matvec", "hss_ulv_factor", "ulv_info", 
            "admm_svm_train", "svm_predict", "svm_train_predict_host", "hss_omega", "hss_tree",
            "hss_kernel_matmul", "hss_kernel_block", "hss_node", "hss_free", "ulv_free",
            "hss_last_error", "hss_version", "hss_launch_count", "hss_comm_nccl_id",
-           "hss_comm_init_nccl", "hss_comm_init_host", "hss_comm_free", "hss_ann_lists"]
+           "hss_comm_init_nccl", "hss_comm_init_host", "hss_comm_free", "hss_ann_lists", "hss_pool_trim"]
 
 _lib = None
 
@@ -87,7 +88,8 @@ def load():
     L.ulv_solve.argtypes = [vp, vp, vp, i32, vp]
     L.admm_svm_train.argtypes = [vp, vp, vp, i32, i32, ct.POINTER(AdmmOpts), vp, vp, vp, vp,
                                  ct.POINTER(AdmmStats), vp]
-    L.svm_predict.argtypes = [vp, vp, i64, i32, dbl, vp, i32, vp, i64, vp, vp, vp]
+    L.svm_predict.argtypes = [vp, vp, vp, i64, i32, dbl, vp, i32, vp, i64, vp, vp, vp, vp]
+    L.hss_pool_trim.argtypes = []
     L.svm_train_predict_host.argtypes = [vp, vp, i64, i32, dbl, ct.POINTER(HssOpts), dbl, vp, i32,
                                          i32, vp, i64, vp, vp, vp, vp, vp]
     L.hss_omega.argtypes = [u64, vp, i64, i32, vp, vp]
@@ -131,7 +133,8 @@ def ptr(t):
     return t.data_ptr()
 
 
-def stream_handle(stream=None):
+def stream_handle(stream=None, device=None):
+    """cudaStream_t of `stream`, else of the current stream of `device` (the tensors' device)."""
     import torch
-    s = torch.cuda.current_stream() if stream is None else stream
+    s = torch.cuda.current_stream(device) if stream is None else stream
     return s.cuda_stream

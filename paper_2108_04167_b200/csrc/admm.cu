@@ -8,34 +8,9 @@
 //     x = y_i v_i - (w^T q / w1) w_i;  z = clip(x - mu/beta, 0, C_c);  mu -= beta (x - z)
 //     q' = 1 + mu + beta z;  next right-hand side y_i q'; per-block partial w^T q'
 //   fixed-order reduction of the partials -> w^T q' for the next iteration.
-#include <cooperative_groups.h>
 #include "solve_dev.cuh"
 
-namespace cg = cooperative_groups;
-
 namespace svmhss {
-
-// Per-leaf fixed-order partials -> pairwise up this rank's subtree (see shard.cu).  The last
-// block to finish (device counter, then reset for the next replay) does the tree reduction,
-// so the reduction adds no launch.
-__device__ void last_block_tree_reduce(double* part, int nl, int ncols, double* out, unsigned* counter) {
-  __shared__ bool last;
-  __threadfence();
-  __syncthreads();
-  if (threadIdx.x == 0) last = (atomicAdd(counter, 1u) == gridDim.x - 1);
-  __syncthreads();
-  if (!last) return;
-  __threadfence();
-  for (int st = 1; st < nl; st <<= 1) {
-    for (int e = threadIdx.x; e < (nl / (2 * st)) * ncols; e += blockDim.x) {
-      const int i = (e / ncols) * 2 * st, c = e % ncols;
-      part[(int64_t)i * ncols + c] += part[(int64_t)(i + st) * ncols + c];
-    }
-    __syncthreads();
-  }
-  for (int c = threadIdx.x; c < ncols; c += blockDim.x) out[c] = part[c];
-  if (threadIdx.x == 0) *counter = 0u;
-}
 
 // The per-point ADMM update (A2-A3, P:164-166 with AMB-1) for problem c:
 //   x = y v - (w^T q / w1) w;  z = clip(x - mu/beta, 0, C);  mu -= beta (x - z)
@@ -130,10 +105,12 @@ __global__ void __launch_bounds__(256) admm_epilogue_kernel(EpiArgs A, const int
         __syncthreads();
       }
     } else {
+      // same pairwise tree as the shared-memory path (i + st < n bound: any leaf count)
       for (int st = 1; st < nleaf_all; st <<= 1) {
-        for (int e = threadIdx.x; e < (nleaf_all / (2 * st)) * A.nC; e += blockDim.x) {
+        const int npair = (nleaf_all + 2 * st - 1) / (2 * st);
+        for (int e = threadIdx.x; e < npair * A.nC; e += blockDim.x) {
           const int i = (e / A.nC) * 2 * st, c = e % A.nC;
-          part[(int64_t)i * A.nC + c] += part[(int64_t)(i + st) * A.nC + c];
+          if (i + st < nleaf_all) part[(int64_t)i * A.nC + c] += part[(int64_t)(i + st) * A.nC + c];
         }
         __syncthreads();
       }
@@ -141,118 +118,6 @@ __global__ void __launch_bounds__(256) admm_epilogue_kernel(EpiArgs A, const int
     }
     if (threadIdx.x == 0) *counter = 0u;
   }
-}
-
-// ---- fused bottom level: for a node t of level L-1 whose
-// two children are pass-through leaves (its rows ARE points), one 8-CTA cluster does
-//   backward sweep (iteration k):  x = M_t^T [x_s; y_r]          (reads M_t from HBM)
-//   ADMM epilogue on the node's points (iteration k)
-//   forward sweep (iteration k+1): t = M_t b'                     (re-reads M_t, from L2)
-// with cluster barriers in between, so each such M_t crosses HBM once per iteration instead
-// of twice.  bwd_cols / fwd_rows / epi_chunk are the level kernels' own device functions:
-// the results are bitwise identical to the unfused sweep.
-struct FusedNode {
-  int64_t moff, roff, koff, yoff, plo;
-  int R, k, ma, mb, leafa, pad;
-};
-constexpr int kFCL = 8;  // CTAs per cluster (one node); kFCL * kCW >= max fused R
-constexpr int kMaxChunks = (kFCL * kCW + 31) / 32 + 2;
-
-template <int NR>
-__global__ void __launch_bounds__(kBW * 32) admm_bottom_kernel(EpiArgs A, const FusedNode* __restrict__ nodes, int nf,
-                                                               const double* __restrict__ M,
-                                                               const double* __restrict__ xs, double* __restrict__ yr,
-                                                               double* __restrict__ xb, double* __restrict__ fb,
-                                                               double* __restrict__ fup, double* __restrict__ chunkp,
-                                                               double* __restrict__ part) {
-  cg::cluster_group cl = cg::this_cluster();
-  const int c = (int)cl.block_rank();
-  const int ncl = gridDim.x / kFCL;
-  const int tid = threadIdx.x, wid = tid >> 5, lane = tid & 31;
-  extern __shared__ double sm[];
-  const int j0 = c * kCW;
-  // persistent clusters: few enough nodes in flight that a node's M_t (read from HBM in (1))
-  // is still in L2 when (3) re-reads it
-  for (int f = blockIdx.x / kFCL; f < nf; f += ncl) {
-  const FusedNode N = nodes[f];
-  const int R = N.R;
-  // (1) backward sweep: x (this CTA's kCW columns)
-  if (j0 < R) {
-    double* ush = sm;
-    double* red = sm + R * NR;
-    const int kn = N.k * NR;
-    for (int e = tid; e < R * NR; e += kBW * 32) ush[e] = (e < kn) ? xs[N.koff * NR + e] : yr[(N.yoff - N.k) * NR + e];
-    __syncthreads();
-    bwd_cols<NR>(M + N.moff, R, ush, j0, red, xb + N.roff * NR);
-  }
-  cl.sync();
-  // (2) epilogue on the node's points, chunk by chunk (leaf a: ca chunks, then leaf b)
-  const int ca = (N.ma + 31) / 32, cb = (N.mb + 31) / 32;
-  for (int ch = c * kBW + wid; ch < ca + cb; ch += kFCL * kBW) {
-    const bool inb = ch >= ca;
-    const int64_t p0 = N.plo + (inb ? N.ma + 32LL * (ch - ca) : 32LL * ch);
-    const int64_t rem = inb ? (N.ma + N.mb) - (p0 - N.plo) : N.ma - (p0 - N.plo);
-    const int cnt = (int)(rem < 32 ? rem : 32);
-    const double t = epi_chunk(A, p0, cnt);
-    if (lane < A.nC) chunkp[((int64_t)f * kMaxChunks + ch) * A.nC + lane] = t;
-  }
-  cl.sync();
-  // (3) leaf partials (fixed chunk order) and the forward sweep of iteration k+1
-  if (c == 0 && tid < 2 * A.nC) {
-    const int which = tid / A.nC, cc = tid % A.nC;
-    double t = 0.0;
-    const int lo = which ? ca : 0, hi = which ? ca + cb : ca;
-    for (int ch = lo; ch < hi; ++ch) t += chunkp[((int64_t)f * kMaxChunks + ch) * A.nC + cc];
-    part[(int64_t)(N.leafa + which) * A.nC + cc] = t;
-  }
-  if (j0 < R) {
-    double* vsh = sm;
-    for (int e = tid; e < R * NR; e += kBW * 32) vsh[e] = fb[N.roff * NR + e];
-    __syncthreads();
-    fwd_rows<NR>(M + N.moff, R, vsh, j0, min(R, j0 + kCW), wid, kBW, N.k, N.koff, N.yoff, fup, yr);
-  }
-  cl.sync();  // smem reuse and yr of this node: next node only after every CTA is done
-  }
-}
-
-template <int NR>
-static void launch_bottom(const EpiArgs& A, const FusedNode* nodes, int nf, const double* M, const double* xs,
-                          double* yr, double* xb, double* fb, double* fup, double* chunkp, double* part,
-                          cudaStream_t s) {
-  const size_t smem = ((size_t)kFCL * kCW + (size_t)kBW * kCW) * NR * sizeof(double);
-  if (smem > 48 * 1024)
-    CUDA_CHECK(cudaFuncSetAttribute(admm_bottom_kernel<NR>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-  static int ncl_env = -1;
-  if (ncl_env < 0) {
-    const char* e = getenv("SVMHSS_FUSE_CLUSTERS");
-    ncl_env = e ? std::max(1, atoi(e)) : 36;
-  }
-  const int ncl = std::min(nf, ncl_env);
-  cudaLaunchConfig_t cfg = {};
-  cfg.gridDim = dim3((unsigned)(ncl * kFCL));
-  cfg.blockDim = dim3(kBW * 32);
-  cfg.dynamicSmemBytes = smem;
-  cfg.stream = s;
-  cudaLaunchAttribute at[1];
-  at[0].id = cudaLaunchAttributeClusterDimension;
-  at[0].val.clusterDim.x = kFCL;
-  at[0].val.clusterDim.y = 1;
-  at[0].val.clusterDim.z = 1;
-  cfg.attrs = at;
-  cfg.numAttrs = 1;
-  CUDA_CHECK(cudaLaunchKernelEx(&cfg, admm_bottom_kernel<NR>, A, nodes, nf, M, xs, yr, xb, fb, fup, chunkp, part));
-}
-
-static void bottom_dispatch(int NR, const EpiArgs& A, const FusedNode* nodes, int nf, const double* M,
-                            const double* xs, double* yr, double* xb, double* fb, double* fup, double* chunkp,
-                            double* part, cudaStream_t s) {
-  switch (NR) {
-#define BC(k) case k: launch_bottom<k>(A, nodes, nf, M, xs, yr, xb, fb, fup, chunkp, part, s); break;
-    BC(1) BC(2) BC(3) BC(4) BC(5) BC(6) BC(7) BC(8)
-#undef BC
-    default: throw Error(HSS_EINVAL, "admm: nC must be 1..8");
-  }
-  LAUNCH_CHECK();
 }
 
 // Per-leaf partials of column sums: out[leaf*ncols + c] = sum_{i in leaf} f(i, c)
@@ -400,6 +265,8 @@ AdmmResult admm_train_impl(const ULVImpl& F, const double* y_orig, const std::ve
     tree_reduce_all(H, part.p, 1, &w1, s);
   }
   R.ms_pre = tpre.stop_ms();
+  static const bool fault_w1 = [] { const char* e = getenv("SVMHSS_FAULT_W1"); return e && e[0] == '1'; }();
+  if (fault_w1) w1 = -w1;  // test hook (include/svmhss.h): exercises the HSS_EW1 path
   R.w1 = w1;
   if (!(w1 > 0.0)) throw Error(HSS_EW1, "w1 = e^T (K~+beta I)^-1 e = " + std::to_string(w1) + " <= 0");
   // ---- state: x0 = z0 = mu0 = 0 (AMB-6); q0 = e
@@ -445,71 +312,10 @@ AdmmResult admm_train_impl(const ULVImpl& F, const double* y_orig, const std::ve
   if (smem_tree) epi_smem = std::max(epi_smem, (size_t)nleaf * sizeof(double));
   if (epi_smem > 48 * 1024)
     CUDA_CHECK(cudaFuncSetAttribute(admm_epilogue_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)epi_smem));
-  // ---- fused bottom level plan: nodes of level b = L-1 (this rank's) whose children are both
-  // pass-through leaves and whose R fits one cluster; the rest ("G" nodes) take the level
-  // kernels restricted to them.  Needs the bottom level below the exchanged level (b >= lg).
-  const int b = L - 1;
-  std::vector<FusedNode> fnodes;
-  std::vector<SolveWork> gwk, gbwk;
-  std::vector<int> gleaves;
-  // Off by default: measured on B200 at cfg 3 the fused level runs at 660 it/s against 686 it/s
-  // level by level; SVMHSS_FUSE_BOTTOM=1 turns it on.
-  const char* env = getenv("SVMHSS_FUSE_BOTTOM");
-  const bool want_fuse = env && env[0] == '1';
-  if (fused && b >= 1 && b >= sh.lg && want_fuse && !F.lv[b].allpt) {
-    const auto& Fb = F.lv[b];
-    std::vector<SolveNode> sn(Fb.nnodes);
-    d2h(sn.data(), Fb.nodes.p, sn.size(), s);
-    CUDA_CHECK(cudaStreamSynchronize(s));
-    for (int q = 0; q < Fb.nnodes; ++q) {
-      const int t = sh.first(b) + q;
-      const auto &ca = H.lv[L][2 * t], &cb = H.lv[L][2 * t + 1];
-      const bool ok = ca.pt && cb.pt && !sn[q].pt && sn[q].R <= kFCL * kCW;
-      if (ok) {
-        fnodes.push_back({sn[q].moff, sn[q].roff, sn[q].koff, sn[q].yoff, ca.lo - H.lo_g, sn[q].R, sn[q].k,
-                          (int)(ca.hi - ca.lo), (int)(cb.hi - cb.lo), 2 * t - sh.first(L), 0});
-      } else {
-        for (int c = 0; c < ceil_div(sn[q].R, Fb.ch); ++c) gwk.push_back({q, c});
-        for (int c = 0; c < ceil_div(sn[q].R, kCW); ++c) gbwk.push_back({q, c});
-        gleaves.push_back(2 * t - sh.first(L));
-        gleaves.push_back(2 * t + 1 - sh.first(L));
-      }
-    }
-  }
-  const bool bottom = !fnodes.empty();
-  auto dfn = upload(fnodes, s);
-  auto dgwk = upload(gwk, s), dgbwk = upload(gbwk, s);
-  auto dgleaves = upload(gleaves, s);
-  DevBuf<double> chunkp((size_t)std::max<size_t>(1, fnodes.size()) * kMaxChunks * nC);
-  CUDA_CHECK(cudaStreamSynchronize(s));
-  if (bottom) {
-    // prologue: the forward sweep of iteration 1 up to level b (the loop body starts above it)
-    ulv_solve_steps(F, ws, {SolveStep{SolveStep::FWD, L, b, /*no_exchange=*/true}}, s);
-  }
   auto iteration = [&](cudaStream_t st) {
-    if (!bottom) {
-      ulv_solve_tree(F, ws, st);
-      launch_pdl(admm_epilogue_kernel, dim3(nleaf), dim3(256), epi_smem, st, EA, H.leaf_lo.p, (const int*)nullptr,
-                 nleaf, part.p, epi_out, counter.p, smem_tree);
-      return;
-    }
-    std::vector<SolveStep> top;
-    if (sh.on() && sh.lg == b) top.push_back(SolveStep{SolveStep::EXCHANGE});
-    top.push_back(SolveStep{SolveStep::FWD, b - 1, 0});
-    top.push_back(SolveStep{SolveStep::BWD, 0, b - 1});
-    ulv_solve_steps(F, ws, top, st);
-    bottom_dispatch(nC, EA, dfn.p, (int)fnodes.size(), F.lv[b].M.p, ws.xout[b - 1], ws.yr[b], ws.xout[b], ws.fin[b],
-                    ws.fin[b - 1], chunkp.p, part.p, st);
-    if (!gleaves.empty()) {
-      ulv_solve_steps(F, ws, {SolveStep{SolveStep::BWD_LIST, b, 0, false, dgbwk.p, (int)gbwk.size()},
-                              SolveStep{SolveStep::BWD, L, L}}, st);
-      admm_epilogue_kernel<<<(unsigned)gleaves.size(), 256, epi_smem, st>>>(EA, H.leaf_lo.p, dgleaves.p, nleaf,
-                                                                           part.p, nullptr, nullptr, 0);
-      LAUNCH_CHECK();
-      ulv_solve_steps(F, ws, {SolveStep{SolveStep::FWD, L, L, true},
-                              SolveStep{SolveStep::FWD_LIST, b, 0, false, dgwk.p, (int)gwk.size()}}, st);
-    }
-    tree_reduce_local(H, part.p, nC, epi_out, st);
+    ulv_solve_tree(F, ws, st);
+    launch_pdl(admm_epilogue_kernel, dim3(nleaf), dim3(256), epi_smem, st, EA, H.leaf_lo.p, (const int*)nullptr,
+               nleaf, part.p, epi_out, counter.p, smem_tree);
   };
   // one iteration as a CUDA graph (needs a capturable exchange when sharded)
   cudaGraphExec_t gexec = nullptr;
@@ -614,13 +420,22 @@ __global__ void predict_finish_kernel(const double* __restrict__ S, int64_t m, i
   if (lab) lab[e] = (d >= 0.0) ? (int8_t)1 : (int8_t)-1;
 }
 
-__global__ void pad_coef_kernel(const double* __restrict__ coef, int64_t n, int nC, int ld,
-                                double* __restrict__ out) {
+// coefficients z_y = y o z, padded to ld columns: out[i*ld + c] = y_i z[i*nC + c] (c < nC)
+__global__ void coef_kernel(const double* __restrict__ y, const double* __restrict__ z, int64_t n, int nC, int ld,
+                            double* __restrict__ out) {
   const int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
   if (e >= n * ld) return;
   const int64_t i = e / ld;
   const int c = (int)(e % ld);
-  out[e] = (c < nC) ? coef[i * nC + c] : 0.0;
+  out[e] = (c < nC) ? y[i] * z[i * nC + c] : 0.0;
+}
+
+__global__ void pad_coef16_kernel(const double* __restrict__ coef, int64_t n, int ld, double* __restrict__ out) {
+  const int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (e >= n * 16) return;
+  const int64_t i = e / 16;
+  const int c = (int)(e % 16);
+  out[e] = (c < ld) ? coef[i * ld + c] : 0.0;
 }
 
 __global__ void copy_cols_kernel(const double* __restrict__ src, int64_t m, int lds, int ldd, double* __restrict__ dst) {
@@ -629,44 +444,82 @@ __global__ void copy_cols_kernel(const double* __restrict__ src, int64_t m, int 
   dst[e] = src[(e / ldd) * lds + e % ldd];
 }
 
-void predict_impl(const double* Ftrain, const double* coef, int64_t n, int r, double h,
-                  const double* bias_host, int nC, const double* Ftest, int64_t m, double* dv,
-                  int8_t* lab, cudaStream_t s) {
-  const int rp = (r + 3) / 4 * 4;
-  const int SA = predict_stride(rp);
-  const int ld = nC <= 1 ? 1 : nC <= 2 ? 2 : nC <= 4 ? 4 : nC <= 8 ? 8 : 16;
-  DevBuf<double> Ftr((size_t)n * SA), Fte((size_t)std::max<int64_t>(1, m) * SA), nutr(n + kNormPad),
-      nute(std::max<int64_t>(1, m) + kNormPad), W((size_t)n * ld + 2), S((size_t)std::max<int64_t>(1, m) * ld), b(nC);
-  pad_rows(Ftrain, n, r, SA, Ftr.p, s);
+// dv / labels of test rows [0, m) (this rank's share when sharded: the caller offsets Ftest)
+static void predict_rows(const double* Ftr, const double* nutr, const double* coef, int64_t n, int r, int rp,
+                         int SA, int ld, const double* Ftrain, double h, const double* bias_dev, int nC,
+                         const double* Ftest, int64_t m, double* dv, int8_t* lab, cudaStream_t s) {
+  if (m <= 0) return;
+  DevBuf<double> Fte((size_t)m * SA), nute(m + kNormPad), S((size_t)m * ld);
   pad_rows(Ftest, m, r, SA, Fte.p, s);
-  row_norms(Ftr.p, n, SA, nutr.p, s);
   row_norms(Fte.p, m, SA, nute.p, s);
-  pad_coef_kernel<<<ceil_div(n * ld, 256), 256, 0, s>>>(coef, n, nC, ld, W.p);
-  LAUNCH_CHECK();
   if (rp <= 128) {
-    predict_sums(Fte.p, nute.p, m, Ftr.p, nutr.p, W.p, n, rp, SA, ld, -1.0 / (2.0 * h * h), S.p, s);
+    predict_sums(Fte.p, nute.p, m, Ftr, nutr, coef, n, rp, SA, ld, -1.0 / (2.0 * h * h), S.p, s);
   } else {
     // wide features (r > 128): the sketch kernel's shared-memory tiling (rows at stride rp),
     // with the coefficients as a 16-column right-hand side
-    DevBuf<double> Ftr2((size_t)n * rp), Fte2((size_t)std::max<int64_t>(1, m) * rp), W16((size_t)n * 16 + 2),
-        S16((size_t)std::max<int64_t>(1, m) * 16);
+    DevBuf<double> Ftr2((size_t)n * rp), Fte2((size_t)m * rp), W16((size_t)n * 16 + 2), S16((size_t)m * 16);
     pad_rows(Ftrain, n, r, rp, Ftr2.p, s);
     pad_rows(Ftest, m, r, rp, Fte2.p, s);
-    pad_coef_kernel<<<ceil_div(n * 16, 256), 256, 0, s>>>(coef, n, nC, 16, W16.p);
+    pad_coef16_kernel<<<ceil_div(n * 16, 256), 256, 0, s>>>(coef, n, ld, W16.p);
     LAUNCH_CHECK();
     KmmArgs a{};
     a.Fa = Fte2.p; a.nua = nute.p; a.na = m;
-    a.Fb = Ftr2.p; a.nub = nutr.p; a.nb = n;
+    a.Fb = Ftr2.p; a.nub = nutr; a.nb = n;
     a.rp = rp; a.W = W16.p; a.ldw = 16; a.ncols = 16; a.S = S16.p; a.lds = 16;
     a.neg_inv_2h2 = -1.0 / (2.0 * h * h);
     a.same_set = 0; a.leaf_a = nullptr; a.leaf_b = nullptr;
     kernel_matmul(a, s);
-    copy_cols_kernel<<<ceil_div(std::max<int64_t>(1, m) * ld, 256), 256, 0, s>>>(S16.p, m, 16, ld, S.p);
+    copy_cols_kernel<<<ceil_div(m * ld, 256), 256, 0, s>>>(S16.p, m, 16, ld, S.p);
     LAUNCH_CHECK();
   }
-  h2d(b.p, bias_host, nC, s);
-  predict_finish_kernel<<<ceil_div(m * nC, 256), 256, 0, s>>>(S.p, m, nC, ld, b.p, dv, lab);
+  predict_finish_kernel<<<ceil_div(m * nC, 256), 256, 0, s>>>(S.p, m, nC, ld, bias_dev, dv, lab);
   LAUNCH_CHECK();
+}
+
+__global__ void labels_kernel(const double* __restrict__ dv, int64_t e_tot, int8_t* __restrict__ lab) {
+  const int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (e < e_tot) lab[e] = (dv[e] >= 0.0) ? (int8_t)1 : (int8_t)-1;
+}
+
+void predict_impl(const double* Ftrain, const double* y, const double* z, int64_t n, int r, double h,
+                  const double* bias_host, int nC, const double* Ftest, int64_t m, double* dv,
+                  int8_t* lab, Comm* comm, cudaStream_t s) {
+  const int rp = (r + 3) / 4 * 4;
+  const int SA = predict_stride(rp);
+  const int ld = nC <= 1 ? 1 : nC <= 2 ? 2 : nC <= 4 ? 4 : nC <= 8 ? 8 : 16;
+  DevBuf<double> Ftr((size_t)n * SA), nutr(n + kNormPad), W((size_t)n * ld + 2), b(nC);
+  pad_rows(Ftrain, n, r, SA, Ftr.p, s);
+  row_norms(Ftr.p, n, SA, nutr.p, s);
+  CUDA_CHECK(cudaMemsetAsync(W.p + (size_t)n * ld, 0, 2 * sizeof(double), s));
+  coef_kernel<<<ceil_div(n * ld, 256), 256, 0, s>>>(y, z, n, nC, ld, W.p);
+  LAUNCH_CHECK();
+  h2d(b.p, bias_host, nC, s);
+  const int P = comm ? comm->size : 1;
+  if (P == 1) {
+    predict_rows(Ftr.p, nutr.p, W.p, n, r, rp, SA, ld, Ftrain, h, b.p, nC, Ftest, m, dv, lab, s);
+    CUDA_CHECK(cudaStreamSynchronize(s));
+    return;
+  }
+  // test points sharded: rank g takes [m g / P, m (g+1) / P); one allgather of the decision values
+  auto lo = [&](int g) { return (int64_t)((__int128)m * g / P); };
+  int64_t slot_rows = 0;
+  for (int g = 0; g < P; ++g) slot_rows = std::max(slot_rows, lo(g + 1) - lo(g));
+  const int64_t slot = std::max<int64_t>(1, slot_rows * nC);
+  const int64_t l0 = lo(comm->rank), cnt = lo(comm->rank + 1) - l0;
+  DevBuf<double> send(slot), recv(slot * P), dfull(dv ? 0 : (size_t)m * nC);
+  predict_rows(Ftr.p, nutr.p, W.p, n, r, rp, SA, ld, Ftrain, h, b.p, nC, Ftest + l0 * r, cnt, send.p, nullptr, s);
+  comm->allgather(send.p, recv.p, slot * sizeof(double), s);
+  double* out = dv ? dv : dfull.p;
+  for (int g = 0; g < P; ++g) {
+    const int64_t c = lo(g + 1) - lo(g);
+    if (c > 0)
+      CUDA_CHECK(cudaMemcpyAsync(out + lo(g) * nC, recv.p + g * slot, (size_t)c * nC * sizeof(double),
+                                 cudaMemcpyDeviceToDevice, s));
+  }
+  if (lab) {
+    labels_kernel<<<ceil_div(m * nC, 256), 256, 0, s>>>(out, m * nC, lab);
+    LAUNCH_CHECK();
+  }
   CUDA_CHECK(cudaStreamSynchronize(s));
 }
 

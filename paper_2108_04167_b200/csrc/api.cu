@@ -3,40 +3,104 @@
 #include <chrono>
 #include <cmath>
 #include <cstring>
+#include <mutex>
 #include "internal.cuh"
 
 namespace svmhss {
 static thread_local std::string g_last_error;
 std::atomic<long long> g_launches{0};
 thread_local cudaStream_t g_alloc_stream = nullptr;
-void init_mem_pool() {
-  static thread_local int done_dev = -1;
+// One pool per device, created on first use (never reconfigure the device's default
+// pool, which torch's cudaMallocAsync backend shares).  live[dev] counts this device's alive
+// hss_t / ulv_t handles; when it drops to zero the pool is trimmed back to nothing.
+static std::mutex g_pool_mu;
+static std::vector<cudaMemPool_t> g_pools;
+static std::vector<int> g_live;
+static std::vector<size_t> g_reserved;   // pool_reserve's current reservation, per device
+
+static int cur_device() {
   int dev = 0;
-  if (cudaGetDevice(&dev) != cudaSuccess || dev == done_dev) return;
-  cudaMemPool_t pool;
-  if (cudaDeviceGetDefaultMemPool(&pool, dev) == cudaSuccess) {
-    uint64_t thr = UINT64_MAX;
-    cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &thr);
-  }
-  done_dev = dev;
+  CUDA_CHECK(cudaGetDevice(&dev));
+  return dev;
 }
+
+cudaMemPool_t lib_pool() {
+  const int dev = cur_device();
+  std::lock_guard<std::mutex> g(g_pool_mu);
+  if ((int)g_pools.size() <= dev) {
+    g_pools.resize(dev + 1, nullptr);
+    g_live.resize(dev + 1, 0);
+    g_reserved.resize(dev + 1, 0);
+  }
+  if (!g_pools[dev]) {
+    cudaMemPoolProps props = {};
+    props.allocType = cudaMemAllocationTypePinned;
+    props.handleTypes = cudaMemHandleTypeNone;
+    props.location.type = cudaMemLocationTypeDevice;
+    props.location.id = dev;
+    cudaMemPool_t pool;
+    CUDA_CHECK(cudaMemPoolCreate(&pool, &props));
+    uint64_t thr = UINT64_MAX;
+    CUDA_CHECK(cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &thr));
+    g_pools[dev] = pool;
+  }
+  return g_pools[dev];
+}
+
+void lib_malloc(void** p, size_t bytes, cudaStream_t s) {
+  CUDA_CHECK(cudaMallocFromPoolAsync(p, bytes, lib_pool(), s));
+}
+
+// handle bookkeeping (hss_t / ulv_t of the current device)
+static void handle_acquired() {
+  const int dev = cur_device();
+  lib_pool();
+  std::lock_guard<std::mutex> g(g_pool_mu);
+  ++g_live[dev];
+}
+static void handle_released(int dev) {
+  cudaMemPool_t pool = nullptr;
+  {
+    std::lock_guard<std::mutex> g(g_pool_mu);
+    if (dev < 0 || dev >= (int)g_live.size()) return;
+    if (--g_live[dev] > 0) return;
+    pool = g_pools[dev];
+    g_reserved[dev] = 0;
+  }
+  if (!pool) return;
+  int prev = 0;
+  cudaGetDevice(&prev);
+  cudaSetDevice(dev);
+  cudaDeviceSynchronize();   // every stream-ordered free of the pool has completed
+  cudaMemPoolTrimTo(pool, 0);
+  cudaSetDevice(prev);
+  cudaGetLastError();
+}
+
 // Memory-pool reservation ahead of a build: one physical chunk of about the problem's peak
 // footprint (sketch operands, generators, factor and its per-level temporaries ~ 24 n (s + r) 8
 // bytes), capped at half the free memory, so the stream-ordered allocations of build / factor /
 // ADMM sub-allocate from it instead of growing the pool (mapping GBs) in the middle of a
 // factorization.  SVMHSS_POOL_RESERVE_GB overrides the estimate (0 disables).
 static void pool_reserve(int64_t n, int r, int s_cols, cudaStream_t st) {
-  static thread_local size_t reserved = 0;
+  const int dev = cur_device();
+  cudaMemPool_t pool = lib_pool();
   const char* e = getenv("SVMHSS_POOL_RESERVE_GB");
   double want = e ? atof(e) * 1e9 : 24.0 * (double)n * (double)(s_cols + r) * 8.0;
   size_t fr = 0, tot = 0;
   if (cudaMemGetInfo(&fr, &tot) != cudaSuccess) { cudaGetLastError(); return; }
+  size_t reserved;
+  {
+    std::lock_guard<std::mutex> g(g_pool_mu);
+    reserved = g_reserved[dev];
+  }
   want = std::min(want, 0.5 * (double)fr + (double)reserved);
   if (want <= (double)reserved + 64e6) return;
   void* p = nullptr;
-  if (cudaMallocAsync(&p, (size_t)want, st) == cudaSuccess) {
+  if (cudaMallocFromPoolAsync(&p, (size_t)want, pool, st) == cudaSuccess) {
     cudaFreeAsync(p, st);
-    reserved = (size_t)want;
+    std::lock_guard<std::mutex> g(g_pool_mu);
+    g_reserved[dev] = (size_t)want;
   } else {
     cudaGetLastError();
   }
@@ -173,8 +237,8 @@ static void validate_opts(const hss_opts* o, int64_t n, int32_t r, double h) {
 
 using namespace svmhss;
 
-struct hss_s { HSSImpl* impl; };
-struct ulv_s { ULVImpl* impl; };
+struct hss_s { HSSImpl* impl; int dev; };
+struct ulv_s { ULVImpl* impl; int dev; };
 struct hss_comm_s { std::shared_ptr<Comm> c; };
 
 static std::shared_ptr<Comm> comm_of(const hss_opts* o) {
@@ -194,7 +258,9 @@ int hss_build(const double* F, int64_t n, int32_t r, double h, const hss_opts* o
     require(out != nullptr && F != nullptr, "hss_build: NULL pointer");
     validate_opts(opt, n, r, h);
     pool_reserve(n, r, opt->max_rank + opt->oversample, (cudaStream_t)stream);
-    *out = new hss_s{build_adaptive(F, n, r, h, *opt, comm_of(opt), (cudaStream_t)stream)};
+    HSSImpl* H = build_adaptive(F, n, r, h, *opt, comm_of(opt), (cudaStream_t)stream);
+    handle_acquired();
+    *out = new hss_s{H, cur_device()};
   });
 }
 
@@ -295,7 +361,8 @@ int hss_ulv_factor(hss_t Hh, double beta, void* stream, ulv_t* out) {
       delete F;
       throw;
     }
-    *out = new ulv_s{F};
+    handle_acquired();
+    *out = new ulv_s{F, cur_device()};
   });
 }
 
@@ -310,17 +377,28 @@ int ulv_solve(ulv_t Uh, const double* b, double* x, int32_t nrhs, void* stream) 
   return guarded([&] {
     StreamScope ss__((cudaStream_t)stream);
     require(Uh && b && x, "ulv_solve: NULL pointer");
-    require(nrhs >= 1 && nrhs <= 8, "ulv_solve: nrhs must be in 1..8");
+    require(nrhs >= 1, "ulv_solve: nrhs must be >= 1");
     const ULVImpl& F = *Uh->impl;
     const HSSImpl& H = *F.H;
     cudaStream_t s = (cudaStream_t)stream;
-    SolveWS ws;
-    solve_ws_alloc(F, nrhs, ws);
-    DevBuf<double> full((size_t)H.n * nrhs);
-    gather_rows(b, H.perm.p + H.lo_g, H.nloc(), nrhs, ws.fin[H.L], s);
+    const int64_t nl = H.nloc();
+    DevBuf<double> bt((size_t)std::max<int64_t>(1, nl) * nrhs), xt((size_t)std::max<int64_t>(1, nl) * nrhs),
+        full((size_t)H.n * nrhs);
+    gather_rows(b, H.perm.p + H.lo_g, nl, nrhs, bt.p, s);
     CUDA_CHECK(cudaStreamSynchronize(s));  // b and x may alias
-    ulv_solve_tree(F, ws, s);
-    gather_points(H, ws.xout[H.L], nrhs, full.p, s);
+    // the sweep kernels take up to 8 right-hand sides: groups of 8 columns
+    for (int c0 = 0; c0 < nrhs; c0 += 8) {
+      const int w = std::min(8, nrhs - c0);
+      SolveWS ws;
+      solve_ws_alloc(F, w, ws);
+      if (nl > 0)
+        CUDA_CHECK(cudaMemcpy2DAsync(ws.fin[H.L], w * 8, bt.p + c0, nrhs * 8, w * 8, nl, cudaMemcpyDeviceToDevice, s));
+      ulv_solve_tree(F, ws, s);
+      if (nl > 0)
+        CUDA_CHECK(cudaMemcpy2DAsync(xt.p + c0, nrhs * 8, ws.xout[H.L], w * 8, w * 8, nl, cudaMemcpyDeviceToDevice, s));
+      CUDA_CHECK(cudaStreamSynchronize(s));
+    }
+    gather_points(H, xt.p, nrhs, full.p, s);
     scatter_rows(full.p, H.perm.p, H.n, nrhs, x, s);
     CUDA_CHECK(cudaStreamSynchronize(s));
   });
@@ -332,35 +410,69 @@ int admm_svm_train(ulv_t Uh, const double* y, const double* C, int32_t nC, int32
   return guarded([&] {
     StreamScope ss__((cudaStream_t)stream);
     require(Uh && y && C && z_out, "admm_svm_train: NULL pointer");
-    require(nC >= 1 && nC <= 8, "admm_svm_train: nC must be in 1..8");
+    require(nC >= 1, "admm_svm_train: nC must be >= 1");
     require(max_it >= 1, "admm_svm_train: max_it must be >= 1");
     std::vector<double> Cs(C, C + nC);
     for (double c : Cs) require(std::isfinite(c) && c > 0, "admm_svm_train: every C must be > 0");
-    AdmmResult r = admm_train_impl(*Uh->impl, y, Cs, max_it, opt, z_out, mu_out, bias_out, obj_out,
-                                   (cudaStream_t)stream);
-    if (st) {
-      st->w1 = r.w1;
-      st->ms_precompute = r.ms_pre;
-      st->ms_loop = r.ms_loop;
-      st->ms_bias = r.ms_bias;
-      st->iterations = max_it;
-      st->graph = r.graph;
-      st->kernel_launches_per_iter = r.launches;
+    cudaStream_t s = (cudaStream_t)stream;
+    const int64_t n = Uh->impl->H->n;
+    if (nC <= 8) {
+      AdmmResult r = admm_train_impl(*Uh->impl, y, Cs, max_it, opt, z_out, mu_out, bias_out, obj_out, s);
+      if (st) {
+        st->w1 = r.w1; st->ms_precompute = r.ms_pre; st->ms_loop = r.ms_loop; st->ms_bias = r.ms_bias;
+        st->iterations = max_it; st->graph = r.graph; st->kernel_launches_per_iter = r.launches;
+      }
+      return;
+    }
+    // groups of at most 8 problems (the sweep kernels' widest right-hand side); each group is an
+    // independent ADMM run, its outputs copied into its columns of the nC-wide outputs
+    const int te = (opt && opt->trace_every > 0) ? opt->trace_every : 0;
+    const int64_t ntr = te ? (max_it + te - 1) / te : 0;
+    if (st) *st = admm_stats{};
+    for (int c0 = 0; c0 < nC; c0 += 8) {
+      const int w = std::min(8, nC - c0);
+      std::vector<double> Cg(Cs.begin() + c0, Cs.begin() + c0 + w), bg(w), og(w);
+      DevBuf<double> zg((size_t)n * w), mg(mu_out ? (size_t)n * w : 0);
+      DevBuf<double> tz((te && opt->trace_z) ? (size_t)ntr * n * w : 0), tm((te && opt->trace_mu) ? (size_t)ntr * n * w : 0);
+      admm_opts og_opt{};
+      if (opt) og_opt = *opt;
+      og_opt.trace_z = tz.p;
+      og_opt.trace_mu = tm.p;
+      AdmmResult r = admm_train_impl(*Uh->impl, y, Cg, max_it, &og_opt, zg.p, mu_out ? mg.p : nullptr,
+                                     bg.data(), og.data(), s);
+      auto put = [&](double* dst, const double* src, int64_t rows) {
+        CUDA_CHECK(cudaMemcpy2DAsync(dst + c0, (size_t)nC * 8, src, (size_t)w * 8, (size_t)w * 8, rows,
+                                     cudaMemcpyDeviceToDevice, s));
+      };
+      put(z_out, zg.p, n);
+      if (mu_out) put(mu_out, mg.p, n);
+      if (tz.p) put(opt->trace_z, tz.p, ntr * n);
+      if (tm.p) put(opt->trace_mu, tm.p, ntr * n);
+      CUDA_CHECK(cudaStreamSynchronize(s));
+      for (int c = 0; c < w; ++c) {
+        if (bias_out) bias_out[c0 + c] = bg[c];
+        if (obj_out) obj_out[c0 + c] = og[c];
+      }
+      if (st) {
+        st->w1 = r.w1; st->ms_precompute += r.ms_pre; st->ms_loop += r.ms_loop; st->ms_bias += r.ms_bias;
+        st->iterations = max_it; st->graph = r.graph; st->kernel_launches_per_iter += r.launches;
+      }
     }
   });
 }
 
-int svm_predict(const double* Ftrain, const double* coef, int64_t n, int32_t r, double h,
+int svm_predict(const double* Ftrain, const double* y, const double* z, int64_t n, int32_t r, double h,
                 const double* bias, int32_t nC, const double* Ftest, int64_t m, double* dv_out,
-                int8_t* label_out, void* stream) {
+                int8_t* label_out, hss_comm_t comm, void* stream) {
   return guarded([&] {
     StreamScope ss__((cudaStream_t)stream);
-    require(Ftrain && coef && bias && (Ftest || m == 0), "svm_predict: NULL pointer");
+    require(Ftrain && y && z && bias && (Ftest || m == 0), "svm_predict: NULL pointer");
     require(n >= 1 && r >= 1 && m >= 0, "svm_predict: bad sizes");
     require(nC >= 1 && nC <= 16, "svm_predict: nC must be in 1..16");
     require(std::isfinite(h) && h > 0, "svm_predict: h must be > 0");
     if (m == 0) return;
-    predict_impl(Ftrain, coef, n, r, h, bias, nC, Ftest, m, dv_out, label_out, (cudaStream_t)stream);
+    predict_impl(Ftrain, y, z, n, r, h, bias, nC, Ftest, m, dv_out, label_out, comm ? comm->c.get() : nullptr,
+                 (cudaStream_t)stream);
   });
 }
 
@@ -372,6 +484,7 @@ int svm_train_predict_host(const double* F, const double* y, int64_t n, int32_t 
   return guarded([&] {
     require(F && y && C && z_out, "svm_train_predict_host: NULL pointer");
     require(nC >= 1 && nC <= 8, "svm_train_predict_host: nC must be in 1..8");
+    require(!(labels_out && m > 0) || Ftest, "svm_train_predict_host: NULL Ftest");
     validate_opts(opt, n, r, h);
     cudaStream_t s;
     CUDA_CHECK(cudaStreamCreateWithFlags(&s, cudaStreamNonBlocking));
@@ -382,7 +495,7 @@ int svm_train_predict_host(const double* F, const double* y, int64_t n, int32_t 
     struct EG { cudaEvent_t* e; ~EG() { for (int i = 0; i < 8; ++i) cudaEventDestroy(e[i]); } } eg{ev};
     CUDA_CHECK(cudaEventRecord(ev[0], s));
     DevBuf<double> dF((size_t)n * r), dy(n), dFt((size_t)std::max<int64_t>(1, m) * r);
-    DevBuf<double> dz((size_t)n * nC), coef((size_t)n * nC);
+    DevBuf<double> dz((size_t)n * nC);
     DevBuf<int8_t> dl((size_t)std::max<int64_t>(1, m) * nC);
     h2d(dF.p, F, (size_t)n * r, s);
     h2d(dy.p, y, n, s);
@@ -402,16 +515,8 @@ int svm_train_predict_host(const double* F, const double* y, int64_t n, int32_t 
     AdmmResult ar = admm_train_impl(Fz, dy.p, Cs, max_it, nullptr, dz.p, nullptr, bias.data(), obj.data(), s);
     CUDA_CHECK(cudaEventRecord(ev[4], s));
     CUDA_CHECK(cudaEventRecord(ev[5], s));
-    if (labels_out && m > 0) {
-      // coef = y * z (original order)
-      std::vector<double> zh((size_t)n * nC);
-      d2h(zh.data(), dz.p, (size_t)n * nC, s);
-      CUDA_CHECK(cudaStreamSynchronize(s));
-      for (int64_t i = 0; i < n; ++i)
-        for (int c = 0; c < nC; ++c) zh[i * nC + c] *= y[i];
-      h2d(coef.p, zh.data(), (size_t)n * nC, s);
-      predict_impl(dF.p, coef.p, n, r, h, bias.data(), nC, dFt.p, m, nullptr, dl.p, s);
-    }
+    if (labels_out && m > 0)
+      predict_impl(dF.p, dy.p, dz.p, n, r, h, bias.data(), nC, dFt.p, m, nullptr, dl.p, comm_of(opt).get(), s);
     CUDA_CHECK(cudaEventRecord(ev[6], s));
     d2h(z_out, dz.p, (size_t)n * nC, s);
     if (labels_out && m > 0) d2h(labels_out, dl.p, (size_t)m * nC, s);
@@ -558,16 +663,37 @@ void hss_comm_free(hss_comm_t c) { delete c; }
 
 void hss_free(hss_t H) {
   if (!H) return;
+  int prev = 0;
+  cudaGetDevice(&prev);
+  cudaSetDevice(H->dev);  // device buffers are released on their own device
   release_hss(H->impl);
+  cudaSetDevice(prev);
+  handle_released(H->dev);
   delete H;
 }
 
 void ulv_free(ulv_t U) {
   if (!U) return;
+  int prev = 0;
+  cudaGetDevice(&prev);
+  cudaSetDevice(U->dev);
   HSSImpl* H = U->impl->H;
   delete U->impl;
   release_hss(H);
+  cudaSetDevice(prev);
+  handle_released(U->dev);
   delete U;
+}
+
+int hss_pool_trim(void) {
+  return guarded([&] {
+    const int dev = cur_device();
+    cudaMemPool_t pool = lib_pool();
+    CUDA_CHECK(cudaDeviceSynchronize());
+    CUDA_CHECK(cudaMemPoolTrimTo(pool, 0));
+    std::lock_guard<std::mutex> g(g_pool_mu);
+    g_reserved[dev] = 0;
+  });
 }
 
 }  // extern "C"

@@ -40,14 +40,17 @@ inline void require(bool ok, const std::string& msg) {
 }
 
 // ------------------------------------------------------------------ device buffers
-// Stream-ordered allocations from the device's default memory pool (release threshold set
-// to "never", so steady-state steps do not call the driver allocator and cudaFree never
-// forces a device synchronization).  The allocation stream is the library call's stream.
+// Stream-ordered allocations from the library's own memory pool on the current device
+// (cudaMemPoolCreate, release threshold "never" while handles are alive, so steady-state steps
+// do not call the driver allocator and cudaFree never forces a device synchronization; trimmed
+// when the device's last hss_t / ulv_t is freed).  The device's default pool (torch's
+// cudaMallocAsync backend) is never touched.  The allocation stream is the library call's stream.
 extern thread_local cudaStream_t g_alloc_stream;
-void init_mem_pool();
+cudaMemPool_t lib_pool();                  // the current device's pool (created on first use)
+void lib_malloc(void** p, size_t bytes, cudaStream_t s);   // throws Error on failure
 struct StreamScope {  // sets the allocation stream for the duration of an API call
   cudaStream_t prev;
-  explicit StreamScope(cudaStream_t s) : prev(g_alloc_stream) { init_mem_pool(); g_alloc_stream = s; }
+  explicit StreamScope(cudaStream_t s) : prev(g_alloc_stream) { g_alloc_stream = s; }
   ~StreamScope() { g_alloc_stream = prev; }
 };
 
@@ -62,7 +65,7 @@ struct DevBuf {
     release();
     n = count;
     st = g_alloc_stream;
-    if (count) CUDA_CHECK(cudaMallocAsync((void**)&p, count * sizeof(T), st));
+    if (count) lib_malloc((void**)&p, count * sizeof(T), st);
   }
   void release() {
     if (p) cudaFreeAsync(p, st);

@@ -1,6 +1,6 @@
 // dense.cu — batched small dense fp64 kernels (one problem = one HSS tree node).
 //
-//  bgemm   : smem-tiled DFMA GEMM with arbitrary strides (sibling updates H4, Omega' = U^T Omega^,
+//  bgemm   : FP64 tensor-core (DMMA) batched GEMM with arbitrary strides (sibling updates H4, Omega' = U^T Omega^,
 //            R_a B R_b^T, Q^T D Q, the explicit solve operators of the ULV).
 //  bpotrf  : left-looking Cholesky, one CTA per node (U: Dc_rr = L_r L_r^T; root).
 //  btrsm   : blocked triangular solve with many right-hand sides (T = R11^-1 R12 in H3;
@@ -19,7 +19,7 @@ namespace cg = cooperative_groups;
 template <typename P>
 static P* upload_probs(const std::vector<P>& v, cudaStream_t s) {
   P* d = nullptr;
-  CUDA_CHECK(cudaMallocAsync((void**)&d, v.size() * sizeof(P), s));
+  lib_malloc((void**)&d, v.size() * sizeof(P), s);
   CUDA_CHECK(cudaMemcpyAsync(d, v.data(), v.size() * sizeof(P), cudaMemcpyHostToDevice, s));
   return d;
 }
@@ -31,197 +31,6 @@ __device__ __forceinline__ void dmma884_(double& d0, double& d1, double a, doubl
 }
 
 // ------------------------------------------------------------------ GEMM
-// 128 x 64 x 8 tiles, 256 threads, 8 x 4 outputs per thread (DFMA), register-prefetched
-// double-buffered shared-memory tiles; any operand strides (coalesced load mapping chosen
-// per operand from its unit stride).
-constexpr int GBM = 128, GBN = 64, GBK = 8;
-
-__global__ void __launch_bounds__(256, 2) bgemm_kernel(const GemmProb* __restrict__ probs) {
-  const GemmProb P = probs[blockIdx.z];
-  const int m0 = blockIdx.y * GBM, n0 = blockIdx.x * GBN;
-  if (m0 >= P.m || n0 >= P.n) return;
-  // rows padded by 2 doubles: the transposing stores (8 consecutive threads -> 8 k-rows) hit
-  // 8 distinct bank pairs instead of one bank 8 times; double2 reads stay 16-byte aligned
-  __shared__ __align__(16) double As[2][GBK][GBM + 2];
-  __shared__ __align__(16) double Bs[2][GBK][GBN + 2];
-  const int tid = threadIdx.x, tx = tid & 15, ty = tid >> 4;
-  const bool a_rm = (P.acs == 1), b_rm = (P.bcs == 1);
-  double acc[8][4];
-#pragma unroll
-  for (int i = 0; i < 8; ++i)
-#pragma unroll
-    for (int j = 0; j < 4; ++j) acc[i][j] = 0.0;
-  double ra[4], rb[2];
-  auto load = [&](int k0) {
-#pragma unroll
-    for (int q = 0; q < 4; ++q) {
-      const int e = tid + 256 * q;
-      int i, kk;
-      if (a_rm) { i = e >> 3; kk = e & 7; } else { i = e & 127; kk = e >> 7; }
-      const int gi = m0 + i, gk = k0 + kk;
-      ra[q] = (gi < P.m && gk < P.k) ? P.A[(long long)gi * P.ars + (long long)gk * P.acs] : 0.0;
-    }
-#pragma unroll
-    for (int q = 0; q < 2; ++q) {
-      const int e = tid + 256 * q;
-      int j, kk;
-      if (b_rm) { kk = e >> 6; j = e & 63; } else { j = e >> 3; kk = e & 7; }
-      const int gj = n0 + j, gk = k0 + kk;
-      rb[q] = (gj < P.n && gk < P.k) ? P.B[(long long)gk * P.brs + (long long)gj * P.bcs] : 0.0;
-    }
-  };
-  auto store = [&](int buf) {
-#pragma unroll
-    for (int q = 0; q < 4; ++q) {
-      const int e = tid + 256 * q;
-      int i, kk;
-      if (a_rm) { i = e >> 3; kk = e & 7; } else { i = e & 127; kk = e >> 7; }
-      As[buf][kk][i] = ra[q];
-    }
-#pragma unroll
-    for (int q = 0; q < 2; ++q) {
-      const int e = tid + 256 * q;
-      int j, kk;
-      if (b_rm) { kk = e >> 6; j = e & 63; } else { j = e >> 3; kk = e & 7; }
-      Bs[buf][kk][j] = rb[q];
-    }
-  };
-  const int nk = (P.k + GBK - 1) / GBK;
-  load(0);
-  store(0);
-  __syncthreads();
-  for (int t = 0; t < nk; ++t) {
-    const int buf = t & 1;
-    if (t + 1 < nk) load((t + 1) * GBK);
-#pragma unroll
-    for (int kk = 0; kk < GBK; ++kk) {
-      const double2* ap = reinterpret_cast<const double2*>(&As[buf][kk][ty * 8]);
-      // columns 2tx, 2tx+1, 32+2tx, 33+2tx: 8 consecutive threads read 128 contiguous bytes
-      const double2 b01 = *reinterpret_cast<const double2*>(&Bs[buf][kk][2 * tx]);
-      const double2 b23 = *reinterpret_cast<const double2*>(&Bs[buf][kk][32 + 2 * tx]);
-      double a[8];
-#pragma unroll
-      for (int q = 0; q < 4; ++q) { const double2 v = ap[q]; a[2 * q] = v.x; a[2 * q + 1] = v.y; }
-#pragma unroll
-      for (int i = 0; i < 8; ++i) {
-        acc[i][0] = fma(a[i], b01.x, acc[i][0]);
-        acc[i][1] = fma(a[i], b01.y, acc[i][1]);
-        acc[i][2] = fma(a[i], b23.x, acc[i][2]);
-        acc[i][3] = fma(a[i], b23.y, acc[i][3]);
-      }
-    }
-    if (t + 1 < nk) store(buf ^ 1);
-    __syncthreads();
-  }
-#pragma unroll
-  for (int i = 0; i < 8; ++i) {
-    const int gi = m0 + ty * 8 + i;
-    if (gi >= P.m) continue;
-#pragma unroll
-    for (int j = 0; j < 4; ++j) {
-      const int gj = n0 + (j < 2 ? 2 * tx + j : 32 + 2 * tx + (j - 2));
-      if (gj >= P.n) continue;
-      double* c = P.C + (long long)gi * P.crs + (long long)gj * P.ccs;
-      const double v = P.alpha * acc[i][j];
-      *c = (P.beta == 0.0) ? v : fma(P.beta, *c, v);
-    }
-  }
-}
-
-// 128 x 128 x 8 tiles, 256 threads, 8 x 8 outputs per thread (rows 8ty.., columns
-// {4tx.., 64+4tx..}): 64 independent FMA chains per k and 8 FMAs per 16-byte shared load; one
-// CTA per SM (registers).  Same per-element k order as bgemm_kernel.
-constexpr int HBM_ = 128, HBN = 128;
-
-__global__ void __launch_bounds__(256, 1) bgemm_big_kernel(const GemmProb* __restrict__ probs) {
-  const GemmProb P = probs[blockIdx.z];
-  const int m0 = blockIdx.y * HBM_, n0 = blockIdx.x * HBN;
-  if (m0 >= P.m || n0 >= P.n) return;
-  __shared__ __align__(16) double As[2][GBK][HBM_ + 2];
-  __shared__ __align__(16) double Bs[2][GBK][HBN + 2];
-  const int tid = threadIdx.x, tx = tid & 15, ty = tid >> 4;
-  const bool a_rm = (P.acs == 1), b_rm = (P.bcs == 1);
-  double acc[8][8];
-#pragma unroll
-  for (int i = 0; i < 8; ++i)
-#pragma unroll
-    for (int j = 0; j < 8; ++j) acc[i][j] = 0.0;
-  double ra[4], rb[4];
-  auto load = [&](int k0) {
-#pragma unroll
-    for (int q = 0; q < 4; ++q) {
-      const int e = tid + 256 * q;
-      int i, kk;
-      if (a_rm) { i = e >> 3; kk = e & 7; } else { i = e & 127; kk = e >> 7; }
-      const int gi = m0 + i, gk = k0 + kk;
-      ra[q] = (gi < P.m && gk < P.k) ? P.A[(long long)gi * P.ars + (long long)gk * P.acs] : 0.0;
-    }
-#pragma unroll
-    for (int q = 0; q < 4; ++q) {
-      const int e = tid + 256 * q;
-      int j, kk;
-      if (b_rm) { kk = e >> 7; j = e & 127; } else { j = e >> 3; kk = e & 7; }
-      const int gj = n0 + j, gk = k0 + kk;
-      rb[q] = (gj < P.n && gk < P.k) ? P.B[(long long)gk * P.brs + (long long)gj * P.bcs] : 0.0;
-    }
-  };
-  auto store = [&](int buf) {
-#pragma unroll
-    for (int q = 0; q < 4; ++q) {
-      const int e = tid + 256 * q;
-      int i, kk;
-      if (a_rm) { i = e >> 3; kk = e & 7; } else { i = e & 127; kk = e >> 7; }
-      As[buf][kk][i] = ra[q];
-    }
-#pragma unroll
-    for (int q = 0; q < 4; ++q) {
-      const int e = tid + 256 * q;
-      int j, kk;
-      if (b_rm) { kk = e >> 7; j = e & 127; } else { j = e >> 3; kk = e & 7; }
-      Bs[buf][kk][j] = rb[q];
-    }
-  };
-  const int nk = (P.k + GBK - 1) / GBK;
-  load(0);
-  store(0);
-  __syncthreads();
-  for (int t = 0; t < nk; ++t) {
-    const int buf = t & 1;
-    if (t + 1 < nk) load((t + 1) * GBK);
-#pragma unroll
-    for (int kk = 0; kk < GBK; ++kk) {
-      const double2* ap = reinterpret_cast<const double2*>(&As[buf][kk][ty * 8]);
-      double a[8], b[8];
-#pragma unroll
-      for (int q = 0; q < 4; ++q) { const double2 v = ap[q]; a[2 * q] = v.x; a[2 * q + 1] = v.y; }
-#pragma unroll
-      for (int q = 0; q < 4; ++q) {  // columns 32q + 2tx, +1: 8 consecutive threads read 128 bytes
-        const double2 v = *reinterpret_cast<const double2*>(&Bs[buf][kk][32 * q + 2 * tx]);
-        b[2 * q] = v.x; b[2 * q + 1] = v.y;
-      }
-#pragma unroll
-      for (int i = 0; i < 8; ++i)
-#pragma unroll
-        for (int j = 0; j < 8; ++j) acc[i][j] = fma(a[i], b[j], acc[i][j]);
-    }
-    if (t + 1 < nk) store(buf ^ 1);
-    __syncthreads();
-  }
-#pragma unroll
-  for (int i = 0; i < 8; ++i) {
-    const int gi = m0 + ty * 8 + i;
-    if (gi >= P.m) continue;
-#pragma unroll
-    for (int j = 0; j < 8; ++j) {
-      const int gj = n0 + 32 * (j >> 1) + 2 * tx + (j & 1);
-      if (gj >= P.n) continue;
-      double* c = P.C + (long long)gi * P.crs + (long long)gj * P.ccs;
-      const double v = P.alpha * acc[i][j];
-      *c = (P.beta == 0.0) ? v : fma(P.beta, *c, v);
-    }
-  }
-}
-
 // FP64 tensor-core (DMMA m8n8k4) batched GEMM.  8 warps as 2 (m) x 4 (n); warp tile
 // (8 MT) x (8 NT), CTA tile (16 MT) x (32 NT), k in 16-wide shared-memory tiles, register
 // prefetch of the next tile (double buffered).  Operands are stored [row][k] (A) and [col][k]
@@ -355,24 +164,10 @@ void bgemm(const std::vector<GemmProb>& probs_in, cudaStream_t s) {
     std::vector<GemmProb> chunk(probs.begin() + b0,
                                 probs.begin() + std::min(probs.size(), b0 + 65535));
     GemmProb* d = upload_probs(chunk, s);
-    static const int dfma = [] { const char* e = getenv("SVMHSS_GEMM_DFMA"); return (e && e[0] == '1') ? 1 : 0; }();
-    if (!dfma) {
-      // FP64 tensor cores: 128 x 128 CTA tiles for the big factor GEMMs, 64 x 64 otherwise
-      static const int tile = [] { const char* e = getenv("SVMHSS_GEMM_TILE"); return e ? atoi(e) : 44; }();
-      if (maxm >= 256 && maxn >= 256) {
-        if (tile == 84) launch_dmma<8, 4, 1>(d, maxm, maxn, (unsigned)chunk.size(), s);
-        else if (tile == 82) launch_dmma<8, 2, 2>(d, maxm, maxn, (unsigned)chunk.size(), s);
-        else launch_dmma<4, 4, 2>(d, maxm, maxn, (unsigned)chunk.size(), s);
-      } else {
-        launch_dmma<4, 2, 2>(d, maxm, maxn, (unsigned)chunk.size(), s);
-      }
-    } else if (maxm >= 256 && maxn >= 256 && !getenv("SVMHSS_GEMM_SMALL")) {  // big batched GEMMs (factor)
-      dim3 grid(ceil_div(maxn, HBN), ceil_div(maxm, HBM_), (unsigned)chunk.size());
-      bgemm_big_kernel<<<grid, 256, 0, s>>>(d);
-    } else {
-      dim3 grid(ceil_div(maxn, GBN), ceil_div(maxm, GBM), (unsigned)chunk.size());
-      bgemm_kernel<<<grid, 256, 0, s>>>(d);
-    }
+    // FP64 tensor cores: 64 x 128 CTA tiles (two CTAs per SM) for the big factor GEMMs, 32 x 64
+    // otherwise (measured: 64 x 128 beat 128 x 128 and 128 x 64 at config 3)
+    if (maxm >= 256 && maxn >= 256) launch_dmma<4, 4, 2>(d, maxm, maxn, (unsigned)chunk.size(), s);
+    else launch_dmma<4, 2, 2>(d, maxm, maxn, (unsigned)chunk.size(), s);
     LAUNCH_CHECK();
     free_probs(d, s);
   }
@@ -533,8 +328,7 @@ void bpotrf(const std::vector<SqProb>& probs, int* d_info, cudaStream_t s) {
   int maxn = 0;
   for (auto& p : probs) maxn = std::max(maxn, p.n);
   SqProb* d = upload_probs(probs, s);
-  static const int tc = [] { const char* e = getenv("SVMHSS_POTRF_TC"); return (e && e[0] == '0') ? 0 : 1; }();
-  if (tc && maxn <= CMAX8) {
+  if (maxn <= CMAX8) {
     // (the panel width is chosen by the batch's largest node; bitwise P-invariance of the
     // sharded build therefore assumes all nodes of a level are on the same side of CMAX)
     if (maxn <= CMAX) {
@@ -773,8 +567,7 @@ void btrsm(const std::vector<TrsmProb>& probs_in, bool lower, cudaStream_t s) {
     std::vector<TrsmProb> chunk(probs.begin() + b0,
                                 probs.begin() + std::min(probs.size(), b0 + 65535));
     TrsmProb* d = upload_probs(chunk, s);
-    static const int tc = [] { const char* e = getenv("SVMHSS_TRSM_TC"); return (e && e[0] == '0') ? 0 : 1; }();
-    if (tc && maxn <= SMAXN) {
+    if (maxn <= SMAXN) {
       const size_t smem = ((size_t)((maxn + 7) & ~7) * SXS + (size_t)((maxn + 15) / 16) * 16 * SDS) * sizeof(double);
       dim3 grid(ceil_div(maxr, SW_), (unsigned)chunk.size());
       std::vector<long long> doff(chunk.size());
@@ -1164,8 +957,7 @@ void bgeqr2(const std::vector<QrProb>& probs, cudaStream_t s) {
   int maxm = 0;
   for (auto& p : probs) maxm = std::max(maxm, p.m);
   QrProb* d = upload_probs(probs, s);
-  static const int tc = [] { const char* e = getenv("SVMHSS_QR_TC"); return (e && e[0] == '0') ? 0 : 1; }();
-  if (tc && maxm <= QMAX) {
+  if (maxm <= QMAX) {
     const size_t smem = ((size_t)QNB * QSP + (size_t)QMAX * QSB + 5 * QNB * QCB) * sizeof(double);
     CUDA_CHECK(cudaFuncSetAttribute(bgeqrf_tc_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
     bgeqrf_tc_kernel<<<(unsigned)probs.size(), 512, smem, s>>>(d);
@@ -1282,10 +1074,9 @@ void blarft(const std::vector<SqProb>& probs, const std::vector<const double*>& 
   for (auto& p : probs) maxn = std::max(maxn, p.n);
   SqProb* d = upload_probs(probs, s);
   const double** dt = upload_probs(taus, s);
-  static const int blk = [] { const char* e = getenv("SVMHSS_LARFT_BLK"); return (e && e[0] == '0') ? 0 : 1; }();
   const int lmax = (maxn + 15) & ~15;
   const size_t sm2 = (size_t)2 * lmax * LNB * sizeof(double);
-  if (blk && sm2 <= 226 * 1024) {
+  if (sm2 <= 226 * 1024) {
     CUDA_CHECK(cudaFuncSetAttribute(blarft_blk_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm2));
     blarft_blk_kernel<<<(unsigned)probs.size(), 512, sm2, s>>>(d, dt, lmax);
     LAUNCH_CHECK();
@@ -1337,6 +1128,11 @@ __global__ void __launch_bounds__(CP_THREADS) bcpqr_kernel(const CpqrProb* __res
   double thr = 0.0;
   int k = 0;
   for (int j = 0; j < kmax; ++j) {
+    if (P.forced) {  // fixed-skeleton mode: the imported column's current position
+      const int want = P.forced[j];
+      for (int c = j + tid; c < rows; c += CP_THREADS)
+        if (piv[c] == want) s_p = c;
+    } else {
     // argmax_{c >= j} norm2[c], ties -> lowest index
     double bv = -1.0;
     int bi = 0x7fffffff;
@@ -1358,6 +1154,7 @@ __global__ void __launch_bounds__(CP_THREADS) bcpqr_kernel(const CpqrProb* __res
       for (int w = 1; w < nw; ++w)
         if (rv[w] > b || (rv[w] == b && ri[w] < ix)) { b = rv[w]; ix = ri[w]; }
       s_p = ix;
+    }
     }
     __syncthreads();
     const int p = s_p;
@@ -1674,14 +1471,21 @@ void bcpqr(const std::vector<CpqrProb>& probs, double rel_tol, double abs_tol, i
   int maxr = 0, maxs = 0;
   for (auto& p : probs) { maxr = std::max(maxr, p.rows); maxs = std::max(maxs, p.s); }
   CpqrProb* d = upload_probs(probs, s);
+  bool forced = false;
+  for (auto& p : probs) forced = forced || (p.forced != nullptr);
   // cluster version when a node's columns fit the 8 CTAs' shared memory
   const int slots = (maxr + CPQ_CL - 1) / CPQ_CL;
   const size_t csm = ((size_t)slots * maxs + 2 * (size_t)maxs + slots) * sizeof(double) + (size_t)slots * sizeof(int) + 16;
-  // default: levels with few nodes (one CTA per node would leave most SMs idle); env 0 = never,
-  // 1 = every level that fits
-  const char* env = getenv("SVMHSS_CPQR_CLUSTER");
-  const int mode = env ? atoi(env) : 2;
-  const bool use = csm <= 200 * 1024 && (mode == 1 || (mode == 2 && probs.size() * CPQ_CL <= 2 * 148));
+  // SVMHSS_CPQR_MODE (A/B while tuning): 0 (default) = unblocked kernels (cluster kernel on levels
+  // with few nodes); 2 = blocked kernel (cpqr.cu) on levels with many nodes; 1 = blocked everywhere
+  static const int mode = [] { const char* e = getenv("SVMHSS_CPQR_MODE"); return e ? atoi(e) : 0; }();
+  const bool few = probs.size() * CPQ_CL <= 2 * 148;
+  if (mode >= 1 && cpqr_blk_fits(maxr, maxs) && (mode == 1 || !few || forced)) {
+    bcpqr_blk(d, (int)probs.size(), maxr, maxs, rel_tol, abs_tol, cap, s);
+    free_probs(d, s);
+    return;
+  }
+  const bool use = csm <= 200 * 1024 && few && !forced;
   if (use) {
     auto launchc = [&](auto kern) {
       CUDA_CHECK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)csm));
@@ -1712,8 +1516,7 @@ void bcpqr(const std::vector<CpqrProb>& probs, double rel_tol, double abs_tol, i
   auto launch = [&](auto kern) {
     if (smem > 48 * 1024)
       CUDA_CHECK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-    static const int pf = [] { const char* e = getenv("SVMHSS_CPQR_PREFETCH"); return (e && e[0] == '0') ? 0 : 1; }();
-    kern<<<(unsigned)probs.size(), CP_THREADS, smem, s>>>(d, rel_tol, abs_tol, cap, pf);
+    kern<<<(unsigned)probs.size(), CP_THREADS, smem, s>>>(d, rel_tol, abs_tol, cap, 1);
   };
   if (maxs <= 96) launch(bcpqr_kernel<3>);
   else if (maxs <= 160) launch(bcpqr_kernel<5>);

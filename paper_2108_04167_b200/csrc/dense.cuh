@@ -38,6 +38,8 @@ struct CpqrProb {  // column-pivoted QR of A = W^T, W rows x s row-major (column
   int kfixed;      // >= 0: fixed rank; < 0: adaptive
   int* k_out;      // out: rank
   int* cap_hit;    // out: 1 if the tolerance was unmet at the cap
+  const int* forced;  // nullable (device): fixed-skeleton mode, the first k pivots (original
+                      // column indices, in pivot order; k = kfixed)
 };
 
 // Batched launchers (problem arrays are HOST vectors; uploaded into a scratch buffer).
@@ -52,6 +54,10 @@ void blarft(const std::vector<SqProb>& probs_T, const std::vector<const double*>
             cudaStream_t s);
 void bcpqr(const std::vector<CpqrProb>& probs, double rel_tol, double abs_tol, int cap,
            cudaStream_t s);
+// blocked (dlaqps-style) CPQR, one CTA per node (cpqr.cu); fits: rows / s within its smem tiles
+bool cpqr_blk_fits(int rows, int s);
+void bcpqr_blk(const CpqrProb* d_probs, int nprob, int maxr, int maxs, double rel_tol, double abs_tol, int cap,
+               cudaStream_t s);
 
 // Small helpers
 void fill_identity(double* A, int n, long long rs, long long cs, cudaStream_t s);

@@ -121,9 +121,21 @@ void hss_build_impl(HSSImpl& H, const double* F, int64_t n, int r, double h, con
   {
     EventTimer tm(s);
     pad_rows(F, n, r, rp, Fpad.p, s);
-    H.perm.alloc(n);
     H.Fp.alloc((size_t)n * rp);
-    build_tree(Fpad.p, n, r, rp, H.m, o.tree_seed, H.perm.p, H.Fp.p, s);
+    if (o.perm) {  // imported tree (parity mode): the permutation only, ranges stay T1's split
+      std::vector<int64_t> pv(o.perm, o.perm + n);
+      std::vector<char> seen(n, 0);
+      for (int64_t v : pv) {
+        require(v >= 0 && v < n && !seen[v], "hss_build: opts.perm is not a permutation of 0..n-1");
+        seen[v] = 1;
+      }
+      H.perm = upload(pv, s);
+      gather_rows(Fpad.p, H.perm.p, n, rp, H.Fp.p, s);
+      CUDA_CHECK(cudaStreamSynchronize(s));
+    } else {
+      H.perm.alloc(n);
+      build_tree(Fpad.p, n, r, rp, H.m, o.tree_seed, H.perm.p, H.Fp.p, s);
+    }
     H.nu.alloc(n + kNormPad);
     row_norms(H.Fp.p, n, rp, H.nu.p, s);
     H.iperm.alloc(n);
@@ -199,6 +211,55 @@ void hss_build_impl(HSSImpl& H, const double* F, int64_t n, int r, double h, con
     kernel_matmul(a, s);
     H.st.ms_sketch = tm.stop_ms();
   }
+  // fixed-skeleton import (AMB-12 diagnostic): every node's rank from `ranks` (as kfix below),
+  // its skeleton from the hss_info layout (levels 1..L, BFS order), its active rows = its points
+  // (leaves) or its children's imported skeletons; the CPQR takes the local indices as pivots.
+  std::vector<std::vector<int>> kall, rall;            // per level, per node (all nodes)
+  std::vector<std::vector<int64_t>> soff;              // offset of node's skeleton in o.skeletons
+  if (o.skeletons) {
+    require(o.ranks != nullptr, "hss_build: opts.skeletons needs opts.ranks");
+    require(!ann && o.adaptive_s0 <= 0, "hss_build: opts.skeletons needs sketch sampling, fixed s");
+    kall.assign(L + 1, {}); rall.assign(L + 1, {}); soff.assign(L + 1, {});
+    for (int l = L; l >= 1; --l) {
+      const int cnt = (int)H.lv[l].size();
+      kall[l].resize(cnt); rall[l].resize(cnt);
+      for (int i = 0; i < cnt; ++i) {
+        const int rows = (l == L) ? (int)(H.lv[l][i].hi - H.lv[l][i].lo) : kall[l + 1][2 * i] + kall[l + 1][2 * i + 1];
+        rall[l][i] = rows;
+        kall[l][i] = std::max(0, std::min(std::min(o.ranks[H.node_id(l, i)], rows), S));
+      }
+    }
+    int64_t off = 0;
+    for (int l = 1; l <= L; ++l) {
+      soff[l].resize(H.lv[l].size());
+      for (size_t i = 0; i < H.lv[l].size(); ++i) { soff[l][i] = off; off += kall[l][i]; }
+    }
+  }
+  auto imported_forced = [&](int l, int i, std::vector<int>& out) {
+    // local pivot indices of node (l, i): positions of its imported skeleton in its active rows
+    std::vector<int64_t> act;
+    if (l == L) {
+      for (int64_t p = H.lv[l][i].lo; p < H.lv[l][i].hi; ++p) act.push_back(p);
+    } else {
+      for (int c = 2 * i; c <= 2 * i + 1; ++c)
+        act.insert(act.end(), o.skeletons + soff[l + 1][c], o.skeletons + soff[l + 1][c] + kall[l + 1][c]);
+    }
+    std::vector<int> used(act.size(), 0);
+    const int64_t* J = o.skeletons + soff[l][i];
+    const bool pt = kall[l][i] == rall[l][i];
+    out.clear();
+    for (int q = 0; q < kall[l][i]; ++q) {
+      int at = -1;
+      for (size_t a = 0; a < act.size(); ++a)
+        if (act[a] == J[q]) { at = (int)a; break; }
+      require(at >= 0 && !used[at], "hss_build: imported skeleton of node " + std::to_string(H.node_id(l, i)) +
+                                        " is not a set of distinct active rows");
+      require(!pt || at == q, "hss_build: imported skeleton of pass-through node " +
+                                  std::to_string(H.node_id(l, i)) + " must be its active rows in order");
+      used[at] = 1;
+      out.push_back(at);
+    }
+  };
   EventTimer tmc(s);
   DevBuf<int64_t> act0(std::max<int64_t>(1, nl));
   iota_off_kernel64<<<ceil_div(std::max<int64_t>(1, nl), 256), 256, 0, s>>>(act0.p, nl, H.lo_g);
@@ -237,12 +298,26 @@ void hss_build_impl(HSSImpl& H, const double* F, int64_t n, int r, double h, con
     }
     DevBuf<int> piv(std::max<int64_t>(1, sumR)), kd(nn), ch(nn);
     CUDA_CHECK(cudaMemsetAsync(ch.p, 0, nn * sizeof(int), s));
+    std::vector<int> fh;                       // imported pivots of this level's nodes
+    std::vector<int64_t> foff(nn, -1);
+    if (o.skeletons) {
+      std::vector<int> one;
+      for (int q = 0; q < nn; ++q) {
+        imported_forced(l, f + q, one);
+        require(kall[l][f + q] == std::max(0, kfix[q]) && rall[l][f + q] == lv[f + q].rows,
+                "hss_build: imported skeletons inconsistent with the ranks");
+        foff[q] = (int64_t)fh.size();
+        fh.insert(fh.end(), one.begin(), one.end());
+      }
+    }
+    auto dforced = upload(fh, s);
     std::vector<CpqrProb> cp;
     for (int q = 0; q < nn; ++q) {
       auto& nd = lv[f + q];
       if (kfix[q] >= 0 && kfix[q] == nd.rows) continue;  // known pass-through
       if (nd.rows == 0) continue;
-      cp.push_back({nd.rows, S, Wk.p + nd.roff * S, piv.p + nd.roff, kfix[q], kd.p + q, ch.p + q});
+      cp.push_back({nd.rows, S, Wk.p + nd.roff * S, piv.p + nd.roff, kfix[q], kd.p + q, ch.p + q,
+                    o.skeletons ? dforced.p + foff[q] : nullptr});
     }
     ptr_.mark("  Y ready");
     bcpqr(cp, o.rel_tol, o.abs_tol, o.max_rank, s);

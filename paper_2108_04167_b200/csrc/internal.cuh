@@ -208,24 +208,6 @@ struct ULVImpl {
 
 void ulv_factor_impl(ULVImpl& F, cudaStream_t s);
 
-// one top level of the cooperative top-levels sweep kernel (ulv.cu)
-struct TopLv {
-  const SolveNode* nodes;
-  const SolveWork* work;
-  const SolveWork* bwork;
-  const double* M;
-  const double* fin;
-  double* fout;
-  double* yr;
-  const double* xin;
-  double* xout;
-  double* bpart;
-  unsigned* bcnt;
-  unsigned* fdone;   // dataflow: per node, finished forward chunks
-  unsigned* bdone;   // dataflow: per node, finalized backward column chunks
-  int nwork, nbwork, ch, nnodes;
-};
-
 // Solve workspace for nrhs right-hand sides (tree order in/out, this rank's points).
 struct SolveWS {
   int nrhs = 0;
@@ -245,22 +227,15 @@ struct SolveWS {
   // ADMM: the caller reads x of pass-through leaves from xout[L-1] and writes their next
   // right-hand side into fin[L-1] itself (via ptmap), so the two leaf copies are skipped.
   bool fused_leaf_io = false;
-  // top levels 0..lt run as one cooperative kernel (lt = -1: per-level kernels)
-  int lt = -1;
-  DevBuf<TopLv> top;
-  DevBuf<unsigned> topbar;
-  int top_mode = 0, top_items = 0;   // top levels: 1 grid barriers, 2 dataflow queue
 };
 void solve_ws_alloc(const ULVImpl& F, int nrhs, SolveWS& ws);
 // x_tree = (K~+beta I)^-1 b_tree.  b is read from ws.fin[L] and x written to ws.xout[L].
 void ulv_solve_tree(const ULVImpl& F, SolveWS& ws, cudaStream_t s);
-// Pieces of the solve, for iterations that reorder / fuse levels (admm.cu).
+// Pieces of the solve (sweeps over level ranges, the sharded exchange).
 struct SolveStep {
-  enum Kind { FWD, BWD, FWD_LIST, BWD_LIST, EXCHANGE, TOP };
+  enum Kind { FWD, BWD, EXCHANGE };
   int kind = FWD, a = 0, b = 0;
   bool no_exchange = false;
-  const SolveWork* work = nullptr;  // *_LIST: level a, this work list
-  int nwork = 0;
 };
 void ulv_solve_steps(const ULVImpl& F, SolveWS& ws, const std::vector<SolveStep>& steps, cudaStream_t s);
 
@@ -270,9 +245,11 @@ struct AdmmResult { double w1; double ms_pre, ms_loop, ms_bias; int graph; int64
 AdmmResult admm_train_impl(const ULVImpl& F, const double* y_orig, const std::vector<double>& Cs,
                            int max_it, const admm_opts* opt, double* z_out, double* mu_out,
                            double* bias_out, double* obj_out, cudaStream_t s);
-void predict_impl(const double* Ftrain, const double* coef, int64_t n, int r, double h,
+// a11: coefficients y o z formed on the device; comm (nullable) shards the
+// test points (one allgather of the decision values).
+void predict_impl(const double* Ftrain, const double* y, const double* z, int64_t n, int r, double h,
                   const double* bias_host, int nC, const double* Ftest, int64_t m, double* dv,
-                  int8_t* lab, cudaStream_t s);
+                  int8_t* lab, Comm* comm, cudaStream_t s);
 
 // ---------------------------------------------------------------- permutation helpers
 void gather_rows(const double* src, const int64_t* idx, int64_t rows, int cols, double* dst,

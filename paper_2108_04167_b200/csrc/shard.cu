@@ -8,12 +8,14 @@
 
 namespace svmhss {
 
-// in-place pairwise reduction of nl (power of two) rows of ncols values: row 0 <- total.
+// in-place pairwise reduction of nl rows of ncols values: row 0 <- total (a[i] += a[i + st]
+// for i = 0 mod 2 st, i + st < nl: the cluster tree's association for any nl)
 __device__ void pairwise_rows(double* a, int nl, int ncols) {
   for (int st = 1; st < nl; st <<= 1) {
-    for (int e = threadIdx.x; e < (nl / (2 * st)) * ncols; e += blockDim.x) {
+    const int npair = (nl + 2 * st - 1) / (2 * st);
+    for (int e = threadIdx.x; e < npair * ncols; e += blockDim.x) {
       const int i = (e / ncols) * 2 * st, c = e % ncols;
-      a[(int64_t)i * ncols + c] += a[(int64_t)(i + st) * ncols + c];
+      if (i + st < nl) a[(int64_t)i * ncols + c] += a[(int64_t)(i + st) * ncols + c];
     }
     __syncthreads();
   }

@@ -1,8 +1,6 @@
-// solve_dev.cuh — device functions of the ULV solve sweeps shared by the level kernels
-// (ulv.cu) and the fused bottom-level ADMM kernel (admm.cu), so both produce bitwise-identical
-// values.  Forward sweep t = M_t b (rows i < k -> the parent's input "up", rows >= k -> y_r);
+// solve_dev.cuh — device functions of the ULV solve sweeps (ulv.cu).  Forward sweep t = M_t b (rows i < k -> the parent's input "up", rows >= k -> y_r);
 // backward sweep x = M_t^T [x_s; y_r], both streaming the same stored M_t (no transposed copy):
-//  - fwd_rows: one warp per row (2-4 rows in flight), lane-strided partial sums + butterfly;
+//  - fwd_rows: one warp per row, lane-strided partial sums + butterfly;
 //  - bwd_cols: a CTA of kBW warps owns kCW consecutive columns (lane l -> columns j0 + l and
 //    j0 + 32 + l: fully coalesced row segments); warp w accumulates rows w, w + kBW, ... in
 //    order; the kBW warp partials are summed in warp order.
@@ -68,56 +66,25 @@ __device__ __forceinline__ void row_store(double (&acc)[NR], int i, int k, int64
   }
 }
 
-// rows i0 + wid, i0 + wid + nw, ... < i1; two rows per warp in flight (8 loads per lane).
-// mode (NR <= 2): 1 = four rows x 4 loads, 2 = two rows x 8 loads, 3 = one row x 16 loads,
-// 4 = four rows x 8 loads, 5 = mode 3 + L2 prefetch of the next row; the results are identical
-// for every mode.
+// rows i0 + wid, i0 + wid + nw, ... < i1.  NR <= 2: one row per warp with all 16 loads per lane
+// in flight (4 KB contiguous per round trip) plus an L2 prefetch of the warp's next row (A/B at
+// config 3: 1.431 ms/iteration vs 1.543 with four rows x 4 loads and 1.501 with two rows x 4);
+// NR > 2: two rows per warp (4 loads each).  The per-element order is the same either way.
 template <int NR>
 __device__ __forceinline__ void fwd_rows(const double* __restrict__ M, int R, const double* __restrict__ vsh,
                                          int i0, int i1, int wid, int nw, int k, int64_t koff, int64_t yoff,
-                                         double* __restrict__ out_up, double* __restrict__ out_yr,
-                                         int mode = 0) {
+                                         double* __restrict__ out_up, double* __restrict__ out_yr) {
   int i = i0 + wid;
-  const bool four = mode == 1;
-  if (NR <= 2 && mode == 2) {
-    for (; i + nw < i1; i += 2 * nw) {
-      const double* Mr[2] = {M + (int64_t)i * R, M + (int64_t)(i + nw) * R};
-      double acc[2][NR];
-      row_partials<NR, 2, 8>(Mr, R, vsh, acc);
-      row_store<NR>(acc[0], i, k, koff, yoff, out_up, out_yr);
-      row_store<NR>(acc[1], i + nw, k, koff, yoff, out_up, out_yr);
-    }
-  }
-  if (NR <= 2 && (mode == 3 || mode == 5)) {
+  if (NR <= 2) {
     for (; i < i1; i += nw) {
       const double* Mr[1] = {M + (int64_t)i * R};
-      // mode 5: L2 prefetch of this warp's next row (one 128-byte line per lane) ahead of this row
-      if (mode == 5 && i + nw < i1 && 16 * (threadIdx.x & 31) < R)
+      if (i + nw < i1 && 16 * (threadIdx.x & 31) < R)
         asm volatile("prefetch.global.L2 [%0];\n" ::"l"(M + (int64_t)(i + nw) * R + 16 * (threadIdx.x & 31)));
       double acc[1][NR];
       row_partials<NR, 1, 16>(Mr, R, vsh, acc);
       row_store<NR>(acc[0], i, k, koff, yoff, out_up, out_yr);
     }
-  }
-  if (NR <= 2 && mode == 4) {
-    for (; i + 3 * nw < i1; i += 4 * nw) {
-      const double* Mr[4] = {M + (int64_t)i * R, M + (int64_t)(i + nw) * R, M + (int64_t)(i + 2 * nw) * R,
-                             M + (int64_t)(i + 3 * nw) * R};
-      double acc[4][NR];
-      row_partials<NR, 4, 8>(Mr, R, vsh, acc);
-#pragma unroll
-      for (int u = 0; u < 4; ++u) row_store<NR>(acc[u], i + u * nw, k, koff, yoff, out_up, out_yr);
-    }
-  }
-  if (NR <= 2 && four) {  // four rows in flight (16 independent loads per lane)
-    for (; i + 3 * nw < i1; i += 4 * nw) {
-      const double* Mr[4] = {M + (int64_t)i * R, M + (int64_t)(i + nw) * R, M + (int64_t)(i + 2 * nw) * R,
-                             M + (int64_t)(i + 3 * nw) * R};
-      double acc[4][NR];
-      row_partials<NR, 4>(Mr, R, vsh, acc);
-#pragma unroll
-      for (int u = 0; u < 4; ++u) row_store<NR>(acc[u], i + u * nw, k, koff, yoff, out_up, out_yr);
-    }
+    return;
   }
   for (; i + nw < i1; i += 2 * nw) {
     const double* Mr[2] = {M + (int64_t)i * R, M + (int64_t)(i + nw) * R};

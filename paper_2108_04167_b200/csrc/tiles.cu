@@ -599,7 +599,7 @@ void kernel_blocks(const double* F, int rp, int r, double h, const std::vector<K
   for (size_t b0 = 0; b0 < probs.size(); b0 += 65535) {
     std::vector<KblkProb> chunk(probs.begin() + b0, probs.begin() + std::min(probs.size(), b0 + 65535));
     KblkProb* d = nullptr;
-    CUDA_CHECK(cudaMallocAsync((void**)&d, chunk.size() * sizeof(KblkProb), s));
+    lib_malloc((void**)&d, chunk.size() * sizeof(KblkProb), s);
     CUDA_CHECK(cudaMemcpyAsync(d, chunk.data(), chunk.size() * sizeof(KblkProb), cudaMemcpyHostToDevice, s));
     dim3 grid(ceil_div(mc, 16), ceil_div(mr, 16), (unsigned)chunk.size());
     size_t smem = 2 * 16 * (size_t)r * sizeof(double);
@@ -659,7 +659,7 @@ void bcopy(const std::vector<CopyProb>& probs_in, cudaStream_t s) {
   for (size_t b0 = 0; b0 < probs.size(); b0 += 65535) {
     std::vector<CopyProb> chunk(probs.begin() + b0, probs.begin() + std::min(probs.size(), b0 + 65535));
     CopyProb* d = nullptr;
-    CUDA_CHECK(cudaMallocAsync((void**)&d, chunk.size() * sizeof(CopyProb), s));
+    lib_malloc((void**)&d, chunk.size() * sizeof(CopyProb), s);
     CUDA_CHECK(cudaMemcpyAsync(d, chunk.data(), chunk.size() * sizeof(CopyProb), cudaMemcpyHostToDevice, s));
     dim3 grid((unsigned)std::min<int64_t>(1024, (mx + 255) / 256), (unsigned)chunk.size());
     bcopy_kernel<<<grid, 256, 0, s>>>(d);

@@ -5,7 +5,7 @@
 //   Dcur = D_t + beta I (leaf) | [[Dh_a, R_a B R_b^T], [., Dh_b]] (internal)
 //   Ucur = U_t (leaf)          | diag(R_a, R_b) U_t (internal)
 //   Householder QR  Q^T Ucur = [R; 0]   (compact WY: Q = I - V T V^T)
-//   Dc = Q^T Dcur Q = Dcur - Z V^T - V Z^T,  Z = Dcur V T - 1/2 V T^T (V^T Dcur V) T
+//   Dc = Q^T Dcur Q = M Dcur M^T with M = Q^T formed explicitly
 //   L_r = chol(Dc_rr);  L_sr = Dc_sr L_r^-T;  Dh_t = Dc_ss - L_sr L_sr^T
 // B200 design: instead of keeping (V, T, L_r, L_sr) and doing two
 // triangular solves per node per sweep, we store the node's solve operator explicitly,
@@ -253,8 +253,7 @@ void ulv_factor_impl(ULVImpl& F, cudaStream_t s) {
       int64_t sRK = 0, sKK = 0;
       for (int i : np) { vo[i] = sRK; sRK += (int64_t)R[i] * K[i]; to[i] = sKK; sKK += (int64_t)K[i] * K[i]; }
       DevBuf<double> tau(std::max<int64_t>(1, sumK)), V(std::max<int64_t>(1, sRK)), T(std::max<int64_t>(1, sKK)),
-          Wt(std::max<int64_t>(1, sRK)), Z(std::max<int64_t>(1, sRK)), Mk(std::max<int64_t>(1, sKK)),
-          X1(std::max<int64_t>(1, sKK)), X2(std::max<int64_t>(1, sKK));
+          Wt(std::max<int64_t>(1, sRK));
       std::vector<int64_t> tauoff(nn);
       { int64_t o = 0; for (int i = 0; i < nn; ++i) { tauoff[i] = o; o += K[i]; } }
       ptr_.mark("  assembled");
@@ -278,12 +277,10 @@ void ulv_factor_impl(ULVImpl& F, cudaStream_t s) {
       std::vector<const double*> taus;
       for (int i : np) { tp.push_back({K[i], T.p + to[i], K[i], 1}); taus.push_back(tau.p + tauoff[i]); }
       blarft(tp, taus, s);
-      // Q^T D Q.  Default: M = Q^T = I - (V T^T) V^T formed first (needed for the solve operator
-      // anyway), then Y = D M^T and D' = M Y (two R x R x R GEMMs, 13% fewer flops than the
-      // compact-WY form and fewer, larger launches).  SVMHSS_FACTOR_QDQ=0: compact WY
-      // (D' = D - Z V^T - V Z^T, Z = D V T - 1/2 V T^T V^T D V T).
-      static const int mfirst = [] { const char* e = getenv("SVMHSS_FACTOR_QDQ"); return (e && e[0] == '0') ? 0 : 1; }();
-      if (mfirst) {
+      // Q^T D Q: M = Q^T = I - (V T^T) V^T is formed first (needed for the solve operator
+      // anyway), then Y = D M^T and D' = M Y (two R x R x R GEMMs; 13% fewer flops than the
+      // compact-WY form D - Z V^T - V Z^T and fewer, larger launches).
+      {
         std::vector<PackDesc> pI0;
         for (int i : np) pI0.push_back({0, moff[i], R[i], K[i], 2, 0});
         run_pack(nullptr, pI0, F_l.M.p, s);
@@ -303,31 +300,6 @@ void ulv_factor_impl(ULVImpl& F, cudaStream_t s) {
         g.clear();
         for (int i : np) g.push_back({R[i], R[i], R[i], F_l.M.p + moff[i], R[i], 1, Yq.p + yo[i], R[i], 1, Dcur.p + coff[i], R[i], 1, 1.0, 0.0});
         bgemm(g, s);  // D' = M Y = Q^T D Q
-      } else {
-      // W = Dcur V ; Mk = V^T W ; X1 = Mk T ; X2 = T^T X1 ; Z = W T - 1/2 V X2
-        g.clear();
-        for (int i : np) g.push_back({R[i], K[i], R[i], Dcur.p + coff[i], R[i], 1, V.p + vo[i], K[i], 1, Wt.p + vo[i], K[i], 1, 1.0, 0.0});
-        bgemm(g, s);
-        g.clear();
-        for (int i : np) g.push_back({K[i], K[i], R[i], V.p + vo[i], 1, K[i], Wt.p + vo[i], K[i], 1, Mk.p + to[i], K[i], 1, 1.0, 0.0});
-        for (int i : np) g.push_back({R[i], K[i], K[i], Wt.p + vo[i], K[i], 1, T.p + to[i], K[i], 1, Z.p + vo[i], K[i], 1, 1.0, 0.0});
-        bgemm(g, s);
-        g.clear();
-        for (int i : np) g.push_back({K[i], K[i], K[i], Mk.p + to[i], K[i], 1, T.p + to[i], K[i], 1, X1.p + to[i], K[i], 1, 1.0, 0.0});
-        bgemm(g, s);
-        g.clear();
-        for (int i : np) g.push_back({K[i], K[i], K[i], T.p + to[i], 1, K[i], X1.p + to[i], K[i], 1, X2.p + to[i], K[i], 1, 1.0, 0.0});
-        bgemm(g, s);
-        g.clear();
-        for (int i : np) g.push_back({R[i], K[i], K[i], V.p + vo[i], K[i], 1, X2.p + to[i], K[i], 1, Z.p + vo[i], K[i], 1, -0.5, 1.0});
-        bgemm(g, s);
-        // Dc = Dcur - Z V^T - V Z^T
-        g.clear();
-        for (int i : np) g.push_back({R[i], R[i], K[i], Z.p + vo[i], K[i], 1, V.p + vo[i], 1, K[i], Dcur.p + coff[i], R[i], 1, -1.0, 1.0});
-        bgemm(g, s);
-        g.clear();
-        for (int i : np) g.push_back({R[i], R[i], K[i], V.p + vo[i], K[i], 1, Z.p + vo[i], 1, K[i], Dcur.p + coff[i], R[i], 1, -1.0, 1.0});
-        bgemm(g, s);
       }
       ptr_.mark("  wy QtDQ");
       // L_r = chol(Dc_rr)   (also nodes with k == 0: whole block)
@@ -355,19 +327,10 @@ void ulv_factor_impl(ULVImpl& F, cudaStream_t s) {
       }
       bgemm(g, s);
       ptr_.mark("  potrf/trsm/Dh");
-      // M = Q^T = I - V T^T V^T (unless formed above) ; G_r = L_r^-1 M[k:, :] ; M[:k, :] -= L_sr G_r
+      // G_r = L_r^-1 M[k:, :] ; M[:k, :] -= L_sr G_r   (k == 0 nodes: M = L^-1)
       std::vector<PackDesc> pI;
-      if (!mfirst) for (int i : np) pI.push_back({0, moff[i], R[i], K[i], 2, 0});
       for (int i : nz) pI.push_back({0, moff[i], R[i], K[i], 2, 0});
       run_pack(nullptr, pI, F_l.M.p, s);
-      if (!mfirst) {
-        g.clear();
-        for (int i : np) g.push_back({R[i], K[i], K[i], V.p + vo[i], K[i], 1, T.p + to[i], 1, K[i], Wt.p + vo[i], K[i], 1, 1.0, 0.0});
-        bgemm(g, s);  // Wt := V T^T (reuse)
-        g.clear();
-        for (int i : np) g.push_back({R[i], R[i], K[i], Wt.p + vo[i], K[i], 1, V.p + vo[i], 1, K[i], F_l.M.p + moff[i], R[i], 1, -1.0, 1.0});
-        bgemm(g, s);
-      }
       tr.clear();
       for (int i : np)
         tr.push_back({R[i] - K[i], R[i], Dcur.p + coff[i] + (int64_t)K[i] * R[i] + K[i], R[i], 1,
@@ -479,25 +442,18 @@ void ulv_factor_impl(ULVImpl& F, cudaStream_t s) {
 }
 
 // ------------------------------------------------------------------ solve sweeps
-// (device functions fwd_rows / bwd_cols: solve_dev.cuh)
-// Work-item bodies shared by the per-level kernels and the cooperative top-levels kernel
-// (same arithmetic either way).  All threads of the CTA take part; they end with a CTA barrier
-// so a CTA may run several items back to back.
-// ld(): inputs written by other CTAs of the same launch (dataflow top kernel) are read L2-coherent
-template <bool CG>
-__device__ __forceinline__ double ld_in(const double* p) { return CG ? __ldcg(p) : *p; }
-
-template <int NR, bool CG = false>
+// (device functions fwd_rows / bwd_cols: solve_dev.cuh).  A forward work item = (node, chunk
+// of `ch` rows) of t = M_t b; all threads of the CTA take part.
+template <int NR>
 __device__ __forceinline__ void fwd_item(const SolveNode* __restrict__ nodes, SolveWork wk, int ch,
                                          const double* __restrict__ M, const double* __restrict__ in,
-                                         double* __restrict__ out_up, double* __restrict__ out_yr, double* vsh,
-                                         int four = 0) {
+                                         double* __restrict__ out_up, double* __restrict__ out_yr, double* vsh) {
   const SolveNode N = nodes[wk.node];
   const int R = N.R, tid = threadIdx.x;
   const int i0 = wk.chunk * ch, i1 = min(R, i0 + ch);
   if (N.pt) {  // identity operator
-    for (int e = tid; e < (i1 - i0) * NR; e += 256) out_up[(N.koff + i0) * NR + e] = ld_in<CG>(in + (N.roff + i0) * NR + e);
-  } else if ((four == 3 || four == 5) && NR <= 2 && R <= 512 && i1 - i0 <= 8) {
+    for (int e = tid; e < (i1 - i0) * NR; e += 256) out_up[(N.koff + i0) * NR + e] = in[(N.roff + i0) * NR + e];
+  } else if (NR <= 2 && R <= 512 && i1 - i0 <= 8) {
     // one row per warp (small chunks: the top levels): the row's 16 loads are issued before the
     // input vector is staged, so the two latencies overlap; same per-row FMA order as fwd_rows
     const int lane = tid & 31, i = i0 + (tid >> 5);
@@ -505,7 +461,7 @@ __device__ __forceinline__ void fwd_item(const SolveNode* __restrict__ nodes, So
     double m[16];
 #pragma unroll
     for (int q = 0; q < 16; ++q) m[q] = (i < i1 && lane + 32 * q < R) ? Mr[lane + 32 * q] : 0.0;
-    for (int e = tid; e < R * NR; e += 256) vsh[e] = ld_in<CG>(in + N.roff * NR + e);
+    for (int e = tid; e < R * NR; e += 256) vsh[e] = in[N.roff * NR + e];
     __syncthreads();
     if (i < i1) {
       double acc[NR];
@@ -522,9 +478,9 @@ __device__ __forceinline__ void fwd_item(const SolveNode* __restrict__ nodes, So
       row_store<NR>(acc, i, N.k, N.koff, N.yoff, out_up, out_yr);
     }
   } else {
-    for (int e = tid; e < R * NR; e += 256) vsh[e] = ld_in<CG>(in + N.roff * NR + e);
+    for (int e = tid; e < R * NR; e += 256) vsh[e] = in[N.roff * NR + e];
     __syncthreads();
-    fwd_rows<NR>(M + N.moff, R, vsh, i0, i1, tid >> 5, 8, N.k, N.koff, N.yoff, out_up, out_yr, four);
+    fwd_rows<NR>(M + N.moff, R, vsh, i0, i1, tid >> 5, 8, N.k, N.koff, N.yoff, out_up, out_yr);
   }
   __syncthreads();
 }
@@ -535,22 +491,11 @@ __global__ void __launch_bounds__(256) ulv_fwd_kernel(const SolveNode* __restric
                                                       const double* __restrict__ M,
                                                       const double* __restrict__ in,
                                                       double* __restrict__ out_up,
-                                                      double* __restrict__ out_yr, int four) {
+                                                      double* __restrict__ out_yr) {
   extern __shared__ double vsh[];  // R * NR
   pdl_trigger();
-  if (four & 2) {  // L2 prefetch of this CTA's rows of M (static data) ahead of the dependency wait
-    const SolveWork wk = work[blockIdx.x];
-    const SolveNode N = nodes[wk.node];
-    if (!N.pt) {
-      const int i0 = wk.chunk * ch, i1 = min(N.R, i0 + ch);
-      const char* base = reinterpret_cast<const char*>(M + N.moff + (int64_t)i0 * N.R);
-      const int64_t bytes = (int64_t)(i1 - i0) * N.R * 8;
-      for (int64_t o = (int64_t)threadIdx.x * 128; o < bytes; o += 256 * 128)
-        asm volatile("prefetch.global.L2 [%0];\n" ::"l"(base + o));
-    }
-  }
   pdl_wait();
-  fwd_item<NR>(nodes, work[blockIdx.x], ch, M, in, out_up, out_yr, vsh, four >> 2);
+  fwd_item<NR>(nodes, work[blockIdx.x], ch, M, in, out_up, out_yr, vsh);
 }
 
 template <int NR>
@@ -585,12 +530,11 @@ __global__ void __launch_bounds__(kBW * 32) ulv_bwd_kernel(const SolveNode* __re
 // i0 + w, i0 + w + kBW, ... in order; warps in order) into a partial slab, and the last CTA of
 // (node, cc) adds the row-chunk partials in rc order.  Used for levels l <= kSplitMaxLevel
 // (l < L-1), a rule of the global tree, so results stay P-invariant.
-template <int NR, bool CG = false>
+template <int NR>
 __device__ __forceinline__ void bwd_split_item(const SolveNode* __restrict__ nodes, SolveWork wk, int item,
                                                const double* __restrict__ M, const double* __restrict__ in_s,
                                                const double* __restrict__ in_r, double* __restrict__ out,
-                                               double* __restrict__ part, unsigned* __restrict__ cnt,
-                                               unsigned* __restrict__ done = nullptr) {
+                                               double* __restrict__ part, unsigned* __restrict__ cnt) {
   const SolveNode N = nodes[wk.node];
   const int R = N.R, tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
   const int nrc = (R + kRB - 1) / kRB, cc = wk.chunk / nrc, rc = wk.chunk % nrc;
@@ -598,12 +542,7 @@ __device__ __forceinline__ void bwd_split_item(const SolveNode* __restrict__ nod
   if (N.pt) {  // identity operator (row chunk 0 copies)
     if (rc == 0) {
       const int j1 = min(R, j0 + kCW);
-      for (int e = tid; e < (j1 - j0) * NR; e += kBW * 32) out[(N.roff + j0) * NR + e] = ld_in<CG>(in_s + (N.koff + j0) * NR + e);
-      if (done) {
-        __threadfence();
-        __syncthreads();
-        if (tid == 0) atomicAdd(done + wk.node, 1u);
-      }
+      for (int e = tid; e < (j1 - j0) * NR; e += kBW * 32) out[(N.roff + j0) * NR + e] = in_s[(N.koff + j0) * NR + e];
     }
     __syncthreads();
     return;
@@ -629,7 +568,7 @@ __device__ __forceinline__ void bwd_split_item(const SolveNode* __restrict__ nod
     }
     for (int e = tid; e < (i1 - i0) * NR; e += kBW * 32) {
       const int i = i0 + e / NR, c = e % NR;
-      ush[e] = (i < N.k) ? ld_in<CG>(in_s + (N.koff + i) * NR + c) : ld_in<CG>(in_r + (N.yoff + i - N.k) * NR + c);
+      ush[e] = (i < N.k) ? in_s[(N.koff + i) * NR + c] : in_r[(N.yoff + i - N.k) * NR + c];
     }
     __syncthreads();
 #pragma unroll
@@ -670,15 +609,10 @@ __device__ __forceinline__ void bwd_split_item(const SolveNode* __restrict__ nod
       const int jj = e / NR;
       if (j0 + jj >= R) continue;
       double t = 0.0;
-      for (int q = 0; q < nrc; ++q) t += ld_in<CG>(part + ((int64_t)(g + q) * kCW) * NR + e);
+      for (int q = 0; q < nrc; ++q) t += part[((int64_t)(g + q) * kCW) * NR + e];
       out[(N.roff + j0) * NR + e] = t;
     }
     if (tid == 0) cnt[g] = 0u;
-    if (done) {  // dataflow: this (node, column chunk) is final
-      __threadfence();
-      __syncthreads();
-      if (tid == 0) atomicAdd(done + wk.node, 1u);
-    }
   }
   __syncthreads();
 }
@@ -695,125 +629,6 @@ __global__ void __launch_bounds__(kBW * 32) ulv_bwd_split_kernel(const SolveNode
   pdl_trigger();
   pdl_wait();
   bwd_split_item<NR>(nodes, work[blockIdx.x], blockIdx.x, M, in_s, in_r, out, part, cnt);
-}
-
-// The top levels (<= lt: few nodes, latency-bound) of BOTH sweeps in one cooperative launch:
-// forward lt..0 then backward 0..lt, a grid barrier between levels instead of a kernel
-// boundary.  Same item bodies as the per-level kernels.
-
-// grid barrier for a co-resident (cooperative) grid: bar[0] counts arrivals (monotone within a
-// launch), bar[1] counts finished blocks; the last block resets both for the next launch.
-__device__ __forceinline__ void grid_barrier(unsigned* bar, unsigned k) {
-  __syncthreads();
-  if (threadIdx.x == 0) {
-    __threadfence();
-    atomicAdd(&bar[0], 1u);
-    const unsigned target = k * gridDim.x;
-    while (atomicAdd(&bar[0], 0u) < target) __nanosleep(64);
-    __threadfence();
-  }
-  __syncthreads();
-}
-
-template <int NR>
-__global__ void __launch_bounds__(256) ulv_top_kernel(const TopLv* __restrict__ lv, int lt, unsigned* bar) {
-  extern __shared__ double vsh[];
-  unsigned nb = 0;
-  for (int l = lt; l >= 0; --l) {
-    const TopLv T = lv[l];
-    for (int it = blockIdx.x; it < T.nwork; it += gridDim.x)
-      fwd_item<NR>(T.nodes, T.work[it], T.ch, T.M, T.fin, T.fout, T.yr, vsh);
-    grid_barrier(bar, ++nb);
-  }
-  for (int l = 0; l <= lt; ++l) {
-    const TopLv T = lv[l];
-    for (int it = blockIdx.x; it < T.nbwork; it += gridDim.x)
-      bwd_split_item<NR>(T.nodes, T.bwork[it], it, T.M, T.xin, T.yr, T.xout, T.bpart, T.bcnt);
-    if (l < lt) grid_barrier(bar, ++nb);
-  }
-  if (threadIdx.x == 0 && atomicAdd(&bar[1], 1u) == gridDim.x - 1) {
-    bar[0] = 0u;
-    bar[1] = 0u;
-  }
-}
-
-// Dataflow variant of the top levels: one persistent launch walks a queue of work items (forward
-// items of levels lt..0, then backward items of levels 0..lt; every dependency points to an
-// earlier item, so the CTA holding the oldest unfinished item can always proceed).  Instead of a
-// grid barrier per level, an item waits only for what it reads: a forward item of node t at level
-// l < lt for all forward items of t's two children (fdone[l+1][child] == their chunk count), a
-// backward item for all column chunks of its parent (bdone[l-1][parent]) or, at the root, for the
-// root's forward items.  Same item bodies (same arithmetic) as the per-level kernels; inputs
-// written in this launch are read L2-coherent (ld.global.cg).  dq[0] = queue head, dq[1] = exits.
-__device__ __forceinline__ void df_wait(const unsigned* flag, unsigned target) {
-  if (threadIdx.x == 0) {
-    while (true) {
-      unsigned v;
-      asm volatile("ld.acquire.gpu.global.u32 %0, [%1];\n" : "=r"(v) : "l"(flag) : "memory");
-      if (v >= target) break;
-      __nanosleep(32);
-    }
-    __threadfence();
-  }
-  __syncthreads();
-}
-
-template <int NR>
-__global__ void __launch_bounds__(256) ulv_top_df_kernel(const TopLv* __restrict__ lv, int lt, int nitems,
-                                                         unsigned* __restrict__ dq) {
-  extern __shared__ double vsh[];
-  __shared__ int s_item;
-  pdl_trigger();
-  pdl_wait();
-  int nf = 0;
-  for (int l = 0; l <= lt; ++l) nf += lv[l].nwork;
-  while (true) {
-    if (threadIdx.x == 0) s_item = (int)atomicAdd(&dq[0], 1u);
-    __syncthreads();
-    int q = s_item;
-    __syncthreads();
-    if (q >= nitems) break;
-    if (q < nf) {  // forward: levels lt, lt-1, ..., 0
-      int l = lt;
-      while (q >= lv[l].nwork) { q -= lv[l].nwork; --l; }
-      const TopLv T = lv[l];
-      const SolveWork wk = T.work[q];
-      if (l < lt) {
-        const TopLv C = lv[l + 1];
-        for (int c = 0; c < 2; ++c) {
-          const int ch = 2 * wk.node + c;
-          df_wait(C.fdone + ch, (unsigned)((C.nodes[ch].R + C.ch - 1) / C.ch));
-        }
-      }
-      fwd_item<NR, true>(T.nodes, wk, T.ch, T.M, T.fin, T.fout, T.yr, vsh);
-      __threadfence();
-      __syncthreads();
-      if (threadIdx.x == 0) atomicAdd(T.fdone + wk.node, 1u);
-    } else {       // backward: levels 0, 1, ..., lt
-      q -= nf;
-      int l = 0;
-      while (q >= lv[l].nbwork) { q -= lv[l].nbwork; ++l; }
-      const TopLv T = lv[l];
-      const SolveWork wk = T.bwork[q];
-      if (l == 0) {
-        df_wait(T.fdone + wk.node, (unsigned)((T.nodes[wk.node].R + T.ch - 1) / T.ch));
-      } else {
-        const TopLv Pp = lv[l - 1];
-        const int pn = wk.node >> 1;
-        df_wait(Pp.bdone + pn, (unsigned)((Pp.nodes[pn].R + kCW - 1) / kCW));
-      }
-      bwd_split_item<NR, true>(T.nodes, wk, q, T.M, T.xin, T.yr, T.xout, T.bpart, T.bcnt, T.bdone);
-    }
-  }
-  // the last CTA out resets the queue and the level counters for the next launch
-  __shared__ bool last;
-  if (threadIdx.x == 0) last = (atomicAdd(&dq[1], 1u) == gridDim.x - 1);
-  __syncthreads();
-  if (last) {
-    for (int l = 0; l <= lt; ++l)
-      for (int i = threadIdx.x; i < lv[l].nnodes; i += blockDim.x) { lv[l].fdone[i] = 0u; lv[l].bdone[i] = 0u; }
-    if (threadIdx.x == 0) { dq[0] = 0u; dq[1] = 0u; }
-  }
 }
 
 // pass-through leaves: fwd  fin_{L-1}[map[p]] = fin_L[p];  bwd  xout_L[p] = xout_{L-1}[map[p]]
@@ -853,9 +668,6 @@ void solve_ws_alloc(const ULVImpl& F, int nrhs, SolveWS& ws) {
   ws.xout[0] = mk(F.lv[0].sumR);
   for (int l = 1; l <= L; ++l) ws.xout[l] = F.lv[l].allpt ? ws.xout[l - 1] : mk(F.lv[l].sumR);
   ws.bpart.assign(L + 1, nullptr);
-  ws.lt = -1;
-  ws.top_items = 0;
-  ws.top_mode = 0;
   ws.bcnt.assign(L + 1, nullptr);
   for (int l = 0; l <= L; ++l)
     if (F.lv[l].split && F.lv[l].nbwork > 0) {
@@ -864,53 +676,6 @@ void solve_ws_alloc(const ULVImpl& F, int nrhs, SolveWS& ws) {
       CUDA_CHECK(cudaMemsetAsync(ws.cnt_own.back().p, 0, F.lv[l].nbwork * sizeof(unsigned), g_alloc_stream));
       ws.bcnt[l] = ws.cnt_own.back().p;
     }
-  // top levels 0..lt in one cooperative launch (split backward levels only, above the exchange).
-  // Off by default: measured at config 3 it is not faster (137.7 us for levels 0-5 of both sweeps
-  // vs ~140 us as 12 level kernels; 665 vs 681 it/s end to end) -- the levels are bound by their
-  // dependency chain, not by launches.  SVMHSS_TOP_MERGE=1 enables it (bitwise-identical results).
-  int lt = std::min(kSplitMaxLevel, L - 2);
-  if (H.sh.on()) lt = std::min(lt, H.sh.lg - 1);
-  const char* env = getenv("SVMHSS_TOP_MERGE");
-  const int tmode = env ? atoi(env) : 0;   // 0 per-level kernels, 1 grid barriers, 2 dataflow
-  if (tmode != 1 && tmode != 2) lt = -1;
-  for (int l = 0; l <= lt && lt >= 0; ++l)
-    if (F.lv[l].allpt) lt = -1;   // dataflow counters assume every top level has its own items
-  if (lt >= 1) {
-    std::vector<TopLv> tv(lt + 1);
-    for (int l = 0; l <= lt; ++l) {
-      const auto& lv = F.lv[l];
-      require(lv.split, "internal: top levels must use the split backward sweep");
-      TopLv T{};
-      T.nodes = lv.nodes.p;
-      T.work = lv.work.p;
-      T.bwork = lv.bwork.p;
-      T.M = lv.M.p;
-      T.fin = ws.fin[l];
-      T.fout = l > 0 ? ws.fin[l - 1] : nullptr;
-      T.yr = ws.yr[l];
-      T.xin = l > 0 ? ws.xout[l - 1] : nullptr;
-      T.xout = ws.xout[l];
-      T.bpart = ws.bpart[l];
-      T.bcnt = ws.bcnt[l];
-      T.nwork = lv.allpt ? 0 : lv.nwork;
-      T.nbwork = lv.allpt ? 0 : lv.nbwork;
-      T.ch = lv.ch;
-      T.nnodes = lv.nnodes;
-      ws.cnt_own.emplace_back((size_t)std::max(1, 2 * lv.nnodes));
-      CUDA_CHECK(cudaMemsetAsync(ws.cnt_own.back().p, 0, (size_t)std::max(1, 2 * lv.nnodes) * sizeof(unsigned),
-                                 g_alloc_stream));
-      T.fdone = ws.cnt_own.back().p;
-      T.bdone = T.fdone + lv.nnodes;
-      tv[l] = T;
-      ws.top_items += T.nwork + T.nbwork;
-    }
-    ws.top_mode = tmode;
-    ws.top = upload(tv, g_alloc_stream);
-    ws.topbar.alloc(2);
-    CUDA_CHECK(cudaMemsetAsync(ws.topbar.p, 0, 2 * sizeof(unsigned), g_alloc_stream));
-    CUDA_CHECK(cudaStreamSynchronize(g_alloc_stream));
-    ws.lt = lt;
-  }
 }
 
 template <int NR>
@@ -918,19 +683,8 @@ static void fwd_level(const ULVImpl& F, SolveWS& ws, int l, const SolveWork* wor
   const auto& lv = F.lv[l];
   if (nwork <= 0) return;
   const size_t sm = (size_t)lv.maxR * NR * sizeof(double);
-  // load pattern of the forward GEMV: SVMHSS_FWD_MODE (solve_dev.cuh fwd_rows); SVMHSS_FWD_ROWS=2: mode 0
-  static const int four = [] {
-    const char* e = getenv("SVMHSS_FWD_ROWS");
-    const char* p = getenv("SVMHSS_FWD_PREFETCH");
-    const char* m = getenv("SVMHSS_FWD_MODE");
-    // default: one row x 16 loads per warp (4 KB contiguous per round trip) plus an L2 prefetch
-    // of the warp's next row (mode 5); A/B at config 3: 1.439 ms/iteration (mode 3) vs 1.543
-    // (four rows x 4 loads) and 1.501 (two rows x 4); mode 5 vs 3: 1.431 vs 1.443; same results
-    const int mode = m ? atoi(m) : ((e && e[0] == '2') ? 0 : 5);
-    return (mode << 2) | ((p && p[0] == '1') ? 2 : 0);
-  }();
   launch_pdl(ulv_fwd_kernel<NR>, dim3(nwork), dim3(256), sm, s, lv.nodes.p, work, lv.ch, lv.M.p, ws.fin[l],
-             l > 0 ? ws.fin[l - 1] : nullptr, ws.yr[l], four);
+             l > 0 ? ws.fin[l - 1] : nullptr, ws.yr[l]);
   g_launches.fetch_add(1);
 }
 
@@ -990,61 +744,7 @@ static void run_step(const ULVImpl& F, SolveWS& ws, const SolveStep& st, cudaStr
         }
       }
       break;
-    case SolveStep::FWD_LIST: fwd_level<NR>(F, ws, st.a, st.work, st.nwork, s); break;
-    case SolveStep::BWD_LIST: bwd_level<NR>(F, ws, st.a, st.work, st.nwork, s); break;
     case SolveStep::EXCHANGE: if (H.sh.on()) exchange_step<NR>(F, ws, s); break;
-    case SolveStep::TOP: {
-      if (ws.top_mode == 2) {
-        int maxR = 0;
-        for (int l = 0; l <= ws.lt; ++l) maxR = std::max(maxR, F.lv[l].maxR);
-        const size_t sm = (size_t)maxR * NR * sizeof(double);
-        static int nsm = 0;
-        if (!nsm) {
-          int dev = 0;
-          CUDA_CHECK(cudaGetDevice(&dev));
-          CUDA_CHECK(cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev));
-        }
-        if (sm > 48 * 1024)
-          CUDA_CHECK(cudaFuncSetAttribute(ulv_top_df_kernel<NR>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm));
-        int per_sm = 0;
-        CUDA_CHECK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, ulv_top_df_kernel<NR>, 256, sm));
-        const int grid = std::max(1, std::min(ws.top_items, nsm * std::max(1, per_sm)));
-        launch_pdl(ulv_top_df_kernel<NR>, dim3(grid), dim3(256), sm, s, (const TopLv*)ws.top.p, ws.lt,
-                   ws.top_items, ws.topbar.p);
-        g_launches.fetch_add(1);
-        break;
-      }
-      int maxR = 0, items = 1;
-      for (int l = 0; l <= ws.lt; ++l) {
-        maxR = std::max(maxR, F.lv[l].maxR);
-        items = std::max(items, std::max(F.lv[l].nwork, F.lv[l].nbwork));
-      }
-      const size_t sm = (size_t)maxR * NR * sizeof(double);
-      static int nsm = 0;
-      if (!nsm) {
-        int dev = 0;
-        CUDA_CHECK(cudaGetDevice(&dev));
-        CUDA_CHECK(cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev));
-      }
-      if (sm > 48 * 1024)
-        CUDA_CHECK(cudaFuncSetAttribute(ulv_top_kernel<NR>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm));
-      int per_sm = 0;
-      CUDA_CHECK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, ulv_top_kernel<NR>, 256, sm));
-      const int grid = std::max(1, std::min(items, nsm * std::max(1, per_sm)));
-      cudaLaunchConfig_t cfg = {};
-      cfg.gridDim = dim3(grid);
-      cfg.blockDim = dim3(256);
-      cfg.dynamicSmemBytes = sm;
-      cfg.stream = s;
-      cudaLaunchAttribute at[1];
-      at[0].id = cudaLaunchAttributeCooperative;
-      at[0].val.cooperative = 1;
-      cfg.attrs = at;
-      cfg.numAttrs = 1;
-      CUDA_CHECK(cudaLaunchKernelEx(&cfg, ulv_top_kernel<NR>, (const TopLv*)ws.top.p, ws.lt, ws.topbar.p));
-      g_launches.fetch_add(1);
-      break;
-    }
   }
 }
 
@@ -1075,11 +775,7 @@ void ulv_solve_steps(const ULVImpl& F, SolveWS& ws, const std::vector<SolveStep>
 
 void ulv_solve_tree(const ULVImpl& F, SolveWS& ws, cudaStream_t s) {
   const int L = F.H->L;
-  if (ws.lt >= 1)
-    ulv_solve_steps(F, ws, {SolveStep{SolveStep::FWD, L, ws.lt + 1}, SolveStep{SolveStep::TOP},
-                            SolveStep{SolveStep::BWD, ws.lt + 1, L}}, s);
-  else
-    ulv_solve_steps(F, ws, {SolveStep{SolveStep::FWD, L, 0}, SolveStep{SolveStep::BWD, 0, L}}, s);
+  ulv_solve_steps(F, ws, {SolveStep{SolveStep::FWD, L, 0}, SolveStep{SolveStep::BWD, 0, L}}, s);
 }
 
 

@@ -31,8 +31,7 @@ def train_h(F, y, Ft, yt, h, C_list, beta, max_it, opts, device="cuda"):
     H = hss_build(Fd, h, **opts)
     U = hss_ulv_factor(H, beta)
     res = admm_svm_train(U, yd, C_list, max_it, want_mu=False)
-    coef = (yd[:, None] * res["z"]).contiguous()
-    dv, lab = svm_predict(Fd, coef, h, res["bias"], Ftd)
+    dv, lab = svm_predict(Fd, yd, res["z"], h, res["bias"], Ftd)
     torch.cuda.synchronize()
     wall = time.perf_counter() - t0
     hi, ui = H.info(), U.info()

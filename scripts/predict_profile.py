@@ -18,11 +18,12 @@ g = np.random.default_rng(5)
 F = torch.from_numpy(g.standard_normal((n, r)) * 0.3).cuda()
 Ft = torch.from_numpy(g.standard_normal((m, r)) * 0.3).cuda()
 coef = torch.from_numpy(g.standard_normal(n)).cuda()
-P.svm_predict(F, coef, 1.0, [0.0], Ft)
+ones = torch.ones(n, dtype=torch.float64, device="cuda")
+P.svm_predict(F, ones, coef, 1.0, [0.0], Ft)
 torch.cuda.synchronize()
 t = time.perf_counter()
 torch.cuda.profiler.start()
-P.svm_predict(F, coef, 1.0, [0.0], Ft)
+P.svm_predict(F, ones, coef, 1.0, [0.0], Ft)
 torch.cuda.synchronize()
 torch.cuda.profiler.stop()
 print(f"predict m={m} n={n}: {time.perf_counter() - t:.4f} s")

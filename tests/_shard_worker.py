@@ -36,6 +36,7 @@ def main():
     if cap is not None:
         cfg["cap"], cfg["s"] = cap, cap + 16
     F, y, _, _ = datagen.generate(cfg_id, n=n, n_test=0)
+    Ft = datagen.generate(cfg_id, n=n, n_test=301)[2]   # test points of a separate draw
     dev = torch.device("cuda:0")
     Fd, yd = torch.from_numpy(F).to(dev), torch.from_numpy(y).to(dev)
     h = cfg["h"][2] if isinstance(cfg["h"], list) else cfg["h"]
@@ -52,7 +53,10 @@ def main():
     Cs = [0.5, 1.0, 10.0]
     res = P.admm_svm_train(U, yd, Cs, max_it, trace_every=20)
     hi = H.info()
+    # a11 with the test points sharded over the ranks (svm_predict's comm)
+    dv, lab = P.svm_predict(Fd, yd, res["z"], h, res["bias"], torch.from_numpy(Ft).to(dev), comm=comm)
     np.savez(os.path.join(out, f"P{world}_r{rank}.npz"), x=x.cpu().numpy(), kv=kv.cpu().numpy(),
+             dv=dv.cpu().numpy(), lab=lab.cpu().numpy(),
              z=res["z"].cpu().numpy(), mu=res["mu"].cpu().numpy(), bias=res["bias"], obj=res["obj"],
              trace_z=res["trace_z"].cpu().numpy(), w1=res["stats"]["w1"], perm=hi["perm"],
              cap_hits=hi["cap_hits"], passthrough=hi["passthrough"], max_rank=hi["max_rank_used"],

@@ -72,10 +72,9 @@ def test_fullsize_admm_properties_and_predict(full):
     assert abs(float(y @ x)) <= 1e-9 * np.linalg.norm(x) * np.sqrt(len(x))
     assert np.allclose(np.clip(x - mu_prev / beta, 0.0, C), z, rtol=0, atol=1e-9 * max(1.0, C))
     # predict on 64 sampled test points vs the oracle's exact decision values
-    coef = (yd * b["z"][:, 0]).contiguous()
     Ft = full["Ft"]
     sel = np.random.default_rng(12).choice(Ft.shape[0], 64, replace=False)
-    dv, lab = P.svm_predict(_t(full["F"]), coef, cfg["h"], b["bias"], _t(Ft[sel]))
+    dv, lab = P.svm_predict(_t(full["F"]), yd, b["z"], cfg["h"], b["bias"], _t(Ft[sel]))
     dv, lab = dv.cpu().numpy()[:, 0], lab.cpu().numpy()[:, 0]
     dvo = o_svm.decision_values(full["F"], y * z, cfg["h"], b["bias"][0], Ft[sel])
     assert np.abs(dv - dvo).max() <= 1e-10 * max(1.0, np.abs(dvo).max())

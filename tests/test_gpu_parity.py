@@ -233,8 +233,8 @@ def test_admm_trace_bias_objective_labels(gpu_lib, name):
         coef_o = y * o["z"][inv]
         dv_o = o_svm.decision_values(c["F"], coef_o, c["h"], b_o, c["Ft"])
         lab_o = o_svm.labels(dv_o)
-        coef_g = _t((y * zg[:, ci]).copy())
-        dv_g, lab_g = P.svm_predict(_t(c["F"]), coef_g, c["h"], [res["bias"][ci]], _t(c["Ft"]))
+        dv_g, lab_g = P.svm_predict(_t(c["F"]), _t(y), _t(zg[:, ci].copy()), c["h"], [res["bias"][ci]],
+                                    _t(c["Ft"]))
         dv_g, lab_g = _np(dv_g)[:, 0], _np(lab_g)[:, 0]
         sure = np.abs(dv_o) > 1e-6
         assert np.array_equal(lab_g[sure], lab_o[sure])

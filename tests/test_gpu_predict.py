@@ -35,7 +35,9 @@ def test_predict_matches_oracle(gpu_lib, n, m, r, nC, h):
     Ft = g.standard_normal((m, r)) * (0.3 if r > 50 else 1.0)
     coef = g.standard_normal((n, nC))
     bias = g.standard_normal(nC)
-    dv, lab = P.svm_predict(_t(F), _t(coef if nC > 1 else coef[:, 0]), h, bias, _t(Ft))
+    y = np.where(g.random(n) < 0.5, -1.0, 1.0)
+    z = y[:, None] * coef          # y o z = coef exactly (sign flips)
+    dv, lab = P.svm_predict(_t(F), _t(y), _t(z if nC > 1 else z[:, 0]), h, bias, _t(Ft))
     dv, lab = dv.cpu().numpy(), lab.cpu().numpy()
     for c in range(nC):
         dvo = o_svm.decision_values(F, coef[:, c], h, bias[c], Ft)
@@ -51,7 +53,7 @@ def test_predict_exact_kernel_values(gpu_lib):
     P = gpu_lib
     f = np.array([[0.5, -1.0, 2.0, 0.25]])
     Ft = np.array([[0.5, -1.0, 2.0, 0.25], [1.5, -1.0, 2.0, 0.25], [100.0, 0.0, 0.0, 0.0]])
-    dv, lab = P.svm_predict(_t(f), _t(np.ones(1)), 1.0, [0.0], _t(Ft))
+    dv, lab = P.svm_predict(_t(f), _t(np.ones(1)), _t(np.ones(1)), 1.0, [0.0], _t(Ft))
     dv = dv.cpu().numpy()[:, 0]
     assert abs(dv[0] - 1.0) <= 1e-15
     assert abs(dv[1] - np.exp(-0.5)) <= 1e-15

@@ -15,7 +15,7 @@ pytestmark = pytest.mark.gpu
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 WORKER = os.path.join(ROOT, "tests", "_shard_worker.py")
 KEYS = ["x", "kv", "z", "mu", "bias", "obj", "trace_z", "w1", "perm", "cap_hits", "passthrough",
-        "max_rank", "gen_bytes"]
+        "max_rank", "gen_bytes", "dv", "lab"]
 
 
 def _port():

@@ -147,3 +147,15 @@ def test_hss_admm_tracks_dense_admm_near_exact():
     ft = svm.objective(lambda v: hss.matvec(H, v), o1["z"], yp)
     fd = svm.objective_dense(K, o2["z"], yp)
     assert abs(ft - fd) / abs(fd) < 1e-6
+
+
+def test_run_multi_columns_converge_to_their_own_bruteforce_qp():
+    """The multi-C driver (one factorization, several C): column c converges to the
+    brute-force QP optimum at box bound C_c (independent of run())."""
+    F, y, K = _toy(8, 7)
+    Cs = [0.3, 1.0, 5.0]
+    out = admm.run_multi(admm.dense_solver(K, 1.0), y, Cs, 1.0, 3000)
+    for c, C in enumerate(Cs):
+        xb, fb = qp.solve_qp_bruteforce(K, y, C)
+        assert np.abs(out["z"][:, c] - xb).max() < 1e-9
+        assert abs(svm.objective_dense(K, out["z"][:, c], y) - fb) < 1e-12

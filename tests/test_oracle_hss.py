@@ -166,3 +166,54 @@ def test_unconverged_rule():
     # s = 48, p = 16: k > 32 and k < min(cap, rows) -> node 1 only (node 3 is full rank)
     assert hss.unconverged(H, 48, 16, None) == [1]
     assert hss.unconverged(H, 48, 16, 40) == []     # node 1 at the cap
+
+
+def test_fixed_skeleton_replay_reproduces_adaptive_generators():
+    """AMB-12 diagnostic mode: replaying the adaptive run's own skeletons (pivot order) and ranks
+    gives the same K~: U (sign-free interpolation coefficients), J, B equal to rounding."""
+    F, perm, ranges, Fp, Om = _setup(700, 4, 64, 48, 1.0, seed=3)
+    H = hss.compress(Fp, 1.0, ranges, Om, rel_tol=1e-3, cap=32)
+    nn = 2 ** (H.L + 1) - 1
+    ranks = np.full(nn, -1)
+    for t, k in H.k.items():
+        ranks[t] = k
+    flat = np.concatenate([H.J[t] for t in range(1, nn)])
+    sk = hss.skeletons_from_flat(flat, ranks, ranges, 48)
+    assert all(np.array_equal(sk[t], H.J[t]) for t in range(1, nn))
+    H2 = hss.compress(Fp, 1.0, ranges, Om, skeletons=sk)
+    for t in range(1, nn):
+        assert H2.k[t] == H.k[t] and np.array_equal(H2.J[t], H.J[t])
+        if H.U[t] is not None:
+            assert np.abs(H2.U[t] - H.U[t]).max() <= 1e-9 * max(1.0, np.abs(H.U[t]).max())
+    for t in H.B:
+        assert np.abs(H2.B[t] - H.B[t]).max() <= 1e-14
+
+
+def test_fixed_skeleton_interpolation_is_least_squares():
+    """For an arbitrary (non-CPQR) skeleton, U's non-skeleton rows are the least-squares
+    interpolation coefficients of Y_t's rows on the skeleton rows (the ID of P:184 with a given
+    column set): U[rest] = (pinv(Y_J^T) Y_rest^T)^T, checked with numpy lstsq (no QR route)."""
+    F, perm, ranges, Fp, Om = _setup(256, 3, 64, 40, 1.0, seed=4)
+    L = len(ranges) - 1
+    g = np.random.default_rng(1)
+    sk = {}
+    k = {}
+    # leaves: 24 random points in a scrambled order; parents: 24 of the children's skeletons
+    for lvl in range(L, 0, -1):
+        for i, (lo, hi) in enumerate(ranges[lvl]):
+            t = (1 << lvl) - 1 + i
+            act = np.arange(lo, hi) if lvl == L else np.concatenate([sk[2 * t + 1], sk[2 * t + 2]])
+            sk[t] = act[g.permutation(len(act))[:24]]
+            k[t] = 24
+    H = hss.compress(Fp, 1.0, ranges, Om, skeletons=sk)
+    S = kernel.sketch(Fp, 1.0, Om)
+    for i, (lo, hi) in enumerate(ranges[L]):
+        t = (1 << L) - 1 + i
+        D = kernel.gaussian_block(Fp[lo:hi], Fp[lo:hi], 1.0)
+        Y = S[lo:hi] - D @ Om[lo:hi]
+        loc = np.array([int(np.where(np.arange(lo, hi) == a)[0][0]) for a in sk[t]])
+        rest = np.setdiff1d(np.arange(hi - lo), loc)
+        X = np.linalg.lstsq(Y[loc].T, Y[rest].T, rcond=None)[0]
+        assert np.array_equal(H.J[t], sk[t])
+        assert np.abs(H.U[t][loc] - np.eye(24)).max() == 0.0
+        assert np.abs(H.U[t][rest] - X.T).max() <= 1e-8 * max(1.0, np.abs(X).max())
