@@ -25,20 +25,46 @@ namespace svmhss {
 
 constexpr int CB_THREADS = 256, CB_WARPS = CB_THREADS / 32;
 
-template <int MAXPL, int NB>
+// VEC-wide global vectors of a column (VEC = 4: 256-bit loads, s = 0 mod 4; VEC = 2: 128-bit)
+template <int VEC> struct Vec { double v[VEC]; };
+template <int VEC>
+__device__ __forceinline__ Vec<VEC> ldv(const double* p) {
+  Vec<VEC> r;
+  if constexpr (VEC == 4)
+    asm volatile("ld.global.L1::no_allocate.v4.f64 {%0,%1,%2,%3}, [%4];"
+                 : "=d"(r.v[0]), "=d"(r.v[1]), "=d"(r.v[2]), "=d"(r.v[3]) : "l"(p));
+  else
+    asm volatile("ld.global.L1::no_allocate.v2.f64 {%0,%1}, [%2];" : "=d"(r.v[0]), "=d"(r.v[1]) : "l"(p));
+  return r;
+}
+template <int VEC>
+__device__ __forceinline__ void stv(double* p, const Vec<VEC>& r) {
+  if constexpr (VEC == 4)
+    asm volatile("st.global.v4.f64 [%0], {%1,%2,%3,%4};" ::"l"(p), "d"(r.v[0]), "d"(r.v[1]), "d"(r.v[2]),
+                 "d"(r.v[3]) : "memory");
+  else
+    asm volatile("st.global.v2.f64 [%0], {%1,%2};" ::"l"(p), "d"(r.v[0]), "d"(r.v[1]) : "memory");
+}
+
+// Shared-memory layout (doubles, each part 32-byte aligned): vn1, vn2 (rows), F (NB x rows,
+// F(c, q) at q*rows + c: lane-consecutive columns, conflict-free), V (NB x s), then piv, pos, flag.
+__host__ __device__ inline int cb_al4(int x) { return (x + 3) & ~3; }
+
+template <int NB, int VEC>
 __global__ void __launch_bounds__(CB_THREADS, 3) bcpqr_blk_kernel(const CpqrProb* __restrict__ probs,
                                                                   double rel_tol, double abs_tol, int cap) {
   const CpqrProb P = probs[blockIdx.x];
   const int rows = P.rows, s = P.s;
   const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
-  extern __shared__ double sm[];
-  double* vn1 = sm;                          // rows: partial column norms (pivoting)
-  double* vn2 = vn1 + rows;                  // rows: reference norms (downdate accuracy test)
-  double* Fm = vn2 + rows;                   // rows x NB: F(c, q)
-  double* Vp = Fm + (size_t)rows * NB;       // NB x s: panel reflectors, Vp[q*s + i] (i >= j0+q)
-  int* piv = (int*)(Vp + (size_t)NB * s);    // rows: original column at each position
-  int* pos = piv + rows;                     // rows: position of each original column
-  int* flag = pos + rows;                    // rows: 1 = norm to be recomputed after the panel
+  const int ra = cb_al4(rows);
+  extern __shared__ __align__(32) double sm[];
+  double* vn1 = sm;                          // partial column norms (pivoting)
+  double* vn2 = vn1 + ra;                    // reference norms (downdate accuracy test)
+  double* Fm = vn2 + ra;                     // NB x ra: F(c, q) at Fm[q*ra + c]
+  double* Vp = Fm + (size_t)NB * ra;         // NB x s: panel reflectors, Vp[q*s + i] (i >= j0+q)
+  int* piv = (int*)(Vp + (size_t)NB * s);    // original column at each position
+  int* pos = piv + rows;                     // position of each original column
+  int* flag = pos + rows;                    // 1 = norm to be recomputed after the panel
   __shared__ double red[32];
   __shared__ double aux[NB];
   __shared__ int s_p, s_any;
@@ -99,9 +125,9 @@ __global__ void __launch_bounds__(CB_THREADS, 3) bcpqr_blk_kernel(const CpqrProb
           W[(size_t)p * s + i] = a;
         }
         for (int q = tid; q < kk; q += CB_THREADS) {
-          const double a = Fm[j * NB + q];
-          Fm[j * NB + q] = Fm[p * NB + q];
-          Fm[p * NB + q] = a;
+          const double a = Fm[q * ra + j];
+          Fm[q * ra + j] = Fm[q * ra + p];
+          Fm[q * ra + p] = a;
         }
         if (tid == 0) {
           double t = vn1[j]; vn1[j] = vn1[p]; vn1[p] = t;
@@ -118,7 +144,7 @@ __global__ void __launch_bounds__(CB_THREADS, 3) bcpqr_blk_kernel(const CpqrProb
       double part = 0.0;
       for (int i = j + tid; i < s; i += CB_THREADS) {
         double x = W[(size_t)j * s + i];
-        for (int q = 0; q < kk; ++q) x = fma(-Vp[(size_t)q * s + i], Fm[j * NB + q], x);
+        for (int q = 0; q < kk; ++q) x = fma(-Vp[(size_t)q * s + i], Fm[q * ra + j], x);
         vk[i] = x;
         if (i > j) part = fma(x, x, part);
       }
@@ -136,13 +162,15 @@ __global__ void __launch_bounds__(CB_THREADS, 3) bcpqr_blk_kernel(const CpqrProb
         tau = (beta - alpha) / beta;
         scal = 1.0 / (alpha - beta);
       }
+      const int jal = j & ~(VEC - 1);
       for (int i = j + 1 + tid; i < s; i += CB_THREADS) {
         const double v = vk[i] * scal;
         vk[i] = v;
         W[(size_t)j * s + i] = v;
       }
       __syncthreads();
-      if (tid == 0) { vk[j] = 1.0; W[(size_t)j * s + j] = beta; }
+      if (tid == 0) { W[(size_t)j * s + j] = beta; vk[j] = 1.0; }
+      if (tid > 0 && tid < VEC && jal + tid - 1 < j) vk[jal + tid - 1] = 0.0;  // masked lead-in of the vectors
       // ---- 4a. aux = -tau V(j:, 0:kk)^T v
       for (int q = wid; q < kk; q += CB_WARPS) {
         double a = 0.0;
@@ -154,68 +182,57 @@ __global__ void __launch_bounds__(CB_THREADS, 3) bcpqr_blk_kernel(const CpqrProb
         if (lane == 0) aux[q] = -tau * a;
       }
       __syncthreads();
-      // ---- 4b-6. read-only pass over the trailing columns (two columns per warp in flight)
-      for (int c = j + 1 + wid; c < rows; c += 2 * CB_WARPS) {
-        const int c2 = c + CB_WARPS;
-        const bool has2 = c2 < rows;
-        const double* col = W + (size_t)c * s;
-        const double* col2 = W + (size_t)(has2 ? c2 : c) * s;
-        double x1[MAXPL], x2[MAXPL];
+      // ---- 4b-6. read-only pass: one trailing column per LANE (VEC-wide vector loads of its
+      // rows jal.., v broadcast from shared memory), then its F entry, row update and norm
+      const int ng = (rows - j - 1 + 31) >> 5;
+      for (int g = wid; g < ng; g += CB_WARPS) {
+        const int c = j + 1 + 32 * g + lane;
+        if (c < rows) {
+          const double* col = W + (size_t)c * s;
+          double d[VEC];
 #pragma unroll
-        for (int q = 0; q < MAXPL; ++q) {
-          const int i = j + lane + 32 * q;
-          x1[q] = (i < s) ? col[i] : 0.0;
-          x2[q] = (i < s && has2) ? col2[i] : 0.0;
-        }
-        double d1 = 0.0, d2 = 0.0;
+          for (int e = 0; e < VEC; ++e) d[e] = 0.0;
+          const Vec<VEC> x0 = ldv<VEC>(col + jal);
+          double xj = x0.v[0];
 #pragma unroll
-        for (int q = 0; q < MAXPL; ++q) {
-          const int i = j + lane + 32 * q;
-          if (i < s) {
-            const double vi = vk[i];
-            d1 = fma(x1[q], vi, d1);
-            d2 = fma(x2[q], vi, d2);
+          for (int e = 1; e < VEC; ++e) if (jal + e == j) xj = x0.v[e];
+#pragma unroll
+          for (int e = 0; e < VEC; ++e) d[e] = fma(x0.v[e], vk[jal + e], d[e]);
+          int i = jal + VEC;
+          for (; i + 4 * VEC <= s; i += 4 * VEC) {
+            Vec<VEC> x[4];
+#pragma unroll
+            for (int u = 0; u < 4; ++u) x[u] = ldv<VEC>(col + i + u * VEC);
+#pragma unroll
+            for (int u = 0; u < 4; ++u)
+#pragma unroll
+              for (int e = 0; e < VEC; ++e) d[e] = fma(x[u].v[e], vk[i + u * VEC + e], d[e]);
           }
-        }
-        // lane q < kk: the F and row-update corrections of panel column q
-        double f1 = 0.0, f2 = 0.0, r1 = 0.0, r2 = 0.0;
-        if (lane < kk) {
-          const double a = aux[lane], vj = Vp[(size_t)lane * s + j];
-          const double F1 = Fm[c * NB + lane];
-          f1 = F1 * a;
-          r1 = vj * F1;
-          if (has2) {
-            const double F2 = Fm[c2 * NB + lane];
-            f2 = F2 * a;
-            r2 = vj * F2;
+          for (; i < s; i += VEC) {
+            const Vec<VEC> x1 = ldv<VEC>(col + i);
+#pragma unroll
+            for (int e = 0; e < VEC; ++e) d[e] = fma(x1.v[e], vk[i + e], d[e]);
           }
-        }
+          double dot = d[0];
 #pragma unroll
-        for (int o = 16; o > 0; o >>= 1) {
-          d1 += __shfl_xor_sync(0xffffffffu, d1, o);
-          d2 += __shfl_xor_sync(0xffffffffu, d2, o);
-          f1 += __shfl_xor_sync(0xffffffffu, f1, o);
-          f2 += __shfl_xor_sync(0xffffffffu, f2, o);
-          r1 += __shfl_xor_sync(0xffffffffu, r1, o);
-          r2 += __shfl_xor_sync(0xffffffffu, r2, o);
-        }
-        if (lane == 0) {
-#pragma unroll
-          for (int u = 0; u < 2; ++u) {
-            if (u == 1 && !has2) break;
-            const int cc = u ? c2 : c;
-            const double F = fma(tau, u ? d2 : d1, u ? f2 : f1);
-            Fm[cc * NB + kk] = F;
-            const double a = (u ? x2[0] : x1[0]) - (u ? r2 : r1) - F;   // V(j, kk) = 1
-            W[(size_t)cc * s + j] = a;
-            const double n1 = vn1[cc];
-            if (n1 != 0.0) {
-              double t = fabs(a) / n1;
-              t = fmax(0.0, (1.0 + t) * (1.0 - t));
-              const double r = n1 / vn2[cc];
-              if (t * r * r <= tol3z) { flag[cc] = 1; s_any = 1; }
-              else vn1[cc] = n1 * sqrt(t);
-            }
+          for (int e = 1; e < VEC; ++e) dot += d[e];
+          double fc = 0.0, rc = 0.0;
+          for (int q = 0; q < kk; ++q) {
+            const double Fq = Fm[q * ra + c];
+            fc = fma(Fq, aux[q], fc);
+            rc = fma(Vp[(size_t)q * s + j], Fq, rc);
+          }
+          const double Fv = fma(tau, dot, fc);
+          Fm[kk * ra + c] = Fv;
+          const double a = xj - rc - Fv;   // V(j, kk) = 1
+          W[(size_t)c * s + j] = a;
+          const double n1 = vn1[c];
+          if (n1 != 0.0) {
+            double t = fabs(a) / n1;
+            t = fmax(0.0, (1.0 + t) * (1.0 - t));
+            const double r = n1 / vn2[c];
+            if (t * r * r <= tol3z) { flag[c] = 1; s_any = 1; }
+            else vn1[c] = n1 * sqrt(t);
           }
         }
       }
@@ -225,30 +242,38 @@ __global__ void __launch_bounds__(CB_THREADS, 3) bcpqr_blk_kernel(const CpqrProb
       if (kk == NB || s_any || j >= kmax) break;
     }
     if (stop) break;
-    // ---- panel end: trailing update A(j:, c) -= V(j:, 0:kk) F(c, 0:kk)^T (c >= j), and the
-    // recomputed norms.  After the last pivot only the flagged norms matter (cap-hit test).
+    // ---- panel end: trailing update A(j:, c) -= V(j:, 0:kk) F(c, 0:kk)^T (c >= j; one column per
+    // lane, vector loads/stores), and the recomputed norms.  After the last pivot only the
+    // flagged norms matter (cap-hit test).
     const bool last = j >= kmax;
     if (last && !s_any) break;
-    for (int c = j + wid; c < rows; c += CB_WARPS) {
+    const int jal = j & ~(VEC - 1);
+    const int ng = (rows - j + 31) >> 5;
+    for (int g = wid; g < ng; g += CB_WARPS) {
+      const int c = j + 32 * g + lane;
+      if (c >= rows) continue;
       const bool fl = flag[c] != 0;
       if (last && !fl) continue;
       double f[NB];
 #pragma unroll
-      for (int q = 0; q < NB; ++q) f[q] = (q < kk) ? Fm[c * NB + q] : 0.0;
+      for (int q = 0; q < NB; ++q) f[q] = (q < kk) ? Fm[q * ra + c] : 0.0;
       double* col = W + (size_t)c * s;
       double nn = 0.0;
-      for (int i = j + lane; i < s; i += 32) {
-        double x = col[i];
+      for (int i = jal; i < s; i += VEC) {
+        Vec<VEC> x = ldv<VEC>(col + i);
 #pragma unroll
-        for (int q = 0; q < NB; ++q)
-          if (q < kk) x = fma(-Vp[(size_t)q * s + i], f[q], x);
-        if (!last) col[i] = x;
-        nn = fma(x, x, nn);
+        for (int e = 0; e < VEC; ++e) {
+          if (i + e < j) continue;          // rows above j are final
+          double y = x.v[e];
+#pragma unroll
+          for (int q = 0; q < NB; ++q)
+            if (q < kk) y = fma(-Vp[(size_t)q * s + i + e], f[q], y);
+          x.v[e] = y;
+          nn = fma(y, y, nn);
+        }
+        if (!last) stv<VEC>(col + i, x);
       }
-      if (fl) {
-        nn = warp_sum(nn);
-        if (lane == 0) { vn1[c] = sqrt(nn); vn2[c] = vn1[c]; flag[c] = 0; }
-      }
+      if (fl) { vn1[c] = sqrt(nn); vn2[c] = vn1[c]; flag[c] = 0; }
     }
     __syncthreads();
     if (tid == 0) s_any = 0;
@@ -276,19 +301,16 @@ __global__ void __launch_bounds__(CB_THREADS, 3) bcpqr_blk_kernel(const CpqrProb
   if (tid == 0) { *P.k_out = k; if (P.cap_hit) *P.cap_hit = hit; }
 }
 
-// panel width: 8 keeps the shared memory (F, V, norms) at ~63 KB for rows = 512, s = 272, so
-// three CTAs share an SM and hide each other's per-step serial phases (SVMHSS_CPQR_NB=4 for A/B)
-static int cpqr_nb() {
-  static const int nb = [] { const char* e = getenv("SVMHSS_CPQR_NB"); return (e && atoi(e) == 4) ? 4 : 8; }();
-  return nb;
-}
+// panel width 8 keeps the shared memory (F, V, norms) at ~63 KB for rows = 512, s = 272, so three
+// CTAs share an SM and hide each other's per-step serial phases
+constexpr int kCpqrNB = 8;
 
 size_t cpqr_blk_smem(int rows, int s) {
-  const int nb = cpqr_nb();
-  return ((size_t)2 * rows + (size_t)rows * nb + (size_t)nb * s) * sizeof(double) + (size_t)3 * rows * sizeof(int);
+  return ((size_t)(2 + kCpqrNB) * cb_al4(rows) + (size_t)kCpqrNB * s) * sizeof(double) +
+         (size_t)3 * rows * sizeof(int);
 }
 
-bool cpqr_blk_fits(int rows, int s) { return s <= 288 && cpqr_blk_smem(rows, s) <= 100 * 1024; }
+bool cpqr_blk_fits(int rows, int s) { return s <= 1152 && s % 2 == 0 && cpqr_blk_smem(rows, s) <= 100 * 1024; }
 
 void bcpqr_blk(const CpqrProb* d, int nprob, int maxr, int maxs, double rel_tol, double abs_tol, int cap,
                cudaStream_t s) {
@@ -297,15 +319,9 @@ void bcpqr_blk(const CpqrProb* d, int nprob, int maxr, int maxs, double rel_tol,
     CUDA_CHECK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
     kern<<<(unsigned)nprob, CB_THREADS, smem, s>>>(d, rel_tol, abs_tol, cap);
   };
-  if (cpqr_nb() == 4) {
-    if (maxs <= 96) launch(bcpqr_blk_kernel<3, 4>);
-    else if (maxs <= 160) launch(bcpqr_blk_kernel<5, 4>);
-    else launch(bcpqr_blk_kernel<9, 4>);
-  } else {
-    if (maxs <= 96) launch(bcpqr_blk_kernel<3, 8>);
-    else if (maxs <= 160) launch(bcpqr_blk_kernel<5, 8>);
-    else launch(bcpqr_blk_kernel<9, 8>);
-  }
+  // every node of a batch has the same s (the level's sample width)
+  if (maxs % 4 == 0) launch(bcpqr_blk_kernel<kCpqrNB, 4>);
+  else launch(bcpqr_blk_kernel<kCpqrNB, 2>);
   LAUNCH_CHECK();
 }
 

@@ -1476,9 +1476,10 @@ void bcpqr(const std::vector<CpqrProb>& probs, double rel_tol, double abs_tol, i
   // cluster version when a node's columns fit the 8 CTAs' shared memory
   const int slots = (maxr + CPQ_CL - 1) / CPQ_CL;
   const size_t csm = ((size_t)slots * maxs + 2 * (size_t)maxs + slots) * sizeof(double) + (size_t)slots * sizeof(int) + 16;
-  // SVMHSS_CPQR_MODE (A/B while tuning): 0 (default) = unblocked kernels (cluster kernel on levels
-  // with few nodes); 2 = blocked kernel (cpqr.cu) on levels with many nodes; 1 = blocked everywhere
-  static const int mode = [] { const char* e = getenv("SVMHSS_CPQR_MODE"); return e ? atoi(e) : 0; }();
+  // SVMHSS_CPQR_MODE (A/B): 2 (default) = blocked kernel (cpqr.cu) on levels with many nodes, the
+  // cluster kernel on levels with few; 1 = blocked everywhere; 0 = unblocked kernels only.
+  // Measured at config 3 (r2d): compression 163.8 ms (2) / 172.2 (1) / 190.6 (0), same pivots.
+  static const int mode = [] { const char* e = getenv("SVMHSS_CPQR_MODE"); return e ? atoi(e) : 2; }();
   const bool few = probs.size() * CPQ_CL <= 2 * 148;
   if (mode >= 1 && cpqr_blk_fits(maxr, maxs) && (mode == 1 || !few || forced)) {
     bcpqr_blk(d, (int)probs.size(), maxr, maxs, rel_tol, abs_tol, cap, s);
