@@ -100,6 +100,8 @@ def _traffic(kernel, workload):
     d = json.load(open(p)).get(kernel)
     if not d or d.get("workload") != workload:
         return None
+    if d.get("dram_bytes") is not None:
+        return d["dram_bytes"]
     return d["dram_bytes_read"] + d["dram_bytes_write"]
 
 
@@ -230,24 +232,30 @@ def oracle_phases(cfg_id, n_sample, iters, sketch_rows=512):
     full-length rows of the sketch S = K Omega (projected by n / sketch_rows).  Every projected
     number is labelled as such."""
     import datagen
-    from oracle import admm, kernel, pipeline, rng, svm, ulv
+    from threadpoolctl import threadpool_limits
+
+    from oracle import admm, hss, kernel, pipeline, rng, svm, ulv
     cfg = datagen.get_config(cfg_id)
     n = cfg["n"]
     F, y, Ft, _ = datagen.generate(cfg_id, n=n_sample, n_test=256)
     tm = {}
-    t0 = time.perf_counter()
-    perm, ranges, Om, H = pipeline.build(F, cfg, timings=tm)
-    t1 = time.perf_counter()
-    fac = ulv.factor(H, cfg["beta"])
-    t2 = time.perf_counter()
-    yp = y[perm]
-    solve = lambda b: ulv.solve(fac, b)  # noqa: E731
-    t3 = time.perf_counter()
-    out = admm.run(solve, yp, cfg["C"][0], cfg["beta"], iters)
-    t4 = time.perf_counter()
-    mv = lambda v: __import__("oracle").hss.matvec(H, v)  # noqa: E731
-    b = svm.bias(mv, out["z"], yp, cfg["C"][0])
-    t5 = time.perf_counter()
+    # per-node phases (small LAPACK/BLAS calls in Python loops) run with one BLAS thread: the
+    # multithreaded BLAS is 10-20x SLOWER on these shapes (measured); the sketch uses every core
+    # through its row-chunk thread pool
+    with threadpool_limits(limits=1):
+        t0 = time.perf_counter()
+        perm, ranges, Om, H = pipeline.build(F, cfg, timings=tm)
+        t1 = time.perf_counter()
+        fac = ulv.factor(H, cfg["beta"])
+        t2 = time.perf_counter()
+        yp = y[perm]
+        solve = lambda b: ulv.solve(fac, b)  # noqa: E731
+        t3 = time.perf_counter()
+        out = admm.run(solve, yp, cfg["C"][0], cfg["beta"], iters)
+        t4 = time.perf_counter()
+        mv = lambda v: hss.matvec(H, v)  # noqa: E731
+        b = svm.bias(mv, out["z"], yp, cfg["C"][0])
+        t5 = time.perf_counter()
     # sketch rows at the full size (the dominant phase): rows of K(F, F) Omega over all n points
     Ff, _, _, _ = datagen.generate(cfg_id)
     idx = np.arange(sketch_rows)
@@ -272,6 +280,7 @@ def oracle_phases(cfg_id, n_sample, iters, sketch_rows=512):
             "admm_per_iter": per_it * sc,
             "bias_objective": (t5 - t4) * sc,
             "predict_per_test_point": (t9 - t8) / Ft.shape[0] * sc},
+        "threads": {"sketch_rows": "numpy default BLAS threads", "per_node_phases": 1},
         "sample": (f"oracle (NumPy/SciPy fp64): HSS build + ULV + {iters} ADMM iterations + bias on an "
                    f"n={n_sample} config-{cfg_id} draw (same leaf/cap/s/tol/seeds; times x n/n_sample = "
                    f"{sc:.1f}: per-node shapes equal the full config's), {sketch_rows} full-length sketch "
@@ -285,22 +294,25 @@ def oracle_sample(cfg_id, n_sample, iters, steps=1, warmup=0):
     metric's unit: ADMM iters/s scaled to the full n (one iteration is O(n): per-node work
     over n / leaf nodes)."""
     import datagen
+    from threadpoolctl import threadpool_limits
+
     from oracle import admm, pipeline, ulv
     cfg = datagen.get_config(cfg_id)
     F, y, _, _ = datagen.generate(cfg_id, n=n_sample, n_test=0)
-    t0 = time.perf_counter()
-    perm, ranges, Om, H = pipeline.build(F, cfg)
-    fac = ulv.factor(H, cfg["beta"])
-    t_build = time.perf_counter() - t0
-    yp = y[perm]
-    solve = lambda b: ulv.solve(fac, b)  # noqa: E731
-    for _ in range(warmup):
-        admm.run(solve, yp, cfg["C"][0], cfg["beta"], iters)
-    times = []
-    for _ in range(max(1, steps)):
-        t = time.perf_counter()
-        admm.run(solve, yp, cfg["C"][0], cfg["beta"], iters)
-        times.append(time.perf_counter() - t)
+    with threadpool_limits(limits=1):   # per-node phases: one BLAS thread (see oracle_phases)
+        t0 = time.perf_counter()
+        perm, ranges, Om, H = pipeline.build(F, cfg)
+        fac = ulv.factor(H, cfg["beta"])
+        t_build = time.perf_counter() - t0
+        yp = y[perm]
+        solve = lambda b: ulv.solve(fac, b)  # noqa: E731
+        for _ in range(warmup):
+            admm.run(solve, yp, cfg["C"][0], cfg["beta"], iters)
+        times = []
+        for _ in range(max(1, steps)):
+            t = time.perf_counter()
+            admm.run(solve, yp, cfg["C"][0], cfg["beta"], iters)
+            times.append(time.perf_counter() - t)
     per_it = float(np.median(times)) / iters
     scale = n_sample / cfg["n"]
     return dict(value=scale / per_it, unit="iters/s", build_ulv_s_sample=t_build, per_iter_s_sample=per_it,
