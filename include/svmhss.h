@@ -74,6 +74,19 @@ int hss_comm_init_nccl(int32_t nranks, int32_t rank, const void* unique_id, hss_
 int hss_comm_init_host(int32_t nranks, int32_t rank, hss_allgather_fn fn, void* ctx,
                        hss_comm_t* out);
 void hss_comm_free(hss_comm_t comm);
+/* in-kernel exchange: with NCCL >= 2.28 and every rank an LSA (NVLink load/store)
+ * peer, the NCCL communicator creates a device communicator (ncclDevCommCreate, one LSA barrier)
+ * and the per-iteration level-lg exchange becomes ONE kernel (inside the ADMM iteration's CUDA
+ * graph): the rank's slot is stored straight into every peer's symmetric window
+ * (ncclCommWindowRegister over ncclMemAlloc memory, two halves used on alternate calls), one LSA
+ * barrier, and every slot is unpacked from the local window.  Otherwise (older NCCL, ranks
+ * not all NVLink peers, or SVMHSS_NCCL_DEVICE=0) ncclAllGather.  Results are bitwise the same.
+ * hss_comm_info reports nranks / rank / whether the device API is in use (each nullable). */
+int hss_comm_info(hss_comm_t comm, int32_t* nranks, int32_t* rank, int32_t* device_api);
+/* Debug: one exchange of `count` doubles per rank through the communicator's per-iteration path
+ * (device API when in use, else allgather); recv: nranks * count device doubles, rank-major.
+ * Window allocation is collective: every rank must call it. */
+int hss_comm_exchange_test(hss_comm_t comm, const double* send, int64_t count, double* recv, void* stream);
 
 /* Build options (P:184-187 and readings T1-T4, R1-R3, H1-H5, AMB-10, AMB-11). */
 typedef struct {

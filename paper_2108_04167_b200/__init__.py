@@ -101,6 +101,24 @@ class Comm:
     def handle(self):
         return self._h
 
+    def info(self):
+        """dict(nranks, rank, device_api): device_api = 1 when the per-iteration exchange runs
+        in-kernel through the NCCL device API."""
+        a, b, c = ct.c_int32(), ct.c_int32(), ct.c_int32()
+        check(_L.hss_comm_info(self.handle, ct.byref(a), ct.byref(b), ct.byref(c)))
+        return dict(nranks=a.value, rank=b.value, device_api=c.value)
+
+    def exchange_test(self, send):
+        """Debug: one exchange of `send` (CUDA float64, count values) through the per-iteration
+        path; returns (nranks * count) values, rank-major."""
+        import torch
+        _cuda_f64(send, "send")
+        recv = torch.empty(self.world * send.numel(), dtype=torch.float64, device=send.device)
+        ctx, d = _on_device(send)
+        with ctx:
+            check(_L.hss_comm_exchange_test(self.handle, ptr(send), send.numel(), ptr(recv), _stream(None, d)))
+        return recv
+
     def free(self):
         if self._h is not None:
             _L.hss_comm_free(self._h)

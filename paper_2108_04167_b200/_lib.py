@@ -66,7 +66,8 @@ EXPORTS = ["hss_build", "hss_info", "hss_matvec", "hss_ulv_factor", "ulv_info", 
            "admm_svm_train", "svm_predict", "svm_train_predict_host", "hss_omega", "hss_tree",
            "hss_kernel_matmul", "hss_kernel_block", "hss_node", "hss_free", "ulv_free",
            "hss_last_error", "hss_version", "hss_launch_count", "hss_comm_nccl_id",
-           "hss_comm_init_nccl", "hss_comm_init_host", "hss_comm_free", "hss_ann_lists", "hss_pool_trim"]
+           "hss_comm_init_nccl", "hss_comm_init_host", "hss_comm_free", "hss_ann_lists", "hss_pool_trim",
+           "hss_comm_info", "hss_comm_exchange_test"]
 
 _lib = None
 
@@ -90,6 +91,8 @@ def load():
                                  ct.POINTER(AdmmStats), vp]
     L.svm_predict.argtypes = [vp, vp, vp, i64, i32, dbl, vp, i32, vp, i64, vp, vp, vp, vp]
     L.hss_pool_trim.argtypes = []
+    L.hss_comm_info.argtypes = [vp, ct.POINTER(i32), ct.POINTER(i32), ct.POINTER(i32)]
+    L.hss_comm_exchange_test.argtypes = [vp, vp, i64, vp, vp]
     L.svm_train_predict_host.argtypes = [vp, vp, i64, i32, dbl, ct.POINTER(HssOpts), dbl, vp, i32,
                                          i32, vp, i64, vp, vp, vp, vp, vp]
     L.hss_omega.argtypes = [u64, vp, i64, i32, vp, vp]

@@ -20,9 +20,28 @@ FLAGS = ["-gencode", "arch=compute_100a,code=sm_100a", "-lineinfo", "-O3", "-std
          "-Xcompiler", "-fPIC", "--expt-relaxed-constexpr", "-Xptxas", "-v"]
 
 
+def _nccl_include():
+    """The NCCL >= 2.28 headers with the device API (nccl_device.h), from the nvidia-nccl wheel
+    torch ships with; None if absent (comm.cu then builds without the N3 device exchange)."""
+    try:
+        import nvidia.nccl as nn
+        for base in list(getattr(nn, "__path__", [])):
+            inc = os.path.join(base, "include")
+            if os.path.exists(os.path.join(inc, "nccl_device.h")):
+                return inc
+    except ImportError:
+        pass
+    return None
+
+
 def _compile(src: str) -> tuple[str, str]:
     obj = os.path.join(BUILD, src.replace(".cu", ".o"))
-    cmd = [NVCC, *FLAGS, "-c", os.path.join(CSRC, src), "-o", obj]
+    extra = []
+    if src == "comm.cu":
+        inc = _nccl_include()
+        if inc:
+            extra = ["-I", inc, "-DSVMHSS_HAVE_NCCL_DEVICE"]
+    cmd = [NVCC, *FLAGS, *extra, "-c", os.path.join(CSRC, src), "-o", obj]
     p = subprocess.run(cmd, capture_output=True, text=True)
     if p.returncode != 0:
         raise RuntimeError(f"nvcc failed for {src}:\n{p.stderr}")

@@ -661,6 +661,43 @@ int hss_comm_init_host(int32_t nranks, int32_t rank, hss_allgather_fn fn, void* 
 
 void hss_comm_free(hss_comm_t c) { delete c; }
 
+int hss_comm_info(hss_comm_t c, int32_t* nranks, int32_t* rank, int32_t* device_api) {
+  return guarded([&] {
+    require(c != nullptr, "hss_comm_info: NULL comm");
+    if (nranks) *nranks = c->c->size;
+    if (rank) *rank = c->c->rank;
+    if (device_api) *device_api = c->c->device_api() ? 1 : 0;
+  }, /*need_device=*/false);
+}
+
+int hss_comm_exchange_test(hss_comm_t c, const double* send, int64_t count, double* recv, void* stream) {
+  return guarded([&] {
+    StreamScope ss__((cudaStream_t)stream);
+    require(c && send && recv, "hss_comm_exchange_test: NULL pointer");
+    require(count >= 1, "hss_comm_exchange_test: count must be >= 1");
+    Comm& C = *c->c;
+    cudaStream_t s = (cudaStream_t)stream;
+    const int P = C.size;
+    if (!C.device_api()) {
+      C.allgather(send, recv, (size_t)count * sizeof(double), s);
+      CUDA_CHECK(cudaStreamSynchronize(s));
+      return;
+    }
+    // the level-lg exchange kernel with a trivial layout: rank p's `count` values at p * count
+    std::vector<int64_t> ko(P), kk(P, count);
+    for (int p = 0; p < P; ++p) ko[p] = (int64_t)p * count;
+    auto dko = upload(ko, s), dkk = upload(kk, s);
+    CUDA_CHECK(cudaMemcpyAsync(recv + (int64_t)C.rank * count, send, (size_t)count * sizeof(double),
+                               cudaMemcpyDeviceToDevice, s));
+    DevWindow w = C.window_alloc((size_t)P * count * sizeof(double));
+    struct WG { Comm& c; DevWindow& w; ~WG() { c.window_free(w); } } wg{C, w};
+    ExchangeArgs a{recv, (int64_t)C.rank * count, (int)count, 1, 0, (int)count, nullptr, nullptr, dko.p, dkk.p, count};
+    C.device_exchange(w, a, s);
+    C.device_exchange(w, a, s);   // twice: both window halves
+    CUDA_CHECK(cudaStreamSynchronize(s));
+  });
+}
+
 void hss_free(hss_t H) {
   if (!H) return;
   int prev = 0;

@@ -148,7 +148,13 @@ void ann_y_level(const HSSImpl& H, int l, const int64_t* act, const int64_t* C, 
 struct ExchWS {
   int ncols = 0, nextra = 0;
   int64_t slot = 0;              // doubles per rank slot: kmax_lg * ncols + nextra
-  DevBuf<double> send, recv;     // slot, P * slot
+  DevBuf<double> send, recv;     // slot, P * slot (ncclAllGather / host backends)
+  std::shared_ptr<Comm> comm;    // device-API backend: the symmetric window below (N3)
+  DevWindow win;
+  ExchWS() {}
+  ExchWS(const ExchWS&) = delete;
+  ExchWS& operator=(const ExchWS&) = delete;
+  ~ExchWS() { if (comm && win.win) comm->window_free(win); }
 };
 void exch_ws_alloc(const HSSImpl& H, int ncols, int nextra, ExchWS& ws);
 // buf: level-lg k-packed vector (global offsets, ncols per row) in which only this rank's

@@ -65,6 +65,11 @@ void exch_ws_alloc(const HSSImpl& H, int ncols, int nextra, ExchWS& ws) {
   ws.ncols = ncols;
   ws.nextra = nextra;
   ws.slot = (int64_t)H.kmax_lg * ncols + nextra;
+  if (H.sh.on() && H.sh.comm->device_api()) {  // N3: symmetric window (collective allocation)
+    ws.comm = H.sh.comm;
+    ws.win = ws.comm->window_alloc((size_t)std::max<int64_t>(1, ws.slot * H.sh.P) * sizeof(double));
+    return;
+  }
   ws.send.alloc(std::max<int64_t>(1, ws.slot));
   ws.recv.alloc(std::max<int64_t>(1, ws.slot * H.sh.P));
 }
@@ -92,6 +97,12 @@ void exchange_lg(const HSSImpl& H, ExchWS& ws, double* buf, const double* extra,
     return;
   }
   const auto& own = H.lv[H.sh.lg][H.sh.g];
+  if (ws.win.win) {  // N3: pack -> NVLink stores into every peer's window -> LSA barrier -> unpack
+    ExchangeArgs a{buf, own.koff, own.k, ws.ncols, ws.nextra, H.kmax_lg, extra, extra_out, H.lg_koff.p, H.lg_k.p,
+                   ws.slot};
+    H.sh.comm->device_exchange(ws.win, a, s);
+    return;
+  }
   if (own.k > 0)
     CUDA_CHECK(cudaMemcpyAsync(ws.send.p, buf + own.koff * ws.ncols, (size_t)own.k * ws.ncols * sizeof(double),
                                cudaMemcpyDeviceToDevice, s));

@@ -19,6 +19,18 @@ def main():
     import datagen
     import paper_2108_04167_b200 as P
     comm = P.Comm.nccl()
+    info = comm.info()
+    # N3: one exchange through the per-iteration path (NCCL device API when available: NVLink
+    # stores into the peers' symmetric windows + LSA barrier; with one rank, the same kernel on
+    # a one-rank team), and once more with the device API disabled (ncclAllGather)
+    send = torch.arange(7, dtype=torch.float64, device="cuda") + 100.0 * rank
+    ex_dev = comm.exchange_test(send).cpu().numpy()
+    os.environ["SVMHSS_NCCL_DEVICE"] = "0"
+    comm0 = P.Comm.nccl()
+    info0 = comm0.info()
+    ex_ag = comm0.exchange_test(send).cpu().numpy()
+    comm0.free()
+    del os.environ["SVMHSS_NCCL_DEVICE"]
     cfg = datagen.get_config(3)
     F, y, _, _ = datagen.generate(3, n=4096, n_test=0)
     Fd, yd = torch.from_numpy(F).cuda(), torch.from_numpy(y).cuda()
@@ -32,7 +44,8 @@ def main():
         U.free()
         H.free()
     np.savez(os.path.join(out, f"nccl_r{rank}.npz"), z_comm=res["comm"][0], z_none=res["none"][0],
-             obj_comm=res["comm"][1], obj_none=res["none"][1], graph=res["comm"][2])
+             obj_comm=res["comm"][1], obj_none=res["none"][1], graph=res["comm"][2],
+             device_api=info["device_api"], device_api_off=info0["device_api"], ex_dev=ex_dev, ex_ag=ex_ag)
     comm.free()
     dist.barrier()
     dist.destroy_process_group()

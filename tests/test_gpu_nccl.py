@@ -1,6 +1,8 @@
 """The library's NCCL communicator on the GPU box: Comm.nccl() over a torch.distributed NCCL group
-(one rank per GPU available here), a build/factor/train through it equals the run without a
-comm, and the ADMM loop is still captured as a CUDA graph (NCCL is graph-capturable)."""
+(one rank per GPU available here, two when there are two), a build/factor/train through it equals
+the run without a comm, and the ADMM loop is still captured as a CUDA graph (NCCL is
+graph-capturable).  The in-kernel exchange through the NCCL device API (N3) runs on hardware:
+with one GPU on a one-rank LSA team (self stores + LSA barrier), with more on NVLink peers."""
 import os
 import socket
 import subprocess
@@ -31,6 +33,12 @@ def test_nccl_comm_single_rank(tmp_path):
         d = np.load(os.path.join(tmp_path, f"nccl_r{k}.npz"))
         assert np.array_equal(d["z_comm"], d["z_none"]) and np.array_equal(d["obj_comm"], d["obj_none"])
         assert int(d["graph"]) == 1
+        expect = np.concatenate([np.arange(7) + 100.0 * q for q in range(world)])
+        assert np.array_equal(d["ex_ag"], expect) and int(d["device_api_off"]) == 0
+        # NCCL 2.28 device API: in use on this NCCL, and the in-kernel exchange
+        # gives the allgather's result
+        assert int(d["device_api"]) == 1
+        assert np.array_equal(d["ex_dev"], expect)
         if ref is None:
             ref = d["z_comm"]
         assert np.array_equal(d["z_comm"], ref)
