@@ -418,6 +418,9 @@ def main():
     if args.impl == "reference":
         return run_reference(args, rank, world)
 
+    # the library's memory pool stays reserved between steps (a process that rebuilds repeatedly;
+    # the default trims it when the last handle is freed, and each build then re-maps ~30 GB)
+    os.environ.setdefault("SVMHSS_POOL_KEEP", "1")
     import torch
     import torch.distributed as dist
 
@@ -529,8 +532,11 @@ def main():
                        "sampling": args.sampling, "n": n, "n_test": nt, "r": cfg["r"], "h": h, "C": Cs,
                        "beta": cfg["beta"], "max_it": max_it, "leaf": cfg["leaf"], "cap": cfg["cap"],
                        "s": cfg["s"], "rel_tol": cfg["rel_tol"],
-                       "parallelism": f"subtree-sharded over {world} (NCCL allgather per phase / iteration)"
+                       "parallelism": (f"subtree-sharded over {world}: per-iteration exchange "
+                                       + ("in-kernel via the NCCL device API (N3)" if comm is not None and comm.info()["device_api"]
+                                          else "ncclAllGather in the iteration graph"))
                        if world > 1 else "1 GPU",
+                       "pool": "library memory pool kept between steps (SVMHSS_POOL_KEEP=%s)" % os.environ.get("SVMHSS_POOL_KEEP"),
                        "l2": "inputs larger than L2 (factor %.2f GB, sketch operands %.2f GB)" % (
                            ui["factor_bytes"] / 1e9, 16.0 * n * cfg["s"] / 1e9)},
             "hss_build_ulv_s": build_ms / 1e3,

@@ -158,7 +158,7 @@ typedef struct {
  * Memory: device buffers come from the library's OWN stream-ordered pool on the current device
  * (cudaMemPoolCreate; never the device's default pool, so torch's allocator is not affected).
  * The pool keeps freed memory reserved while any hss_t / ulv_t of the device is alive and is
- * trimmed to zero when the last one is freed.  Before the first build of a given size the pool
+ * trimmed to zero when the last one is freed (unless SVMHSS_POOL_KEEP=1; hss_pool_trim releases).  Before the first build of a given size the pool
  * is grown once to about 24 n (s + r) 8 bytes (at most half the free memory;
  * SVMHSS_POOL_RESERVE_GB overrides, 0 disables) so later phases do not map memory mid-call. */
 int hss_build(const double* F, int64_t n, int32_t r, double h, const hss_opts* opt,

@@ -60,10 +60,13 @@ static void handle_acquired() {
 }
 static void handle_released(int dev) {
   cudaMemPool_t pool = nullptr;
+  // SVMHSS_POOL_KEEP=1: keep the reservation when the last handle goes (a process that rebuilds
+  // repeatedly, e.g. bench.py's steps, avoids re-mapping GBs per build; hss_pool_trim releases)
+  static const bool keep = [] { const char* e = getenv("SVMHSS_POOL_KEEP"); return e && e[0] == '1'; }();
   {
     std::lock_guard<std::mutex> g(g_pool_mu);
     if (dev < 0 || dev >= (int)g_live.size()) return;
-    if (--g_live[dev] > 0) return;
+    if (--g_live[dev] > 0 || keep) return;
     pool = g_pools[dev];
     g_reserved[dev] = 0;
   }
