@@ -120,6 +120,132 @@ __global__ void __launch_bounds__(256) admm_epilogue_kernel(EpiArgs A, const int
   }
 }
 
+// ---- the leaf level of both sweeps fused with the epilogue (one CTA per leaf; the leaves with
+// their own transform first, the pass-through leaves after):
+//   leaf t with M_t:  x_t = M_t^T [x_s; y_r]  ->  ADMM update of its points (next right-hand side
+//                     b_t kept in shared memory)  ->  t' = M_t b_t: up -> level L-1 input, y_r
+//                     (the next iteration's level-L forward sweep)
+//   pass-through leaf: the ADMM update reading x from level L-1's solution, writing the next
+//                     right-hand side into level L-1's input
+// bwd_cols / fwd_rows are the level kernels' device functions and the point update is
+// epi_point's formula in the same order, so the results are bitwise those of the unfused
+// ulv_bwd_kernel -> admm_epilogue_kernel -> ulv_fwd_kernel sequence.
+template <int NR>
+__global__ void __launch_bounds__(256) admm_leaf_kernel(EpiArgs A, const SolveNode* __restrict__ nodes,
+                                                        const int* __restrict__ order,
+                                                        const int64_t* __restrict__ leaf_lo, int nleaf_all,
+                                                        const double* __restrict__ M,
+                                                        const double* __restrict__ xs_in, double* __restrict__ yr,
+                                                        double* __restrict__ fin_up, double* __restrict__ part,
+                                                        double* __restrict__ out, unsigned* __restrict__ counter,
+                                                        int smem_tree, int maxR) {
+  extern __shared__ double sm[];
+  pdl_trigger();
+  pdl_wait();
+  const int leaf = order[blockIdx.x];
+  const SolveNode N = nodes[leaf];
+  const int64_t i0 = leaf_lo[leaf], i1 = leaf_lo[leaf + 1];
+  const int npt = (int)(i1 - i0);
+  const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
+  double* ush = sm;                          // maxR x NR: [x_s; y_r], then the next rhs
+  double* xv = ush + (size_t)maxR * NR;      // maxR x NR: x of the leaf's points
+  double* red = xv + (size_t)maxR * NR;      // kBW x kCW x NR
+  double* cs = red + (size_t)kBW * kCW * NR; // chunk sums (last block: the leaf-partial tree)
+  if (!N.pt) {
+    const int R = N.R, kn = N.k * NR;
+    for (int e = tid; e < R * NR; e += 256) ush[e] = (e < kn) ? xs_in[N.koff * NR + e] : yr[(N.yoff - N.k) * NR + e];
+    __syncthreads();
+    for (int j0 = 0; j0 < R; j0 += kCW) bwd_cols<NR>(M + N.moff, R, ush, j0, red, xv);
+  }
+  const int nch = (npt + 31) / 32;
+  for (int ch = wid; ch < nch; ch += 8) {
+    const int ii = 32 * ch + lane;
+    const int64_t p = i0 + ii;
+    const bool valid = ii < npt;
+    double mine = 0.0;
+#pragma unroll
+    for (int c = 0; c < NR; ++c) {
+      double v = 0.0;
+      if (valid) {
+        const double coef = A.swq[c] / A.w1, C = A.Cv[c];
+        const int64_t e = p * NR + c;
+        const double vi = N.pt ? xs_in[(N.koff + ii) * NR + c] : xv[ii * NR + c];
+        const double yi = A.y[p], wi = A.w[p];
+        const double x = yi * vi - coef * wi;
+        const double m = A.mu[e];
+        const double zn = fmin(fmax(x - m / A.beta, 0.0), C);
+        const double mn = m - A.beta * (x - zn);
+        A.z[e] = zn;
+        A.mu[e] = mn;
+        const double qn = 1.0 + mn + A.beta * zn;
+        if (N.pt) fin_up[(N.koff + ii) * NR + c] = yi * qn;
+        else ush[ii * NR + c] = yi * qn;
+        v = wi * qn;
+      }
+      const double t = warp_sum(v);
+      if (lane == c) mine = t;
+    }
+    if (lane < NR) cs[ch * NR + lane] = mine;
+  }
+  __syncthreads();
+  if (tid < NR) {
+    double t = 0.0;
+    for (int ch = 0; ch < nch; ++ch) t += cs[ch * NR + tid];
+    part[(int64_t)leaf * NR + tid] = t;
+  }
+  if (!N.pt) fwd_rows<NR>(M + N.moff, N.R, ush, 0, N.R, wid, 8, N.k, N.koff, N.yoff, fin_up, yr);
+  // the last block to finish reduces the leaf partials up the subtree (as admm_epilogue_kernel)
+  __shared__ bool last;
+  __threadfence();
+  __syncthreads();
+  if (tid == 0) last = (atomicAdd(counter, 1u) == gridDim.x - 1);
+  __syncthreads();
+  if (!last) return;
+  __threadfence();
+  if (smem_tree) {
+    for (int c = 0; c < NR; ++c) {
+      for (int i = tid; i < nleaf_all; i += 256) cs[i] = __ldcg(part + (int64_t)i * NR + c);
+      __syncthreads();
+      for (int st = 1; st < nleaf_all; st <<= 1) {
+        for (int i = tid * 2 * st; i + st < nleaf_all; i += 256 * 2 * st) cs[i] += cs[i + st];
+        __syncthreads();
+      }
+      if (tid == 0) { out[c] = cs[0]; part[c] = cs[0]; }
+      __syncthreads();
+    }
+  } else {
+    for (int st = 1; st < nleaf_all; st <<= 1) {
+      const int npair = (nleaf_all + 2 * st - 1) / (2 * st);
+      for (int e = tid; e < npair * NR; e += 256) {
+        const int i = (e / NR) * 2 * st, c = e % NR;
+        if (i + st < nleaf_all) part[(int64_t)i * NR + c] += __ldcg(part + (int64_t)(i + st) * NR + c);
+      }
+      __syncthreads();
+    }
+    for (int c = tid; c < NR; c += 256) out[c] = part[c];
+  }
+  if (tid == 0) *counter = 0u;
+}
+
+static void leaf_dispatch(int NR, dim3 grid, size_t smem, cudaStream_t s, const EpiArgs& A, const SolveNode* nodes,
+                          const int* order, const int64_t* leaf_lo, int nleaf, const double* M, const double* xs_in,
+                          double* yr, double* fin_up, double* part, double* out, unsigned* counter, int smem_tree,
+                          int maxR) {
+  switch (NR) {
+#define LC(k)                                                                                                     \
+  case k:                                                                                                         \
+    if (smem > 48 * 1024)                                                                                         \
+      CUDA_CHECK(cudaFuncSetAttribute(admm_leaf_kernel<k>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem)); \
+    launch_pdl(admm_leaf_kernel<k>, grid, dim3(256), smem, s, A, nodes, order, leaf_lo, nleaf, M, xs_in, yr, fin_up, \
+               part, out, counter, smem_tree, maxR);                                                              \
+    break;
+    LC(1) LC(2) LC(3) LC(4) LC(5) LC(6) LC(7) LC(8)
+#undef LC
+    default: throw Error(HSS_EINVAL, "admm: nC must be 1..8");
+  }
+  g_launches.fetch_add(1);
+}
+
 // Per-leaf partials of column sums: out[leaf*ncols + c] = sum_{i in leaf} f(i, c)
 //   mode 0: A[i*ncols + c]   mode 1: A[i*ncols + c] * B[i*ncols + c]
 __global__ void leaf_colsum_kernel(const int64_t* __restrict__ leaf_lo, int ncols, const double* __restrict__ A,
@@ -312,7 +438,35 @@ AdmmResult admm_train_impl(const ULVImpl& F, const double* y_orig, const std::ve
   if (smem_tree) epi_smem = std::max(epi_smem, (size_t)nleaf * sizeof(double));
   if (epi_smem > 48 * 1024)
     CUDA_CHECK(cudaFuncSetAttribute(admm_epilogue_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)epi_smem));
+  // leaf level fused with the epilogue (admm_leaf_kernel): needs the leaves strictly below the
+  // exchanged level; bitwise the same as the unfused sequence (SVMHSS_LEAF_FUSE=0 runs that)
+  static const bool leaf_fuse_env = [] { const char* e = getenv("SVMHSS_LEAF_FUSE"); return !(e && e[0] == '0'); }();
+  const bool leaf_fuse = fused && leaf_fuse_env && L > sh.lg && !F.lv[L].allpt;
+  DevBuf<int> lorder;
+  size_t leaf_smem = 0;
+  int maxRL = 1;
+  if (leaf_fuse) {
+    std::vector<int> ord;
+    for (int i = sh.first(L); i < sh.last(L); ++i)
+      if (!H.lv[L][i].pt) ord.push_back(i - sh.first(L));
+    for (int i = sh.first(L); i < sh.last(L); ++i)
+      if (H.lv[L][i].pt) ord.push_back(i - sh.first(L));
+    lorder = upload(ord, s);
+    maxRL = std::max(1, F.lv[L].maxR);
+    const size_t chs = (size_t)((maxleaf + 31) / 32) * nC;
+    leaf_smem = ((size_t)2 * maxRL * nC + (size_t)kBW * kCW * nC + std::max(chs, smem_tree ? (size_t)nleaf : 0)) *
+                sizeof(double);
+    // prologue: the level-L forward sweep of iteration 1 (the loop body's leaf kernel produces it
+    // for the next iteration)
+    ulv_solve_steps(F, ws, {SolveStep{SolveStep::FWD, L, L}}, s);
+  }
   auto iteration = [&](cudaStream_t st) {
+    if (leaf_fuse) {
+      ulv_solve_steps(F, ws, {SolveStep{SolveStep::FWD, L - 1, 0}, SolveStep{SolveStep::BWD, 0, L - 1}}, st);
+      leaf_dispatch(nC, dim3(nleaf), leaf_smem, st, EA, F.lv[L].nodes.p, lorder.p, H.leaf_lo.p, nleaf, F.lv[L].M.p,
+                    ws.xout[L - 1], ws.yr[L], ws.fin[L - 1], part.p, epi_out, counter.p, smem_tree, maxRL);
+      return;
+    }
     ulv_solve_tree(F, ws, st);
     launch_pdl(admm_epilogue_kernel, dim3(nleaf), dim3(256), epi_smem, st, EA, H.leaf_lo.p, (const int*)nullptr,
                nleaf, part.p, epi_out, counter.p, smem_tree);
