@@ -26,23 +26,30 @@ struct EpiArgs {
   double *z, *mu, *bL, *bL1;
   int nC;
 };
+// One point's update with every rounding spelled out (no compiler FMA contraction choices), so
+// the epilogue kernel and the fused leaf kernel produce bitwise the same values.
+__device__ __forceinline__ double admm_update(double vi, double yi, double wi, double m, double coef, double C,
+                                              double beta, double& zn, double& mn, double& rhs) {
+  const double x = __fma_rn(yi, vi, -__dmul_rn(coef, wi));      // x = y v - (w^T q / w1) w
+  zn = fmin(fmax(__dsub_rn(x, __ddiv_rn(m, beta)), 0.0), C);    // z = clip(x - mu / beta, 0, C)
+  mn = __fma_rn(-beta, __dsub_rn(x, zn), m);                    // mu - beta (x - z)
+  const double qn = __fma_rn(beta, zn, __dadd_rn(1.0, mn));     // q' = 1 + mu + beta z
+  rhs = __dmul_rn(yi, qn);                                      // next right-hand side y q'
+  return __dmul_rn(wi, qn);                                     // w_i q'_i
+}
 __device__ __forceinline__ double epi_point(const EpiArgs& A, int64_t i, int c) {
-  const double coef = A.swq[c] / A.w1, C = A.Cv[c];
+  const double coef = __ddiv_rn(A.swq[c], A.w1), C = A.Cv[c];
   const int nC = A.nC;
   const int64_t e = i * nC + c;
   const int64_t q = A.ptmap ? A.ptmap[i] : -1;
   const double vi = (q >= 0) ? A.xL1[q * nC + c] : A.xL[e];
-  const double yi = A.y[i], wi = A.w[i];
-  const double x = yi * vi - coef * wi;
-  const double m = A.mu[e];
-  const double zn = fmin(fmax(x - m / A.beta, 0.0), C);
-  const double mn = m - A.beta * (x - zn);
+  double zn, mn, rhs;
+  const double r = admm_update(vi, A.y[i], A.w[i], A.mu[e], coef, C, A.beta, zn, mn, rhs);
   A.z[e] = zn;
   A.mu[e] = mn;
-  const double qn = 1.0 + mn + A.beta * zn;
-  if (q >= 0) A.bL1[q * nC + c] = yi * qn;
-  else A.bL[e] = yi * qn;
-  return wi * qn;
+  if (q >= 0) A.bL1[q * nC + c] = rhs;
+  else A.bL[e] = rhs;
+  return r;
 }
 // A leaf's w^T q' partial is defined chunk-wise (both epilogue kernels below): chunks of 32
 // consecutive points from the leaf's start, each summed by a warp butterfly, then the chunk sums
@@ -130,35 +137,20 @@ __global__ void __launch_bounds__(256) admm_epilogue_kernel(EpiArgs A, const int
 // bwd_cols / fwd_rows are the level kernels' device functions and the point update is
 // epi_point's formula in the same order, so the results are bitwise those of the unfused
 // ulv_bwd_kernel -> admm_epilogue_kernel -> ulv_fwd_kernel sequence.
+constexpr int kLeafThreads = 512, kLeafGroups = kLeafThreads / (kBW * 32);
+constexpr int kLeafWarps = kLeafThreads / 32;
+
+// ADMM update (epi_point's formula, same order) of one leaf's points by warps [w0, w0 + nw): chunk
+// ch (32 points) by warp w0 + ch mod nw; chunk sums (lane c: problem c) into cs[ch * NR + c].
+// x from xv (the leaf's own transform, shared memory) or level L-1's solution (pass-through);
+// the next right-hand side into rhs_sm (shared) or level L-1's input (pass-through).
 template <int NR>
-__global__ void __launch_bounds__(256) admm_leaf_kernel(EpiArgs A, const SolveNode* __restrict__ nodes,
-                                                        const int* __restrict__ order,
-                                                        const int64_t* __restrict__ leaf_lo, int nleaf_all,
-                                                        const double* __restrict__ M,
-                                                        const double* __restrict__ xs_in, double* __restrict__ yr,
-                                                        double* __restrict__ fin_up, double* __restrict__ part,
-                                                        double* __restrict__ out, unsigned* __restrict__ counter,
-                                                        int smem_tree, int maxR) {
-  extern __shared__ double sm[];
-  pdl_trigger();
-  pdl_wait();
-  const int leaf = order[blockIdx.x];
-  const SolveNode N = nodes[leaf];
-  const int64_t i0 = leaf_lo[leaf], i1 = leaf_lo[leaf + 1];
-  const int npt = (int)(i1 - i0);
-  const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
-  double* ush = sm;                          // maxR x NR: [x_s; y_r], then the next rhs
-  double* xv = ush + (size_t)maxR * NR;      // maxR x NR: x of the leaf's points
-  double* red = xv + (size_t)maxR * NR;      // kBW x kCW x NR
-  double* cs = red + (size_t)kBW * kCW * NR; // chunk sums (last block: the leaf-partial tree)
-  if (!N.pt) {
-    const int R = N.R, kn = N.k * NR;
-    for (int e = tid; e < R * NR; e += 256) ush[e] = (e < kn) ? xs_in[N.koff * NR + e] : yr[(N.yoff - N.k) * NR + e];
-    __syncthreads();
-    for (int j0 = 0; j0 < R; j0 += kCW) bwd_cols<NR>(M + N.moff, R, ush, j0, red, xv);
-  }
+__device__ __forceinline__ void leaf_update(const EpiArgs& A, const SolveNode& N, int64_t i0, int npt, int w0, int nw,
+                                            const double* __restrict__ xs_in, const double* xv,
+                                            double* __restrict__ fin_up, double* rhs_sm, double* cs) {
+  const int lane = threadIdx.x & 31, wid = (threadIdx.x >> 5) - w0;
   const int nch = (npt + 31) / 32;
-  for (int ch = wid; ch < nch; ch += 8) {
+  for (int ch = wid; ch < nch; ch += nw) {
     const int ii = 32 * ch + lane;
     const int64_t p = i0 + ii;
     const bool valid = ii < npt;
@@ -167,33 +159,89 @@ __global__ void __launch_bounds__(256) admm_leaf_kernel(EpiArgs A, const SolveNo
     for (int c = 0; c < NR; ++c) {
       double v = 0.0;
       if (valid) {
-        const double coef = A.swq[c] / A.w1, C = A.Cv[c];
+        const double coef = __ddiv_rn(A.swq[c], A.w1), C = A.Cv[c];
         const int64_t e = p * NR + c;
         const double vi = N.pt ? xs_in[(N.koff + ii) * NR + c] : xv[ii * NR + c];
-        const double yi = A.y[p], wi = A.w[p];
-        const double x = yi * vi - coef * wi;
-        const double m = A.mu[e];
-        const double zn = fmin(fmax(x - m / A.beta, 0.0), C);
-        const double mn = m - A.beta * (x - zn);
+        double zn, mn, rhs;
+        v = admm_update(vi, A.y[p], A.w[p], A.mu[e], coef, C, A.beta, zn, mn, rhs);
         A.z[e] = zn;
         A.mu[e] = mn;
-        const double qn = 1.0 + mn + A.beta * zn;
-        if (N.pt) fin_up[(N.koff + ii) * NR + c] = yi * qn;
-        else ush[ii * NR + c] = yi * qn;
-        v = wi * qn;
+        if (N.pt) fin_up[(N.koff + ii) * NR + c] = rhs;
+        else rhs_sm[ii * NR + c] = rhs;
       }
       const double t = warp_sum(v);
       if (lane == c) mine = t;
     }
     if (lane < NR) cs[ch * NR + lane] = mine;
   }
-  __syncthreads();
-  if (tid < NR) {
-    double t = 0.0;
-    for (int ch = 0; ch < nch; ++ch) t += cs[ch * NR + tid];
-    part[(int64_t)leaf * NR + tid] = t;
+}
+
+// work[b] = {leaf a, leaf b}: a leaf with its own transform alone ({a, -1}, all warps), or one or
+// two pass-through leaves (half of the warps each) -- pass-through leaves are only an ADMM update,
+// so two per CTA halve the number of short CTAs.
+template <int NR>
+__global__ void __launch_bounds__(kLeafThreads) admm_leaf_kernel(EpiArgs A, const SolveNode* __restrict__ nodes,
+                                                                 const int2* __restrict__ work,
+                                                                 const int64_t* __restrict__ leaf_lo, int nleaf_all,
+                                                                 const double* __restrict__ M,
+                                                                 const double* __restrict__ xs_in,
+                                                                 double* __restrict__ yr, double* __restrict__ fin_up,
+                                                                 double* __restrict__ part, double* __restrict__ out,
+                                                                 unsigned* __restrict__ counter, int smem_tree,
+                                                                 int maxR, int maxch) {
+  extern __shared__ double sm[];
+  pdl_trigger();
+  pdl_wait();
+  const int2 wk = work[blockIdx.x];
+  const int leaf = wk.x;
+  const SolveNode N = nodes[leaf];
+  const int64_t i0 = leaf_lo[leaf], i1 = leaf_lo[leaf + 1];
+  const int npt = (int)(i1 - i0);
+  const int tid = threadIdx.x;
+  double* ush = sm;                          // maxR x NR: [x_s; y_r], then the next rhs
+  double* xv = ush + (size_t)maxR * NR;      // maxR x NR: x of the leaf's points
+  double* red = xv + (size_t)maxR * NR;      // groups x kBW x kCW x NR
+  double* cs = red + (size_t)kLeafGroups * kBW * kCW * NR; // chunk sums (2 x maxch x NR; last block: the tree)
+  if (!N.pt) {
+    const int R = N.R, kn = N.k * NR;
+    for (int e = tid; e < R * NR; e += kLeafThreads) ush[e] = (e < kn) ? xs_in[N.koff * NR + e] : yr[(N.yoff - N.k) * NR + e];
+    __syncthreads();
+    // the column chunks in parallel, one group of kBW warps per chunk
+    const int grp = tid / (kBW * 32), tig = tid % (kBW * 32);
+    const int nrounds = ((R + kCW - 1) / kCW + kLeafGroups - 1) / kLeafGroups;  // uniform over the CTA
+    for (int rd = 0; rd < nrounds; ++rd) {
+      const int j0 = (rd * kLeafGroups + grp) * kCW;
+      bwd_cols<NR>(M + N.moff, R, ush, j0, red + (size_t)grp * kBW * kCW * NR, xv, tig, j0 >= R);
+    }
+    leaf_update<NR>(A, N, i0, npt, 0, kLeafWarps, xs_in, xv, fin_up, ush, cs);
+    __syncthreads();
+    if (tid < NR) {
+      double t = 0.0;
+      for (int ch = 0; ch < (npt + 31) / 32; ++ch) t += cs[ch * NR + tid];
+      part[(int64_t)leaf * NR + tid] = t;
+    }
+    fwd_rows<NR>(M + N.moff, N.R, ush, 0, N.R, tid >> 5, kLeafWarps, N.k, N.koff, N.yoff, fin_up, yr);
+  } else {
+    const int half = (tid >> 5) >= kLeafWarps / 2;
+    const int lf = half ? wk.y : leaf;
+    if (lf >= 0) {
+      const SolveNode Nh = half ? nodes[lf] : N;
+      const int64_t j0 = leaf_lo[lf];
+      leaf_update<NR>(A, Nh, j0, (int)(leaf_lo[lf + 1] - j0), half * (kLeafWarps / 2), kLeafWarps / 2, xs_in,
+                      nullptr, fin_up, nullptr, cs + (size_t)half * maxch * NR);
+    }
+    __syncthreads();
+    if (tid < 2 * NR) {
+      const int h = tid / NR, c = tid % NR;
+      const int lh = h ? wk.y : leaf;
+      if (lh >= 0) {
+        const int nc = (int)((leaf_lo[lh + 1] - leaf_lo[lh] + 31) / 32);
+        double t = 0.0;
+        for (int ch = 0; ch < nc; ++ch) t += cs[((size_t)h * maxch + ch) * NR + c];
+        part[(int64_t)lh * NR + c] = t;
+      }
+    }
   }
-  if (!N.pt) fwd_rows<NR>(M + N.moff, N.R, ush, 0, N.R, wid, 8, N.k, N.koff, N.yoff, fin_up, yr);
   // the last block to finish reduces the leaf partials up the subtree (as admm_epilogue_kernel)
   __shared__ bool last;
   __threadfence();
@@ -204,10 +252,10 @@ __global__ void __launch_bounds__(256) admm_leaf_kernel(EpiArgs A, const SolveNo
   __threadfence();
   if (smem_tree) {
     for (int c = 0; c < NR; ++c) {
-      for (int i = tid; i < nleaf_all; i += 256) cs[i] = __ldcg(part + (int64_t)i * NR + c);
+      for (int i = tid; i < nleaf_all; i += kLeafThreads) cs[i] = __ldcg(part + (int64_t)i * NR + c);
       __syncthreads();
       for (int st = 1; st < nleaf_all; st <<= 1) {
-        for (int i = tid * 2 * st; i + st < nleaf_all; i += 256 * 2 * st) cs[i] += cs[i + st];
+        for (int i = tid * 2 * st; i + st < nleaf_all; i += kLeafThreads * 2 * st) cs[i] += cs[i + st];
         __syncthreads();
       }
       if (tid == 0) { out[c] = cs[0]; part[c] = cs[0]; }
@@ -216,28 +264,28 @@ __global__ void __launch_bounds__(256) admm_leaf_kernel(EpiArgs A, const SolveNo
   } else {
     for (int st = 1; st < nleaf_all; st <<= 1) {
       const int npair = (nleaf_all + 2 * st - 1) / (2 * st);
-      for (int e = tid; e < npair * NR; e += 256) {
+      for (int e = tid; e < npair * NR; e += kLeafThreads) {
         const int i = (e / NR) * 2 * st, c = e % NR;
         if (i + st < nleaf_all) part[(int64_t)i * NR + c] += __ldcg(part + (int64_t)(i + st) * NR + c);
       }
       __syncthreads();
     }
-    for (int c = tid; c < NR; c += 256) out[c] = part[c];
+    for (int c = tid; c < NR; c += kLeafThreads) out[c] = part[c];
   }
   if (tid == 0) *counter = 0u;
 }
 
 static void leaf_dispatch(int NR, dim3 grid, size_t smem, cudaStream_t s, const EpiArgs& A, const SolveNode* nodes,
-                          const int* order, const int64_t* leaf_lo, int nleaf, const double* M, const double* xs_in,
+                          const int2* order, const int64_t* leaf_lo, int nleaf, const double* M, const double* xs_in,
                           double* yr, double* fin_up, double* part, double* out, unsigned* counter, int smem_tree,
-                          int maxR) {
+                          int maxR, int maxch) {
   switch (NR) {
 #define LC(k)                                                                                                     \
   case k:                                                                                                         \
     if (smem > 48 * 1024)                                                                                         \
       CUDA_CHECK(cudaFuncSetAttribute(admm_leaf_kernel<k>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem)); \
-    launch_pdl(admm_leaf_kernel<k>, grid, dim3(256), smem, s, A, nodes, order, leaf_lo, nleaf, M, xs_in, yr, fin_up, \
-               part, out, counter, smem_tree, maxR);                                                              \
+    launch_pdl(admm_leaf_kernel<k>, grid, dim3(kLeafThreads), smem, s, A, nodes, order, leaf_lo, nleaf, M, xs_in, yr, fin_up, \
+               part, out, counter, smem_tree, maxR, maxch);                                                       \
     break;
     LC(1) LC(2) LC(3) LC(4) LC(5) LC(6) LC(7) LC(8)
 #undef LC
@@ -442,20 +490,24 @@ AdmmResult admm_train_impl(const ULVImpl& F, const double* y_orig, const std::ve
   // exchanged level; bitwise the same as the unfused sequence (SVMHSS_LEAF_FUSE=0 runs that)
   static const bool leaf_fuse_env = [] { const char* e = getenv("SVMHSS_LEAF_FUSE"); return !(e && e[0] == '0'); }();
   const bool leaf_fuse = fused && leaf_fuse_env && L > sh.lg && !F.lv[L].allpt;
-  DevBuf<int> lorder;
+  DevBuf<int2> lorder;
   size_t leaf_smem = 0;
-  int maxRL = 1;
+  int maxRL = 1, nleafw = 0;
+  const int maxch = (maxleaf + 31) / 32;
   if (leaf_fuse) {
-    std::vector<int> ord;
-    for (int i = sh.first(L); i < sh.last(L); ++i)
-      if (!H.lv[L][i].pt) ord.push_back(i - sh.first(L));
-    for (int i = sh.first(L); i < sh.last(L); ++i)
-      if (H.lv[L][i].pt) ord.push_back(i - sh.first(L));
+    std::vector<int2> ord;
+    std::vector<int> pts;
+    for (int i = sh.first(L); i < sh.last(L); ++i) {
+      if (!H.lv[L][i].pt) ord.push_back(make_int2(i - sh.first(L), -1));
+      else pts.push_back(i - sh.first(L));
+    }
+    for (size_t q = 0; q < pts.size(); q += 2)
+      ord.push_back(make_int2(pts[q], q + 1 < pts.size() ? pts[q + 1] : -1));
+    nleafw = (int)ord.size();
     lorder = upload(ord, s);
     maxRL = std::max(1, F.lv[L].maxR);
-    const size_t chs = (size_t)((maxleaf + 31) / 32) * nC;
-    leaf_smem = ((size_t)2 * maxRL * nC + (size_t)kBW * kCW * nC + std::max(chs, smem_tree ? (size_t)nleaf : 0)) *
-                sizeof(double);
+    leaf_smem = ((size_t)2 * maxRL * nC + (size_t)kLeafGroups * kBW * kCW * nC +
+                 std::max((size_t)2 * maxch * nC, smem_tree ? (size_t)nleaf : 0)) * sizeof(double);
     // prologue: the level-L forward sweep of iteration 1 (the loop body's leaf kernel produces it
     // for the next iteration)
     ulv_solve_steps(F, ws, {SolveStep{SolveStep::FWD, L, L}}, s);
@@ -463,8 +515,8 @@ AdmmResult admm_train_impl(const ULVImpl& F, const double* y_orig, const std::ve
   auto iteration = [&](cudaStream_t st) {
     if (leaf_fuse) {
       ulv_solve_steps(F, ws, {SolveStep{SolveStep::FWD, L - 1, 0}, SolveStep{SolveStep::BWD, 0, L - 1}}, st);
-      leaf_dispatch(nC, dim3(nleaf), leaf_smem, st, EA, F.lv[L].nodes.p, lorder.p, H.leaf_lo.p, nleaf, F.lv[L].M.p,
-                    ws.xout[L - 1], ws.yr[L], ws.fin[L - 1], part.p, epi_out, counter.p, smem_tree, maxRL);
+      leaf_dispatch(nC, dim3(nleafw), leaf_smem, st, EA, F.lv[L].nodes.p, lorder.p, H.leaf_lo.p, nleaf, F.lv[L].M.p,
+                    ws.xout[L - 1], ws.yr[L], ws.fin[L - 1], part.p, epi_out, counter.p, smem_tree, maxRL, maxch);
       return;
     }
     ulv_solve_tree(F, ws, st);

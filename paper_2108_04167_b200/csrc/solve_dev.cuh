@@ -103,10 +103,20 @@ __device__ __forceinline__ void fwd_rows(const double* __restrict__ M, int R, co
 
 // x[j] for j in [j0, min(R, j0 + kCW)); ush = u (R x NR) in shared memory; red: kBW*kCW*NR
 // doubles of shared scratch.  Must be called by all kBW*32 threads of the CTA.
+// tig: the thread's index within its group of kBW*32 threads (several groups of one CTA may run
+// different column chunks at once; every thread of the CTA must call this the same number of
+// times).  idle: a group with no chunk (still takes part in the CTA barriers).
 template <int NR>
 __device__ __forceinline__ void bwd_cols(const double* __restrict__ M, int R, const double* __restrict__ ush,
-                                         int j0, double* __restrict__ red, double* __restrict__ out) {
-  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+                                         int j0, double* __restrict__ red, double* __restrict__ out,
+                                         int tig = -1, bool idle = false) {
+  if (tig < 0) tig = threadIdx.x;
+  const int lane = tig & 31, wid = tig >> 5;
+  if (idle) {
+    __syncthreads();
+    __syncthreads();
+    return;
+  }
   const int ja = j0 + lane, jb = j0 + 32 + lane;
   const bool va = ja < R, vb = jb < R;
   double aa[NR], ab[NR];
@@ -149,7 +159,7 @@ __device__ __forceinline__ void bwd_cols(const double* __restrict__ M, int R, co
     red[(wid * kCW + 32 + lane) * NR + c] = ab[c];
   }
   __syncthreads();
-  for (int e = threadIdx.x; e < kCW * NR; e += kBW * 32) {
+  for (int e = tig; e < kCW * NR; e += kBW * 32) {
     const int jj = e / NR, c = e % NR;
     if (j0 + jj < R) {
       double t = red[jj * NR + c];
