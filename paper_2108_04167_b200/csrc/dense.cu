@@ -53,6 +53,7 @@ __global__ void __launch_bounds__(256, MINB) bgemm_dmma_kernel(const GemmProb* _
   const GemmProb P = probs[blockIdx.z];
   const int m0 = blockIdx.y * BM, n0 = blockIdx.x * BN;
   if (m0 >= P.m || n0 >= P.n) return;
+  if (P.lower && n0 > m0 + BM - 1) return;  // strictly above the diagonal: not needed
   extern __shared__ __align__(16) double dsm[];
   double* As = dsm;                       // DNS x BM x DSK
   double* Bs = dsm + DNS * BM * DSK;      // DNS x BN x DSK

@@ -12,6 +12,7 @@ struct GemmProb {  // C = alpha * A(m x k) * B(k x n) + beta * C   (beta == 0: C
   const double* B; long long brs, bcs;
   double* C; long long crs, ccs;
   double alpha, beta;
+  int lower;       // 1: C is symmetric, only CTA tiles touching the lower triangle are computed
 };
 
 struct SqProb {    // square matrix problem (Cholesky / larft / trsm matrix)

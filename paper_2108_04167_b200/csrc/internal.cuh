@@ -52,7 +52,9 @@ void kernel_blocks(const double* F, int rp, int r, double h, const std::vector<K
 void pad_rows(const double* F, int64_t n, int r, int rp, double* out, cudaStream_t s);
 void row_norms(const double* F, int64_t n, int rp, double* nu, cudaStream_t s);
 
-struct CopyProb {  // dst[i*drs + j] (+)= src[i*srs + j], rows x cols
+struct CopyProb {  // rows x cols: mode 0 dst[i*drs + j] = src[i*srs + j]; 1: +=; 2: transposed,
+                   // dst[j*drs + i] = src[i*srs + j]; 3 (square): symmetric from the lower triangle,
+                   // dst[i*drs + j] = src[max(i,j)*srs + min(i,j)]
   int rows, cols;
   const double* src; long long srs;
   double* dst; long long drs;

@@ -641,10 +641,32 @@ void row_norms(const double* F, int64_t n, int rp, double* nu, cudaStream_t s) {
 
 __global__ void bcopy_kernel(const CopyProb* __restrict__ probs) {
   const CopyProb P = probs[blockIdx.y];
+  if (P.accumulate == 2) {  // transpose through 32 x 33 shared tiles (coalesced both ways)
+    __shared__ double tile[32][33];
+    const int tr = (P.rows + 31) / 32, tc = (P.cols + 31) / 32;
+    for (int t = blockIdx.x; t < tr * tc; t += gridDim.x) {
+      const int i0 = (t / tc) * 32, j0 = (t % tc) * 32;
+      for (int e = threadIdx.x; e < 1024; e += blockDim.x) {
+        const int ii = e / 32, jj = e % 32;
+        if (i0 + ii < P.rows && j0 + jj < P.cols) tile[ii][jj] = P.src[(int64_t)(i0 + ii) * P.srs + j0 + jj];
+      }
+      __syncthreads();
+      for (int e = threadIdx.x; e < 1024; e += blockDim.x) {
+        const int jj = e / 32, ii = e % 32;
+        if (i0 + ii < P.rows && j0 + jj < P.cols) P.dst[(int64_t)(j0 + jj) * P.drs + i0 + ii] = tile[ii][jj];
+      }
+      __syncthreads();
+    }
+    return;
+  }
   const int64_t tot = (int64_t)P.rows * P.cols;
   for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < tot;
        e += (int64_t)gridDim.x * blockDim.x) {
     const int64_t i = e / P.cols, j = e % P.cols;
+    if (P.accumulate == 3) {
+      P.dst[i * P.drs + j] = (j <= i) ? P.src[i * P.srs + j] : P.src[j * P.srs + i];
+      continue;
+    }
     const double v = P.src[i * P.srs + j];
     double* d = P.dst + i * P.drs + j;
     *d = P.accumulate ? *d + v : v;

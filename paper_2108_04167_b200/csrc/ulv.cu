@@ -122,7 +122,7 @@ void ulv_factor_impl(ULVImpl& F, cudaStream_t s) {
     } else {
       const NodeInfo* cv = H.lv[l + 1].data() + 2 * f0;  // children of hv[i]: cv[2i], cv[2i+1]
       const int64_t* dho = dhoffC.data() + 2 * f0;
-      std::vector<CopyProb> cp;
+      std::vector<CopyProb> cp, tp;
       std::vector<GemmProb> g1, g2;
       int64_t sumT = 0;
       std::vector<int64_t> toff(nn);
@@ -140,14 +140,15 @@ void ulv_factor_impl(ULVImpl& F, cudaStream_t s) {
         cp.push_back({kb, kb, Dhb, kb, Dc + (int64_t)ka * Rn + ka, Rn, 0});
         if (ka > 0 && kb > 0) {
           g1.push_back({ka, kb, ka, Ra, ka, 1, Bp, kb, 1, tmp.p + toff[i], kb, 1, 1.0, 0.0});
-          // off = tmp R_b^T -> upper-right block, and its transpose -> lower-left block
+          // off = tmp R_b^T -> upper-right block; its transpose -> lower-left block (copy)
           g2.push_back({ka, kb, kb, tmp.p + toff[i], kb, 1, Rb, 1, kb, Dc + ka, Rn, 1, 1.0, 0.0});
-          g2.push_back({ka, kb, kb, tmp.p + toff[i], kb, 1, Rb, 1, kb, Dc + (int64_t)ka * Rn, 1, Rn, 1.0, 0.0});
+          tp.push_back({ka, kb, Dc + ka, Rn, Dc + (int64_t)ka * Rn, Rn, 2});
         }
       }
       bcopy(cp, s);
       bgemm(g1, s);
       bgemm(g2, s);
+      bcopy(tp, s);
       CUDA_CHECK(cudaStreamSynchronize(s));
     }
     // ---- root: Cholesky + M_0 = L^-1
@@ -298,8 +299,8 @@ void ulv_factor_impl(ULVImpl& F, cudaStream_t s) {
         for (int i : np) g.push_back({R[i], R[i], R[i], Dcur.p + coff[i], R[i], 1, F_l.M.p + moff[i], 1, R[i], Yq.p + yo[i], R[i], 1, 1.0, 0.0});
         bgemm(g, s);  // Y = D M^T
         g.clear();
-        for (int i : np) g.push_back({R[i], R[i], R[i], F_l.M.p + moff[i], R[i], 1, Yq.p + yo[i], R[i], 1, Dcur.p + coff[i], R[i], 1, 1.0, 0.0});
-        bgemm(g, s);  // D' = M Y = Q^T D Q
+        for (int i : np) g.push_back({R[i], R[i], R[i], F_l.M.p + moff[i], R[i], 1, Yq.p + yo[i], R[i], 1, Dcur.p + coff[i], R[i], 1, 1.0, 0.0, 1});
+        bgemm(g, s);  // D' = M Y = Q^T D Q, symmetric: the lower-triangle tiles only (L_r, L_sr, D^ read it)
       }
       ptr_.mark("  wy QtDQ");
       // L_r = chol(Dc_rr)   (also nodes with k == 0: whole block)
@@ -317,8 +318,8 @@ void ulv_factor_impl(ULVImpl& F, cudaStream_t s) {
                       Dcur.p + coff[i] + (int64_t)K[i] * R[i], R[i], 1});
       btrsm(tr, true, s);
       // Dh = Dc_ss - L_sr L_sr^T
-      std::vector<CopyProb> cpy;
-      for (int i : np) cpy.push_back({K[i], K[i], Dcur.p + coff[i], R[i], DhP.p + koff2[i], K[i], 0});
+      std::vector<CopyProb> cpy;   // D^ starts from the symmetric Dc_ss (from its lower triangle)
+      for (int i : np) cpy.push_back({K[i], K[i], Dcur.p + coff[i], R[i], DhP.p + koff2[i], K[i], 3});
       bcopy(cpy, s);
       g.clear();
       for (int i : np) {
