@@ -1545,3 +1545,194 @@ void fill_identity(double* A, int n, long long rs, long long cs, cudaStream_t s)
 }
 
 }  // namespace svmhss
+
+namespace svmhss {
+// ------------------------------------------------------------------ skinny GEMM as streaming GEMV
+// C (m x n, n <= 16 right-hand sides) = alpha op(A) B + beta C, B and C row-major with unit column
+// stride (the HSS mat-vec's shapes, reading M: P:200).  op(A) row-major (acs == 1): one warp per
+// row, lanes over k, a butterfly per column; op(A) transposed in memory (ars == 1): a CTA owns 64
+// output rows (= stored columns: lanes read contiguous 256-byte row segments), 8 warps stride the
+// stored rows, partials summed in warp order.  Both stream A once (HBM-bound), fixed order.
+constexpr int GV_ROWS = 128;  // rows per CTA of the row GEMV (8 warps x 16 rows)
+template <int NR>
+__global__ void __launch_bounds__(256) gemv_rows_kernel(const GemmProb* __restrict__ probs,
+                                                        const int2* __restrict__ items) {
+  extern __shared__ double bsh[];   // B staged once per CTA: k x NR (zero beyond n)
+  const int2 it = items[blockIdx.x];
+  const GemmProb P = probs[it.x];
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  const int i0 = it.y * GV_ROWS, i1 = min(P.m, i0 + GV_ROWS);
+  // the first row's segments are requested before B is staged (the two latencies overlap)
+  const double* a0 = P.A + (long long)min(i0 + w, P.m - 1) * P.ars;
+  double pre[8];
+#pragma unroll
+  for (int u = 0; u < 8; ++u) pre[u] = (lane + 32 * u < P.k) ? a0[lane + 32 * u] : 0.0;
+  for (int e = threadIdx.x; e < P.k * NR; e += 256) {
+    const int j = e / NR, c = e % NR;
+    bsh[e] = (c < P.n) ? P.B[(long long)j * P.brs + c] : 0.0;
+  }
+  __syncthreads();
+  for (int i = i0 + w; i < i1; i += 8) {
+    const double* a = P.A + (long long)i * P.ars;
+    double acc[NR];
+#pragma unroll
+    for (int c = 0; c < NR; ++c) acc[c] = 0.0;
+    int j = lane;
+    for (; j + 32 * 7 < P.k; j += 256) {   // eight row segments in flight per lane
+      double av[8];
+      if (i == i0 + w && j == lane) {
+#pragma unroll
+        for (int u = 0; u < 8; ++u) av[u] = pre[u];
+      } else {
+#pragma unroll
+        for (int u = 0; u < 8; ++u) av[u] = a[j + 32 * u];
+      }
+#pragma unroll
+      for (int u = 0; u < 8; ++u)
+#pragma unroll
+        for (int c = 0; c < NR; ++c) acc[c] = fma(av[u], bsh[(j + 32 * u) * NR + c], acc[c]);
+    }
+    for (; j < P.k; j += 32) {
+      const double av = a[j];
+#pragma unroll
+      for (int c = 0; c < NR; ++c) acc[c] = fma(av, bsh[j * NR + c], acc[c]);
+    }
+#pragma unroll
+    for (int c = 0; c < NR; ++c) acc[c] = warp_sum(acc[c]);
+    if (lane < P.n) {
+      double v = acc[0];
+#pragma unroll
+      for (int c = 1; c < NR; ++c) if (lane == c) v = acc[c];
+      double* d = P.C + (long long)i * P.crs + lane;
+      *d = (P.beta == 0.0) ? P.alpha * v : fma(P.beta, *d, P.alpha * v);
+    }
+  }
+}
+
+template <int NR>
+__global__ void __launch_bounds__(256) gemv_cols_kernel(const GemmProb* __restrict__ probs,
+                                                        const int2* __restrict__ items) {
+  __shared__ double red[8][64][NR];
+  const int2 it = items[blockIdx.x];
+  const GemmProb P = probs[it.x];
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  const int i0 = it.y * 64, ia = i0 + lane, ib = i0 + 32 + lane;
+  const bool va = ia < P.m, vb = ib < P.m;
+  double aa[NR], ab[NR];
+#pragma unroll
+  for (int c = 0; c < NR; ++c) aa[c] = ab[c] = 0.0;
+  int j = w;
+  for (; j + 24 < P.k; j += 32) {   // four stored rows in flight per warp
+    double xa[4], xb[4];
+#pragma unroll
+    for (int u = 0; u < 4; ++u) {
+      const double* row = P.A + (long long)(j + 8 * u) * P.acs;
+      xa[u] = va ? row[ia] : 0.0;
+      xb[u] = vb ? row[ib] : 0.0;
+    }
+#pragma unroll
+    for (int u = 0; u < 4; ++u) {
+      const double* b = P.B + (long long)(j + 8 * u) * P.brs;
+#pragma unroll
+      for (int c = 0; c < NR; ++c)
+        if (c < P.n) {
+          const double bv = b[c];
+          aa[c] = fma(xa[u], bv, aa[c]);
+          ab[c] = fma(xb[u], bv, ab[c]);
+        }
+    }
+  }
+  for (; j < P.k; j += 8) {
+    const double* row = P.A + (long long)j * P.acs;
+    const double xa = va ? row[ia] : 0.0, xb = vb ? row[ib] : 0.0;
+    const double* b = P.B + (long long)j * P.brs;
+#pragma unroll
+    for (int c = 0; c < NR; ++c)
+      if (c < P.n) {
+        const double bv = b[c];
+        aa[c] = fma(xa, bv, aa[c]);
+        ab[c] = fma(xb, bv, ab[c]);
+      }
+  }
+#pragma unroll
+  for (int c = 0; c < NR; ++c) { red[w][lane][c] = aa[c]; red[w][32 + lane][c] = ab[c]; }
+  __syncthreads();
+  for (int e = threadIdx.x; e < 64 * P.n; e += 256) {
+    const int ii = e / P.n, c = e % P.n;
+    if (i0 + ii >= P.m) continue;
+    double t = red[0][ii][c];
+#pragma unroll
+    for (int q = 1; q < 8; ++q) t += red[q][ii][c];
+    double* d = P.C + (long long)(i0 + ii) * P.crs + c;
+    *d = (P.beta == 0.0) ? P.alpha * t : fma(P.beta, *d, P.alpha * t);
+  }
+}
+
+template <int NR, bool COLS>
+static void launch_gemv(const std::vector<GemmProb>& probs, cudaStream_t s) {
+  const bool cols = COLS;
+  std::vector<int2> items;
+  int kmax = 1;
+  for (size_t q = 0; q < probs.size(); ++q) {
+    const int per = cols ? (probs[q].m + 63) / 64 : (probs[q].m + GV_ROWS - 1) / GV_ROWS;
+    for (int t = 0; t < per; ++t) items.push_back(make_int2((int)q, t));
+    kmax = std::max(kmax, probs[q].k);
+  }
+  if (items.empty()) return;
+  const size_t smem = COLS ? 0 : (size_t)kmax * NR * sizeof(double);
+  if constexpr (!COLS)
+    if (smem > 48 * 1024) CUDA_CHECK(cudaFuncSetAttribute(gemv_rows_kernel<NR>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+  GemmProb* d = upload_probs(probs, s);
+  int2* di = upload_probs(items, s);
+  for (size_t b0 = 0; b0 < items.size(); b0 += (1u << 30)) {
+    const unsigned nb = (unsigned)std::min<size_t>(1u << 30, items.size() - b0);
+    if constexpr (COLS) gemv_cols_kernel<NR><<<nb, 256, 0, s>>>(d, di + b0);
+    else gemv_rows_kernel<NR><<<nb, 256, smem, s>>>(d, di + b0);
+    LAUNCH_CHECK();
+  }
+  free_probs(d, s);
+  free_probs(di, s);
+}
+
+template <int NR>
+static void gemv_split(const std::vector<GemmProb>& probs, cudaStream_t s) {
+  std::vector<GemmProb> rows, cols;
+  int cmax = 0;
+  for (const auto& p : probs) {
+    if (p.acs == 1) { rows.push_back(p); continue; }
+    for (int c0 = 0; c0 < p.n; c0 += 8) {   // the column kernel takes <= 8 right-hand sides
+      GemmProb q = p;
+      q.B += c0;
+      q.C += c0;
+      q.n = std::min(8, p.n - c0);
+      cmax = std::max(cmax, q.n);
+      cols.push_back(q);
+    }
+  }
+  launch_gemv<NR, false>(rows, s);
+  if (cmax <= 2) launch_gemv<2, true>(cols, s);
+  else if (cmax <= 4) launch_gemv<4, true>(cols, s);
+  else launch_gemv<8, true>(cols, s);
+}
+
+void bgemv(const std::vector<GemmProb>& probs_in, cudaStream_t s) {
+  std::vector<GemmProb> sk, other;
+  int nmax = 0;
+  for (const auto& p : probs_in) {
+    if (p.m <= 0 || p.n <= 0) continue;
+    const bool skinny = p.n <= 16 && p.bcs == 1 && p.ccs == 1 && (p.acs == 1 || p.ars == 1) && !p.lower &&
+                        (p.ars == 1 || (size_t)p.k * 16 * sizeof(double) <= 200 * 1024);
+    (skinny ? sk : other).push_back(p);
+    if (skinny) nmax = std::max(nmax, p.n);
+  }
+  bgemm(other, s);
+  if (sk.empty()) return;
+  if (nmax <= 2) { gemv_split<2>(sk, s); return; }
+  switch ((nmax + 3) / 4) {   // NR = 4, 8, 12, 16 (columns beyond n are skipped)
+    case 1: gemv_split<4>(sk, s); break;
+    case 2: gemv_split<8>(sk, s); break;
+    case 3: gemv_split<12>(sk, s); break;
+    default: gemv_split<16>(sk, s); break;
+  }
+}
+}  // namespace svmhss

@@ -45,6 +45,9 @@ struct CpqrProb {  // column-pivoted QR of A = W^T, W rows x s row-major (column
 
 // Batched launchers (problem arrays are HOST vectors; uploaded into a scratch buffer).
 void bgemm(const std::vector<GemmProb>& probs, cudaStream_t s);
+// The same contract; problems with n <= 16 columns (B, C unit column stride, A row-major or
+// transposed) run as streaming GEMV kernels (HSS mat-vec), the rest through bgemm.
+void bgemv(const std::vector<GemmProb>& probs, cudaStream_t s);
 // Cholesky (lower, in place, upper triangle zeroed).  info[i] = 0 ok, j+1 if breakdown at j.
 void bpotrf(const std::vector<SqProb>& probs, int* d_info, cudaStream_t s);
 // lower: forward substitution with T lower (non-unit); !lower: back substitution, T upper.

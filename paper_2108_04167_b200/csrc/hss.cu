@@ -515,7 +515,7 @@ void hss_matvec_tree(const HSSImpl& H, const double* V, double* out, int nrhs, c
   const Shard& sh = H.sh;
   if (L == 0) {
     const int n = (int)H.n;
-    bgemm({{n, nrhs, n, H.D.p, n, 1, V, nrhs, 1, out, nrhs, 1, 1.0, 0.0}}, s);
+    bgemv({{n, nrhs, n, H.D.p, n, 1, V, nrhs, 1, out, nrhs, 1, 1.0, 0.0}}, s);
     return;
   }
   std::vector<DevBuf<double>> up(L + 1), dn(L + 1);
@@ -540,7 +540,7 @@ void hss_matvec_tree(const HSSImpl& H, const double* V, double* out, int nrhs, c
                       up[l].p + nd.koff * nrhs, nrhs, 1, 1.0, 0.0});
     }
     bcopy(cp, s);
-    bgemm(gp, s);
+    bgemv(gp, s);
     if (l == sh.lg && sh.on()) exchange_lg(H, xw, up[l].p, nullptr, nullptr, s);
   }
   // downward: children of t get U_t g_t (split) + sibling couplings B up_sibling
@@ -566,7 +566,7 @@ void hss_matvec_tree(const HSSImpl& H, const double* V, double* out, int nrhs, c
       }
     }
     bcopy(cp, s);
-    bgemm(gp, s);
+    bgemv(gp, s);
     std::vector<GemmProb> g2;
     for (int p = sh.first(l); p < sh.last(l); ++p) {
       auto &a = cv[2 * p], &b = cv[2 * p + 1];
@@ -578,7 +578,7 @@ void hss_matvec_tree(const HSSImpl& H, const double* V, double* out, int nrhs, c
                       dn[l + 1].p + b.koff * nrhs, nrhs, 1, 1.0, 1.0});
       }
     }
-    bgemm(g2, s);
+    bgemv(g2, s);
   }
   // leaves: out = D V + U g
   std::vector<GemmProb> gp;
@@ -590,7 +590,7 @@ void hss_matvec_tree(const HSSImpl& H, const double* V, double* out, int nrhs, c
     gp.push_back({mloc, nrhs, mloc, H.D.p + nd.doff, mloc, 1, V + lo * nrhs, nrhs, 1,
                   out + lo * nrhs, nrhs, 1, 1.0, 0.0});
   }
-  bgemm(gp, s);
+  bgemv(gp, s);
   gp.clear();
   for (int i = sh.first(L); i < sh.last(L); ++i) {
     const auto& nd = H.lv[L][i];
@@ -601,7 +601,7 @@ void hss_matvec_tree(const HSSImpl& H, const double* V, double* out, int nrhs, c
                     out + lo * nrhs, nrhs, 1, 1.0, 1.0});
   }
   bcopy(cp, s);
-  bgemm(gp, s);
+  bgemv(gp, s);
   CUDA_CHECK(cudaStreamSynchronize(s));
 }
 
