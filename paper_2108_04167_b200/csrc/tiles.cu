@@ -44,36 +44,54 @@ static inline int pad_stride(int x) {  // smallest S >= x with S % 16 == 4
 
 constexpr int KBM = 64;
 
-// exp(x) for the Gaussian kernel entries (x = -d2 / (2h^2) <= 0): Cody-Waite reduction
-// x = n ln2 + r, |r| <= ln2/2, Taylor polynomial of degree 13 (truncation < 5e-18), and the
-// scale 2^n applied as two exact power-of-two factors (gradual underflow; 0 below -745).
-// Only DFMA/DADD and integer moves: no libdevice call, few live registers (the sketch kernel's
-// 34 accumulator doubles stay in registers) and no special-case branches.  Accuracy <= 2 ulp
-// against the correctly rounded exp (tests/test_gpu_parity.py pins the sketch at 1e-12).
-__device__ __forceinline__ double exp_kernel(double x) {
+// exp(x) for the Gaussian kernel entries (x = -d2 / (2h^2) <= 0), table-driven: x = (64 m + j)
+// ln2/64 + r with |r| <= ln2/128 (Cody-Waite split of ln2/64), exp(x) = 2^m 2^(j/64) e^r,
+// 2^(j/64) from a 64-entry table in shared memory (correctly rounded constants,
+// scripts/gen_exp_table.py), e^r by a degree-5 Taylor polynomial (truncation < r^6/720 < 4e-17),
+// 2^m as two exact power-of-two factors (gradual underflow; 0 below -745).  13 FP64 operations
+// per entry instead of the 20 of a degree-13 polynomial on |r| <= ln2/2 (the FP64 pipe also
+// runs the DMMAs of the sketch and prediction kernels).  <= 2 ulp against the correctly rounded
+// exp (tests/test_gpu_parity.py pins the sketch at 1e-12, tests/test_gpu_predict.py at 1e-12).
+__constant__ double c_exp2_64[64] = {
+    0x1.0000000000000p+0, 0x1.02c9a3e778061p+0, 0x1.059b0d3158574p+0, 0x1.0874518759bc8p+0,
+    0x1.0b5586cf9890fp+0, 0x1.0e3ec32d3d1a2p+0, 0x1.11301d0125b51p+0, 0x1.1429aaea92de0p+0,
+    0x1.172b83c7d517bp+0, 0x1.1a35beb6fcb75p+0, 0x1.1d4873168b9aap+0, 0x1.2063b88628cd6p+0,
+    0x1.2387a6e756238p+0, 0x1.26b4565e27cddp+0, 0x1.29e9df51fdee1p+0, 0x1.2d285a6e4030bp+0,
+    0x1.306fe0a31b715p+0, 0x1.33c08b26416ffp+0, 0x1.371a7373aa9cbp+0, 0x1.3a7db34e59ff7p+0,
+    0x1.3dea64c123422p+0, 0x1.4160a21f72e2ap+0, 0x1.44e086061892dp+0, 0x1.486a2b5c13cd0p+0,
+    0x1.4bfdad5362a27p+0, 0x1.4f9b2769d2ca7p+0, 0x1.5342b569d4f82p+0, 0x1.56f4736b527dap+0,
+    0x1.5ab07dd485429p+0, 0x1.5e76f15ad2148p+0, 0x1.6247eb03a5585p+0, 0x1.6623882552225p+0,
+    0x1.6a09e667f3bcdp+0, 0x1.6dfb23c651a2fp+0, 0x1.71f75e8ec5f74p+0, 0x1.75feb564267c9p+0,
+    0x1.7a11473eb0187p+0, 0x1.7e2f336cf4e62p+0, 0x1.82589994cce13p+0, 0x1.868d99b4492edp+0,
+    0x1.8ace5422aa0dbp+0, 0x1.8f1ae99157736p+0, 0x1.93737b0cdc5e5p+0, 0x1.97d829fde4e50p+0,
+    0x1.9c49182a3f090p+0, 0x1.a0c667b5de565p+0, 0x1.a5503b23e255dp+0, 0x1.a9e6b5579fdbfp+0,
+    0x1.ae89f995ad3adp+0, 0x1.b33a2b84f15fbp+0, 0x1.b7f76f2fb5e47p+0, 0x1.bcc1e904bc1d2p+0,
+    0x1.c199bdd85529cp+0, 0x1.c67f12e57d14bp+0, 0x1.cb720dcef9069p+0, 0x1.d072d4a07897cp+0,
+    0x1.d5818dcfba487p+0, 0x1.da9e603db3285p+0, 0x1.dfc97337b9b5fp+0, 0x1.e502ee78b3ff6p+0,
+    0x1.ea4afa2a490dap+0, 0x1.efa1bee615a27p+0, 0x1.f50765b6e4540p+0, 0x1.fa7c1819e90d8p+0,
+};
+
+__device__ __forceinline__ void exp_table_load(double* t) {
+  for (int e = threadIdx.x; e < 64; e += blockDim.x) t[e] = c_exp2_64[e];
+}
+__device__ __forceinline__ double exp_kernel(double x, const double* __restrict__ tab) {
   x = fmax(x, -1100.0);
-  const double kShift = 6755399441055744.0;  // 1.5 * 2^52: t's low word holds round(x log2 e)
-  const double t = fma(x, 1.4426950408889634, kShift);
+  const double kShift = 6755399441055744.0;  // 1.5 * 2^52: t's low word holds round(64 x / ln2)
+  const double t = fma(x, 0x1.71547652b82fep+6, kShift);
   const double n = t - kShift;
   const int ni = __double2loint(t);
-  double r = fma(n, -6.93147180369123816490e-01, x);
-  r = fma(n, -1.90821492927058770002e-10, r);
-  double p = 1.6059043836821614599e-10;        // 1/13!
-  p = fma(p, r, 2.0876756987868098979e-09);    // 1/12!
-  p = fma(p, r, 2.5052108385441718775e-08);    // 1/11!
-  p = fma(p, r, 2.7557319223985890653e-07);    // 1/10!
-  p = fma(p, r, 2.7557319223985890653e-06);    // 1/9!
-  p = fma(p, r, 2.4801587301587301566e-05);    // 1/8!
-  p = fma(p, r, 1.9841269841269841253e-04);    // 1/7!
-  p = fma(p, r, 1.3888888888888889419e-03);    // 1/6!
-  p = fma(p, r, 8.3333333333333332177e-03);    // 1/5!
-  p = fma(p, r, 4.1666666666666664354e-02);    // 1/4!
-  p = fma(p, r, 1.6666666666666665741e-01);    // 1/3!
+  double r = fma(n, -0x1.62e42fefa0000p-7, x);
+  r = fma(n, -0x1.cf79abc9e3b3ap-46, r);
+  double p = 1.0 / 120.0;
+  p = fma(p, r, 1.0 / 24.0);
+  p = fma(p, r, 1.0 / 6.0);
   p = fma(p, r, 0.5);
   p = fma(p, r, 1.0);
   p = fma(p, r, 1.0);
-  const int h1 = ni >> 1, h2 = ni - h1;         // 2^n = 2^h1 * 2^h2, each a normal number
-  return (p * __hiloint2double((h1 + 1023) << 20, 0)) * __hiloint2double((h2 + 1023) << 20, 0);
+  const double tj = tab[ni & 63];
+  const int m = ni >> 6;                       // floor(n / 64)
+  const int h1 = m >> 1, h2 = m - h1;          // 2^m = 2^h1 * 2^h2, each a normal number
+  return ((tj * p) * __hiloint2double((h1 + 1023) << 20, 0)) * __hiloint2double((h2 + 1023) << 20, 0);
 }
 
 // --- mbarrier / bulk-copy (TMA) helpers
@@ -134,6 +152,8 @@ __global__ void __launch_bounds__(512, 1) kmm_kernel(KmmArgs a, int SA, unsigned
   int* lbuf = (int*)(fbuf + 2 * (BJ * SA + BJ));  // 2 x BJ
   __shared__ __align__(8) uint64_t full[2];   // stage filled (TMA transaction count)
   __shared__ __align__(8) uint64_t empty[2];  // stage released by all 16 warps
+  __shared__ double exp_t[64];
+  exp_table_load(exp_t);
 
   const int tid = threadIdx.x, lane = tid & 31, w = tid >> 5, g = lane >> 2, t = lane & 3;
   const int mt = w & 7, hf = w >> 3;
@@ -259,7 +279,7 @@ __global__ void __launch_bounds__(512, 1) kmm_kernel(KmmArgs a, int SA, unsigned
         for (int e = 0; e < 2; ++e) {
           const int jj = hf * (BJ / 2) + q * 8 + 2 * t + e;
           double d2 = fmax(nui + nub_s[jj] - 2.0 * dacc[q][e], 0.0);
-          double v = exp_kernel(d2 * a.neg_inv_2h2);
+          double v = exp_kernel(d2 * a.neg_inv_2h2, exp_t);
           if (a.same_set && j0 + jj == my_row + a.diag_off) v = 1.0;
           if (a.leaf_b && lb[jj] == my_leaf) v = 0.0;
           if (jj >= jvalid || !row_ok) v = 0.0;
@@ -416,6 +436,8 @@ __global__ void __launch_bounds__(NW * 32, 1) predict_kernel(const double* __res
   const int stage_d = PBJ * SA + PBJ + cpad;          // doubles per stage (16-byte multiples)
   __shared__ __align__(8) uint64_t full[PST];
   __shared__ __align__(8) uint64_t empty[PST];
+  __shared__ double exp_t[64];
+  exp_table_load(exp_t);
   const int tid = threadIdx.x, lane = tid & 31, w = tid >> 5, g = lane >> 2, t = lane & 3;
   const int64_t row0 = (int64_t)blockIdx.x * (8 * NW);
   const int64_t nsteps = (nb + PBJ - 1) / PBJ;
@@ -482,7 +504,7 @@ __global__ void __launch_bounds__(NW * 32, 1) predict_kernel(const double* __res
       for (int e = 0; e < 2; ++e) {
         const int jj = q * 8 + 2 * t + e;
         const double d2 = fmax(nui + ns[jj] - 2.0 * d[q][e], 0.0);
-        double v = exp_kernel(d2 * neg_inv_2h2);
+        double v = exp_kernel(d2 * neg_inv_2h2, exp_t);
         if (jj >= jv) v = 0.0;
 #pragma unroll
         for (int c = 0; c < NC; ++c) acc[c] = fma(v, cs[jj * NC + c], acc[c]);
