@@ -14,7 +14,7 @@ HERE = os.path.dirname(os.path.abspath(__file__))
 CSRC = os.path.join(HERE, "csrc")
 BUILD = os.path.join(HERE, "_build")
 LIB = os.path.join(HERE, "libsvmhss.so")
-SOURCES = ["dense.cu", "cpqr.cu", "tiles.cu", "tree.cu", "hss.cu", "ulv.cu", "admm.cu", "comm.cu", "shard.cu", "ann.cu", "api.cu"]
+SOURCES = ["dense.cu", "cpqr.cu", "sort.cu", "tiles.cu", "tree.cu", "hss.cu", "ulv.cu", "admm.cu", "comm.cu", "shard.cu", "ann.cu", "api.cu"]
 NVCC = shutil.which("nvcc") or "/usr/local/cuda/bin/nvcc"
 FLAGS = ["-gencode", "arch=compute_100a,code=sm_100a", "-lineinfo", "-O3", "-std=c++17",
          "-Xcompiler", "-fPIC", "--expt-relaxed-constexpr", "-Xptxas", "-v"]

@@ -10,7 +10,6 @@
 //       from splitmix64 when fewer exist, sorted by position.
 // Selection is a warp-wide repeated lexicographic argmin over register-resident candidates.
 #include <algorithm>
-#include <cub/cub.cuh>
 #include "internal.cuh"
 
 namespace svmhss {
@@ -381,21 +380,16 @@ void ann_sample_level(const HSSImpl& H, int l, const int64_t* act, const int64_t
   }
   samp_keys_kernel<<<nn, 256, 0, s>>>(dsn.p, kappa, act, ann_pos, ann_d, qb, nall, k1.p, d1.p);
   LAUNCH_CHECK();
-  size_t t1 = 0, t2 = 0, t3 = 0;
-  CUDA_CHECK(cub::DeviceRadixSort::SortPairs(nullptr, t1, k1.p, k2.p, d1.p, d2.p, np, 0, qb + nb, s));
-  CUDA_CHECK(cub::DeviceRadixSort::SortPairs(nullptr, t2, k1.p, k2.p, v1.p, v2.p, np, 0, 64, s));
-  CUDA_CHECK(cub::DeviceRadixSort::SortPairs(nullptr, t3, nk1.p, nk2.p, v2.p, v1.p, np, 0, std::max(1, nb), s));
-  DevBuf<unsigned char> tmp(std::max(t1, std::max(t2, t3)) + 16);
   // (node, q) order
-  CUDA_CHECK(cub::DeviceRadixSort::SortPairs(tmp.p, t1, k1.p, k2.p, d1.p, d2.p, np, 0, qb + nb, s));
+  radix_sort_pairs(k1.p, k2.p, d1.p, d2.p, np, 0, qb + nb, s);
   const unsigned g = (unsigned)((np + 255) / 256);
   samp_runmin_kernel<<<g, 256, 0, s>>>(np, qb, nall, k2.p, d2.p, k1.p, v1.p);
   LAUNCH_CHECK();
   // stable by dmin, then stable by node: (node, dmin, q)
-  CUDA_CHECK(cub::DeviceRadixSort::SortPairs(tmp.p, t2, k1.p, k2.p, v1.p, v2.p, np, 0, 64, s));
+  radix_sort_pairs(k1.p, k2.p, v1.p, v2.p, np, 0, 64, s);
   samp_nodekey_kernel<<<g, 256, 0, s>>>(np, qb, v2.p, nk1.p);
   LAUNCH_CHECK();
-  CUDA_CHECK(cub::DeviceRadixSort::SortPairs(tmp.p, t3, nk1.p, nk2.p, v2.p, v1.p, np, 0, std::max(1, nb), s));
+  radix_sort_pairs(nk1.p, nk2.p, v2.p, v1.p, np, 0, std::max(1, nb), s);
   samp_q_kernel<<<g, 256, 0, s>>>(np, qb, nall, v1.p, q1.p);
   LAUNCH_CHECK();
   DevBuf<int> cnt(nn);

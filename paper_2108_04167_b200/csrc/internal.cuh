@@ -62,6 +62,19 @@ struct CopyProb {  // rows x cols: mode 0 dst[i*drs + j] = src[i*srs + j]; 1: +=
 };
 void bcopy(const std::vector<CopyProb>& probs, cudaStream_t s);
 
+// ---------------------------------------------------------------- stable radix sort (sort.cu)
+// (key, value) pairs sorted stably by key bits [begin_bit, end_bit); bits above end_bit must be 0.
+void radix_sort_pairs(const uint64_t* kin, uint64_t* kout, const int* vin, int* vout, int64_t n, int begin_bit,
+                      int end_bit, cudaStream_t s);
+void radix_sort_pairs(const unsigned* kin, unsigned* kout, const int* vin, int* vout, int64_t n, int begin_bit,
+                      int end_bit, cudaStream_t s);
+void radix_sort_pairs(const uint64_t* kin, uint64_t* kout, const uint64_t* vin, uint64_t* vout, int64_t n,
+                      int begin_bit, int end_bit, cudaStream_t s);
+void radix_sort_pairs(const unsigned* kin, unsigned* kout, const uint64_t* vin, uint64_t* vout, int64_t n,
+                      int begin_bit, int end_bit, cudaStream_t s);
+void radix_sort_pairs(const uint64_t* kin, uint64_t* kout, const double* vin, double* vout, int64_t n,
+                      int begin_bit, int end_bit, cudaStream_t s);
+
 // ---------------------------------------------------------------- tree (tree.cu)
 // T1-T4 on the GPU. F: n x rp (padded, device). Outputs perm (n int64, device) and the
 // permuted features Fp (n x rp) / norms nu.

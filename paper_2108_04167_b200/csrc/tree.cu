@@ -4,9 +4,9 @@
 // Per level (all nodes of the level at once, features kept in the current tree order):
 //   chunk partial sums -> node means (fixed chunk order) -> chunk partial covariances ->
 //   per-node reduction + 20 normalized power steps from the counter-RNG start vector ->
-//   projections p_i = (f_i - c).v -> two stable segmented sorts (by original index, then by
-//   an order-preserving key of p) = stable sort by (p, original index) -> permute rows.
-#include <cub/cub.cuh>
+//   projections p_i = (f_i - c).v -> three stable global radix sorts (sort.cu: by original
+//   index, by an order-preserving key of p, by node) = within every node the stable order by
+//   (p, original index) -> permute rows.
 #include "internal.cuh"
 
 namespace svmhss {
@@ -273,23 +273,18 @@ void build_tree(const double* Fpad, int64_t n, int r, int rp, int m, uint64_t tr
     // land in its own range)
     const int qb = std::max(1, bits_for((uint64_t)std::max<int64_t>(1, n - 1)));
     const int nbits = std::max(1, bits_for((uint64_t)std::max(1, nn - 1)));
-    size_t tb1 = 0, tb2 = 0, tb3 = 0;
     const uint64_t* iak = reinterpret_cast<const uint64_t*>(ia.p);
     uint64_t* ikk = reinterpret_cast<uint64_t*>(ik.p);
-    CUDA_CHECK(cub::DeviceRadixSort::SortPairs(nullptr, tb1, iak, ikk, p1.p, p2.p, (int)n, 0, qb, s));
-    CUDA_CHECK(cub::DeviceRadixSort::SortPairs(nullptr, tb2, k1.p, k2.p, p2.p, p1.p, (int)n, 0, 64, s));
-    CUDA_CHECK(cub::DeviceRadixSort::SortPairs(nullptr, tb3, nk1.p, nk2.p, p1.p, p2.p, (int)n, 0, nbits, s));
-    DevBuf<unsigned char> tmp(std::max(tb1, std::max(tb2, tb3)) + 16);
     // keys1 (the projection keys) must survive pass 1: keep a copy in k2 for the gather
     CUDA_CHECK(cudaMemcpyAsync(k2.p, k1.p, n * sizeof(uint64_t), cudaMemcpyDeviceToDevice, s));
-    CUDA_CHECK(cub::DeviceRadixSort::SortPairs(tmp.p, tb1, iak, ikk, p1.p, p2.p, (int)n, 0, qb, s));
+    radix_sort_pairs(iak, ikk, p1.p, p2.p, n, 0, qb, s);
     // p2 = positions ordered by original index; gather their projection keys
     gather_key_kernel<<<ceil_div(n, 256), 256, 0, s>>>(k2.p, p2.p, n, k1.p);
     LAUNCH_CHECK();
-    CUDA_CHECK(cub::DeviceRadixSort::SortPairs(tmp.p, tb2, k1.p, k2.p, p2.p, p1.p, (int)n, 0, 64, s));
+    radix_sort_pairs(k1.p, k2.p, p2.p, p1.p, n, 0, 64, s);
     node_key_kernel<<<ceil_div(n, 256), 256, 0, s>>>(d_nof.p, p1.p, n, nk1.p);
     LAUNCH_CHECK();
-    CUDA_CHECK(cub::DeviceRadixSort::SortPairs(tmp.p, tb3, nk1.p, nk2.p, p1.p, p2.p, (int)n, 0, nbits, s));
+    radix_sort_pairs(nk1.p, nk2.p, p1.p, p2.p, n, 0, nbits, s);
     std::swap(p1, p2);   // final order of positions in p1
     permute_kernel<<<ceil_div(n * rp, 256), 256, 0, s>>>(Fa.p, ia.p, p1.p, n, rp, Fb.p, ib.p);
     LAUNCH_CHECK();
