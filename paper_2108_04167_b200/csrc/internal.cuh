@@ -204,7 +204,7 @@ struct SolveWork { int node, chunk; };
 
 constexpr int kCW = 64;  // backward sweep: columns per CTA
 constexpr int kBW = 8;   // backward sweep: warps per CTA
-constexpr int kSplitMaxLevel = 5;  // bwd row split for levels l <= 5 (l < L-1): <= 32 nodes
+constexpr int kSplitMaxLevel = 4;  // bwd row split for levels l <= 4 (l < L-1): <= 16 nodes (A/B at cfg 3: 4 best of -1..7)
 constexpr int kRB = 64;            // bwd row split: rows per chunk
 struct ULVLevel {
   int nnodes = 0, maxR = 0, allpt = 1;
