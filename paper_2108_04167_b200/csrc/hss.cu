@@ -27,6 +27,35 @@ __global__ void iota_kernel64(int64_t* a, int64_t n) {
 
 struct SelNode { int64_t roff, koff, uoff; int rows, k, pt, pad; };
 
+// Pass-through certificate for a node whose rank could be all of its rows (adaptive rank rule,
+// AMB-10): G = Y Y^T (rows x rows, Y = the node's sample block, rows x s).  The CPQR threshold is
+// thr = max(rel_tol |R_11|, abs_tol sqrt(s)) with |R_11| = the largest column norm of Y^T =
+// sqrt(max_i G_ii).  Every |R_jj| of a QR of Y^T is >= sigma_min(Y^T) (R triangular: |R_jj| are its
+// eigenvalues), so if G - (1.01 thr)^2 I has a Cholesky factor, every |R_jj| > thr and the rank
+// rule gives k = rows: the node is pass-through without running the CPQR (the 1% margin covers
+// the rounding of G and of the CPQR's |R_jj|).  Nodes that fail the test take the CPQR as usual.
+__global__ void cert_shift_kernel(double* __restrict__ G, const int64_t* __restrict__ goff,
+                                  const int* __restrict__ rows, double rel_tol, double abs_tol, int s) {
+  const int q = blockIdx.x;
+  const int R = rows[q];
+  double* g = G + goff[q];
+  __shared__ double red[32];
+  double m = 0.0;
+  for (int i = threadIdx.x; i < R; i += blockDim.x) m = fmax(m, g[(int64_t)i * R + i]);
+  for (int o = 16; o > 0; o >>= 1) m = fmax(m, __shfl_xor_sync(0xffffffffu, m, o));
+  if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = m;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    double b = 0.0;
+    for (int w = 0; w < (int)(blockDim.x + 31) / 32; ++w) b = fmax(b, red[w]);
+    red[0] = b;
+  }
+  __syncthreads();
+  const double thr = fmax(rel_tol * sqrt(red[0]), abs_tol * sqrt((double)s));
+  const double sh = (1.01 * thr) * (1.01 * thr);
+  for (int i = threadIdx.x; i < R; i += blockDim.x) g[(int64_t)i * R + i] -= sh;
+}
+
 // U scatter: U[piv[c]][j] = (c < k) ? delta_cj : T[j][c-k]  (T stored in W[(roff+c)*s + j])
 __global__ void scatter_u_kernel(const SelNode* __restrict__ nd, const int* __restrict__ piv,
                                  const double* __restrict__ W, int s, double* __restrict__ U) {
@@ -311,10 +340,46 @@ void hss_build_impl(HSSImpl& H, const double* F, int64_t n, int r, double h, con
       }
     }
     auto dforced = upload(fh, s);
+    // pass-through certificates (cert_shift_kernel): adaptive nodes whose rank could be all rows
+    std::vector<char> cert(nn, 0);
+    if (!o.ranks && !ann) {
+      std::vector<int> cq, crow;
+      std::vector<int64_t> goff;
+      int64_t gtot = 0;
+      for (int q = 0; q < nn; ++q) {
+        const auto& nd = lv[f + q];
+        if (nd.rows == 0 || nd.rows > std::min(o.max_rank, S) || nd.rows > 512) continue;
+        cq.push_back(q); crow.push_back(nd.rows); goff.push_back(gtot);
+        gtot += (int64_t)nd.rows * nd.rows;
+      }
+      if (!cq.empty()) {
+        DevBuf<double> G(gtot);
+        std::vector<GemmProb> gp;
+        for (size_t u = 0; u < cq.size(); ++u) {
+          const auto& nd = lv[f + cq[u]];
+          const double* Y = Wk.p + nd.roff * S;
+          gp.push_back({nd.rows, nd.rows, S, Y, S, 1, Y, 1, S, G.p + goff[u], nd.rows, 1, 1.0, 0.0});
+        }
+        bgemm(gp, s);
+        auto dgo = upload(goff, s);
+        auto drw = upload(crow, s);
+        cert_shift_kernel<<<(unsigned)cq.size(), 256, 0, s>>>(G.p, dgo.p, drw.p, o.rel_tol, o.abs_tol, S);
+        LAUNCH_CHECK();
+        std::vector<SqProb> pp;
+        for (size_t u = 0; u < cq.size(); ++u) pp.push_back({crow[u], G.p + goff[u], crow[u], 1});
+        DevBuf<int> info(cq.size());
+        bpotrf(pp, info.p, s);
+        std::vector<int> hi(cq.size());
+        d2h(hi.data(), info.p, cq.size(), s);
+        CUDA_CHECK(cudaStreamSynchronize(s));
+        for (size_t u = 0; u < cq.size(); ++u) cert[cq[u]] = (hi[u] == 0) ? 1 : 0;
+      }
+    }
     std::vector<CpqrProb> cp;
     for (int q = 0; q < nn; ++q) {
       auto& nd = lv[f + q];
       if (kfix[q] >= 0 && kfix[q] == nd.rows) continue;  // known pass-through
+      if (cert[q]) continue;                             // certified pass-through
       if (nd.rows == 0) continue;
       cp.push_back({nd.rows, S, Wk.p + nd.roff * S, piv.p + nd.roff, kfix[q], kd.p + q, ch.p + q,
                     o.skeletons ? dforced.p + foff[q] : nullptr});
@@ -329,7 +394,7 @@ void hss_build_impl(HSSImpl& H, const double* F, int64_t n, int r, double h, con
     int64_t sumK = 0, sumU = 0;
     for (int q = 0; q < nn; ++q) {
       auto& nd = lv[f + q];
-      if ((kfix[q] >= 0 && kfix[q] == nd.rows) || nd.rows == 0) nd.k = nd.rows;
+      if ((kfix[q] >= 0 && kfix[q] == nd.rows) || nd.rows == 0 || cert[q]) { nd.k = nd.rows; chh[q] = 0; }
       else nd.k = kh[q];
       nd.pt = (nd.k == nd.rows);
       nd.cap_hit = chh[q];
