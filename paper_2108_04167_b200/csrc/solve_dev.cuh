@@ -106,10 +106,27 @@ __device__ __forceinline__ void fwd_rows(const double* __restrict__ M, int R, co
 // tig: the thread's index within its group of kBW*32 threads (several groups of one CTA may run
 // different column chunks at once; every thread of the CTA must call this the same number of
 // times).  idle: a group with no chunk (still takes part in the CTA barriers).
+// first-batch preload for bwd_cols (rows wid + q kBW, q < BWD_BQ, of this thread's two columns),
+// issued before a dependency wait; pass the arrays as pre_a / pre_b.
+__device__ __forceinline__ void bwd_cols_preload(const double* __restrict__ M, int R, int j0, double* pa,
+                                                 double* pb) {
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  const int ja = j0 + lane, jb = j0 + 32 + lane;
+#pragma unroll
+  for (int q = 0; q < BWD_BQ; ++q) {
+    const int i = wid + q * kBW;
+    const bool ok = (BWD_BQ - 1) * kBW < R;
+    const double* Mr = M + (int64_t)i * R;
+    pa[q] = (ok && ja < R) ? Mr[ja] : 0.0;
+    pb[q] = (ok && jb < R) ? Mr[jb] : 0.0;
+  }
+}
+
 template <int NR>
 __device__ __forceinline__ void bwd_cols(const double* __restrict__ M, int R, const double* __restrict__ ush,
                                          int j0, double* __restrict__ red, double* __restrict__ out,
-                                         int tig = -1, bool idle = false) {
+                                         int tig = -1, bool idle = false, const double* pre_a = nullptr,
+                                         const double* pre_b = nullptr) {
   if (tig < 0) tig = threadIdx.x;
   const int lane = tig & 31, wid = tig >> 5;
   if (idle) {
@@ -126,6 +143,19 @@ __device__ __forceinline__ void bwd_cols(const double* __restrict__ M, int R, co
   // BQ rows in flight per warp (16 loads / lane at BQ = 8); the per-column order (rows i, i + kBW,
   // ... sequentially) does not depend on BQ
   constexpr int BQ = BWD_BQ;
+  if (pre_a) {  // the first batch was loaded by the caller (before its dependency wait)
+    if ((BQ - 1) * kBW < R) {
+#pragma unroll
+      for (int q = 0; q < BQ; ++q)
+#pragma unroll
+        for (int c = 0; c < NR; ++c) {
+          const double u = ush[(i + q * kBW) * NR + c];
+          aa[c] = fma(pre_a[q], u, aa[c]);
+          ab[c] = fma(pre_b[q], u, ab[c]);
+        }
+      i += BQ * kBW;
+    }
+  }
   for (; i + (BQ - 1) * kBW < R; i += BQ * kBW) {
     double ma[BQ], mb[BQ];
 #pragma unroll

@@ -453,15 +453,18 @@ __device__ __forceinline__ void fwd_item(const SolveNode* __restrict__ nodes, So
   const int R = N.R, tid = threadIdx.x;
   const int i0 = wk.chunk * ch, i1 = min(R, i0 + ch);
   if (N.pt) {  // identity operator
+    pdl_wait();
     for (int e = tid; e < (i1 - i0) * NR; e += 256) out_up[(N.koff + i0) * NR + e] = in[(N.roff + i0) * NR + e];
   } else if (NR <= 2 && R <= 512 && i1 - i0 <= 8) {
-    // one row per warp (small chunks: the top levels): the row's 16 loads are issued before the
-    // input vector is staged, so the two latencies overlap; same per-row FMA order as fwd_rows
+    // one row per warp (small chunks: the top levels): the row's 16 loads (M is static) are issued
+    // BEFORE the wait for the previous level (programmatic dependent launch), so they overlap its
+    // tail; then the input vector is staged.  Same per-row FMA order as fwd_rows.
     const int lane = tid & 31, i = i0 + (tid >> 5);
     const double* Mr = M + N.moff + (int64_t)i * R;
     double m[16];
 #pragma unroll
     for (int q = 0; q < 16; ++q) m[q] = (i < i1 && lane + 32 * q < R) ? Mr[lane + 32 * q] : 0.0;
+    pdl_wait();
     for (int e = tid; e < R * NR; e += 256) vsh[e] = in[N.roff * NR + e];
     __syncthreads();
     if (i < i1) {
@@ -478,7 +481,34 @@ __device__ __forceinline__ void fwd_item(const SolveNode* __restrict__ nodes, So
       }
       row_store<NR>(acc, i, N.k, N.koff, N.yoff, out_up, out_yr);
     }
+  } else if (NR <= 2 && R <= 512) {
+    // this warp's first row loaded before the wait for the previous level (as above), the rest
+    // by fwd_rows; the per-row FMA order is fwd_rows' (j = lane, lane + 32, ...)
+    const int lane = tid & 31, wid = tid >> 5, i = i0 + wid;
+    const double* Mr = M + N.moff + (int64_t)i * R;
+    double m[16];
+#pragma unroll
+    for (int q = 0; q < 16; ++q) m[q] = (i < i1 && lane + 32 * q < R) ? Mr[lane + 32 * q] : 0.0;
+    pdl_wait();
+    for (int e = tid; e < R * NR; e += 256) vsh[e] = in[N.roff * NR + e];
+    __syncthreads();
+    if (i < i1) {
+      double acc[NR];
+#pragma unroll
+      for (int c = 0; c < NR; ++c) acc[c] = 0.0;
+#pragma unroll
+      for (int q = 0; q < 16; ++q) {
+        const int j = lane + 32 * q;
+        if (j < R) {
+#pragma unroll
+          for (int c = 0; c < NR; ++c) acc[c] = fma(m[q], vsh[j * NR + c], acc[c]);
+        }
+      }
+      row_store<NR>(acc, i, N.k, N.koff, N.yoff, out_up, out_yr);
+    }
+    fwd_rows<NR>(M + N.moff, R, vsh, i0 + 8, i1, wid, 8, N.k, N.koff, N.yoff, out_up, out_yr);
   } else {
+    pdl_wait();
     for (int e = tid; e < R * NR; e += 256) vsh[e] = in[N.roff * NR + e];
     __syncthreads();
     fwd_rows<NR>(M + N.moff, R, vsh, i0, i1, tid >> 5, 8, N.k, N.koff, N.yoff, out_up, out_yr);
@@ -495,8 +525,7 @@ __global__ void __launch_bounds__(256) ulv_fwd_kernel(const SolveNode* __restric
                                                       double* __restrict__ out_yr) {
   extern __shared__ double vsh[];  // R * NR
   pdl_trigger();
-  pdl_wait();
-  fwd_item<NR>(nodes, work[blockIdx.x], ch, M, in, out_up, out_yr, vsh);
+  fwd_item<NR>(nodes, work[blockIdx.x], ch, M, in, out_up, out_yr, vsh);  // waits (pdl_wait) inside
 }
 
 template <int NR>
@@ -507,12 +536,12 @@ __global__ void __launch_bounds__(kBW * 32) ulv_bwd_kernel(const SolveNode* __re
                                                            const double* __restrict__ in_r,
                                                            double* __restrict__ out) {
   pdl_trigger();
-  pdl_wait();
   const SolveWork wk = work[blockIdx.x];
   const SolveNode N = nodes[wk.node];
   const int R = N.R, tid = threadIdx.x;
   const int j0 = wk.chunk * kCW;
   if (N.pt) {  // identity operator
+    pdl_wait();
     const int j1 = min(R, j0 + kCW);
     for (int e = tid; e < (j1 - j0) * NR; e += kBW * 32) out[(N.roff + j0) * NR + e] = in_s[(N.koff + j0) * NR + e];
     return;
@@ -520,10 +549,14 @@ __global__ void __launch_bounds__(kBW * 32) ulv_bwd_kernel(const SolveNode* __re
   extern __shared__ double sm[];  // u: R * NR, then red: kBW * kCW * NR
   double* ush = sm;
   double* red = sm + R * NR;
+  // the first batch of M rows (static) before the wait for the previous level
+  double pa[BWD_BQ], pb[BWD_BQ];
+  bwd_cols_preload(M + N.moff, R, j0, pa, pb);
+  pdl_wait();
   const int kn = N.k * NR;
   for (int e = tid; e < R * NR; e += kBW * 32) ush[e] = (e < kn) ? in_s[N.koff * NR + e] : in_r[(N.yoff - N.k) * NR + e];
   __syncthreads();
-  bwd_cols<NR>(M + N.moff, R, ush, j0, red, out + N.roff * NR);
+  bwd_cols<NR>(M + N.moff, R, ush, j0, red, out + N.roff * NR, -1, false, pa, pb);
 }
 
 // Backward sweep of a small level (few nodes: latency-bound): the rows are split too.  Work item
@@ -541,6 +574,7 @@ __device__ __forceinline__ void bwd_split_item(const SolveNode* __restrict__ nod
   const int nrc = (R + kRB - 1) / kRB, cc = wk.chunk / nrc, rc = wk.chunk % nrc;
   const int j0 = cc * kCW, i0 = rc * kRB, i1 = min(R, i0 + kRB);
   if (N.pt) {  // identity operator (row chunk 0 copies)
+    pdl_wait();
     if (rc == 0) {
       const int j1 = min(R, j0 + kCW);
       for (int e = tid; e < (j1 - j0) * NR; e += kBW * 32) out[(N.roff + j0) * NR + e] = in_s[(N.koff + j0) * NR + e];
@@ -559,7 +593,8 @@ __device__ __forceinline__ void bwd_split_item(const SolveNode* __restrict__ nod
   {  // this warp's rows i0 + wid + q*kBW (q < kRB/kBW): all loads in flight, then FMAs in row order
     constexpr int NQ = kRB / kBW;
     double ma[NQ], mb[NQ];
-    // M (static) first: its loads overlap the input-vector load and the barrier below
+    // M (static) first, BEFORE the wait for the previous level: its loads overlap that level's
+    // tail, the input-vector load and the barrier below
 #pragma unroll
     for (int q = 0; q < NQ; ++q) {
       const int i = i0 + wid + q * kBW;
@@ -567,6 +602,7 @@ __device__ __forceinline__ void bwd_split_item(const SolveNode* __restrict__ nod
       ma[q] = (i < i1 && va) ? Mr[ja] : 0.0;
       mb[q] = (i < i1 && vb) ? Mr[jb] : 0.0;
     }
+    pdl_wait();
     for (int e = tid; e < (i1 - i0) * NR; e += kBW * 32) {
       const int i = i0 + e / NR, c = e % NR;
       ush[e] = (i < N.k) ? in_s[(N.koff + i) * NR + c] : in_r[(N.yoff + i - N.k) * NR + c];
@@ -628,8 +664,7 @@ __global__ void __launch_bounds__(kBW * 32) ulv_bwd_split_kernel(const SolveNode
                                                                  double* __restrict__ part,
                                                                  unsigned* __restrict__ cnt) {
   pdl_trigger();
-  pdl_wait();
-  bwd_split_item<NR>(nodes, work[blockIdx.x], blockIdx.x, M, in_s, in_r, out, part, cnt);
+  bwd_split_item<NR>(nodes, work[blockIdx.x], blockIdx.x, M, in_s, in_r, out, part, cnt);  // waits inside
 }
 
 // pass-through leaves: fwd  fin_{L-1}[map[p]] = fin_L[p];  bwd  xout_L[p] = xout_{L-1}[map[p]]
