@@ -32,3 +32,33 @@ def test_reference_arm_other_ranks_silent():
     r = _run({"RANK": "1", "WORLD_SIZE": "2"})
     assert r.returncode == 0, r.stderr[-2000:]
     assert r.stdout.strip() == ""
+
+
+def test_solve_algorithmic_bytes_formula():
+    """roofline_solve's byte count: with every rank at the cap (config 3: leaves
+    pass-through, every other node R = 512, k = 256) it reproduces the survey's independently
+    computed 7.56 GB per iteration; one more compressing leaf adds exactly its compact factor
+    twice; the compression flop count matches 4 s R k + 4 k^2 s per node."""
+    sys.path.insert(0, ROOT)
+    import bench
+    n, leaf, L = 524288, 256, 11
+    ranks = [-1] + [256] * (2 ** (L + 1) - 2)
+    shapes, root_R = bench.node_shapes(ranks, n, leaf)
+    assert root_R == 512 and len(shapes) == 2 ** (L + 1) - 2
+    b = bench.solve_algorithmic_bytes(shapes, root_R, n, 1)
+    assert abs(b / 1e9 - 7.557) < 0.001
+    ranks2 = list(ranks)
+    ranks2[2 ** L - 1] = 200                   # first leaf compresses: R = 256, k = 200
+    shapes2, r2 = bench.node_shapes(ranks2, n, leaf)
+    R, k = 256, 200
+    e = R - k
+    leafb = R * k - k * (k - 1) // 2 + k * (k + 1) // 2 + e * (e + 1) // 2 + k * e
+    # its parent now has R = 456: compact factor changes too
+    Rp, kp = 456, 256
+    ep = Rp - kp
+    par_new = Rp * kp - kp * (kp - 1) // 2 + kp * (kp + 1) // 2 + ep * (ep + 1) // 2 + kp * ep
+    par_old = 512 * 256 - 256 * 255 // 2 + 256 * 257 // 2 + 256 * 257 // 2 + 256 * 256
+    b2 = bench.solve_algorithmic_bytes(shapes2, r2, n, 1)
+    assert b2 - b == 16 * (leafb + par_new - par_old)
+    fl, by = bench.compress_work([(1, 512, 256)], 272)
+    assert fl == 4 * 272 * 512 * 256 + 4 * 256 * 256 * 272 and by == 16 * 512 * 272
