@@ -54,42 +54,53 @@ __global__ void node_mean_kernel(const double* __restrict__ part, const int* __r
   }
 }
 
-// partial covariance over a chunk: sum (f-c)(f-c)^T, full r x r; blockIdx.y selects a
-// block of 2048 (a, b) pairs (8 per thread)
+// partial covariance over a chunk: sum (f-c)(f-c)^T, full r x r.  Thread = a 4 x 4 block of
+// (a, b) pairs (register blocking: 8 shared loads per 16 FMAs); blockIdx.y selects a group of 256
+// blocks.  Every pair accumulates its rows in order (32-row shared blocks in order), as before.
 __global__ void __launch_bounds__(256) chunk_cov_kernel(const double* __restrict__ F, int rp, int r,
                                                         const Chunk* __restrict__ ch,
                                                         const double* __restrict__ mean,
                                                         double* __restrict__ part) {
   const Chunk c = ch[blockIdx.x];
-  extern __shared__ double xs[];  // 32 x r centred rows
+  extern __shared__ double xs[];  // 32 x r4 centred rows (r4 = r rounded up to 4, zero padded)
+  const int r4 = (r + 3) & ~3, nb4 = r4 / 4;
   const double* mu = mean + (int64_t)c.node * r;
-  const int npair = r * r;
-  const int pb = blockIdx.y * 2048;
-  double acc[8];
-  for (int q = 0; q < 8; ++q) acc[q] = 0.0;
+  const int blk = blockIdx.y * 256 + threadIdx.x;
+  const bool on = blk < nb4 * nb4;
+  const int a0 = on ? (blk / nb4) * 4 : 0, b0 = on ? (blk % nb4) * 4 : 0;
+  double acc[4][4];
+#pragma unroll
+  for (int u = 0; u < 4; ++u)
+#pragma unroll
+    for (int v = 0; v < 4; ++v) acc[u][v] = 0.0;
   for (int64_t i0 = c.lo; i0 < c.hi; i0 += 32) {
     const int nb = (int)min((int64_t)32, c.hi - i0);
     __syncthreads();
-    for (int e = threadIdx.x; e < nb * r; e += blockDim.x) {
-      const int ii = e / r, f = e % r;
-      xs[e] = F[(i0 + ii) * rp + f] - mu[f];
+    for (int e = threadIdx.x; e < nb * r4; e += blockDim.x) {
+      const int ii = e / r4, f = e % r4;
+      xs[e] = (f < r) ? F[(i0 + ii) * rp + f] - mu[f] : 0.0;
     }
     __syncthreads();
+    if (on) {
+      for (int ii = 0; ii < nb; ++ii) {
+        const double* x = xs + ii * r4;
+        double xa[4], xb[4];
 #pragma unroll
-    for (int q = 0; q < 8; ++q) {
-      const int pr = pb + threadIdx.x + q * 256;
-      if (pr < npair) {
-        const int a = pr / r, b = pr % r;
-        double s = acc[q];
-        for (int ii = 0; ii < nb; ++ii) s = fma(xs[ii * r + a], xs[ii * r + b], s);
-        acc[q] = s;
+        for (int u = 0; u < 4; ++u) { xa[u] = x[a0 + u]; xb[u] = x[b0 + u]; }
+#pragma unroll
+        for (int u = 0; u < 4; ++u)
+#pragma unroll
+          for (int v = 0; v < 4; ++v) acc[u][v] = fma(xa[u], xb[v], acc[u][v]);
       }
     }
   }
+  if (on) {
+    const int npair = r * r;
 #pragma unroll
-  for (int q = 0; q < 8; ++q) {
-    const int pr = pb + threadIdx.x + q * 256;
-    if (pr < npair) part[(int64_t)blockIdx.x * npair + pr] = acc[q];
+    for (int u = 0; u < 4; ++u)
+#pragma unroll
+      for (int v = 0; v < 4; ++v)
+        if (a0 + u < r && b0 + v < r) part[(int64_t)blockIdx.x * npair + (a0 + u) * r + b0 + v] = acc[u][v];
   }
 }
 
@@ -254,8 +265,11 @@ void build_tree(const double* Fpad, int64_t n, int r, int rp, int m, uint64_t tr
     node_mean_kernel<<<nn, 128, 0, s>>>(part.p, d_cb.p, d_ce.p, d_cnt.p, r, mean.p);
     LAUNCH_CHECK();
     {
-      size_t sm = 32 * (size_t)r * sizeof(double);
-      dim3 gcov(nch, ceil_div(r * r, 2048));
+      const int r4 = (r + 3) & ~3;
+      size_t sm = 32 * (size_t)r4 * sizeof(double);
+      dim3 gcov(nch, ceil_div((r4 / 4) * (r4 / 4), 256));
+      if (sm > 48 * 1024)
+        CUDA_CHECK(cudaFuncSetAttribute(chunk_cov_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm));
       chunk_cov_kernel<<<gcov, 256, sm, s>>>(Fa.p, rp, r, d_ch.p, mean.p, part.p);
       LAUNCH_CHECK();
       size_t sm2 = ((size_t)r * r + 2 * r) * sizeof(double);
