@@ -986,30 +986,14 @@ void bgeqr2(const std::vector<QrProb>& probs, cudaStream_t s) {
 }
 
 // ------------------------------------------------------------------ larft
-__global__ void __launch_bounds__(256) blarft_kernel(const SqProb* __restrict__ probs,
-                                                     const double* const* __restrict__ taus) {
-  const SqProb P = probs[blockIdx.x];
-  const double* tau = taus[blockIdx.x];
-  const int n = P.n, tid = threadIdx.x;
-  extern __shared__ double scol[];   // n doubles: S[0:j, j]
-  for (int j = 0; j < n; ++j) {
-    for (int p = tid; p < j; p += blockDim.x) scol[p] = AT(P, p, j);
-    __syncthreads();
-    const double tj = tau[j];
-    for (int i = tid; i < j; i += blockDim.x) {
-      double acc = 0.0;
-      for (int p = i; p < j; ++p) acc = fma(AT(P, i, p), scol[p], acc);
-      AT(P, i, j) = -tj * acc;
-    }
-    if (tid == 0) AT(P, j, j) = tj;
-    __syncthreads();
-  }
-  for (long long e = tid; e < (long long)n * n; e += blockDim.x) {
-    const int i = (int)(e / n), j = (int)(e % n);
-    if (i > j) AT(P, i, j) = 0.0;
-  }
-}
-
+// Compact-WY T (Q = H_1 ... H_n = I - V T V^T, H_i = I - tau_i v_i v_i^T) from S = V^T V by one
+// triangular solve instead of LAPACK's column recurrence: with D = diag(tau) and U = striu(S),
+// T^-1 = D^-1 + U, i.e. T = (I + D U)^-1 D — a unit upper-triangular system with the diagonal
+// right-hand side D (no division by tau, so tau_i = 0 gives a zero column as in dlarft).  The
+// solve runs on btrsm's DMMA kernel (16 CTAs per node for n = 256) rather than one CTA per node
+// walking the n columns in order: the few-node top levels of the factor are latency-bound
+// (by_solve); wide levels keep the recurrence (blarft_blk_kernel: one CTA per node, faster
+// there).  The caller picks by GLOBAL tree level, so the choice does not depend on the shard.
 // Blocked larft: block columns of LNB = 16.  With S = V^T V on input (in place), for block
 // column J: the diagonal block T_JJ by the column recurrence (warp 0), Y = S[0:J, J] T_JJ,
 // and T[0:J, J] = -T[0:J, 0:J] Y (Q = Q_1 Q_2: T = [T1, -T1 V1^T V2 T2; 0, T2]); the block
@@ -1068,16 +1052,42 @@ __global__ void __launch_bounds__(512) blarft_blk_kernel(const SqProb* __restric
   }
 }
 
-void blarft(const std::vector<SqProb>& probs, const std::vector<const double*>& taus,
+__global__ void __launch_bounds__(256) larft_system_kernel(const SqProb* __restrict__ probs,
+                                                            const double* const* __restrict__ taus,
+                                                            double* const* __restrict__ xs) {
+  const SqProb P = probs[blockIdx.x];
+  const double* tau = taus[blockIdx.x];
+  double* X = xs[blockIdx.x];
+  const int n = P.n;
+  for (long long e = threadIdx.x; e < (long long)n * n; e += blockDim.x) {
+    const int i = (int)(e / n), j = (int)(e % n);
+    const double sij = AT(P, i, j);
+    AT(P, i, j) = (j > i) ? tau[i] * sij : (j == i ? 1.0 : 0.0);   // I + D U
+    X[e] = (i == j) ? tau[i] : 0.0;                                  // D
+  }
+}
+
+__global__ void __launch_bounds__(256) larft_store_kernel(const SqProb* __restrict__ probs,
+                                                           double* const* __restrict__ xs) {
+  const SqProb P = probs[blockIdx.x];
+  const double* X = xs[blockIdx.x];
+  const int n = P.n;
+  for (long long e = threadIdx.x; e < (long long)n * n; e += blockDim.x) {
+    const int i = (int)(e / n), j = (int)(e % n);
+    AT(P, i, j) = (j >= i) ? X[e] : 0.0;
+  }
+}
+
+void blarft(const std::vector<SqProb>& probs, const std::vector<const double*>& taus, bool by_solve,
             cudaStream_t s) {
   if (probs.empty()) return;
   int maxn = 0;
   for (auto& p : probs) maxn = std::max(maxn, p.n);
-  SqProb* d = upload_probs(probs, s);
-  const double** dt = upload_probs(taus, s);
   const int lmax = (maxn + 15) & ~15;
   const size_t sm2 = (size_t)2 * lmax * LNB * sizeof(double);
-  if (sm2 <= 226 * 1024) {
+  if (!by_solve && sm2 <= 226 * 1024) {  // the column recurrence, one CTA per node
+    SqProb* d = upload_probs(probs, s);
+    const double** dt = upload_probs(taus, s);
     CUDA_CHECK(cudaFuncSetAttribute(blarft_blk_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm2));
     blarft_blk_kernel<<<(unsigned)probs.size(), 512, sm2, s>>>(d, dt, lmax);
     LAUNCH_CHECK();
@@ -1085,14 +1095,28 @@ void blarft(const std::vector<SqProb>& probs, const std::vector<const double*>& 
     free_probs((void*)dt, s);
     return;
   }
-  size_t smem = (size_t)std::max(1, maxn) * sizeof(double);
-  if (smem > 48 * 1024)
-    CUDA_CHECK(cudaFuncSetAttribute(blarft_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                    (int)smem));
-  blarft_kernel<<<(unsigned)probs.size(), 256, smem, s>>>(d, dt);
+  int64_t tot = 0;
+  std::vector<int64_t> off(probs.size());
+  for (size_t q = 0; q < probs.size(); ++q) { off[q] = tot; tot += (int64_t)probs[q].n * probs[q].n; }
+  DevBuf<double> xbuf(std::max<int64_t>(1, tot));
+  std::vector<double*> xp(probs.size());
+  std::vector<TrsmProb> tp(probs.size());
+  for (size_t q = 0; q < probs.size(); ++q) {
+    const SqProb& P = probs[q];
+    xp[q] = xbuf.p + off[q];
+    tp[q] = {P.n, P.n, P.A, P.rs, P.cs, xp[q], (long long)P.n, 1};
+  }
+  SqProb* d = upload_probs(probs, s);
+  const double** dt = upload_probs(taus, s);
+  double** dx = upload_probs(xp, s);
+  larft_system_kernel<<<(unsigned)probs.size(), 256, 0, s>>>(d, dt, dx);
+  LAUNCH_CHECK();
+  btrsm(tp, false, s);   // X := (I + D U)^-1 D
+  larft_store_kernel<<<(unsigned)probs.size(), 256, 0, s>>>(d, dx);
   LAUNCH_CHECK();
   free_probs(d, s);
   free_probs((void*)dt, s);
+  free_probs((void*)dx, s);
 }
 
 // ------------------------------------------------------------------ column-pivoted QR (H3)

@@ -54,7 +54,8 @@ void bpotrf(const std::vector<SqProb>& probs, int* d_info, cudaStream_t s);
 void btrsm(const std::vector<TrsmProb>& probs, bool lower, cudaStream_t s);
 void bgeqr2(const std::vector<QrProb>& probs, cudaStream_t s);
 // T (n x n upper) from V'V (S, n x n, in T's place on input) and tau: compact WY, Q = I - V T V^T.
-void blarft(const std::vector<SqProb>& probs_T, const std::vector<const double*>& taus,
+// by_solve: T = (I + D U)^-1 D by btrsm (few-node levels), else the blocked column recurrence.
+void blarft(const std::vector<SqProb>& probs_T, const std::vector<const double*>& taus, bool by_solve,
             cudaStream_t s);
 void bcpqr(const std::vector<CpqrProb>& probs, double rel_tol, double abs_tol, int cap,
            cudaStream_t s);

@@ -205,6 +205,7 @@ struct SolveWork { int node, chunk; };
 constexpr int kCW = 64;  // backward sweep: columns per CTA
 constexpr int kBW = 8;   // backward sweep: warps per CTA
 constexpr int kSplitMaxLevel = 4;  // bwd row split for levels l <= 4 (l < L-1): <= 16 nodes (A/B at cfg 3: 4 best of -1..7)
+constexpr int kLarftSolveMaxLevel = 7;  // factor: T by the triangular solve on levels l <= 7 (<= 128 nodes; A/B at cfg 3: 1.02 -> 0.53 ms per single-node level, slower from 256 nodes)
 constexpr int kRB = 64;            // bwd row split: rows per chunk
 struct ULVLevel {
   int nnodes = 0, maxR = 0, allpt = 1;

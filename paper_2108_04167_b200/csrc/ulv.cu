@@ -277,7 +277,7 @@ void ulv_factor_impl(ULVImpl& F, cudaStream_t s) {
       std::vector<SqProb> tp;
       std::vector<const double*> taus;
       for (int i : np) { tp.push_back({K[i], T.p + to[i], K[i], 1}); taus.push_back(tau.p + tauoff[i]); }
-      blarft(tp, taus, s);
+      blarft(tp, taus, l <= kLarftSolveMaxLevel, s);
       // Q^T D Q: M = Q^T = I - (V T^T) V^T is formed first (needed for the solve operator
       // anyway), then Y = D M^T and D' = M Y (two R x R x R GEMMs; 13% fewer flops than the
       // compact-WY form D - Z V^T - V Z^T and fewer, larger launches).
