@@ -180,7 +180,7 @@ __device__ __forceinline__ void leaf_update(const EpiArgs& A, const SolveNode& N
 // two pass-through leaves (half of the warps each) -- pass-through leaves are only an ADMM update,
 // so two per CTA halve the number of short CTAs.
 template <int NR>
-__global__ void __launch_bounds__(kLeafThreads) admm_leaf_kernel(EpiArgs A, const SolveNode* __restrict__ nodes,
+__global__ void __launch_bounds__(kLeafThreads, 2) admm_leaf_kernel(EpiArgs A, const SolveNode* __restrict__ nodes,
                                                                  const int2* __restrict__ work,
                                                                  const int64_t* __restrict__ leaf_lo, int nleaf_all,
                                                                  const double* __restrict__ M,
@@ -191,13 +191,18 @@ __global__ void __launch_bounds__(kLeafThreads) admm_leaf_kernel(EpiArgs A, cons
                                                                  int maxR, int maxch) {
   extern __shared__ double sm[];
   pdl_trigger();
-  pdl_wait();
+  // static data first (work list, node descriptor, the first batch of the leaf's M columns),
+  // then the wait for the previous kernel (programmatic dependent launch)
   const int2 wk = work[blockIdx.x];
   const int leaf = wk.x;
   const SolveNode N = nodes[leaf];
   const int64_t i0 = leaf_lo[leaf], i1 = leaf_lo[leaf + 1];
   const int npt = (int)(i1 - i0);
   const int tid = threadIdx.x;
+  double pa[BWD_BQ], pb[BWD_BQ];
+  if (!N.pt && (tid / (kBW * 32)) * kCW < N.R)
+    bwd_cols_preload(M + N.moff, N.R, (tid / (kBW * 32)) * kCW, pa, pb, tid % (kBW * 32));
+  pdl_wait();
   double* ush = sm;                          // maxR x NR: [x_s; y_r], then the next rhs
   double* xv = ush + (size_t)maxR * NR;      // maxR x NR: x of the leaf's points
   double* red = xv + (size_t)maxR * NR;      // groups x kBW x kCW x NR
@@ -211,7 +216,8 @@ __global__ void __launch_bounds__(kLeafThreads) admm_leaf_kernel(EpiArgs A, cons
     const int nrounds = ((R + kCW - 1) / kCW + kLeafGroups - 1) / kLeafGroups;  // uniform over the CTA
     for (int rd = 0; rd < nrounds; ++rd) {
       const int j0 = (rd * kLeafGroups + grp) * kCW;
-      bwd_cols<NR>(M + N.moff, R, ush, j0, red + (size_t)grp * kBW * kCW * NR, xv, tig, j0 >= R);
+      bwd_cols<NR>(M + N.moff, R, ush, j0, red + (size_t)grp * kBW * kCW * NR, xv, tig, j0 >= R,
+                   rd == 0 ? pa : nullptr, rd == 0 ? pb : nullptr);
     }
     leaf_update<NR>(A, N, i0, npt, 0, kLeafWarps, xs_in, xv, fin_up, ush, cs);
     __syncthreads();
@@ -220,7 +226,10 @@ __global__ void __launch_bounds__(kLeafThreads) admm_leaf_kernel(EpiArgs A, cons
       for (int ch = 0; ch < (npt + 31) / 32; ++ch) t += cs[ch * NR + tid];
       part[(int64_t)leaf * NR + tid] = t;
     }
-    fwd_rows<NR>(M + N.moff, N.R, ush, 0, N.R, tid >> 5, kLeafWarps, N.k, N.koff, N.yoff, fin_up, yr);
+    if (NR <= 2 && N.R <= 256)
+      fwd_rows_short<NR>(M + N.moff, N.R, ush, 0, N.R, tid >> 5, kLeafWarps, N.k, N.koff, N.yoff, fin_up, yr);
+    else
+      fwd_rows<NR>(M + N.moff, N.R, ush, 0, N.R, tid >> 5, kLeafWarps, N.k, N.koff, N.yoff, fin_up, yr);
   } else {
     const int half = (tid >> 5) >= kLeafWarps / 2;
     const int lf = half ? wk.y : leaf;

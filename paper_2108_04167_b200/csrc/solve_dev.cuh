@@ -101,6 +101,29 @@ __device__ __forceinline__ void fwd_rows(const double* __restrict__ M, int R, co
   }
 }
 
+// fwd_rows for short rows (R <= 256, NR <= 2: the leaves): two rows per warp per pass, 8 loads
+// each, so all loads of both rows are in flight at once (fwd_rows' one-row mode would leave half
+// of its 16 lane loads idle).  Same per-row FMA order.
+template <int NR>
+__device__ __forceinline__ void fwd_rows_short(const double* __restrict__ M, int R, const double* __restrict__ vsh,
+                                               int i0, int i1, int wid, int nw, int k, int64_t koff, int64_t yoff,
+                                               double* __restrict__ out_up, double* __restrict__ out_yr) {
+  int i = i0 + wid;
+  for (; i + nw < i1; i += 2 * nw) {
+    const double* Mr[2] = {M + (int64_t)i * R, M + (int64_t)(i + nw) * R};
+    double acc[2][NR];
+    row_partials<NR, 2, 8>(Mr, R, vsh, acc);
+    row_store<NR>(acc[0], i, k, koff, yoff, out_up, out_yr);
+    row_store<NR>(acc[1], i + nw, k, koff, yoff, out_up, out_yr);
+  }
+  if (i < i1) {
+    const double* Mr[1] = {M + (int64_t)i * R};
+    double acc[1][NR];
+    row_partials<NR, 1, 8>(Mr, R, vsh, acc);
+    row_store<NR>(acc[0], i, k, koff, yoff, out_up, out_yr);
+  }
+}
+
 // x[j] for j in [j0, min(R, j0 + kCW)); ush = u (R x NR) in shared memory; red: kBW*kCW*NR
 // doubles of shared scratch.  Must be called by all kBW*32 threads of the CTA.
 // tig: the thread's index within its group of kBW*32 threads (several groups of one CTA may run
@@ -109,8 +132,9 @@ __device__ __forceinline__ void fwd_rows(const double* __restrict__ M, int R, co
 // first-batch preload for bwd_cols (rows wid + q kBW, q < BWD_BQ, of this thread's two columns),
 // issued before a dependency wait; pass the arrays as pre_a / pre_b.
 __device__ __forceinline__ void bwd_cols_preload(const double* __restrict__ M, int R, int j0, double* pa,
-                                                 double* pb) {
-  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+                                                 double* pb, int tig = -1) {
+  if (tig < 0) tig = threadIdx.x;
+  const int lane = tig & 31, wid = tig >> 5;
   const int ja = j0 + lane, jb = j0 + 32 + lane;
 #pragma unroll
   for (int q = 0; q < BWD_BQ; ++q) {

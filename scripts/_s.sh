@@ -1,2 +1,2 @@
-for k in 2 4 2 4; do cp abso/lib_k$k.so paper_2108_04167_b200/libsvmhss.so; echo "KCH=$k"; timeout 300 python scripts/kmm_probe.py 131072; done > gpurun_out/kch.log 2>&1
-cat gpurun_out/kch.log
+for v in a b c a b c; do cp abso/lib_$v.so paper_2108_04167_b200/libsvmhss.so; echo "V=$v"; timeout 300 python scripts/admm_loop_time.py; done > gpurun_out/leafab.log 2>&1
+cat gpurun_out/leafab.log

@@ -16,6 +16,8 @@ kw = dict(leaf_size=cfg["leaf"], rel_tol=cfg["rel_tol"], abs_tol=cfg["abs_tol"],
 H = P.hss_build(torch.from_numpy(F).cuda(), cfg["h"], **kw)
 U = P.hss_ulv_factor(H, cfg["beta"])
 yd = torch.from_numpy(y).cuda()
+import hashlib  # noqa: E402
 for r in range(3):
     res = P.admm_svm_train(U, yd, [1.0], 300)
-    print(f"loop ms/it {res['stats']['ms_loop'] / 300:.4f}", flush=True)
+    dig = hashlib.sha256(res["z"].cpu().numpy().tobytes()).hexdigest()[:12]
+    print(f"loop ms/it {res['stats']['ms_loop'] / 300:.4f} z {dig}", flush=True)
