@@ -75,7 +75,7 @@ __device__ __forceinline__ void fwd_rows(const double* __restrict__ M, int R, co
                                          int i0, int i1, int wid, int nw, int k, int64_t koff, int64_t yoff,
                                          double* __restrict__ out_up, double* __restrict__ out_yr) {
   int i = i0 + wid;
-  if (NR <= 2) {
+  if constexpr (NR <= 2) {
     for (; i < i1; i += nw) {
       const double* Mr[1] = {M + (int64_t)i * R};
       if (i + nw < i1 && 16 * (threadIdx.x & 31) < R)
@@ -84,20 +84,20 @@ __device__ __forceinline__ void fwd_rows(const double* __restrict__ M, int R, co
       row_partials<NR, 1, 16>(Mr, R, vsh, acc);
       row_store<NR>(acc[0], i, k, koff, yoff, out_up, out_yr);
     }
-    return;
-  }
-  for (; i + nw < i1; i += 2 * nw) {
-    const double* Mr[2] = {M + (int64_t)i * R, M + (int64_t)(i + nw) * R};
-    double acc[2][NR];
-    row_partials<NR, 2>(Mr, R, vsh, acc);
-    row_store<NR>(acc[0], i, k, koff, yoff, out_up, out_yr);
-    row_store<NR>(acc[1], i + nw, k, koff, yoff, out_up, out_yr);
-  }
-  if (i < i1) {
-    const double* Mr[1] = {M + (int64_t)i * R};
-    double acc[1][NR];
-    row_partials<NR, 1>(Mr, R, vsh, acc);
-    row_store<NR>(acc[0], i, k, koff, yoff, out_up, out_yr);
+  } else {
+    for (; i + nw < i1; i += 2 * nw) {
+      const double* Mr[2] = {M + (int64_t)i * R, M + (int64_t)(i + nw) * R};
+      double acc[2][NR];
+      row_partials<NR, 2>(Mr, R, vsh, acc);
+      row_store<NR>(acc[0], i, k, koff, yoff, out_up, out_yr);
+      row_store<NR>(acc[1], i + nw, k, koff, yoff, out_up, out_yr);
+    }
+    if (i < i1) {
+      const double* Mr[1] = {M + (int64_t)i * R};
+      double acc[1][NR];
+      row_partials<NR, 1>(Mr, R, vsh, acc);
+      row_store<NR>(acc[0], i, k, koff, yoff, out_up, out_yr);
+    }
   }
 }
 
