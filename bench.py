@@ -524,7 +524,8 @@ def main():
     ach_gbs = solve_alg * max_it / (loop_ms / 1e3) / 1e9
     cf_flops, cf_bytes = compress_work(shapes, cfg["s"])
     tree_bytes = 3.0 * hi["L"] * 8.0 * n * cfg["r"]
-    solve_traffic = _traffic("admm_iteration", cfg["name"]) if args.n is None else None
+    # the committed captures are of the dense-sketch build (scripts/admm_profile.py sketch)
+    solve_traffic = _traffic("admm_iteration", cfg["name"]) if args.n is None and args.sampling == "sketch" else None
     line = {"metric": METRIC, "value": value, "unit": "iters/s", "n_gpus": world, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": ms_total / args.steps, "higher_is_better": True,
             "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
@@ -575,7 +576,7 @@ def main():
                                   "frac": cf_flops / (hi["ms_compress"] / 1e3) / 1e12 / fp64_peak,
                                   "hbm_achieved_gbs": cf_bytes / (hi["ms_compress"] / 1e3) / 1e9,
                                   "hbm_frac": cf_bytes / (hi["ms_compress"] / 1e3) / 1e9 / peaks["hbm_gbs"],
-                                  "cpqr_dram_bytes_ncu": _traffic("cpqr_level_sum", cfg["name"]) if args.n is None else None,
+                                  "cpqr_dram_bytes_ncu": _traffic("cpqr_level_sum", cfg["name"]) if args.n is None and args.sampling == "sketch" else None,
                                   "work": "SURVEY 8(d) a6: sum over CPQR'd nodes 4sRk + 4k^2 s flops = %.3e; "
                                           "algorithmic bytes 16 R s per node (sample block read + written once) "
                                           "= %.3e" % (cf_flops, cf_bytes)},

@@ -1,7 +1,9 @@
 """Fill profiles/traffic.json (the ncu DRAM bytes bench.py reports beside its rooflines) from
 committed launch lists:
-  admm_iteration  : scripts/admm_profile.py capture (precompute solve + 3 iterations + bias):
-                    per iteration = sum(ulv_* kernels) / 4 + sum(admm_epilogue) / 3
+  admm_iteration  : scripts/admm_profile.py capture (precompute solve + prologue + 3 iterations +
+                    bias): an iteration = the launches after one admm_leaf_kernel up to and
+                    including the next (forward L-1..0, backward 0..L-1, fused leaf kernel),
+                    averaged over the complete iterations
   cpqr_level_sum  : scripts/build_profile.py capture: sum over the CPQR launches of one build
     python scripts/update_traffic.py ADMM_CSV BUILD_CSV TAG"""
 import csv
@@ -27,15 +29,16 @@ def main():
     d = json.load(open(p))
     L = launches(admm_csv)
     by = lambda v: v.get("dram__bytes_read.sum", 0) + v.get("dram__bytes_write.sum", 0)  # noqa: E731
-    ulv = sum(by(v) for k, v in L if "ulv_" in k)
-    epi = sum(by(v) for k, v in L if "admm_epilogue" in k)
-    t_ulv = sum(v.get("gpu__time_duration.sum", 0) for k, v in L if "ulv_" in k)
-    t_epi = sum(v.get("gpu__time_duration.sum", 0) for k, v in L if "admm_epilogue" in k)
-    d["admm_iteration"] = {"workload": "cfg3_mixed524k", "dram_bytes_read": None, "dram_bytes_write": None,
-                           "dram_bytes": ulv / 4 + epi / 3, "ncu_serialised_us": (t_ulv / 4 + t_epi / 3) / 1e3,
+    leaf = [i for i, (k, _) in enumerate(L) if "admm_leaf_kernel" in k]
+    its = [L[a + 1:b + 1] for a, b in zip(leaf, leaf[1:])]
+    assert its, "no complete ADMM iteration (fused leaf kernel) in the capture"
+    nb = sum(sum(by(v) for _, v in it) for it in its) / len(its)
+    nt = sum(sum(v.get("gpu__time_duration.sum", 0) for _, v in it) for it in its) / len(its)
+    d["admm_iteration"] = {"workload": "cfg3_mixed524k", "dram_bytes": nb, "launches": len(its[0]),
+                           "ncu_serialised_us": nt / 1e3,
                            "source": f"{admm_csv} ({tag}): ncu dram__bytes_read.sum + dram__bytes_write.sum over "
-                                     "the ULV sweep and epilogue kernels; sum(ulv_*) / 4 (precompute solve + 3 "
-                                     "iterations) + sum(epilogue) / 3"}
+                                     f"the launches of one iteration (forward L-1..0, backward 0..L-1, fused leaf "
+                                     f"kernel), mean of {len(its)} complete iterations"}
     B = launches(build_csv)
     cp = [(k, v) for k, v in B if "cpqr" in k]
     d["cpqr_level_sum"] = {"workload": "cfg3_mixed524k", "dram_bytes": sum(by(v) for _, v in cp),
