@@ -1577,15 +1577,17 @@ namespace svmhss {
 // row, lanes over k, a butterfly per column; op(A) transposed in memory (ars == 1): a CTA owns 64
 // output rows (= stored columns: lanes read contiguous 256-byte row segments), 8 warps stride the
 // stored rows, partials summed in warp order.  Both stream A once (HBM-bound), fixed order.
-constexpr int GV_ROWS = 128;  // rows per CTA of the row GEMV (8 warps x 16 rows)
+constexpr int GV_ROWS = 128;  // rows per CTA of the row GEMV (8 warps x 16 rows) on big batches
+// rows per CTA rpc (8..128, a multiple of 8) is chosen per launch so that small batches (the top
+// tree levels) still spread over the SMs; a row's arithmetic does not depend on it
 template <int NR>
 __global__ void __launch_bounds__(256) gemv_rows_kernel(const GemmProb* __restrict__ probs,
-                                                        const int2* __restrict__ items) {
+                                                        const int2* __restrict__ items, int rpc) {
   extern __shared__ double bsh[];   // B staged once per CTA: k x NR (zero beyond n)
   const int2 it = items[blockIdx.x];
   const GemmProb P = probs[it.x];
   const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
-  const int i0 = it.y * GV_ROWS, i1 = min(P.m, i0 + GV_ROWS);
+  const int i0 = it.y * rpc, i1 = min(P.m, i0 + rpc);
   // the first row's segments are requested before B is staged (the two latencies overlap)
   const double* a0 = P.A + (long long)min(i0 + w, P.m - 1) * P.ars;
   double pre[8];
@@ -1596,39 +1598,61 @@ __global__ void __launch_bounds__(256) gemv_rows_kernel(const GemmProb* __restri
     bsh[e] = (c < P.n) ? P.B[(long long)j * P.brs + c] : 0.0;
   }
   __syncthreads();
-  for (int i = i0 + w; i < i1; i += 8) {
-    const double* a = P.A + (long long)i * P.ars;
-    double acc[NR];
+  // NR <= 4: rows i and i + 8 together (16 loads per lane in flight; the per-row FMA order is the
+  // one-row loop's), else one row at a time
+  constexpr int RW = NR <= 4 ? 2 : 1;
+  for (int i = i0 + w; i < i1; i += 8 * RW) {
+    const double* a[RW];
+    bool ok[RW];
 #pragma unroll
-    for (int c = 0; c < NR; ++c) acc[c] = 0.0;
+    for (int r = 0; r < RW; ++r) {
+      ok[r] = i + 8 * r < i1;
+      a[r] = P.A + (long long)(ok[r] ? i + 8 * r : i) * P.ars;
+    }
+    double acc[RW][NR];
+#pragma unroll
+    for (int r = 0; r < RW; ++r)
+#pragma unroll
+      for (int c = 0; c < NR; ++c) acc[r][c] = 0.0;
     int j = lane;
-    for (; j + 32 * 7 < P.k; j += 256) {   // eight row segments in flight per lane
-      double av[8];
-      if (i == i0 + w && j == lane) {
+    for (; j + 32 * 7 < P.k; j += 256) {   // eight row segments per row in flight per lane
+      double av[RW][8];
 #pragma unroll
-        for (int u = 0; u < 8; ++u) av[u] = pre[u];
-      } else {
+      for (int r = 0; r < RW; ++r) {
+        if (r == 0 && i == i0 + w && j == lane) {
 #pragma unroll
-        for (int u = 0; u < 8; ++u) av[u] = a[j + 32 * u];
+          for (int u = 0; u < 8; ++u) av[r][u] = pre[u];
+        } else {
+#pragma unroll
+          for (int u = 0; u < 8; ++u) av[r][u] = ok[r] ? a[r][j + 32 * u] : 0.0;
+        }
       }
 #pragma unroll
       for (int u = 0; u < 8; ++u)
 #pragma unroll
-        for (int c = 0; c < NR; ++c) acc[c] = fma(av[u], bsh[(j + 32 * u) * NR + c], acc[c]);
+        for (int r = 0; r < RW; ++r)
+#pragma unroll
+          for (int c = 0; c < NR; ++c) acc[r][c] = fma(av[r][u], bsh[(j + 32 * u) * NR + c], acc[r][c]);
     }
     for (; j < P.k; j += 32) {
-      const double av = a[j];
 #pragma unroll
-      for (int c = 0; c < NR; ++c) acc[c] = fma(av, bsh[j * NR + c], acc[c]);
+      for (int r = 0; r < RW; ++r) {
+        const double av = ok[r] ? a[r][j] : 0.0;
+#pragma unroll
+        for (int c = 0; c < NR; ++c) acc[r][c] = fma(av, bsh[j * NR + c], acc[r][c]);
+      }
     }
 #pragma unroll
-    for (int c = 0; c < NR; ++c) acc[c] = warp_sum(acc[c]);
-    if (lane < P.n) {
-      double v = acc[0];
+    for (int r = 0; r < RW; ++r) {
 #pragma unroll
-      for (int c = 1; c < NR; ++c) if (lane == c) v = acc[c];
-      double* d = P.C + (long long)i * P.crs + lane;
-      *d = (P.beta == 0.0) ? P.alpha * v : fma(P.beta, *d, P.alpha * v);
+      for (int c = 0; c < NR; ++c) acc[r][c] = warp_sum(acc[r][c]);
+      if (ok[r] && lane < P.n) {
+        double v = acc[r][0];
+#pragma unroll
+        for (int c = 1; c < NR; ++c) if (lane == c) v = acc[r][c];
+        double* d = P.C + (long long)(i + 8 * r) * P.crs + lane;
+        *d = (P.beta == 0.0) ? P.alpha * v : fma(P.beta, *d, P.alpha * v);
+      }
     }
   }
 }
@@ -1646,16 +1670,16 @@ __global__ void __launch_bounds__(256) gemv_cols_kernel(const GemmProb* __restri
 #pragma unroll
   for (int c = 0; c < NR; ++c) aa[c] = ab[c] = 0.0;
   int j = w;
-  for (; j + 24 < P.k; j += 32) {   // four stored rows in flight per warp
-    double xa[4], xb[4];
+  for (; j + 56 < P.k; j += 64) {   // eight stored rows in flight per warp (rows j, j + 8, ... in order)
+    double xa[8], xb[8];
 #pragma unroll
-    for (int u = 0; u < 4; ++u) {
+    for (int u = 0; u < 8; ++u) {
       const double* row = P.A + (long long)(j + 8 * u) * P.acs;
       xa[u] = va ? row[ia] : 0.0;
       xb[u] = vb ? row[ib] : 0.0;
     }
 #pragma unroll
-    for (int u = 0; u < 4; ++u) {
+    for (int u = 0; u < 8; ++u) {
       const double* b = P.B + (long long)(j + 8 * u) * P.brs;
 #pragma unroll
       for (int c = 0; c < NR; ++c)
@@ -1697,8 +1721,14 @@ static void launch_gemv(const std::vector<GemmProb>& probs, cudaStream_t s) {
   const bool cols = COLS;
   std::vector<int2> items;
   int kmax = 1;
+  int rpc = GV_ROWS;   // row kernel: halve the rows per CTA until the batch gives >= 4 CTAs per SM
+  if (!cols) {
+    int64_t mrows = 0;
+    for (const auto& p : probs) mrows += p.m;
+    while (rpc > 8 && mrows / rpc < 4 * 148) rpc /= 2;
+  }
   for (size_t q = 0; q < probs.size(); ++q) {
-    const int per = cols ? (probs[q].m + 63) / 64 : (probs[q].m + GV_ROWS - 1) / GV_ROWS;
+    const int per = cols ? (probs[q].m + 63) / 64 : (probs[q].m + rpc - 1) / rpc;
     for (int t = 0; t < per; ++t) items.push_back(make_int2((int)q, t));
     kmax = std::max(kmax, probs[q].k);
   }
@@ -1711,7 +1741,7 @@ static void launch_gemv(const std::vector<GemmProb>& probs, cudaStream_t s) {
   for (size_t b0 = 0; b0 < items.size(); b0 += (1u << 30)) {
     const unsigned nb = (unsigned)std::min<size_t>(1u << 30, items.size() - b0);
     if constexpr (COLS) gemv_cols_kernel<NR><<<nb, 256, 0, s>>>(d, di + b0);
-    else gemv_rows_kernel<NR><<<nb, 256, smem, s>>>(d, di + b0);
+    else gemv_rows_kernel<NR><<<nb, 256, smem, s>>>(d, di + b0, rpc);
     LAUNCH_CHECK();
   }
   free_probs(d, s);
