@@ -55,7 +55,15 @@ def main():
     hi = H.info()
     # a11 with the test points sharded over the ranks (svm_predict's comm)
     dv, lab = P.svm_predict(Fd, yd, res["z"], h, res["bias"], torch.from_numpy(Ft).to(dev), comm=comm)
+    # the end-to-end host call (the bench's e2e path) with the same communicator
+    e2e = P.svm_train_predict_host(F, y, h, beta, Cs, max_it, Ftest=Ft, leaf_size=cfg["leaf"],
+                                   rel_tol=cfg["rel_tol"], abs_tol=cfg["abs_tol"], max_rank=cfg["cap"],
+                                   oversample=cfg["s"] - cfg["cap"], omega_seed=cfg["seed_omega"],
+                                   tree_seed=cfg["seed_tree"], comm=comm, sampling=sampling,
+                                   ann_neighbors=cfg["ann_neighbors"], ann_trees=cfg["ann_trees"],
+                                   ann_leaf=cfg["ann_leaf"], ann_seed=cfg["ann_seed"])
     np.savez(os.path.join(out, f"P{world}_r{rank}.npz"), x=x.cpu().numpy(), kv=kv.cpu().numpy(),
+             e2e_z=e2e["z"], e2e_bias=e2e["bias"], e2e_lab=e2e["labels"],
              dv=dv.cpu().numpy(), lab=lab.cpu().numpy(),
              z=res["z"].cpu().numpy(), mu=res["mu"].cpu().numpy(), bias=res["bias"], obj=res["obj"],
              trace_z=res["trace_z"].cpu().numpy(), w1=res["stats"]["w1"], perm=hi["perm"],

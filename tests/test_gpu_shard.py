@@ -14,7 +14,7 @@ import pytest
 pytestmark = pytest.mark.gpu
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 WORKER = os.path.join(ROOT, "tests", "_shard_worker.py")
-KEYS = ["x", "kv", "z", "mu", "bias", "obj", "trace_z", "w1", "perm", "cap_hits", "passthrough",
+KEYS = ["x", "kv", "z", "mu", "bias", "obj", "trace_z", "w1", "perm", "cap_hits", "passthrough", "e2e_z", "e2e_bias", "e2e_lab",
         "max_rank", "gen_bytes", "dv", "lab"]
 
 
@@ -43,6 +43,9 @@ def _run(out, P, args):
 ])
 def test_subtree_sharding_is_bitwise_p_invariant(tmp_path, args, Ps):
     ref = _run(tmp_path, 1, args)[0]
+    # the end-to-end host call is the step-by-step API's result
+    assert np.array_equal(ref["e2e_z"], ref["z"]) and np.array_equal(ref["e2e_bias"], ref["bias"])
+    assert np.array_equal(ref["e2e_lab"], ref["lab"].reshape(ref["e2e_lab"].shape))
     for P in Ps:
         outs = _run(tmp_path, P, args)
         for k, o in enumerate(outs):
