@@ -632,6 +632,7 @@ def main():
                                "ADMM + bias + predict + d2h; iterations / total call time (max over "
                                "ranks; bytes summed over ranks: every rank copies F, y and F_test in "
                                "and z and the labels out)"}
+    hi_a = None
     if world == 1 and args.sampling == "sketch" and not args.no_variants and args.n is None:
         # the same step with HSS-ANN compression (the paper's P:186-187 construction),
         # its own calibrated beta; one warm-up + one timed step, device-timed like the main line
@@ -640,15 +641,23 @@ def main():
 
         def step_ann():
             H = P.hss_build(Fd, h, **opts_a)
-            U = P.hss_ulv_factor(H, beta_a)
-            res = P.admm_svm_train(U, yd, Cs, max_it, want_mu=False)
-            hi_a, ui_a = H.info(), U.info()
-            U.free()
-            H.free()
-            return hi_a, ui_a, res["stats"]
+            try:
+                U = P.hss_ulv_factor(H, beta_a)
+                try:
+                    res = P.admm_svm_train(U, yd, Cs, max_it, want_mu=False)
+                    return H.info(), U.info(), res["stats"]
+                finally:
+                    U.free()
+            finally:
+                H.free()
 
-        step_ann()
-        hi_a, ui_a, st_a = step_ann()
+        try:
+            step_ann()
+            hi_a, ui_a, st_a = step_ann()
+        except P.HssError as ex:   # e.g. a config whose ANN K~ has no calibrated beta (only cfg 3 has one)
+            hi_a = None
+            line["variants"] = {"ann": {"sampling": "ann", "beta": beta_a, "error": str(ex)}}
+    if hi_a is not None:
         line["variants"] = {"ann": {
             "sampling": "ann", "beta": beta_a, "admm_iters_per_s": max_it * len(Cs) / (st_a["ms_loop"] / 1e3),
             "hss_build_ulv_s": (hi_a["ms_tree"] + hi_a["ms_sketch"] + hi_a["ms_compress"] + ui_a["ms_factor"]) / 1e3,
