@@ -129,8 +129,23 @@ typedef struct {
    *   (its points at the leaves, its children's skeletons above), else HSS_EINVAL. */
   const int64_t* perm;
   const int64_t* skeletons;
+  /* Interpolation of the compression (SPD-preserving compression; DESIGN.md
+   * "N4"):
+   *  HSS_INTERP_ID (0): the paper's interpolative decomposition (H3): U_t = P[I; T^T],
+   *    T = R11^-1 R12 of the CPQR of Y_t^T.  K~ can be indefinite once ranks are capped, so
+   *    beta must exceed -lambda_min(K~) (AMB-9 calibration).
+   *  HSS_INTERP_SPD (1): the same skeletons J_t (same CPQR, rank rule, imports), but
+   *    U_t = K(A_t, J_t) (K(J_t, J_t) + spd_eps I)^-1 (kernel interpolation onto the skeleton;
+   *    A_t = the node's active rows), by a Cholesky factor of K(J_t,J_t) + spd_eps I and two
+   *    triangular solves.  K~ is then positive semidefinite for every rank choice, so
+   *    K~ + beta I is SPD for every beta > 0 (the paper's beta schedule, applies).
+   *    spd_eps >= 0 (relative to K_ii = 1; 1e-12 recommended).  HSS_ENOTSPD (naming the node)
+   *    if a K(J_t,J_t) + spd_eps I has no Cholesky factor (e.g. repeated points, spd_eps = 0). */
+  int32_t interp;
+  double spd_eps;
 } hss_opts;
 enum { HSS_SAMPLING_SKETCH = 0, HSS_SAMPLING_ANN = 1 };
+enum { HSS_INTERP_ID = 0, HSS_INTERP_SPD = 1 };
 
 /* Build statistics (D6 / P:366-367 "Compression", "Memory"). */
 typedef struct {

@@ -18,6 +18,16 @@ construction the paper cites ([MR2854612]) with V = U (K symmetric):
       Y_t = [Y_sk,a - B Omega'_b ; Y_sk,b - B^T Omega'_a];  Omega^_t = [Omega'_a; Omega'_b];
       active rows = [J_a; J_b].
   H5  root: B only.
+N4 (SPD-preserving compression; our construction): with
+  interp="spd" every non-pass-through node keeps the skeleton J_t that H3 picks, but its
+  interpolation matrix is the kernel (Nystrom) interpolant onto the skeleton instead of the
+  CPQR's R11^-1 R12:
+      U_t = K(A_t, J_t) (K(J_t, J_t) + eps I)^-1       (A_t = the node's active rows)
+  computed by a Cholesky factor of K(J_t, J_t) + eps I and two triangular solves.  Then
+  D_t - U_t K(J_t,J_t) U_t^T >= 0 for every node (a generalized Schur complement), and K~ is a
+  sum of such PSD terms pushed through the nested bases plus the root's principal submatrix of
+  K, so K~ is positive semidefinite for every rank choice and K~ + beta I is SPD for every
+  beta > 0.  Y_sk, Omega' = U^T Omega^, B = K(J_a, J_b) and the leaf D follow H2-H5 unchanged.
 Also the HSS mat-vec (reading M) and an independent dense assembly from the
 generators (used by tests).  All indices into points are TREE (permuted) positions.
 """
@@ -81,15 +91,28 @@ def choose_rank(rdiag: np.ndarray, rows: int, s: int, *, fixed_rank=None,
     return int(k), cap_hit
 
 
+def nystrom_u(Fp: np.ndarray, h: float, act: np.ndarray, J: np.ndarray, eps: float) -> np.ndarray:
+    """N4: U = K(A, J) (K(J, J) + eps I)^-1 (rows x k), by the Cholesky factor of K(J,J) + eps I."""
+    G = gaussian_block(Fp[J], Fp[J], h) + eps * np.eye(len(J))
+    c = sla.cho_factor(G, lower=True)
+    return sla.cho_solve(c, gaussian_block(Fp[J], Fp[act], h)).T
+
+
 def compress(Fp: np.ndarray, h: float, ranges, Omega_p: np.ndarray, *, ranks=None,
-             rel_tol=0.0, abs_tol=0.0, cap=None, S=None, skeletons=None) -> HSS:
+             rel_tol=0.0, abs_tol=0.0, cap=None, S=None, skeletons=None,
+             interp: str = "id", spd_eps: float = 1e-10) -> HSS:
     """H1-H5.  `ranks` (dict or array indexed by BFS node id) selects fixed-rank mode.
 
     `skeletons` (dict: node id -> tree positions J_t in pivot order, every non-root node)
     selects the fixed-skeleton diagnostic mode (AMB-12): in H3 the pivots are J_t's local
     indices followed by the other active rows in increasing order, the QR of Y_t^T is taken
     WITHOUT pivoting in that column order, k = len(J_t), and U, J, Y_sk, Omega' follow as usual
-    (U[piv[k:]] = (R11^-1 R12)^T, the interpolation coefficients of the given skeleton)."""
+    (U[piv[k:]] = (R11^-1 R12)^T, the interpolation coefficients of the given skeleton).
+
+    `interp` = "id" (H3, the paper's interpolative decomposition) or "spd" (N4: the same
+    skeletons, U_t = K(A_t, J_t)(K(J_t, J_t) + spd_eps I)^-1; module docstring)."""
+    if interp not in ("id", "spd"):
+        raise ValueError(f"interp must be 'id' or 'spd', got {interp!r}")
     n, s = Omega_p.shape
     L = len(ranges) - 1
     hss = HSS(n=n, L=L, ranges=ranges, Fp=Fp, h=h)
@@ -133,10 +156,13 @@ def compress(Fp: np.ndarray, h: float, ranges, Omega_p: np.ndarray, *, ranks=Non
                         raise ValueError(f"pass-through node {t}: skeleton must be its active rows in order")
                     hss.U[t], hss.Jloc[t], hss.J[t] = None, np.arange(rows), act[t]
                 else:
-                    T = sla.solve_triangular(R[:k, :k], R[:k, k:], lower=False)
-                    U = np.zeros((rows, k))
-                    U[piv[:k]] = np.eye(k)
-                    U[piv[k:]] = T.T
+                    if interp == "spd":
+                        U = nystrom_u(Fp, h, act[t], act[t][piv[:k]], spd_eps)
+                    else:
+                        T = sla.solve_triangular(R[:k, :k], R[:k, k:], lower=False)
+                        U = np.zeros((rows, k))
+                        U[piv[:k]] = np.eye(k)
+                        U[piv[k:]] = T.T
                     hss.U[t], hss.Jloc[t], hss.J[t] = U, piv[:k].copy(), act[t][piv[:k]]
                     Y[t] = Yt[piv[:k]]
                     Om[t] = U.T @ Om[t]
@@ -158,10 +184,13 @@ def compress(Fp: np.ndarray, h: float, ranges, Omega_p: np.ndarray, *, ranks=Non
                 hss.J[t] = act[t]
                 # Y[t] (= Y_sk) and Om[t] (= Omega') unchanged
             else:
-                T = sla.solve_triangular(R[:k, :k], R[:k, k:], lower=False)
-                U = np.zeros((rows, k))
-                U[piv[:k]] = np.eye(k)
-                U[piv[k:]] = T.T
+                if interp == "spd":                               # N4
+                    U = nystrom_u(Fp, h, act[t], act[t][piv[:k]], spd_eps)
+                else:
+                    T = sla.solve_triangular(R[:k, :k], R[:k, k:], lower=False)
+                    U = np.zeros((rows, k))
+                    U[piv[:k]] = np.eye(k)
+                    U[piv[k:]] = T.T
                 hss.U[t] = U
                 hss.Jloc[t] = piv[:k].copy()
                 hss.J[t] = act[t][piv[:k]]

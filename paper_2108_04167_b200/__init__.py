@@ -279,12 +279,15 @@ class ULV:
 
 
 SAMPLING = {"sketch": 0, "ann": 1}
+INTERP = {"id": 0, "spd": 1}
 
 
 def make_opts(leaf_size, rel_tol=0.0, abs_tol=0.0, max_rank=64, oversample=16, omega_seed=0,
               tree_seed=0, ranks=None, comm=None, sampling="sketch", ann_neighbors=64, ann_trees=4,
-              ann_leaf=256, ann_seed=0, adaptive_s0=0, adaptive_ds=0, perm=None, skeletons=None):
+              ann_leaf=256, ann_seed=0, adaptive_s0=0, adaptive_ds=0, perm=None, skeletons=None,
+              interp="id", spd_eps=1e-12):
     o = HssOpts()
+    o.interp, o.spd_eps = INTERP[interp], float(spd_eps)
     o.adaptive_s0, o.adaptive_ds = int(adaptive_s0), int(adaptive_ds)
     o.comm = comm.handle if comm is not None else None
     o.sampling = SAMPLING[sampling]
@@ -311,11 +314,12 @@ def make_opts(leaf_size, rel_tol=0.0, abs_tol=0.0, max_rank=64, oversample=16, o
 def hss_build(F, h, leaf_size, rel_tol=0.0, abs_tol=0.0, max_rank=64, oversample=16, omega_seed=0,
               tree_seed=0, ranks=None, comm=None, sampling="sketch", ann_neighbors=64, ann_trees=4,
               ann_leaf=256, ann_seed=0, adaptive_s0=0, adaptive_ds=0, perm=None, skeletons=None,
-              stream=None) -> HSS:
+              interp="id", spd_eps=1e-12, stream=None) -> HSS:
     """hss_build (Alg. 3 line 1): F is a CUDA float64 (n, r) tensor, original order
     (all n points on every rank when `comm` shards the tree).  sampling="ann" selects HSS-ANN
     column sampling instead of the randomized sketch.  perm / skeletons (host
-    arrays) import a tree / fixed skeletons (parity modes; include/svmhss.h)."""
+    arrays) import a tree / fixed skeletons (parity modes; include/svmhss.h).  interp="spd"
+    selects the SPD-preserving kernel interpolation onto the skeletons (N4; include/svmhss.h)."""
     _cuda_f64(F, "F")
     _shape(F.dim() == 2, "F must be (n, r)")
     n, r = F.shape
@@ -323,7 +327,7 @@ def hss_build(F, h, leaf_size, rel_tol=0.0, abs_tol=0.0, max_rank=64, oversample
         _shape(np.asarray(perm).shape == (n,), f"perm must have {n} entries")
     o, keep = make_opts(leaf_size, rel_tol, abs_tol, max_rank, oversample, omega_seed, tree_seed, ranks, comm,
                         sampling, ann_neighbors, ann_trees, ann_leaf, ann_seed, adaptive_s0, adaptive_ds,
-                        perm, skeletons)
+                        perm, skeletons, interp, spd_eps)
     hdl = ct.c_void_p()
     ctx, d = _on_device(F)
     with ctx:

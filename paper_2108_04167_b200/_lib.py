@@ -31,7 +31,8 @@ class HssOpts(ct.Structure):
                 ("sampling", ct.c_int32), ("ann_neighbors", ct.c_int32), ("ann_trees", ct.c_int32),
                 ("ann_leaf", ct.c_int32), ("ann_seed", ct.c_uint64),
                 ("adaptive_s0", ct.c_int32), ("adaptive_ds", ct.c_int32),
-                ("perm", ct.POINTER(ct.c_int64)), ("skeletons", ct.POINTER(ct.c_int64))]
+                ("perm", ct.POINTER(ct.c_int64)), ("skeletons", ct.POINTER(ct.c_int64)),
+                ("interp", ct.c_int32), ("spd_eps", ct.c_double)]
 
 
 # int (*hss_allgather_fn)(void* ctx, const void* send, void* recv, size_t bytes)

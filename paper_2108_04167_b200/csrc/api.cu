@@ -223,6 +223,9 @@ static void validate_opts(const hss_opts* o, int64_t n, int32_t r, double h) {
   require(s % 2 == 0, "hss_build: s = max_rank + oversample must be even");
   require(o->rel_tol >= 0 && o->abs_tol >= 0, "hss_build: tolerances must be >= 0");
   require(o->sampling == HSS_SAMPLING_SKETCH || o->sampling == HSS_SAMPLING_ANN, "hss_build: unknown sampling");
+  require(o->interp == HSS_INTERP_ID || o->interp == HSS_INTERP_SPD, "hss_build: unknown interp");
+  require(o->interp == HSS_INTERP_ID || (std::isfinite(o->spd_eps) && o->spd_eps >= 0),
+          "hss_build: spd_eps must be finite and >= 0");
   if (o->adaptive_s0 > 0) {
     require(o->sampling == HSS_SAMPLING_SKETCH, "hss_build: adaptive sampling needs the sketch sampling");
     require(o->adaptive_ds > 0, "hss_build: adaptive_ds must be > 0");

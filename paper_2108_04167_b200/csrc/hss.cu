@@ -100,6 +100,58 @@ struct RootRec {
   int64_t sub_cap_hits, sub_pt, sub_maxk, sub_bytes;  // this rank's subtree (levels >= lg)
 };
 
+// N4 (SPD-preserving compression): for every non-pass-through node t of level l
+// this rank holds, U_t = K(A_t, J_t) (K(J_t, J_t) + eps I)^-1 (rows x k, row-major), with the
+// skeleton J_t already selected (select_kernel).  K(A_t, J_t) is written straight into U_t's
+// storage; read as a k x rows matrix with unit row stride it is K(J_t, A_t) (K symmetric), so
+// two triangular solves with the Cholesky factor L of G = K(J_t, J_t) + eps I (L then L^T, a
+// stride swap) turn it into G^-1 K(J_t, A_t) = U_t^T in place, i.e. U_t row-major.
+static void spd_interp_level(HSSImpl& H, int l, const int64_t* act, double eps, cudaStream_t s) {
+  auto& lv = H.lv[l];
+  const int f = H.sh.first(l), e = H.sh.last(l);
+  std::vector<int> ids;
+  std::vector<int64_t> goff;
+  int64_t gtot = 0;
+  for (int i = f; i < e; ++i) {
+    const auto& nd = lv[i];
+    if (nd.pt || nd.k == 0) continue;
+    ids.push_back(i);
+    goff.push_back(gtot);
+    gtot += (int64_t)nd.k * nd.k;
+  }
+  if (ids.empty()) return;
+  DevBuf<double> G(gtot);
+  std::vector<KblkProb> kp;
+  for (size_t q = 0; q < ids.size(); ++q) {
+    const auto& nd = lv[ids[q]];
+    const int64_t* J = H.J[l].p + nd.koff;
+    kp.push_back({nd.rows, nd.k, act + nd.roff, 0, J, 0, H.U[l].p + nd.uoff, nd.k, 0.0});
+    kp.push_back({nd.k, nd.k, J, 0, J, 0, G.p + goff[q], nd.k, eps});
+  }
+  kernel_blocks(H.Fp.p, H.rp, H.r, H.h, kp, s);
+  std::vector<SqProb> pp;
+  for (size_t q = 0; q < ids.size(); ++q) pp.push_back({lv[ids[q]].k, G.p + goff[q], lv[ids[q]].k, 1});
+  DevBuf<int> info(ids.size());
+  bpotrf(pp, info.p, s);
+  std::vector<int> hi(ids.size());
+  d2h(hi.data(), info.p, ids.size(), s);
+  CUDA_CHECK(cudaStreamSynchronize(s));
+  for (size_t q = 0; q < ids.size(); ++q)
+    if (hi[q] != 0)
+      throw Error(HSS_ENOTSPD, "hss_build (interp=spd): K(J,J) + spd_eps I not SPD at node " +
+                                   std::to_string(H.node_id(l, ids[q])) + " (pivot " + std::to_string(hi[q] - 1) +
+                                   "); raise spd_eps");
+  std::vector<TrsmProb> lo, up;
+  for (size_t q = 0; q < ids.size(); ++q) {
+    const auto& nd = lv[ids[q]];
+    double* X = H.U[l].p + nd.uoff;
+    lo.push_back({nd.k, nd.rows, G.p + goff[q], nd.k, 1, X, 1, nd.k});
+    up.push_back({nd.k, nd.rows, G.p + goff[q], 1, nd.k, X, 1, nd.k});
+  }
+  btrsm(lo, true, s);
+  btrsm(up, false, s);
+}
+
 void hss_build_impl(HSSImpl& H, const double* F, int64_t n, int r, double h, const hss_opts& o,
                     std::shared_ptr<Comm> comm, cudaStream_t s, int s_cols) {
   H.n = n;
@@ -417,7 +469,8 @@ void hss_build_impl(HSSImpl& H, const double* F, int64_t n, int r, double h, con
       if (!nd.pt && nd.k > 0 && nd.rows > nd.k)
         tp.push_back({nd.k, nd.rows - nd.k, Wk.p + nd.roff * S, 1, S, Wk.p + (nd.roff + nd.k) * S, 1, S});
     }
-    btrsm(tp, false, s);
+    const bool spd = o.interp == HSS_INTERP_SPD;
+    if (!spd) btrsm(tp, false, s);
     H.U[l].alloc(std::max<int64_t>(1, sumU));
     H.J[l].alloc(std::max<int64_t>(1, sumK));
     DevBuf<double> Ysk(ann ? 1 : (size_t)std::max<int64_t>(1, sumK) * S), Omp(ann ? 1 : (size_t)std::max<int64_t>(1, sumK) * S);
@@ -427,10 +480,13 @@ void hss_build_impl(HSSImpl& H, const double* F, int64_t n, int r, double h, con
       sn[q] = {nd.roff, nd.koff, nd.uoff, nd.rows, nd.k, nd.pt ? 1 : 0, 0};
     }
     auto dsn = upload(sn, s);
-    scatter_u_kernel<<<nn, 256, 0, s>>>(dsn.p, piv.p, Wk.p, S, H.U[l].p);
-    LAUNCH_CHECK();
+    if (!spd) {
+      scatter_u_kernel<<<nn, 256, 0, s>>>(dsn.p, piv.p, Wk.p, S, H.U[l].p);
+      LAUNCH_CHECK();
+    }
     select_kernel<<<nn, 256, 0, s>>>(dsn.p, piv.p, act, ann ? nullptr : Ycur.p, omcur, S, H.J[l].p, Ysk.p, Omp.p);
     LAUNCH_CHECK();
+    if (spd) spd_interp_level(H, l, act, o.spd_eps, s);
     // Omega'_t = U_t^T Omega^_t
     std::vector<GemmProb> gp;
     for (int i = f; i < e && !ann; ++i) {
