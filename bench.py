@@ -127,13 +127,18 @@ def measure_dgemm(dev, N=8192, reps=5):
     return 2.0 * N ** 3 / best / 1e12
 
 
-def cfg_opts(cfg, sampling="sketch"):
+def cfg_opts(cfg, sampling="sketch", interp="id"):
     o = dict(leaf_size=cfg["leaf"], rel_tol=cfg["rel_tol"], abs_tol=cfg["abs_tol"], max_rank=cfg["cap"],
              oversample=cfg["s"] - cfg["cap"], omega_seed=cfg["seed_omega"], tree_seed=cfg["seed_tree"])
+    if interp == "spd":
+        o.update(interp="spd", spd_eps=SPD_EPS)
     if sampling == "ann":
         o.update(sampling="ann", ann_neighbors=cfg["ann_neighbors"], ann_trees=cfg["ann_trees"],
                  ann_leaf=cfg["ann_leaf"], ann_seed=cfg["ann_seed"])
     return o
+
+
+SPD_EPS = 1e-12  # N4 jitter on K(J,J) (relative to K_ii = 1)
 
 
 def node_shapes(ranks, n, leaf):
@@ -408,6 +413,9 @@ def main():
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-predict", action="store_true")
     ap.add_argument("--no-variants", action="store_true", help="skip the HSS-ANN variant sub-line")
+    ap.add_argument("--interp", default="id", choices=["id", "spd"],
+                    help="interpolation of the compression: the paper's ID (default) or the SPD-preserving "
+                         "kernel interpolant (SURVEY 8(f) N4; beta = the paper's schedule)")
     ap.add_argument("--sampling", default="sketch", choices=["sketch", "ann"],
                     help="compression sampling: the randomized sketch (north star, default) or HSS-ANN "
                          "column sampling (SURVEY 8(f) N1)")
@@ -441,6 +449,8 @@ def main():
     cfg = datagen.get_config(args.config)
     if args.sampling == "ann":
         cfg["beta"] = cfg["beta_ann"]  # AMB-9 calibrated on the ANN K~ (datagen/configs.py)
+    if args.interp == "spd":
+        cfg["beta"] = datagen.configs.beta_schedule(args.n or cfg["n"])  # N4: K~ PSD, no calibration
     if args.beta is not None:
         cfg["beta"] = args.beta
     n = args.n or cfg["n"]
@@ -456,7 +466,7 @@ def main():
     t0, t1 = rank * nt // world, (rank + 1) * nt // world
     Fd, yd, Ftd = (torch.from_numpy(a).to(dev) for a in (F, y, np.ascontiguousarray(Ft[t0:t1])))
     stream = torch.cuda.current_stream()
-    opts = cfg_opts(cfg, args.sampling)
+    opts = cfg_opts(cfg, args.sampling, args.interp)
     opts["comm"] = comm
 
     def step():
@@ -468,10 +478,11 @@ def main():
         if not args.no_predict and Ftd.shape[0] > 0:
             p0, p1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
             p0.record(stream)
-            P.svm_predict(Fd, yd, res["z"], h, res["bias"], Ftd)
+            _, lab = P.svm_predict(Fd, yd, res["z"], h, res["bias"], Ftd)
             p1.record(stream)
             p1.synchronize()
             st["ms_predict"] = p0.elapsed_time(p1)
+            st["labels"] = lab
         hi, ui = H.info(), U.info()
         U.free()
         H.free()
@@ -506,6 +517,16 @@ def main():
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
     ms_total, loop_ms, build_ms, sketch_ms = t.tolist()
     hi, ui, ast = (dict(d) for d in recs[-1])
+    # test accuracy of the last step's labels against the synthetic test labels (after the timed
+    # region; each rank holds its share of the test points)
+    acc = None
+    if "labels" in ast:
+        lab = ast.pop("labels")
+        hit = torch.tensor([float((lab[:, 0].cpu().numpy() == yt[t0:t1]).sum()), float(t1 - t0)],
+                           dtype=torch.float64, device=dev)
+        if world > 1:
+            dist.all_reduce(hit)
+        acc = hit[0].item() / max(1.0, hit[1].item())
     # phase times: per-phase medians over the timed steps (one step can hit a memory-pool growth)
     for j, d in enumerate((hi, ui, ast)):
         for k in list(d):
@@ -529,8 +550,9 @@ def main():
     line = {"metric": METRIC, "value": value, "unit": "iters/s", "n_gpus": world, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": ms_total / args.steps, "higher_is_better": True,
             "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-            "config": {"workload": cfg["name"] + ("" if args.sampling == "sketch" else "+ann"),
-                       "sampling": args.sampling, "n": n, "n_test": nt, "r": cfg["r"], "h": h, "C": Cs,
+            "config": {"workload": cfg["name"] + ("" if args.sampling == "sketch" else "+ann")
+                       + ("" if args.interp == "id" else "+spd"),
+                       "sampling": args.sampling, "interp": args.interp, "n": n, "n_test": nt, "r": cfg["r"], "h": h, "C": Cs,
                        "beta": cfg["beta"], "max_it": max_it, "leaf": cfg["leaf"], "cap": cfg["cap"],
                        "s": cfg["s"], "rel_tol": cfg["rel_tol"],
                        "parallelism": (f"subtree-sharded over {world}: per-iteration exchange "
@@ -541,6 +563,7 @@ def main():
                        "l2": "inputs larger than L2 (factor %.2f GB, sketch operands %.2f GB)" % (
                            ui["factor_bytes"] / 1e9, 16.0 * n * cfg["s"] / 1e9)},
             "hss_build_ulv_s": build_ms / 1e3,
+            "test_accuracy": acc,
             "phases_ms": {"tree": hi["ms_tree"], "omega": hi["ms_omega"], "sketch": hi["ms_sketch"],
                           "compress": hi["ms_compress"], "factor": ui["ms_factor"],
                           "admm_precompute": ast["ms_precompute"], "admm_loop": ast["ms_loop"],
@@ -668,6 +691,40 @@ def main():
             "factor_bytes": ui_a["factor_bytes"],
             "note": "HSS-ANN sampling (ann_neighbors/trees/leaf from datagen/configs.py); not the north-star "
                     "dense sketch - reported beside it"}}
+    if world == 1 and args.sampling == "sketch" and args.interp == "id" and not args.no_variants and args.n is None:
+        # N4: the same dense-sketch step with the SPD-preserving interpolation at the
+        # paper's beta schedule - K~ is PSD, so no calibration; one warm-up + one timed step
+        opts_s = cfg_opts(cfg, "sketch", "spd")
+        beta_s = datagen.configs.beta_schedule(n)
+
+        def step_spd():
+            H = P.hss_build(Fd, h, **opts_s)
+            try:
+                U = P.hss_ulv_factor(H, beta_s)
+                try:
+                    res = P.admm_svm_train(U, yd, Cs, max_it, want_mu=False)
+                    _, lab = P.svm_predict(Fd, yd, res["z"], h, res["bias"], Ftd)
+                    acc_s = float((lab[:, 0].cpu().numpy() == yt[t0:t1]).mean())
+                    return H.info(), U.info(), res["stats"], acc_s
+                finally:
+                    U.free()
+            finally:
+                H.free()
+
+        step_spd()
+        hi_s, ui_s, st_s, acc_s = step_spd()
+        line.setdefault("variants", {})["spd"] = {
+            "interp": "spd", "beta": beta_s, "test_accuracy": acc_s,
+            "test_accuracy_id": acc, "beta_id": cfg["beta"],
+            "admm_iters_per_s": max_it * len(Cs) / (st_s["ms_loop"] / 1e3),
+            "hss_build_ulv_s": (hi_s["ms_tree"] + hi_s["ms_omega"] + hi_s["ms_sketch"] + hi_s["ms_compress"]
+                                + ui_s["ms_factor"]) / 1e3,
+            "phases_ms": {"tree": hi_s["ms_tree"], "sketch": hi_s["ms_sketch"], "compress": hi_s["ms_compress"],
+                          "factor": ui_s["ms_factor"], "admm_loop": st_s["ms_loop"]},
+            "ranks_max": hi_s["max_rank_used"], "passthrough": hi_s["passthrough"],
+            "note": "N4 SPD-preserving compression (H3's skeletons, U = K(A,J)(K(J,J)+eps I)^-1): K~ PSD, "
+                    "beta = the paper's schedule; test_accuracy on the synthetic test points vs the "
+                    "main line's (ID form at the calibrated beta)"}
     if rank == 0 and world == 1 and not args.no_cpu_baseline and args.n is None:
         r = oracle_phases(args.config, args.ref_n, args.ref_iters)
         hinfo = host_info()
