@@ -41,6 +41,7 @@ import datagen  # noqa: E402
 from oracle import admm, hss, kernel, pipeline, rng, svm, tree, ulv  # noqa: E402
 
 CACHE = os.path.join(ROOT, ".golden_cache")
+SPD_EPS = 1e-12  # N4 jitter (bench.py / tests use the same)
 GOLD = os.path.join(ROOT, "tests", "golden")
 
 
@@ -52,7 +53,7 @@ def log(*a):
     print(time.strftime("%H:%M:%S"), *a, flush=True)
 
 
-def build_cached(tag, cfg, F):
+def build_cached(tag, cfg, F, interp="id"):
     path = os.path.join(CACHE, f"{tag}_hss.pkl")
     if os.path.exists(path):
         log("loading cached HSS", path)
@@ -71,7 +72,7 @@ def build_cached(tag, cfg, F):
     log("sketch", tm["sketch"])
     t0 = time.time()
     H = hss.compress(Fp, cfg["h"], ranges, Om, rel_tol=cfg["rel_tol"], abs_tol=cfg["abs_tol"],
-                     cap=cfg["cap"], S=S)
+                     cap=cfg["cap"], S=S, interp=interp, spd_eps=SPD_EPS)
     tm["compress_after_sketch"] = time.time() - t0
     log("compress", tm["compress_after_sketch"])
     g = np.random.default_rng(50 + cfg["id"])
@@ -91,6 +92,8 @@ def main():
     ap.add_argument("--beta", type=float, default=None)
     ap.add_argument("--h", type=float, default=None, help="config 4: one grid width")
     ap.add_argument("--no-chaos", action="store_true")
+    ap.add_argument("--interp", default="id", choices=["id", "spd"],
+                    help="spd: N4 SPD-preserving compression at the paper's beta schedule (tag cfg{c}_spd)")
     ap.add_argument("--n", type=int, default=None, help="smoke-test size (writes under --out)")
     ap.add_argument("--out", default=None)
     a = ap.parse_args()
@@ -104,13 +107,16 @@ def main():
         cfg["h"] = a.h if a.h is not None else cfg["h"][0]
         cfg["beta"] = cfg["beta_per_h"][cfg["h"]]
         tag = f"cfg{c}_h{cfg['h']:g}"
+    if a.interp == "spd":
+        tag += "_spd"
+        cfg["beta"] = datagen.configs.beta_schedule(cfg["n"] if a.n is None else a.n)
     beta = cfg["beta"] if a.beta is None else a.beta
     C = cfg["C"][0]
     max_it = cfg["max_it"]
     F, y, Ft, _ = datagen.generate(c, n=a.n, n_test=None if a.n is None else 2048)
     n = F.shape[0]
     log("config", c, "n", n, "beta", beta)
-    B = build_cached(tag, cfg, F)
+    B = build_cached(tag, cfg, F, a.interp)
     perm, H = B["perm"], B["H"]
     L = H.L
     nn = 2 ** (L + 1) - 1
@@ -120,7 +126,7 @@ def main():
     nsamp = min(n, 65536)
     vidx = np.sort(g.choice(n, nsamp, replace=False)) if nsamp < n else np.arange(n)
 
-    meta = dict(config=c, n=n, r=F.shape[1], h=cfg["h"], C=C, beta=beta, max_it=max_it,
+    meta = dict(config=c, n=n, r=F.shape[1], h=cfg["h"], C=C, beta=beta, max_it=max_it, interp=a.interp,
                 leaf=cfg["leaf"], cap=cfg["cap"], s=cfg["s"], rel_tol=cfg["rel_tol"],
                 seed_omega=cfg["seed_omega"], seed_tree=cfg["seed_tree"], L=L,
                 oracle_timings_s=dict(B["timings"]),
@@ -227,7 +233,7 @@ def main():
         z0 = 1e-12 * np.random.default_rng(0).standard_normal(n)
         o2 = admm.run(solve, yp, C, beta, max_it, z0=z0)
         div = float(np.abs(o["z"] - o2["z"]).max())
-        rec = dict(config=c, n=n, h=cfg["h"], beta=beta, chaos_it=max_it, chaos_div=div,
+        rec = dict(config=c, n=n, h=cfg["h"], beta=beta, interp=a.interp, chaos_it=max_it, chaos_div=div,
                    chaos_pass=bool(div < 1e-9), secs=time.time() - t0, source="make_fullsize_goldens")
         if not a.out:
             with open(os.path.join(ROOT, "configs", "beta_calibration.jsonl"), "a") as f:

@@ -138,19 +138,28 @@ def test_cfg4_full_size_live_oracle_all_C(gpu_lib, h):
 
 
 # ------------------------------------------------------------------ goldens: configs 2 and 3
-@pytest.mark.parametrize("c", [2, 3])
-def test_full_size_goldens(gpu_lib, c):
+@pytest.mark.parametrize("c,interp", [(2, "id"), (3, "id"), (2, "spd")])
+def test_full_size_goldens(gpu_lib, c, interp):
+    """interp = "spd": N4 (SPD-preserving compression) at the paper's beta schedule, against the
+    oracle's compress(..., interp="spd") goldens (scripts/make_fullsize_goldens.py --interp spd)."""
     P = gpu_lib
-    jp, zp = os.path.join(GOLD, f"cfg{c}_full.json"), os.path.join(GOLD, f"cfg{c}_full.npz")
+    tag = f"cfg{c}" + ("_spd" if interp == "spd" else "")
+    jp, zp = os.path.join(GOLD, f"{tag}_full.json"), os.path.join(GOLD, f"{tag}_full.npz")
     if not (os.path.exists(jp) and os.path.exists(zp)):
-        pytest.fail(f"golden cfg{c}_full missing: run scripts/make_fullsize_goldens.py --config {c}")
+        pytest.fail(f"golden {tag}_full missing: run scripts/make_fullsize_goldens.py --config {c} --interp {interp}")
     g = json.load(open(jp))
     A = dict(np.load(zp))
     cfg = datagen.get_config(c)
+    if interp == "spd":
+        cfg["beta"] = datagen.configs.beta_schedule(cfg["n"])
     assert g["n"] == cfg["n"] and g["beta"] == cfg["beta"] and g["max_it"] == cfg["max_it"]
+    assert g.get("interp", "id") == interp
     F, y, Ft, _ = datagen.generate(c)
     n = F.shape[0]
-    Hg = P.hss_build(_t(F), cfg["h"], **_kw(cfg))
+    kw = _kw(cfg)
+    if interp == "spd":
+        kw.update(interp="spd", spd_eps=1e-12)
+    Hg = P.hss_build(_t(F), cfg["h"], **kw)
     info = Hg.info()
     perm = info["perm"]
     assert sha(perm.astype(np.int64)) == g["perm_sha256"]
