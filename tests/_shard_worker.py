@@ -23,6 +23,7 @@ def main():
     beta = float(sys.argv[5]) if len(sys.argv) > 5 else 1e4
     max_it = int(sys.argv[6]) if len(sys.argv) > 6 else 60
     sampling = sys.argv[7] if len(sys.argv) > 7 else "sketch"
+    interp = sys.argv[8] if len(sys.argv) > 8 else "id"       # N4: "spd"
     rank = int(os.environ.get("RANK", 0))
     world = int(os.environ.get("WORLD_SIZE", 1))
     import datagen
@@ -44,7 +45,7 @@ def main():
                     max_rank=cfg["cap"], oversample=cfg["s"] - cfg["cap"], omega_seed=cfg["seed_omega"],
                     tree_seed=cfg["seed_tree"], comm=comm, sampling=sampling,
                     ann_neighbors=cfg["ann_neighbors"], ann_trees=cfg["ann_trees"], ann_leaf=cfg["ann_leaf"],
-                    ann_seed=cfg["ann_seed"])
+                    ann_seed=cfg["ann_seed"], interp=interp)
     U = P.hss_ulv_factor(H, beta)
     g = np.random.default_rng(7)
     b = torch.from_numpy(g.standard_normal((n, 2))).to(dev)
@@ -59,7 +60,7 @@ def main():
     e2e = P.svm_train_predict_host(F, y, h, beta, Cs, max_it, Ftest=Ft, leaf_size=cfg["leaf"],
                                    rel_tol=cfg["rel_tol"], abs_tol=cfg["abs_tol"], max_rank=cfg["cap"],
                                    oversample=cfg["s"] - cfg["cap"], omega_seed=cfg["seed_omega"],
-                                   tree_seed=cfg["seed_tree"], comm=comm, sampling=sampling,
+                                   tree_seed=cfg["seed_tree"], comm=comm, sampling=sampling, interp=interp,
                                    ann_neighbors=cfg["ann_neighbors"], ann_trees=cfg["ann_trees"],
                                    ann_leaf=cfg["ann_leaf"], ann_seed=cfg["ann_seed"])
     np.savez(os.path.join(out, f"P{world}_r{rank}.npz"), x=x.cpu().numpy(), kv=kv.cpu().numpy(),

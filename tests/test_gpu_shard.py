@@ -40,6 +40,8 @@ def _run(out, P, args):
     ((1, 2600, 128, 1e4, 40), (2, 8)),        # cfg-1 knobs (r = 22), L = 5: lg = 1, 3
     ((3, 1000, 256, 1e4, 40), (4,)),          # L = 2 = lg: the exchanged level is the leaves
     ((3, 4096, 256, 1e2, 40, "ann"), (2, 4)),  # HSS-ANN sampling (N1-N3), sharded
+    ((3, 4096, 256, 1e2, 40, "sketch", "spd"), (2, 4)),  # N4 SPD-preserving interpolation, sharded
+    ((3, 3000, 96, 1e2, 40, "sketch", "spd"), (2,)),     # N4, ragged n, every node compresses
 ])
 def test_subtree_sharding_is_bitwise_p_invariant(tmp_path, args, Ps):
     ref = _run(tmp_path, 1, args)[0]
