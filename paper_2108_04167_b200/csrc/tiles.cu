@@ -573,41 +573,70 @@ void omega_rows(uint64_t seed, const int64_t* idx, int64_t rows, int s, double* 
 }
 
 // ------------------------------------------------------------------ direct kernel blocks
-__global__ void kblock_kernel(const double* __restrict__ F, int rp, int r, double two_h2,
-                              const KblkProb* __restrict__ probs) {
+// 64 x 64 entries per CTA, 4 x 4 per thread (rows ty + 16a, columns tx + 16b): the gathered
+// feature rows staged in shared memory (32 features at a time, odd row stride: conflict-free
+// column reads), each
+// entry d2 = sum_f (a_f - b_f)^2 by fma in feature order, then exp(-d2 / 2h^2) -- the per-entry
+// arithmetic of the direct-difference definition (AMB-4), unchanged by the register blocking.
+constexpr int KBT = 64, KBF = 32, KBS = KBF + 1;  // features staged KBF at a time, odd stride
+__global__ void __launch_bounds__(256) kblock_kernel(const double* __restrict__ F, int rp, int r, double two_h2,
+                                                     const KblkProb* __restrict__ probs) {
   const KblkProb P = probs[blockIdx.z];
-  const int i0 = blockIdx.y * 16, j0 = blockIdx.x * 16;
+  const int i0 = blockIdx.y * KBT, j0 = blockIdx.x * KBT;
   if (i0 >= P.na || j0 >= P.nb) return;
-  extern __shared__ double sh[];
-  double* As = sh;            // 16 x r
-  double* Bs = sh + 16 * r;   // 16 x r
-  __shared__ int64_t ia_s[16], ib_s[16];
+  __shared__ double As[KBT * KBS], Bs[KBT * KBS];
+  __shared__ int64_t ia_s[KBT], ib_s[KBT];
   const int tid = threadIdx.y * 16 + threadIdx.x;
-  if (tid < 16) {
+  if (tid < KBT) {
     const int i = i0 + tid;
     ia_s[tid] = (i < P.na) ? (P.ia ? P.ia[i] : P.a0 + i) : -1;
-  } else if (tid < 32) {
-    const int j = j0 + tid - 16;
-    ib_s[tid - 16] = (j < P.nb) ? (P.ib ? P.ib[j] : P.b0 + j) : -1;
+  } else if (tid < 2 * KBT) {
+    const int j = j0 + tid - KBT;
+    ib_s[tid - KBT] = (j < P.nb) ? (P.ib ? P.ib[j] : P.b0 + j) : -1;
   }
-  __syncthreads();
-  for (int e = tid; e < 16 * r; e += 256) {
-    const int q = e / r, f = e % r;
-    As[e] = ia_s[q] >= 0 ? F[ia_s[q] * rp + f] : 0.0;
-    Bs[e] = ib_s[q] >= 0 ? F[ib_s[q] * rp + f] : 0.0;
+  const int ty = threadIdx.y, tx = threadIdx.x;
+  double d2[4][4];
+#pragma unroll
+  for (int a = 0; a < 4; ++a)
+#pragma unroll
+    for (int b = 0; b < 4; ++b) d2[a][b] = 0.0;
+  for (int f0 = 0; f0 < r; f0 += KBF) {
+    const int nf = min(KBF, r - f0);
+    __syncthreads();
+    for (int e = tid; e < KBT * nf; e += 256) {
+      const int q = e / nf, f = e % nf;
+      As[q * KBS + f] = ia_s[q] >= 0 ? F[ia_s[q] * rp + f0 + f] : 0.0;
+      Bs[q * KBS + f] = ib_s[q] >= 0 ? F[ib_s[q] * rp + f0 + f] : 0.0;
+    }
+    __syncthreads();
+    for (int f = 0; f < nf; ++f) {
+      double av[4], bv[4];
+#pragma unroll
+      for (int a = 0; a < 4; ++a) av[a] = As[(ty + 16 * a) * KBS + f];
+#pragma unroll
+      for (int b = 0; b < 4; ++b) bv[b] = Bs[(tx + 16 * b) * KBS + f];
+#pragma unroll
+      for (int a = 0; a < 4; ++a)
+#pragma unroll
+        for (int b = 0; b < 4; ++b) {
+          const double d = av[a] - bv[b];
+          d2[a][b] = fma(d, d, d2[a][b]);
+        }
+    }
   }
-  __syncthreads();
-  const int ti = threadIdx.y, tj = threadIdx.x;
-  const int i = i0 + ti, j = j0 + tj;
-  if (i >= P.na || j >= P.nb) return;
-  double d2 = 0.0;
-  for (int f = 0; f < r; ++f) {
-    const double d = As[ti * r + f] - Bs[tj * r + f];
-    d2 = fma(d, d, d2);
+#pragma unroll
+  for (int a = 0; a < 4; ++a) {
+    const int il = ty + 16 * a, i = i0 + il;
+    if (i >= P.na) continue;
+#pragma unroll
+    for (int b = 0; b < 4; ++b) {
+      const int jl = tx + 16 * b, j = j0 + jl;
+      if (j >= P.nb) continue;
+      double v = exp(-d2[a][b] / two_h2);
+      if (ia_s[il] == ib_s[jl]) v = 1.0 + P.diag_add;
+      P.out[(long long)i * P.ld + j] = v;
+    }
   }
-  double v = exp(-d2 / two_h2);
-  if (ia_s[ti] == ib_s[tj]) v = 1.0 + P.diag_add;
-  P.out[(long long)i * P.ld + j] = v;
 }
 
 void kernel_blocks(const double* F, int rp, int r, double h, const std::vector<KblkProb>& probs_in,
@@ -623,11 +652,8 @@ void kernel_blocks(const double* F, int rp, int r, double h, const std::vector<K
     KblkProb* d = nullptr;
     lib_malloc((void**)&d, chunk.size() * sizeof(KblkProb), s);
     CUDA_CHECK(cudaMemcpyAsync(d, chunk.data(), chunk.size() * sizeof(KblkProb), cudaMemcpyHostToDevice, s));
-    dim3 grid(ceil_div(mc, 16), ceil_div(mr, 16), (unsigned)chunk.size());
-    size_t smem = 2 * 16 * (size_t)r * sizeof(double);
-    if (smem > 48 * 1024)
-      CUDA_CHECK(cudaFuncSetAttribute(kblock_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-    kblock_kernel<<<grid, dim3(16, 16), smem, s>>>(F, rp, r, two_h2, d);
+    dim3 grid(ceil_div(mc, KBT), ceil_div(mr, KBT), (unsigned)chunk.size());
+    kblock_kernel<<<grid, dim3(16, 16), 0, s>>>(F, rp, r, two_h2, d);
     LAUNCH_CHECK();
     CUDA_CHECK(cudaFreeAsync(d, s));
   }
