@@ -37,7 +37,7 @@ from __future__ import annotations
 import numpy as np
 import scipy.linalg as sla
 
-from .hss import HSS, choose_rank
+from .hss import HSS, choose_rank, nystrom_u
 from .kernel import gaussian_block
 from .rng import splitmix64
 from .tree import node_ranges, num_levels
@@ -150,9 +150,12 @@ def sample_columns(node_id: int, lo: int, hi: int, n: int, active_pos: np.ndarra
 
 def compress_ann(Fp: np.ndarray, h: float, ranges, perm: np.ndarray, ann_idx: np.ndarray,
                  ann_d: np.ndarray, s: int, seed: int, *, ranks=None, rel_tol=0.0, abs_tol=0.0,
-                 cap=None) -> HSS:
+                 cap=None, interp: str = "id", spd_eps: float = 1e-10) -> HSS:
     """H2-H5 with N2-N3 in place of the sketch.  ann_idx: n x kappa ORIGINAL indices (knn());
-    rows of ann_* are indexed by ORIGINAL index."""
+    rows of ann_* are indexed by ORIGINAL index.  interp="spd": N4's kernel interpolant onto the
+    same skeletons (oracle/hss.py; the sampled columns do not depend on U here)."""
+    if interp not in ("id", "spd"):
+        raise ValueError(f"interp must be 'id' or 'spd', got {interp!r}")
     n = Fp.shape[0]
     L = len(ranges) - 1
     hss = HSS(n=n, L=L, ranges=ranges, Fp=Fp, h=h)
@@ -191,10 +194,13 @@ def compress_ann(Fp: np.ndarray, h: float, ranges, perm: np.ndarray, ann_idx: np
                 hss.Jloc[t] = np.arange(rows)
                 hss.J[t] = A
             else:
-                T = sla.solve_triangular(R[:k, :k], R[:k, k:], lower=False)
-                U = np.zeros((rows, k))
-                U[piv[:k]] = np.eye(k)
-                U[piv[k:]] = T.T
+                if interp == "spd":                                               # N4
+                    U = nystrom_u(Fp, h, A, A[piv[:k]], spd_eps)
+                else:
+                    T = sla.solve_triangular(R[:k, :k], R[:k, k:], lower=False)
+                    U = np.zeros((rows, k))
+                    U[piv[:k]] = np.eye(k)
+                    U[piv[k:]] = T.T
                 hss.U[t] = U
                 hss.Jloc[t] = piv[:k].copy()
                 hss.J[t] = A[piv[:k]]

@@ -34,7 +34,7 @@ def build(F, cfg, h=None, ranks=None, S=None, timings=None):
     return perm, ranges, Om, H
 
 
-def build_ann(F, cfg, h=None, ranks=None, timings=None):
+def build_ann(F, cfg, h=None, ranks=None, timings=None, interp="id", spd_eps=1e-12):
     """Tree + ANN lists + HSS-ANN compression (N1-N3).  Returns (perm, ranges, (idx, d), hss)."""
     from . import ann as _ann
     t = time.perf_counter()
@@ -45,7 +45,8 @@ def build_ann(F, cfg, h=None, ranks=None, timings=None):
     t2 = time.perf_counter()
     kw = dict(ranks=ranks) if ranks is not None else dict(
         rel_tol=cfg["rel_tol"], abs_tol=cfg["abs_tol"], cap=cfg["cap"])
-    H = _ann.compress_ann(F[perm], h, ranges, perm, idx, d, cfg["s"], cfg["ann_seed"], **kw)
+    H = _ann.compress_ann(F[perm], h, ranges, perm, idx, d, cfg["s"], cfg["ann_seed"], interp=interp,
+                          spd_eps=spd_eps, **kw)
     if timings is not None:
         timings["tree"] = t1 - t
         timings["ann"] = t2 - t1

@@ -46,6 +46,7 @@ CASES = {
     "cfg1a": dict(cfg=1, n=3000, max_it=100, beta=1e2),
     "cfg4a": dict(cfg=4, n=3000, max_it=100, beta=1e2, h=1.0),
     "cfg3small": dict(cfg=3, n=700, max_it=60, beta=1e2),
+    "cfg3a_spd": dict(cfg=3, n=5000, max_it=100, beta=1e2, interp="spd"),   # N4 with HSS-ANN sampling
 }
 _CACHE = {}
 
@@ -59,12 +60,13 @@ def run_case(P, name):
         cfg["h"] = d["h"]
     cfg["beta"] = d["beta"]
     F, y, _, _ = datagen.generate(d["cfg"], n=d["n"], n_test=0)
-    perm, ranges, _, H = o_pipe.build_ann(F, cfg)
+    interp = d.get("interp", "id")
+    perm, ranges, _, H = o_pipe.build_ann(F, cfg, interp=interp, spd_eps=1e-12)
     fac = o_ulv.factor(H, cfg["beta"])
     Hg = P.hss_build(_t(F), cfg["h"], leaf_size=cfg["leaf"], rel_tol=cfg["rel_tol"], abs_tol=cfg["abs_tol"],
                      max_rank=cfg["cap"], oversample=cfg["s"] - cfg["cap"], tree_seed=cfg["seed_tree"],
                      sampling="ann", ann_neighbors=cfg["ann_neighbors"], ann_trees=cfg["ann_trees"],
-                     ann_leaf=cfg["ann_leaf"], ann_seed=cfg["ann_seed"])
+                     ann_leaf=cfg["ann_leaf"], ann_seed=cfg["ann_seed"], interp=interp, spd_eps=1e-12)
     Ug = P.hss_ulv_factor(Hg, cfg["beta"])
     out = dict(d=d, cfg=cfg, F=F, y=y, perm=perm, H=H, fac=fac, Hg=Hg, Ug=Ug)
     _CACHE[name] = out

@@ -145,3 +145,22 @@ def test_spd_eps_bound_keeps_psd():
         Ksum, terms = _telescoping_sum(H)
         assert np.abs(Kt - Ksum).max() <= 1e-12 * np.abs(Kt).max()
         assert np.linalg.eigvalsh(Kt)[0] >= -1e-12 * np.abs(Kt).max()
+
+
+def test_spd_with_ann_sampling_is_psd_and_keeps_skeletons():
+    """N4 with HSS-ANN sampling (N1-N3): the sampled columns do not depend on U, so the skeletons
+    equal the ID form's; the assembled K~ is the PSD decomposition's sum, and PSD."""
+    from oracle import ann
+    cfg = datagen.get_config(3)
+    F, *_ = datagen.generate(3, n=1024, n_test=1)
+    perm, ranges = tree.build_tree(F, 128, cfg["seed_tree"])
+    idx, d = ann.knn(F, cfg["ann_neighbors"], cfg["ann_trees"], cfg["ann_leaf"], cfg["ann_seed"])
+    kw = dict(rel_tol=1e-3, cap=48)
+    Hid = ann.compress_ann(F[perm], 1.0, ranges, perm, idx, d, 64, cfg["ann_seed"], **kw)
+    Hs = ann.compress_ann(F[perm], 1.0, ranges, perm, idx, d, 64, cfg["ann_seed"], interp="spd", spd_eps=0.0, **kw)
+    assert all(np.array_equal(Hid.J[t], Hs.J[t]) for t in Hid.J)
+    assert sum(u is not None for u in Hs.U.values()) > 4
+    Kt = hss.assemble_dense(Hs)
+    Ksum, terms = _telescoping_sum(Hs)
+    assert np.abs(Kt - Ksum).max() <= 1e-12 * np.abs(Kt).max()
+    assert np.linalg.eigvalsh(Kt)[0] >= -1e-12 * np.abs(Kt).max()
