@@ -242,6 +242,7 @@ def oracle_phases(cfg_id, n_sample, iters, sketch_rows=512):
     from oracle import admm, hss, kernel, pipeline, rng, svm, ulv
     cfg = datagen.get_config(cfg_id)
     n = cfg["n"]
+    n_sample = min(n_sample, n)   # config 0 (n = 2000): the whole config, nothing projected
     F, y, Ft, _ = datagen.generate(cfg_id, n=n_sample, n_test=256)
     tm = {}
     # per-node phases (small LAPACK/BLAS calls in Python loops) run with one BLAS thread: the
@@ -303,6 +304,7 @@ def oracle_sample(cfg_id, n_sample, iters, steps=1, warmup=0):
 
     from oracle import admm, pipeline, ulv
     cfg = datagen.get_config(cfg_id)
+    n_sample = min(n_sample, cfg["n"])
     F, y, _, _ = datagen.generate(cfg_id, n=n_sample, n_test=0)
     with threadpool_limits(limits=1):   # per-node phases: one BLAS thread (see oracle_phases)
         t0 = time.perf_counter()

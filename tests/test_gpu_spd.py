@@ -160,3 +160,53 @@ def test_spd_invalid_eps_rejected(gpu_lib):
     with pytest.raises(P.HssError) as ei:
         P.hss_build(F, 1.0, leaf_size=32, max_rank=8, interp="spd", spd_eps=-1.0)
     assert ei.value.code == -1
+
+
+def test_spd_config3_full_size_sampled_nodes_and_psd(gpu_lib):
+    """Config 3 at its stated size (n = 524288), in the launch configuration bench.py's
+    variants.spd times: the oracle recomputes U_t = K(A_t, J_t)(K(J_t, J_t) + eps I)^-1 of sampled
+    nodes of every level from the GPU's own tree and skeletons (the N4 definition, oracle/hss.py
+    nystrom_u; 1e-9), and K~ + beta I factors at beta = 1e-6 (a property of the N4 form at any
+    size: K~ is PSD), then ADMM runs at the paper's beta schedule (1e3)."""
+    import torch
+    P = gpu_lib
+    cfg = datagen.get_config(3)
+    F, y, _, _ = datagen.generate(3, n_test=0)
+    Fd = _t(F)
+    H = P.hss_build(Fd, cfg["h"], leaf_size=cfg["leaf"], rel_tol=cfg["rel_tol"], abs_tol=cfg["abs_tol"],
+                    max_rank=cfg["cap"], oversample=cfg["s"] - cfg["cap"], omega_seed=cfg["seed_omega"],
+                    tree_seed=cfg["seed_tree"], interp="spd", spd_eps=EPS)
+    info = H.info()
+    perm, ks, skel = info["perm"], info["ranks"].astype(np.int64), info["skeletons"].astype(np.int64)
+    L = int(info["L"])
+    Fp = F[perm]
+    J, off = {}, 0
+    for lvl in range(1, L + 1):
+        for t in range((1 << lvl) - 1, (1 << (lvl + 1)) - 1):
+            J[t] = skel[off:off + ks[t]]
+            off += ks[t]
+    ranges = o_tree.node_ranges(F.shape[0], L)
+    g = np.random.default_rng(11)
+    checked = 0
+    for lvl in range(1, L + 1):
+        lo_id = (1 << lvl) - 1
+        for t in sorted({lo_id, lo_id + int(g.integers(0, 1 << lvl))}):
+            if lvl == L:
+                a, b = ranges[lvl][t - lo_id]
+                A = np.arange(a, b)
+            else:
+                A = np.concatenate([J[2 * t + 1], J[2 * t + 2]])
+            if ks[t] == len(A):
+                continue                                     # pass-through: U = I
+            gen = H.node_generators(t, L)
+            U = o_hss.nystrom_u(Fp, cfg["h"], A, J[t], EPS)
+            assert np.abs(gen["U"] - U).max() <= 1e-9 * max(1.0, np.abs(U).max()), (lvl, t)
+            checked += 1
+    assert checked >= L - 2
+    U6 = P.hss_ulv_factor(H, 1e-6)                           # PSD: factors at a tiny shift
+    U6.free()
+    Ug = P.hss_ulv_factor(H, datagen.configs.beta_schedule(F.shape[0]))
+    res = P.admm_svm_train(Ug, _t(y), [1.0], 10)
+    assert torch.isfinite(res["z"]).all() and res["stats"]["w1"] > 0
+    Ug.free()
+    H.free()
