@@ -296,6 +296,8 @@ void ulv_free(ulv_t U);
  * the device.  Memory of live handles is not affected. */
 int hss_pool_trim(void);
 const char* hss_last_error(void);
+/* "svmhss 0.2 (sm_100a)": 0.2 appended hss_opts.interp / spd_eps (N4); callers must zero-initialize
+ * the whole hss_opts (the library reads every field). */
 const char* hss_version(void);
 
 #ifdef __cplusplus

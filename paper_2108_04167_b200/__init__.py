@@ -286,6 +286,10 @@ def make_opts(leaf_size, rel_tol=0.0, abs_tol=0.0, max_rank=64, oversample=16, o
               tree_seed=0, ranks=None, comm=None, sampling="sketch", ann_neighbors=64, ann_trees=4,
               ann_leaf=256, ann_seed=0, adaptive_s0=0, adaptive_ds=0, perm=None, skeletons=None,
               interp="id", spd_eps=1e-12):
+    if interp not in INTERP:
+        raise ValueError(f"interp must be one of {sorted(INTERP)}, got {interp!r}")
+    if sampling not in SAMPLING:
+        raise ValueError(f"sampling must be one of {sorted(SAMPLING)}, got {sampling!r}")
     o = HssOpts()
     o.interp, o.spd_eps = INTERP[interp], float(spd_eps)
     o.adaptive_s0, o.adaptive_ds = int(adaptive_s0), int(adaptive_ds)

@@ -254,7 +254,7 @@ static std::shared_ptr<Comm> comm_of(const hss_opts* o) {
 extern "C" {
 
 const char* hss_last_error(void) { return g_last_error.c_str(); }
-const char* hss_version(void) { return "svmhss 0.1 (sm_100a)"; }
+const char* hss_version(void) { return "svmhss 0.2 (sm_100a)"; }
 int64_t hss_launch_count(void) { return (int64_t)g_launches.load(); }
 
 int hss_build(const double* F, int64_t n, int32_t r, double h, const hss_opts* opt, void* stream,
