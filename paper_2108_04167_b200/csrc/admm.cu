@@ -532,30 +532,44 @@ AdmmResult admm_train_impl(const ULVImpl& F, const double* y_orig, const std::ve
     launch_pdl(admm_epilogue_kernel, dim3(nleaf), dim3(256), epi_smem, st, EA, H.leaf_lo.p, (const int*)nullptr,
                nleaf, part.p, epi_out, counter.p, smem_tree);
   };
-  // one iteration as a CUDA graph (needs a capturable exchange when sharded)
-  cudaGraphExec_t gexec = nullptr;
+  // one iteration as a CUDA graph (needs a capturable exchange when sharded); without traces,
+  // also a graph of `gb` consecutive iterations, so the programmatic (PDL) edges continue from one
+  // iteration into the next instead of draining at every graph launch
+  cudaGraphExec_t gexec = nullptr, gexecB = nullptr;
   const bool use_graph = !sh.on() || sh.comm->capturable();
+  const int te = (opt && opt->trace_every > 0) ? opt->trace_every : 0;
+  static const int gb_env = [] { const char* e = getenv("SVMHSS_GRAPH_ITERS"); return e ? std::max(1, atoi(e)) : 4; }();
+  const int gb = (use_graph && !te && max_it >= 2 * gb_env) ? gb_env : 1;
   const long long g0 = g_launches.load();  // launches are counted per executed iteration below
-  if (use_graph) {
+  auto capture = [&](int iters, cudaGraphExec_t* out) {
     cudaStream_t cs;
     CUDA_CHECK(cudaStreamCreateWithFlags(&cs, cudaStreamNonBlocking));
     cudaGraph_t graph = nullptr;
     CUDA_CHECK(cudaStreamBeginCapture(cs, cudaStreamCaptureModeThreadLocal));
-    iteration(cs);
+    for (int q = 0; q < iters; ++q) iteration(cs);
     CUDA_CHECK(cudaStreamEndCapture(cs, &graph));
-    CUDA_CHECK(cudaGraphInstantiate(&gexec, graph, 0));
+    CUDA_CHECK(cudaGraphInstantiate(out, graph, 0));
     CUDA_CHECK(cudaGraphDestroy(graph));
     CUDA_CHECK(cudaStreamDestroy(cs));
+  };
+  if (use_graph) {
+    capture(1, &gexec);
     R.graph = 1;
     R.launches = g_launches.load() - g0;
+    if (gb > 1) capture(gb, &gexecB);
     g_launches.store(g0);
   }
-  const int te = (opt && opt->trace_every > 0) ? opt->trace_every : 0;
   DevBuf<double> full((te && (opt->trace_z || opt->trace_mu)) ? (size_t)N * nC : 0);
   EventTimer tloop(s);
   int tcount = 0;
   for (int it = 1; it <= max_it; ++it) {
     const long long gi = g_launches.load();
+    if (gexecB && it + gb - 1 <= max_it) {
+      CUDA_CHECK(cudaGraphLaunch(gexecB, s));
+      g_launches.store(gi + (long long)gb * R.launches);
+      it += gb - 1;
+      continue;
+    }
     if (use_graph) {
       CUDA_CHECK(cudaGraphLaunch(gexec, s));
       g_launches.store(gi + R.launches);
@@ -577,6 +591,7 @@ AdmmResult admm_train_impl(const ULVImpl& F, const double* y_orig, const std::ve
   }
   R.ms_loop = tloop.stop_ms();
   if (gexec) cudaGraphExecDestroy(gexec);
+  if (gexecB) cudaGraphExecDestroy(gexecB);
   {
     DevBuf<double> zf((size_t)N * nC);
     gather_points(H, z.p, nC, zf.p, s);
